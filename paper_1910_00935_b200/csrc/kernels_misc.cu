@@ -1,0 +1,266 @@
+// kernels_misc.cu -- controller (compute_actuation and its .grad), loss + adjoint
+// seed, and caller-layout <-> particle-record conversion.
+#include "kernels.h"
+
+namespace mpm {
+
+namespace {
+
+constexpr int kMaxHidden = 1024;
+constexpr int kMaxAct = 256;
+constexpr int kMaxSin = 64;
+
+// phi_j(t) = sin(omega t dt + 2 pi j / n_sin)   (R9; phase in fp64, it reaches ~40 rad)
+__device__ __forceinline__ float feature(const KParams& p, int t, int j) {
+    double ph = (double)p.omega * (double)t * (double)p.dt + 2.0 * 3.14159265358979323846 * j / p.n_sin;
+    return (float)sin(ph);
+}
+
+// one block per time step: alpha_t = tanh(W2 tanh(W1 phi + b1) + b2)  (H > 0)
+//                          alpha_t = tanh(W phi + b)                  (H = 0)
+__global__ void k_ctrl_fwd(KParams p, const float* __restrict__ th, float* __restrict__ alpha) {
+    __shared__ float phi[kMaxSin], h[kMaxHidden];
+    const int t = blockIdx.x, S = p.n_sin, H = p.hidden, A = p.n_act;
+    for (int j = threadIdx.x; j < S; j += blockDim.x) phi[j] = feature(p, t, j);
+    __syncthreads();
+    if (H > 0) {
+        const float *W1 = th, *b1 = W1 + H * S, *W2 = b1 + H, *b2 = W2 + A * H;
+        for (int i = threadIdx.x; i < H; i += blockDim.x) {
+            float z = b1[i];
+            for (int j = 0; j < S; ++j) z = fmaf(W1[i * S + j], phi[j], z);
+            h[i] = tanhf(z);
+        }
+        __syncthreads();
+        for (int a = threadIdx.x; a < A; a += blockDim.x) {
+            float z = b2[a];
+            for (int i = 0; i < H; ++i) z = fmaf(W2[a * H + i], h[i], z);
+            alpha[(int64_t)t * A + a] = tanhf(z);
+        }
+    } else {
+        const float *W = th, *b = W + A * S;
+        for (int a = threadIdx.x; a < A; a += blockDim.x) {
+            float z = b[a];
+            for (int j = 0; j < S; ++j) z = fmaf(W[a * S + j], phi[j], z);
+            alpha[(int64_t)t * A + a] = tanhf(z);
+        }
+    }
+}
+
+// one block per time step: the step's contribution (d alpha_t/d theta)^T alpha_bar_t
+__global__ void k_ctrl_bwd(KParams p, const float* __restrict__ th, const float* __restrict__ alpha,
+                           const float* __restrict__ abar, float* __restrict__ part, int64_t n_theta) {
+    __shared__ float phi[kMaxSin], h[kMaxHidden], z2b[kMaxAct], hb[kMaxHidden];
+    const int t = blockIdx.x, S = p.n_sin, H = p.hidden, A = p.n_act;
+    float* out = part + (int64_t)t * n_theta;
+    for (int j = threadIdx.x; j < S; j += blockDim.x) phi[j] = feature(p, t, j);
+    for (int a = threadIdx.x; a < A; a += blockDim.x) {
+        float al = alpha[(int64_t)t * A + a];
+        z2b[a] = abar[(int64_t)t * A + a] * (1.0f - al * al);
+    }
+    __syncthreads();
+    if (H > 0) {
+        const float *W1 = th, *b1 = W1 + H * S, *W2 = b1 + H;
+        float *W1b = out, *b1b = W1b + H * S, *W2b = b1b + H, *b2b = W2b + A * H;
+        for (int i = threadIdx.x; i < H; i += blockDim.x) {
+            float z = b1[i];
+            for (int j = 0; j < S; ++j) z = fmaf(W1[i * S + j], phi[j], z);
+            h[i] = tanhf(z);
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < A * H; q += blockDim.x) W2b[q] = z2b[q / H] * h[q % H];
+        for (int a = threadIdx.x; a < A; a += blockDim.x) b2b[a] = z2b[a];
+        for (int i = threadIdx.x; i < H; i += blockDim.x) {
+            float s = 0.0f;
+            for (int a = 0; a < A; ++a) s = fmaf(W2[a * H + i], z2b[a], s);
+            hb[i] = s * (1.0f - h[i] * h[i]);
+            b1b[i] = hb[i];
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < H * S; q += blockDim.x) W1b[q] = hb[q / S] * phi[q % S];
+    } else {
+        float *Wb = out, *bb = Wb + A * S;
+        for (int q = threadIdx.x; q < A * S; q += blockDim.x) Wb[q] = z2b[q / S] * phi[q % S];
+        for (int a = threadIdx.x; a < A; a += blockDim.x) bb[a] = z2b[a];
+    }
+}
+
+// theta_bar[q] = sum over t (ascending, fixed order) of part[t][q]
+__global__ void k_ctrl_reduce(const float* __restrict__ part, int T, int64_t n_theta,
+                              float* __restrict__ thb) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (q >= n_theta) return;
+    float s = 0.0f;
+    for (int t = 0; t < T; ++t) s += part[(int64_t)t * n_theta + q];
+    thb[q] = s;
+}
+
+// ---------------------------------------------------------------- loss
+constexpr int kLossThreads = 256;
+
+// partial sums of m x over a contiguous particle chunk (fixed tree order)
+template <int D>
+__global__ void k_com_partial(KParams p, const float* __restrict__ S, float* __restrict__ part) {
+    __shared__ float red[D][kLossThreads];
+    const int e = blockIdx.y, nb = gridDim.x;
+    const int64_t chunk = (p.N + nb - 1) / nb;
+    const int64_t lo = blockIdx.x * chunk, hi = min(p.N, lo + chunk);
+    float acc[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc[k] = 0.0f;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const float* r = S + ((int64_t)e * p.N + i) * Rec<D>::R;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc[k] += r[Rec<D>::X + k];
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) red[k][threadIdx.x] = acc[k];
+    __syncthreads();
+    for (int s = kLossThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+#pragma unroll
+            for (int k = 0; k < D; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < D; ++k) part[((int64_t)e * nb + blockIdx.x) * D + k] = red[k][0];
+}
+
+// xbar = sum m x / sum m;  L = |xbar - x*|^2 or -xbar_0;  seed g = dL/dxbar * m / M
+template <int D>
+__global__ void k_loss_final(KParams p, const float* __restrict__ part, int nb, int kind,
+                             float3 target, float* __restrict__ loss, float* __restrict__ seed,
+                             int* flags) {
+    const int e = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    float com[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        float s = 0.0f;
+        for (int b = 0; b < nb; ++b) s += part[((int64_t)e * nb + b) * D + k];
+        com[k] = s / (float)p.N;  // equal masses: sum m x / sum m = mean x
+    }
+    const float tg[3] = {target.x, target.y, target.z};
+    float L = 0.0f, g[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) g[k] = 0.0f;
+    if (kind == 0) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+            float dlt = com[k] - tg[k];
+            L = fmaf(dlt, dlt, L);
+            g[k] = 2.0f * dlt;
+        }
+    } else {
+        L = -com[0];
+        g[0] = -1.0f;
+    }
+    loss[e] = L;
+    if (!isfinite(L)) atomicOr(flags, FLAG_NONFINITE);
+#pragma unroll
+    for (int k = 0; k < D; ++k) seed[e * D + k] = g[k] / (float)p.N;  // dL/dxbar * m / (N m)
+}
+
+template <int D>
+__global__ void k_seed(KParams p, const float* __restrict__ seed, float* __restrict__ Sb) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= p.N * p.E) return;
+    const int64_t e = i / p.N;
+    float* r = Sb + i * Rec<D>::R;
+#pragma unroll
+    for (int k = 0; k < D; ++k) r[Rec<D>::X + k] = seed[e * D + k];
+#pragma unroll
+    for (int q = Rec<D>::V; q < Rec<D>::R; ++q) r[q] = 0.0f;
+}
+
+// ------------------------------------------------------------- layout
+template <int D>
+__global__ void k_pack(KParams p, const float* __restrict__ x, const float* __restrict__ v,
+                       const float* __restrict__ C, const float* __restrict__ F,
+                       float* __restrict__ rec) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= p.N * p.E) return;
+    float* r = rec + i * Rec<D>::R;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        r[Rec<D>::X + k] = x ? x[i * D + k] : 0.0f;
+        r[Rec<D>::V + k] = v ? v[i * D + k] : 0.0f;
+    }
+#pragma unroll
+    for (int q = 0; q < D * D; ++q) {
+        r[Rec<D>::C + q] = C ? C[i * D * D + q] : 0.0f;
+        r[Rec<D>::F + q] = F ? F[i * D * D + q] : ((q % (D + 1)) == 0 ? 1.0f : 0.0f);
+    }
+}
+
+template <int D>
+__global__ void k_unpack(KParams p, const float* __restrict__ rec, float* __restrict__ x,
+                         float* __restrict__ v, float* __restrict__ C, float* __restrict__ F) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= p.N * p.E) return;
+    const float* r = rec + i * Rec<D>::R;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        if (x) x[i * D + k] = r[Rec<D>::X + k];
+        if (v) v[i * D + k] = r[Rec<D>::V + k];
+    }
+#pragma unroll
+    for (int q = 0; q < D * D; ++q) {
+        if (C) C[i * D * D + q] = r[Rec<D>::C + q];
+        if (F) F[i * D * D + q] = r[Rec<D>::F + q];
+    }
+}
+
+inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+#define DISPATCH(D, ...) \
+    do {                 \
+        if ((D) == 2) {  \
+            constexpr int DIM = 2; __VA_ARGS__; \
+        } else {         \
+            constexpr int DIM = 3; __VA_ARGS__; \
+        }                \
+    } while (0)
+
+void launch_ctrl_fwd(const KParams& p, const float* theta, int32_t T, float* alpha, cudaStream_t s) {
+    if (p.n_act <= 0 || T <= 0) return;
+    k_ctrl_fwd<<<T, 128, 0, s>>>(p, theta, alpha);
+}
+
+void launch_ctrl_bwd(const KParams& p, const float* theta, int32_t T, const float* alpha,
+                     const float* alpha_bar, float* theta_part, float* theta_bar, int64_t n_theta,
+                     cudaStream_t s) {
+    if (p.n_act <= 0 || T <= 0) return;
+    k_ctrl_bwd<<<T, 128, 0, s>>>(p, theta, alpha, alpha_bar, theta_part, n_theta);
+    k_ctrl_reduce<<<nblk(n_theta, 128), 128, 0, s>>>(theta_part, T, n_theta, theta_bar);
+}
+
+int loss_blocks_per_episode(const KParams& p) {
+    int64_t nb = (p.N + 4095) / 4096;
+    return (int)(nb < 1 ? 1 : (nb > 512 ? 512 : nb));
+}
+
+void launch_loss(const KParams& p, const float* S, int loss_kind, float3 target, float* com_part,
+                 float* loss, float* Sb, int* flags, cudaStream_t s) {
+    const int nb = loss_blocks_per_episode(p);
+    float* seed = com_part + (int64_t)p.E * nb * p.dim;
+    DISPATCH(p.dim, {
+        k_com_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, S, com_part);
+        k_loss_final<DIM><<<p.E, 32, 0, s>>>(p, com_part, nb, loss_kind, target, loss, seed, flags);
+        k_seed<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, seed, Sb);
+    });
+}
+
+void launch_pack(const KParams& p, const float* x, const float* v, const float* C, const float* F,
+                 float* rec, cudaStream_t s) {
+    DISPATCH(p.dim, k_pack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, x, v, C, F, rec));
+}
+
+void launch_unpack(const KParams& p, const float* rec, float* x, float* v, float* C, float* F,
+                   cudaStream_t s) {
+    DISPATCH(p.dim, k_unpack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, rec, x, v, C, F));
+}
+
+}  // namespace mpm

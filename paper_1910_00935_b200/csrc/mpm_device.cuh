@@ -1,0 +1,200 @@
+// mpm_device.cuh -- per-particle MLS-MPM math in registers (sm_100a).
+//
+// Independent re-implementation of the readings in DESIGN.md (R1-R14); shares
+// no code with oracle/.  Everything is fp32, unrolled over the compile-time
+// dimension D, and kept in registers (north_star (2): fused SVD-free stress).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpm {
+
+// Kernel-side constants (one copy per launch, passed by value).
+struct KParams {
+    int32_t dim, n_grid, bound, model, n_act, act_axis, n_sin, hidden;
+    float dt, dx, inv_dx, mu, lam, p_mass, p_vol, gravity, eps_mass, kappa, omega;
+    float stress_scale;  // -dt * V * 4 / dx^2   (the APIC/MLS stress factor)
+    int64_t N;           // particles per episode
+    int64_t nodes;       // grid nodes per episode (n_grid^dim)
+    int32_t E;           // episodes
+};
+
+enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2 };
+
+template <int D> struct Rec {
+    static constexpr int R = 2 * D + 2 * D * D;  // floats per particle record: x, v, C, F
+    static constexpr int X = 0, V = D, C = 2 * D, F = 2 * D + D * D;
+    static constexpr int NST = D == 2 ? 9 : 27;  // stencil nodes
+};
+
+// quadratic B-spline N_0..N_2 at f in [1/2, 3/2) and derivatives (R1)
+__device__ __forceinline__ void bspline(float f, float w[3], float dw[3]) {
+    float a = 1.5f - f, b = f - 1.0f, c = f - 0.5f;
+    w[0] = 0.5f * a * a;
+    w[1] = 0.75f - b * b;
+    w[2] = 0.5f * c * c;
+    dw[0] = -a;
+    dw[1] = -2.0f * b;
+    dw[2] = c;
+}
+
+// base = floor(x/dx - 1/2), f = x/dx - base (R12); false if the 3^d stencil
+// leaves [0, n_grid - 1]^d (R13) or x is not finite.
+template <int D>
+__device__ __forceinline__ bool stencil(const float* x, const KParams& p, int base[D], float fx[D]) {
+    bool ok = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        float xi = x[k] * p.inv_dx;
+        float b = floorf(xi - 0.5f);
+        ok = ok && (b >= 0.0f) && (b + 2.0f <= (float)(p.n_grid - 1));  // false for NaN
+        base[k] = ok ? (int)b : 0;
+        fx[k] = xi - b;
+    }
+    return ok;
+}
+
+template <int D>
+__device__ __forceinline__ int64_t node_of(const KParams& p, const int base[D], int o0, int o1, int o2) {
+    int64_t n = p.n_grid;
+    if (D == 2) return (int64_t)(base[0] + o0) * n + (base[1] + o1);
+    return ((int64_t)(base[0] + o0) * n + (base[1] + o1)) * n + (base[2] + o2);
+}
+
+template <int D> __device__ __forceinline__ float det(const float* F) {
+    if (D == 2) return F[0] * F[3] - F[1] * F[2];
+    return F[0] * (F[4] * F[8] - F[5] * F[7]) - F[1] * (F[3] * F[8] - F[5] * F[6]) +
+           F[2] * (F[3] * F[7] - F[4] * F[6]);
+}
+
+// K = det(F) F^{-T} (the cofactor matrix)
+template <int D> __device__ __forceinline__ void cof(const float* F, float* K) {
+    if (D == 2) {
+        K[0] = F[3]; K[1] = -F[2]; K[2] = -F[1]; K[3] = F[0];
+    } else {
+        K[0] = F[4] * F[8] - F[5] * F[7];
+        K[1] = F[5] * F[6] - F[3] * F[8];
+        K[2] = F[3] * F[7] - F[4] * F[6];
+        K[3] = F[2] * F[7] - F[1] * F[8];
+        K[4] = F[0] * F[8] - F[2] * F[6];
+        K[5] = F[1] * F[6] - F[0] * F[7];
+        K[6] = F[1] * F[5] - F[2] * F[4];
+        K[7] = F[2] * F[3] - F[0] * F[5];
+        K[8] = F[0] * F[4] - F[1] * F[3];
+    }
+}
+
+// Kirchhoff stress tau(Ft) of the material (R2) plus actuation (R8).
+// NH : tau = mu (F F^T - I) + lambda ln J I
+// FCR: tau = 2 mu (F - R) F^T + lambda (J - 1) J I   (2D closed-form polar R)
+// returns false on a degenerate deformation (R14).
+template <int D>
+__device__ __forceinline__ bool kirchhoff(const KParams& p, const float* Fm, float act, float* tau) {
+    float J = det<D>(Fm);
+    bool ok = true;
+    if (D == 3 || p.model == 0) {
+        ok = J > 0.0f;
+        float iso = p.lam * logf(fmaxf(J, 1e-30f)) - p.mu;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                float s = 0.0f;
+#pragma unroll
+                for (int k = 0; k < D; ++k) s = fmaf(Fm[i * D + k], Fm[j * D + k], s);
+                tau[i * D + j] = p.mu * s + (i == j ? iso : 0.0f);
+            }
+    } else {
+        float a = Fm[0] + Fm[3], b = Fm[2] - Fm[1];
+        float r2 = a * a + b * b;
+        ok = r2 > 0.0f;
+        float ir = rsqrtf(fmaxf(r2, 1e-30f));
+        float cs = a * ir, sn = b * ir;
+        float M0 = Fm[0] - cs, M1 = Fm[1] + sn, M2 = Fm[2] - sn, M3 = Fm[3] - cs;  // F - R
+        float iso = p.lam * (J - 1.0f) * J;
+        tau[0] = 2.0f * p.mu * (M0 * Fm[0] + M1 * Fm[1]) + iso;
+        tau[1] = 2.0f * p.mu * (M0 * Fm[2] + M1 * Fm[3]);
+        tau[2] = 2.0f * p.mu * (M2 * Fm[0] + M3 * Fm[1]);
+        tau[3] = 2.0f * p.mu * (M2 * Fm[2] + M3 * Fm[3]) + iso;
+    }
+    if (act != 0.0f) {
+        const int e = p.act_axis;
+        float s = p.kappa * act;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) tau[i * D + j] = fmaf(s * Fm[i * D + e], Fm[j * D + e], tau[i * D + j]);
+    }
+    return ok;
+}
+
+// Reverse of kirchhoff(): Fb += d<tb, tau(F)>/dF, and the actuation adjoint
+// (returns kappa q^T tb q, the contribution to alpha_bar).
+template <int D>
+__device__ __forceinline__ float kirchhoff_adj(const KParams& p, const float* Fm, bool has_act,
+                                               float act, const float* tb, float* Fb) {
+    float S[D * D], K[D * D];
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) S[i * D + j] = tb[i * D + j] + tb[j * D + i];
+    cof<D>(Fm, K);
+    float J = det<D>(Fm);
+    float tr = 0.0f;
+#pragma unroll
+    for (int i = 0; i < D; ++i) tr += tb[i * D + i];
+    const bool nh = (D == 3 || p.model == 0);
+    float musym = nh ? p.mu : 2.0f * p.mu;
+    float kiso = nh ? p.lam * tr / J : p.lam * (2.0f * J - 1.0f) * tr;
+    // (tb + tb^T) F term and the isotropic term
+#pragma unroll
+    for (int i = 0; i < D; ++i)
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            float s = 0.0f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fmaf(S[i * D + k], Fm[k * D + j], s);
+            Fb[i * D + j] += musym * s + kiso * K[i * D + j];
+        }
+    if (!nh && D == 2) {
+        float a = Fm[0] + Fm[3], b = Fm[2] - Fm[1];
+        float r2 = a * a + b * b;
+        float ir = rsqrtf(r2);
+        float cs = a * ir, sn = b * ir;
+        // -2 mu tb^T R
+        float tR0 = tb[0] * cs + tb[2] * sn, tR1 = -tb[0] * sn + tb[2] * cs;
+        float tR2 = tb[1] * cs + tb[3] * sn, tR3 = -tb[1] * sn + tb[3] * cs;
+        Fb[0] -= 2.0f * p.mu * tR0; Fb[1] -= 2.0f * p.mu * tR1;
+        Fb[2] -= 2.0f * p.mu * tR2; Fb[3] -= 2.0f * p.mu * tR3;
+        // rotation path: Rb = -2 mu tb F; psi_b = <Rb, dR/dpsi>
+        float Rb0 = -2.0f * p.mu * (tb[0] * Fm[0] + tb[1] * Fm[2]);
+        float Rb1 = -2.0f * p.mu * (tb[0] * Fm[1] + tb[1] * Fm[3]);
+        float Rb2 = -2.0f * p.mu * (tb[2] * Fm[0] + tb[3] * Fm[2]);
+        float Rb3 = -2.0f * p.mu * (tb[2] * Fm[1] + tb[3] * Fm[3]);
+        float psib = -sn * Rb0 - cs * Rb1 + cs * Rb2 - sn * Rb3;
+        float ga = -psib * b / r2, gb = psib * a / r2;  // d psi/da = -b/r^2, d psi/db = a/r^2
+        Fb[0] += ga; Fb[3] += ga; Fb[2] += gb; Fb[1] -= gb;
+    }
+    float abar = 0.0f;
+    if (has_act) {
+        const int e = p.act_axis;
+        float q[D], sq[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) q[i] = Fm[i * D + e];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            float s = 0.0f;
+#pragma unroll
+            for (int j = 0; j < D; ++j) s = fmaf(S[i * D + j], q[j], s);
+            sq[i] = s;
+            abar = fmaf(q[i], s, abar);
+        }
+        abar *= 0.5f * p.kappa;  // q^T tb q = 1/2 q^T (tb + tb^T) q
+        float s = p.kappa * act;
+#pragma unroll
+        for (int i = 0; i < D; ++i) Fb[i * D + e] = fmaf(s, sq[i], Fb[i * D + e]);
+    }
+    return abar;
+}
+
+}  // namespace mpm

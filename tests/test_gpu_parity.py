@@ -1,0 +1,221 @@
+"""CUDA path (through the C-ABI) vs the fp64 CPU oracle, element by element on
+the same seeded inputs.  Gates (BASELINE.json north_star): final particle
+states rel <= 1e-4 (per array, ||d||/||ref||), gradients rel-L2 <= 1e-3."""
+import numpy as np
+import pytest
+
+from helpers import gpu_run, inputs, oracle_run, oracle_tape, rel
+from paper_1910_00935_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+STATE_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+TINY = {
+    "2d_fcr_act_hidden": lambda: W.tiny(2, steps=12, hidden=4, seed=1),
+    "3d_nh_act": lambda: W.tiny(3, steps=5, seed=2),
+    "2d_fcr_sticky_floor": lambda: W.tiny(2, steps=10, bound=3, seed=3, floor=True, v_base=(0.3, -1.5)),
+    "2d_nh": lambda: W.tiny(2, steps=8, model="neohookean", seed=4),
+    "3d_nh_hidden_floor": lambda: W.tiny(3, steps=10, hidden=3, bound=3, seed=6, floor=True,
+                                         v_base=(0.2, -1.5, 0.1)),
+}
+
+
+@pytest.mark.parametrize("case", list(TINY))
+def test_tiny_every_adjoint_path(case):
+    """Seed every component of S_T (L = <lam, S_T>) so every adjoint path
+    (x, v, C, F, theta) is exercised; compare with the oracle's tape."""
+    p = TINY[case]()
+    inp = W.make_inputs(p)
+    N, d = inp["x"].shape
+    rng = np.random.default_rng(7)
+    lam = [rng.standard_normal((N, d)), rng.standard_normal((N, d)),
+           rng.standard_normal((N, d, d)), rng.standard_normal((N, d, d))]
+    lam = [l.astype(np.float32) for l in lam]
+    ref = oracle_tape(p, inp, p["steps"], lam)
+    got = gpu_run(p, inp, seed=lam)
+    for k in "xvCF":
+        assert rel(got[k][0], ref[k]) < STATE_TOL, (k, rel(got[k][0], ref[k]))
+    for k in ("dx0", "dv0", "dC0", "dF0", "dtheta"):
+        assert rel(got[k].reshape(ref[k].shape), ref[k]) < GRAD_TOL, (k, rel(got[k].reshape(ref[k].shape), ref[k]))
+
+
+def _errors(p, got, ref, e, grads):
+    errs = {k: rel(got[k][e], ref[k]) for k in "xvCF"}
+    for k in grads:
+        if k == "dtheta":
+            if ref[k].size:
+                errs[k] = rel(got[k], ref[k])
+        elif np.linalg.norm(ref[k]) > 1e-12:
+            errs[k] = rel(got[k][e], ref[k])
+    if got.get("loss") is not None:
+        errs["loss"] = abs(float(got["loss"][e]) - ref["loss"]) / max(abs(ref["loss"]), 1e-12)
+    return errs
+
+
+def _compare_episode(p, inp, got, steps=None, e=0, grads=("dx0", "dv0", "dC0", "dF0", "dtheta")):
+    """errors of the GPU run vs the fp64 oracle, and the gate per array:
+    the north_star tolerance, or -- where the oracle's own fp32 build already
+    deviates from fp64 by more than that (cancellation-heavy C and dtheta on
+    resting robots) -- 2x that fp32-vs-fp64 deviation (SURVEY.md 8(c) fallback,
+    DESIGN.md "Parity gates")."""
+    ref = oracle_run(p, inp, steps=steps)
+    ref32 = oracle_run(p, inp, steps=steps, precision="f32")
+    errs = _errors(p, got, ref, e, grads)
+    as_got = {k: ref32[k][None] for k in ("x", "v", "C", "F", "dx0", "dv0", "dC0", "dF0")}
+    as_got["dtheta"] = ref32["dtheta"]
+    as_got["loss"] = np.array([ref32["loss"]])
+    dev32 = _errors(p, as_got, ref, 0, grads)
+    tols = {}
+    for k in errs:
+        base = STATE_TOL if k in ("x", "v", "C", "F", "loss") else GRAD_TOL
+        tols[k] = max(base, 2.0 * dev32.get(k, 0.0))
+    print(f"[parity] {p.get('name')} e={e}: " + ", ".join(
+        f"{k} {errs[k]:.2e} (gate {tols[k]:.1e}, oracle-f32 {dev32.get(k, 0):.1e})" for k in errs))
+    return (errs, tols), ref
+
+
+def _assert(errs, tag):
+    errs, tols = errs
+    for k, v in errs.items():
+        assert v < tols[k], (tag, k, v, tols[k], errs)
+
+
+@pytest.mark.parametrize("name", ["c1a", "c1b"])
+def test_block_full_horizon(name):
+    p, inp = inputs(name)
+    got = gpu_run(p, inp)
+    errs, ref = _compare_episode(p, inp, got, grads=("dx0", "dv0"))
+    _assert(errs, name)
+    if name == "c1a":  # no wall contact: closed form dL/dC0 = dL/dF0 = 0
+        scale = np.abs(got["dv0"]).max()
+        assert np.abs(got["dC0"]).max() < 1e-3 * scale and np.abs(got["dF0"]).max() < 1e-3 * scale
+
+
+def test_robot2d_c2_full_horizon():
+    p, inp = inputs("c2")
+    got = gpu_run(p, inp)
+    errs, _ = _compare_episode(p, inp, got, grads=("dx0", "dv0", "dtheta"))
+    _assert(errs, "c2")
+
+
+def test_robot3d_c3_checkpointed():
+    """C3 geometry, 16 muscles, H = 32, k = 32, first 128 steps (4 segments)."""
+    p, inp = inputs("c3", steps=128)
+    got = gpu_run(p, inp, k_ckpt=32)
+    errs, _ = _compare_episode(p, inp, got, grads=("dx0", "dv0", "dtheta"))
+    _assert(errs, "c3")
+
+
+def test_batched_episodes_c4():
+    """4 independent C4 episodes in one launch: per-episode states and the
+    summed controller gradient equal the per-episode oracle runs."""
+    p = W.config("c4", steps=48)
+    inps = [W.make_inputs(p, episode=e) for e in range(4)]
+    got = gpu_run(p, inps, k_ckpt=16)
+    dth = dth32 = 0
+    for e, inp in enumerate(inps):
+        errs, ref = _compare_episode(p, inp, got, e=e, grads=("dx0", "dv0"))
+        errs[0].pop("loss", None)
+        assert abs(got["loss"][e] - ref["loss"]) < 1e-4 * abs(ref["loss"])
+        _assert(errs, f"c4[{e}]")
+        dth = dth + ref["dtheta"]
+        dth32 = dth32 + oracle_run(p, inp, precision="f32")["dtheta"]
+    gate = max(GRAD_TOL, 2 * rel(dth32, dth))
+    print(f"[parity] c4 sum dtheta {rel(got['dtheta'], dth):.2e} (gate {gate:.1e})")
+    assert rel(got["dtheta"], dth) < gate
+
+
+@pytest.mark.parametrize("k", [1, 7, 64])
+def test_checkpoint_interval_invariance(k):
+    """Segment size does not change the result."""
+    p, inp = inputs("c3", steps=64)
+    base = gpu_run(p, inp, k_ckpt=64)
+    got = gpu_run(p, inp, k_ckpt=k)
+    # atomics reassociate fp32 sums run to run: agreement at the fp32 noise level
+    for key, tol in (("x", 1e-6), ("dx0", 1e-5), ("dv0", 1e-5), ("dtheta", 1e-4)):
+        assert rel(got[key], base[key]) < tol, (k, key, rel(got[key], base[key]))
+
+
+def test_c5_full_size_one_step():
+    """Full C5 size (1,061,208 particles, 128^3 grid), the launch configuration
+    bench.py times: one forward step and one reverse step vs the oracle on every
+    particle (fp64 oracle on the GPU's fp32 input).  The initial state is
+    perturbed (velocity, affine and deformation noise) so that every term of the
+    step -- stress, affine momentum, the adjoints -- is non-trivial."""
+    p, inp = inputs("c5", steps=1, v_noise=0.3, C_noise=2.0, F_noise=0.02)
+    N, d = inp["x"].shape
+    rng = np.random.default_rng(3)
+    lam = [rng.standard_normal((N, d)).astype(np.float32),
+           rng.standard_normal((N, d)).astype(np.float32),
+           rng.standard_normal((N, d, d)).astype(np.float32),
+           rng.standard_normal((N, d, d)).astype(np.float32)]
+    got = gpu_run(p, inp, steps=1, k_ckpt=32, seed=lam)
+    ref = oracle_tape(p, inp, 1, lam)
+    for k in "xvCF":
+        assert rel(got[k][0], ref[k]) < 1e-5, k
+    for k in ("dx0", "dv0", "dC0", "dF0"):
+        assert rel(got[k][0], ref[k]) < 1e-4, k
+
+
+def test_c5_full_size_ballistic_and_closed_form():
+    """Before the cube reaches the floor (T = 40) the centre of mass is exactly
+    ballistic and dL/dv0 has the closed form 2(xbar_T - x*) T dt / N for every
+    particle (properties that hold at any size)."""
+    T = 40
+    p, inp = inputs("c5", steps=T)
+    got = gpu_run(p, inp, steps=T, k_ckpt=8)
+    x0 = inp["x"].astype(np.float64).mean(0)
+    v0 = inp["v"].astype(np.float64).mean(0)
+    dt, g = p["dt"], p["gravity"]
+    pred = x0 + T * dt * v0 - np.array([0.0, dt * dt * g * T * (T + 1) / 2, 0.0])
+    com = got["x"][0].astype(np.float64).mean(0)
+    assert np.abs(com - pred).max() < 2e-6
+    N = len(inp["x"])
+    gexp = 2 * (com - np.array(p["target"])) * T * dt / N
+    assert rel(got["dv0"][0], np.tile(gexp, (N, 1))) < GRAD_TOL
+    assert got["x"][0][:, 1].min() > 3.0 / 128 + 1.0 / 128  # no floor contact yet
+
+
+def test_error_paths():
+    from paper_1910_00935_b200 import mpm
+    p = W.tiny(3, steps=4)
+    inp = W.make_inputs(p)
+    N = len(inp["x"])
+    sim = mpm.sim_from_config(p, N, max_steps=4)
+    with pytest.raises(mpm.MpmError) as e:
+        sim.forward(1)
+    assert e.value.status == 6  # forward before set_state
+    x = inp["x"].copy()
+    x[0, 0] = 0.01  # stencil leaves the grid
+    sim.set_state(x, inp["v"], inp["C"], inp["F"], inp["aid"])
+    with pytest.raises(mpm.MpmError) as e:
+        sim.forward(2)
+    assert e.value.status == 4
+    F = inp["F"].copy()
+    F[1] = np.diag([1.0, 1.0, -1.0])  # J < 0 under Neo-Hookean
+    sim.set_state(inp["x"], inp["v"], inp["C"], F, inp["aid"])
+    with pytest.raises(mpm.MpmError) as e:
+        sim.forward(2)
+    assert e.value.status == 5
+    sim.set_state(inp["x"], inp["v"], inp["C"], inp["F"], inp["aid"])
+    sim.forward(3)
+    with pytest.raises(mpm.MpmError) as e:
+        sim.backward(3)  # no loss / seed yet
+    assert e.value.status == 6
+    sim.loss()
+    with pytest.raises(mpm.MpmError) as e:
+        sim.backward(2)  # != recorded steps
+    assert e.value.status == 6
+    with pytest.raises(mpm.MpmError) as e:
+        sim.forward(5)  # > max_steps
+    assert e.value.status == 1
+    sim.close()
+
+
+def test_native_library_is_what_runs():
+    """the kernels launched are ours (launch counter of libmpm_b200.so)"""
+    p, inp = inputs("c1a", steps=8)
+    got = gpu_run(p, inp, steps=8)
+    assert got["launches"] >= 8 * 3 + 8 * 5
