@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark: fwd+bwd particle-steps/s of the differentiable MLS-MPM hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
+
+One bench "step" = one optimisation iteration of the whole hot path on one
+batch of synthetic input: set_state -> forward(T) (checkpointed tape) -> loss
+-> backward(T) -> grads -> NCCL all-reduce of the shared-parameter gradient
+(N > 1).  value = particles x time steps x K (all ranks) / max-over-ranks
+device time.  Default workload: C5 (BASELINE.json configs[4]: 1,061,208
+particles, 128^3 grid, 2,048 steps, k = 32), one episode per GPU (weak scaling).
+
+--impl reference times the CPU oracle (oracle/, the only reference this paper
+has) on the host cores: each step is a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fwd+bwd particle-steps/s (2D/3D MLS-MPM) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "particle-steps/s"
+
+
+# ------------------------------------------------------------------ helpers
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy bandwidth)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+def _workload(name: str, world: int):
+    from paper_1910_00935_b200 import workloads as W
+    p = W.config(name)
+    if name == "c4":
+        total = int(p["episodes"])
+        per = max(1, total // world)
+        scaling = "strong"
+    else:
+        per = 1
+        scaling = "weak"
+    return p, per, scaling
+
+
+def _describe(p, n_particles, episodes, world, k):
+    shape = {"cube3d": "3D elastic cube", "robot3d": "3D robot (16 muscles)",
+             "robot2d": "2D robot (4 muscles)", "block2d": "2D elastic block"}[p["shape"]]
+    return {"workload": f"{p['name']}: {shape}, {n_particles:,} particles x {episodes} episode(s)/GPU, "
+                        f"{p['n_grid']}^{p['dim']} grid, {p['steps']} steps, checkpoint every {k}",
+            "config_index": {"c1a": 0, "c1b": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}[p["name"]],
+            "dim": p["dim"], "particles_per_episode": n_particles, "episodes_per_gpu": episodes,
+            "episodes_total": episodes * world, "n_grid": p["n_grid"], "time_steps": p["steps"],
+            "k_ckpt": k, "model": p["model"], "parallelism": f"episodes x{world} (dp{world})",
+            "l2": "inputs larger than L2 (per-step state stream > 126 MB L2; tape holds GBs)"}
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock/throttle sampling (NVML) during the timed region."""
+    NAMES = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+             0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+             0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.stop_ev = [], 0, threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            self.stop_ev.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples),
+                "reasons": [n for b, n in self.NAMES.items() if self.reasons & b and b != 0x1]}
+
+
+def algorithmic_bytes(dim: int, N: int, A: float) -> dict:
+    """Per-launch algorithmic bytes of each kernel class:
+    the minimum HBM traffic of the kernel's own inputs/outputs, N particles and
+    A active grid nodes per launch (fp32; record s = 4(2d + 2d^2) bytes)."""
+    s = 4 * (2 * dim + 2 * dim * dim)
+    dd, d = 4 * dim * dim, 4 * dim
+    node = 16  # (P, M) or (U, z) float4 per node
+    return {
+        "p2g": N * (s + 4 + dd) + A * node,                      # S_t, aid -> F_{t+1}; grid flush
+        "grid_op": A * 2 * node,                                  # (P, M) -> (U, z)
+        "g2p": N * (d + d + d + dd) + A * node,                   # x_t -> x, v, C; read U
+        "g2p_grad": N * (d + 2 * d + dd + d) + A * 2 * node,      # x_t, (xb, vb, Cb)' -> xb; U, Ub
+        "grid_op_grad": A * 4 * node,                             # P,M, U, Ub -> (Pb, Mb)
+        "p2g_grad": N * (s + 4 + dd + d + s) + A * node,          # S_t, aid, Fb', xb -> S_bar_t
+    }
+
+
+def _traffic(kernel: str):
+    """dram bytes per launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(kernel, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# -------------------------------------------------------------- CPU oracle
+def oracle_sample(p, inp, steps=1):
+    """time the CPU oracle (as it stands) on a bounded sample: all particles of the
+    episode, `steps` time steps of forward + loss + backward, fp64, one thread."""
+    from oracle import Oracle
+    o = Oracle(p)
+    t0 = time.perf_counter()
+    o.run(inp["x"], inp["v"], inp["C"], inp["F"], inp["aid"], inp["theta"], steps=steps,
+          k_ckpt=steps)
+    dt = time.perf_counter() - t0
+    return len(inp["x"]) * steps / dt, dt
+
+
+def run_reference(args):
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    from paper_1910_00935_b200 import workloads as W
+    p, per, scaling = _workload(args.config, 1)
+    inp = W.make_inputs(p)
+    steps = 1
+    for _ in range(args.warmup):
+        oracle_sample(p, inp, steps)
+    times = []
+    for _ in range(args.steps):
+        _, dt = oracle_sample(p, inp, steps)
+        times.append(dt)
+    N = len(inp["x"])
+    total = sum(times)
+    value = N * steps * args.steps / total
+    sample = (f"{p['name']} rank-0 episode, all {N:,} particles, {steps} time step(s) of "
+              f"forward + loss + backward per bench step (fp64 oracle)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _describe(p, N, 1, 1, p["k_ckpt"]),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# -------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1910_00935_b200 import mpm, workloads as W
+
+    rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    p, per, scaling = _workload(args.config, world)
+    k = int(args.k_ckpt or p["k_ckpt"])
+    T = int(p["steps"])
+    if args.config == "c4":
+        inps = [W.make_inputs(p, episode=rank * per + e) for e in range(per)]
+    else:
+        inps = [W.make_inputs(p, rank=rank)]
+    N = len(inps[0]["x"])
+    cat = lambda key: np.ascontiguousarray(np.stack([i[key] for i in inps]))  # noqa: E731
+    host = {key: torch.from_numpy(cat(key)).pin_memory() for key in ("x", "v", "C", "F", "aid")}
+    host["theta"] = torch.from_numpy(inps[0]["theta"]).pin_memory()
+    devin = {key: t.to(dev) for key, t in host.items()}
+
+    sim = mpm.sim_from_config(p, N, episodes=per, max_steps=T, k_ckpt=k)
+    nth = sim.n_theta
+    shared_len = nth if nth > 0 else per * p["dim"]
+    loss_d = torch.zeros(per, device=dev)
+    shared_d = torch.zeros(shared_len, device=dev)
+    gdev = {"dx0": torch.empty((per, N, p["dim"]), device=dev),
+            "dv0": torch.empty((per, N, p["dim"]), device=dev),
+            "dC0": torch.empty((per, N, p["dim"], p["dim"]), device=dev),
+            "dF0": torch.empty((per, N, p["dim"], p["dim"]), device=dev),
+            "dtheta": torch.empty(max(nth, 1), device=dev)}
+    loss_h = torch.zeros(per).pin_memory()
+    shared_h = torch.zeros(shared_len).pin_memory()
+
+    def step(src, loss_buf, shared_buf, grads_out):
+        sim.set_state(src["x"], src["v"], src["C"], src["F"], src["aid"])
+        sim.set_controller(src["theta"])
+        sim.forward(T)
+        sim.loss(loss_buf)
+        sim.backward(T)
+        if nth > 0:
+            sim.grads({"dtheta": shared_buf, **(grads_out or {})})
+        else:
+            if grads_out:
+                sim.grads(grads_out)
+            sim.grad_v0_sum(shared_buf)
+        if world > 1:
+            # the one exchange of the path: sum of the shared-parameter gradient over ranks
+            if shared_buf.is_cuda:
+                dist.all_reduce(shared_buf)
+            else:
+                t = shared_buf.to(dev)
+                dist.all_reduce(t)
+                shared_buf.copy_(t)
+
+    def timed(K, fn):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(K):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = s.elapsed_time(e)
+        if world > 1:
+            t = torch.tensor([ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    dev_step = lambda: step(devin, loss_d, shared_d, gdev)  # noqa: E731
+    host_step = lambda: step(host, loss_h, shared_h, None)  # noqa: E731
+
+    for _ in range(args.warmup):
+        dev_step()
+    # active grid nodes (A) for the algorithmic byte count: after a forward, the
+    # grid holds step T-1's; after the backward, step 0's -- use their mean
+    sim.set_state(devin["x"], devin["v"], devin["C"], devin["F"], devin["aid"])
+    sim.set_controller(devin["theta"])
+    sim.forward(T)
+    A_end = sim.active_nodes()
+    sim.loss(loss_d)
+    sim.backward(T)
+    A_start = sim.active_nodes()
+    A = 0.5 * (A_end + A_start) / per
+
+    sim.reset_kernel_stats()
+    sim.set_profiling(True)
+    l0 = sim.launch_count()
+    clocks = ClockSampler(local)
+    with clocks:
+        ms = timed(args.steps, dev_step)
+    launches = sim.launch_count() - l0
+    stats = sim.kernel_stats()
+    sim.set_profiling(False)
+    ms_e2e = timed(args.steps, host_step)
+
+    particle_steps = float(N) * per * T * world * args.steps
+    value = particle_steps / (ms / 1e3)
+    e2e_value = particle_steps / (ms_e2e / 1e3)
+    h2d = sum(int(t.numel() * t.element_size()) for t in host.values())
+    d2h = int(loss_h.numel() * 4 + shared_h.numel() * 4)
+
+    # roofline of the dominant kernel (largest share of device time)
+    peak, peak_src = _peaks()
+    alg = algorithmic_bytes(p["dim"], N * per, A * per)
+    kern = {kname: v for kname, v in stats.items() if kname in alg and v[1] > 0}
+    dom = max(kern, key=lambda kk: kern[kk][0])
+    dom_ms, dom_n = kern[dom]
+    total_ms = sum(v[0] for v in stats.values())
+    achieved = alg[dom] / (dom_ms / dom_n / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": _traffic(dom), "peak_source": peak_src,
+                "alg_bytes_per_launch": alg[dom], "avg_launch_us": 1e3 * dom_ms / dom_n,
+                "share_of_kernel_time": dom_ms / total_ms if total_ms else None,
+                "active_nodes_per_episode": A,
+                "kernel_ms": {kk: round(v[0] / args.steps, 3) for kk, v in stats.items() if v[1]},
+                "kernel_launches_per_step": {kk: v[1] // args.steps for kk, v in stats.items() if v[1]}}
+    # whole-step effective bandwidth against the SURVEY 8(d) byte model
+    s_rec = 4 * (2 * p["dim"] + 2 * p["dim"] ** 2)
+    B_p = (2 * s_rec + 4) * (1 + (k - 1) / k) + (3 * s_rec + 12 * p["dim"] + 4)
+    B_g = 8 * (p["dim"] + 1) * (1 + (k - 1) / k) + 8 * (p["dim"] + 1) + 8 * p["dim"]
+    step_bytes = (N * B_p + A * B_g) * per * T
+    roofline["step_model_bytes"] = step_bytes
+    roofline["step_effective_GBps_per_gpu"] = step_bytes / (ms / args.steps / 1e3) / 1e9
+    roofline["step_frac"] = roofline["step_effective_GBps_per_gpu"] / peak
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v_cpu, dt_cpu = oracle_sample(p, inps[0], steps=1)
+        cpu = {"value": v_cpu, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{p['name']} episode 0, all {N:,} particles, 1 time step of forward + "
+                         f"loss + backward, fp64, single thread ({dt_cpu:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": _describe(p, N, per, world, k), "roofline": roofline,
+                "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps},
+                "gpu_launches": int(launches), "clocks": clocks.summary(),
+                "loss": [float(x) for x in loss_d.cpu()]}
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c1a", "c1b", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--k-ckpt", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

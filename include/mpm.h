@@ -145,12 +145,30 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps);
 mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF0,
                      float* dtheta);
 
+/* Gradient w.r.t. a uniform initial velocity shared by all particles of an
+ * episode (the "initial state parameterisation" of Fig. 1):
+ * out[E][d] = sum_p dL/dv0_p (fixed-order reduction).  Host or device pointer. */
+mpm_status mpm_grad_v0_sum(mpm_handle h, float* out);
+
 /* Current state S_T of the recorded forward (or S_0 before any forward). */
 mpm_status mpm_get_state(mpm_handle h, float* x, float* v, float* C, float* F);
 
 /* Number of library kernel launches enqueued since the handle was created
  * (for the benchmark's gpu_launches count). */
 mpm_status mpm_launch_count(mpm_handle h, int64_t* count);
+
+/* ---- measurement hooks (bench.py) ------------------------------------------
+ * Per-kernel device time: with profiling on, every library launch is
+ * bracketed by CUDA events on the bound stream; durations are harvested at the
+ * next synchronising call.  idx enumerates kernel classes 0..n-1
+ * (MPM_ERR_INVALID_ARG past the end); *name is a static string. */
+mpm_status mpm_set_profiling(mpm_handle h, int32_t enable);
+mpm_status mpm_reset_kernel_stats(mpm_handle h);
+mpm_status mpm_kernel_stats(mpm_handle h, int32_t idx, const char** name, double* total_ms,
+                            int64_t* count);
+/* Grid nodes with M > 0 in the grid of the last executed step, summed over episodes
+ * (the "active nodes" A of the algorithmic byte count). Synchronises. */
+mpm_status mpm_active_nodes(mpm_handle h, int64_t* count);
 
 #ifdef __cplusplus
 }

@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "../../include/mpm.h"
 #include "kernels.h"
@@ -13,6 +15,22 @@ using namespace mpm;
 namespace {
 
 enum Phase { kCreated = 0, kBound, kHasState, kForward, kSeeded, kBackward };
+
+// kernel classes for the per-kernel device-time accounting (mpm_kernel_stats)
+enum KClass { KC_P2G = 0, KC_GRID_OP, KC_G2P, KC_G2P_GRAD, KC_GRID_OP_GRAD, KC_P2G_GRAD,
+              KC_REDUCE_ABAR, KC_CLEAR, KC_CTRL, KC_LOSS, KC_LAYOUT, KC_N };
+const char* const kClassNames[KC_N] = {"p2g", "grid_op", "g2p", "g2p_grad", "grid_op_grad",
+                                        "p2g_grad", "reduce_abar", "clear_grid", "controller",
+                                        "loss", "layout"};
+
+struct Profiler {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<std::pair<int, size_t>> pending;
+    double ms[KC_N] = {0};
+    int64_t n[KC_N] = {0};
+};
 
 size_t align_up(size_t n) { return (n + 255) & ~size_t(255); }
 
@@ -60,6 +78,8 @@ struct mpm_ctx {
     int32_t t_final = 0;        // T whose state lives in final_state (0 = none)
     int window_seg = -1;        // segment whose intermediate states are in the window
     int sbar_cur = 0;           // index of the adjoint buffer holding S_bar of the current step
+    Profiler prof;
+    int64_t* com_part_count = nullptr;  // scratch counter (active nodes)
 };
 
 namespace {
@@ -154,7 +174,9 @@ size_t carve(mpm_ctx* h, char* base) {
     float* loss = (float*)take(sizeof(float) * E);
     float* com_part = (float*)take(sizeof(float) * E * (lblk + 1) * 3);
     int* flags = (int*)take(sizeof(int) * 4);
+    int64_t* cnt = (int64_t*)take(sizeof(int64_t) * 2);
     if (base) {
+        h->com_part_count = cnt;
         h->state_floats = sf;
         h->n_ckpt = n_ckpt;
         h->ckpt = ckpt; h->window = window; h->final_state = final_state; h->sbar[0] = sb0; h->sbar[1] = sb1;
@@ -175,11 +197,49 @@ float* state_ptr(mpm_ctx* h, int t) {
     return h->window + (size_t)(t % k) * h->state_floats;
 }
 
+// collect pending event pairs (the stream must be synchronised)
+void prof_harvest(mpm_ctx* h) {
+    for (auto& pr : h->prof.pending) {
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, h->prof.pool[pr.second], h->prof.pool[pr.second + 1]) == cudaSuccess) {
+            h->prof.ms[pr.first] += ms;
+            h->prof.n[pr.first] += 1;
+        }
+    }
+    h->prof.pending.clear();
+    h->prof.used = 0;
+}
+
+// brackets one library launch with CUDA events when profiling is on
+struct KScope {
+    mpm_ctx* h;
+    int cls;
+    size_t idx = 0;
+    bool active = false;
+    KScope(mpm_ctx* h_, int c) : h(h_), cls(c) {
+        if (!h->prof.on) return;
+        if (h->prof.used + 2 > h->prof.pool.size()) {
+            cudaStreamSynchronize(h->stream);
+            prof_harvest(h);
+        }
+        idx = h->prof.used;
+        h->prof.used += 2;
+        cudaEventRecord(h->prof.pool[idx], h->stream);
+        active = true;
+    }
+    ~KScope() {
+        if (!active) return;
+        cudaEventRecord(h->prof.pool[idx + 1], h->stream);
+        h->prof.pending.emplace_back(cls, idx);
+    }
+};
+
 // check + clear the device flags; synchronises the stream
 mpm_status sync_flags(mpm_handle h, const char* where) {
     CU(cudaMemcpyAsync(h->h_flags, h->flags, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     CU(cudaGetLastError());
+    prof_harvest(h);
     const int f = *h->h_flags;
     if (f) {
         CU(cudaMemsetAsync(h->flags, 0, sizeof(int), h->stream));
@@ -196,11 +256,11 @@ mpm_status sync_flags(mpm_handle h, const char* where) {
 // advance(): clear_grid, p2g (actuation precomputed), grid_op, g2p
 void step_forward(mpm_ctx* h, const KParams& k, int t, const float* S, float* Sn) {
     const size_t gbytes = sizeof(float4) * (size_t)k.nodes * k.E;
-    cudaMemsetAsync(h->grid, 0, gbytes, h->stream);
+    { KScope sc(h, KC_CLEAR); cudaMemsetAsync(h->grid, 0, gbytes, h->stream); }
     const float* al = h->alpha + (size_t)t * (k.n_act > 0 ? k.n_act : 1);
-    launch_p2g(k, S, h->has_aid ? h->aid : nullptr, al, h->grid, Sn, h->flags, h->stream);
-    launch_grid_op(k, h->grid, h->U, h->stream);
-    launch_g2p(k, S, h->U, Sn, h->flags, h->stream);
+    { KScope sc(h, KC_P2G); launch_p2g(k, S, h->has_aid ? h->aid : nullptr, al, h->grid, Sn, h->flags, h->stream); }
+    { KScope sc(h, KC_GRID_OP); launch_grid_op(k, h->grid, h->U, h->stream); }
+    { KScope sc(h, KC_G2P); launch_g2p(k, S, h->U, Sn, h->flags, h->stream); }
     h->launches += 3;
 }
 
@@ -209,16 +269,17 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const float* S, const fl
     const size_t gbytes = sizeof(float4) * (size_t)k.nodes * k.E;
     const int A = k.n_act > 0 ? k.n_act : 1;
     const float* al = h->alpha + (size_t)t * A;
-    cudaMemsetAsync(h->grid, 0, gbytes, h->stream);
-    launch_p2g(k, S, h->has_aid ? h->aid : nullptr, al, h->grid, nullptr, h->flags, h->stream);
-    launch_grid_op(k, h->grid, h->U, h->stream);
-    cudaMemsetAsync(h->Ubar, 0, gbytes, h->stream);
-    launch_g2p_grad(k, S, h->U, Sbn, h->Ubar, Sb, h->stream);
-    launch_grid_op_grad(k, h->grid, h->U, h->Ubar, h->gbar, h->stream);
-    launch_p2g_grad(k, S, h->has_aid ? h->aid : nullptr, al, h->gbar, Sbn, Sb, h->abar_part,
-                    h->flags, h->stream);
+    { KScope sc(h, KC_CLEAR); cudaMemsetAsync(h->grid, 0, gbytes, h->stream); }
+    { KScope sc(h, KC_P2G); launch_p2g(k, S, h->has_aid ? h->aid : nullptr, al, h->grid, nullptr, h->flags, h->stream); }
+    { KScope sc(h, KC_GRID_OP); launch_grid_op(k, h->grid, h->U, h->stream); }
+    { KScope sc(h, KC_CLEAR); cudaMemsetAsync(h->Ubar, 0, gbytes, h->stream); }
+    { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, S, h->U, Sbn, h->Ubar, Sb, h->stream); }
+    { KScope sc(h, KC_GRID_OP_GRAD); launch_grid_op_grad(k, h->grid, h->U, h->Ubar, h->gbar, h->stream); }
+    { KScope sc(h, KC_P2G_GRAD);
+      launch_p2g_grad(k, S, h->has_aid ? h->aid : nullptr, al, h->gbar, Sbn, Sb, h->abar_part, h->flags, h->stream); }
     h->launches += 5;
     if (k.n_act > 0) {
+        KScope sc(h, KC_REDUCE_ABAR);
         launch_reduce_abar(k, h->abar_part, p2g_grad_blocks(k), h->alpha_bar + (size_t)t * A, h->stream);
         h->launches += 1;
     }
@@ -285,6 +346,7 @@ mpm_status mpm_create(int64_t n_particles, int32_t n_grid, int32_t dim, float dt
 mpm_status mpm_destroy(mpm_handle h) {
     if (!h) return MPM_ERR_INVALID_ARG;
     if (h->h_flags) cudaFreeHost(h->h_flags);
+    for (auto ev : h->prof.pool) cudaEventDestroy(ev);
     delete h;
     return MPM_OK;
 }
@@ -360,7 +422,7 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
     if (v && (st = copy_in(h, sv, v, sizeof(float) * EN * d))) return st;
     if (C && (st = copy_in(h, sC, C, sizeof(float) * EN * d * d))) return st;
     if (F && (st = copy_in(h, sF, F, sizeof(float) * EN * d * d))) return st;
-    launch_pack(k, sx, v ? sv : nullptr, C ? sC : nullptr, F ? sF : nullptr, h->ckpt, h->stream);
+    { KScope sc(h, KC_LAYOUT); launch_pack(k, sx, v ? sv : nullptr, C ? sC : nullptr, F ? sF : nullptr, h->ckpt, h->stream); }
     h->launches += 1;
     h->has_aid = actuator_id != nullptr;
     if (actuator_id && (st = copy_in(h, h->aid, actuator_id, sizeof(int32_t) * EN))) return st;
@@ -394,7 +456,7 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
         return fail(h, MPM_ERR_INVALID_ARG, "steps must be in [1, max_steps]");
     const KParams k = kparams(h);
     h->t_final = steps;
-    launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream);
+    { KScope sc(h, KC_CTRL); launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream); }
     if (k.n_act > 0) h->launches += 1;
     for (int t = 0; t < steps; ++t) step_forward(h, k, t, state_ptr(h, t), state_ptr(h, t + 1));
     CU(cudaGetLastError());
@@ -412,8 +474,9 @@ mpm_status mpm_loss(mpm_handle h, float* loss_out) {
     const KParams k = kparams(h);
     const float3 tgt = make_float3(h->prm.loss_target[0], h->prm.loss_target[1], h->prm.loss_target[2]);
     h->sbar_cur = 0;
-    launch_loss(k, state_ptr(h, h->recorded), h->prm.loss_kind, tgt, h->com_part, h->loss,
-                h->sbar[0], h->flags, h->stream);
+    { KScope sc(h, KC_LOSS);
+      launch_loss(k, state_ptr(h, h->recorded), h->prm.loss_kind, tgt, h->com_part, h->loss,
+                  h->sbar[0], h->flags, h->stream); }
     h->launches += 3;
     if (loss_out) CU(cudaMemcpyAsync(loss_out, h->loss, sizeof(float) * k.E, cudaMemcpyDefault, h->stream));
     mpm_status st = sync_flags(h, "mpm_loss");
@@ -438,7 +501,7 @@ mpm_status mpm_seed_adjoint(mpm_handle h, const float* dx, const float* dv, cons
     if (dC && (st = copy_in(h, sC, dC, sizeof(float) * EN * d * d))) return st;
     if (dF && (st = copy_in(h, sF, dF, sizeof(float) * EN * d * d))) return st;
     if (!dF) CU(cudaMemsetAsync(sF, 0, sizeof(float) * EN * d * d, h->stream));
-    launch_pack(k, dx ? sx : nullptr, dv ? sv : nullptr, dC ? sC : nullptr, sF, h->sbar[0], h->stream);
+    { KScope sc(h, KC_LAYOUT); launch_pack(k, dx ? sx : nullptr, dv ? sv : nullptr, dC ? sC : nullptr, sF, h->sbar[0], h->stream); }
     h->launches += 1;
     CU(cudaGetLastError());
     h->sbar_cur = 0;
@@ -469,6 +532,7 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     }
     const int64_t nth = n_theta_of(h->prm);
     if (nth > 0) {
+        KScope sc(h, KC_CTRL);
         launch_ctrl_bwd(k, h->theta, T, h->alpha, h->alpha_bar, h->theta_part, h->theta_bar, nth, h->stream);
         h->launches += 2;
     }
@@ -488,7 +552,7 @@ mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF
     float* sv = sx + EN * d;
     float* sC = sv + EN * d;
     float* sF = sC + EN * d * d;
-    launch_unpack(k, h->sbar[h->sbar_cur], sx, sv, sC, sF, h->stream);
+    { KScope sc(h, KC_LAYOUT); launch_unpack(k, h->sbar[h->sbar_cur], sx, sv, sC, sF, h->stream); }
     h->launches += 1;
     if (dx0) CU(cudaMemcpyAsync(dx0, sx, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
     if (dv0) CU(cudaMemcpyAsync(dv0, sv, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
@@ -497,6 +561,19 @@ mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF
     const int64_t nth = n_theta_of(h->prm);
     if (dtheta && nth > 0)
         CU(cudaMemcpyAsync(dtheta, h->theta_bar, sizeof(float) * nth, cudaMemcpyDefault, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    CU(cudaGetLastError());
+    return MPM_OK;
+}
+
+mpm_status mpm_grad_v0_sum(mpm_handle h, float* out) {
+    if (!h || !out) return MPM_ERR_INVALID_ARG;
+    if (h->phase != kBackward) return fail(h, MPM_ERR_BAD_SEQUENCE, "grad_v0_sum before backward");
+    const KParams k = kparams(h);
+    float* res = h->com_part + (size_t)k.E * loss_blocks_per_episode(k) * 3;  // tail of com_part
+    { KScope sc(h, KC_LOSS); launch_v_sum(k, h->sbar[h->sbar_cur], h->com_part, res, h->stream); }
+    h->launches += 2;
+    CU(cudaMemcpyAsync(out, res, sizeof(float) * k.E * h->dim, cudaMemcpyDefault, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     CU(cudaGetLastError());
     return MPM_OK;
@@ -511,7 +588,7 @@ mpm_status mpm_get_state(mpm_handle h, float* x, float* v, float* C, float* F) {
     float* sv = sx + EN * d;
     float* sC = sv + EN * d;
     float* sF = sC + EN * d * d;
-    launch_unpack(k, state_ptr(h, h->recorded), sx, sv, sC, sF, h->stream);
+    { KScope sc(h, KC_LAYOUT); launch_unpack(k, state_ptr(h, h->recorded), sx, sv, sC, sF, h->stream); }
     h->launches += 1;
     if (x) CU(cudaMemcpyAsync(x, sx, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
     if (v) CU(cudaMemcpyAsync(v, sv, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
@@ -519,6 +596,52 @@ mpm_status mpm_get_state(mpm_handle h, float* x, float* v, float* C, float* F) {
     if (F) CU(cudaMemcpyAsync(F, sF, sizeof(float) * EN * d * d, cudaMemcpyDefault, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     CU(cudaGetLastError());
+    return MPM_OK;
+}
+
+mpm_status mpm_set_profiling(mpm_handle h, int32_t enable) {
+    if (!h) return MPM_ERR_INVALID_ARG;
+    if (enable && h->prof.pool.empty()) {
+        h->prof.pool.resize(2 * 16384);
+        for (auto& ev : h->prof.pool) CU(cudaEventCreate(&ev));
+    }
+    if (!enable && h->prof.on) {
+        CU(cudaStreamSynchronize(h->stream));
+        prof_harvest(h);
+    }
+    h->prof.on = enable != 0;
+    return MPM_OK;
+}
+
+mpm_status mpm_reset_kernel_stats(mpm_handle h) {
+    if (!h) return MPM_ERR_INVALID_ARG;
+    CU(cudaStreamSynchronize(h->stream));
+    prof_harvest(h);
+    for (int c = 0; c < KC_N; ++c) { h->prof.ms[c] = 0; h->prof.n[c] = 0; }
+    return MPM_OK;
+}
+
+mpm_status mpm_kernel_stats(mpm_handle h, int32_t idx, const char** name, double* total_ms,
+                            int64_t* count) {
+    if (!h || idx < 0 || idx >= KC_N) return MPM_ERR_INVALID_ARG;
+    CU(cudaStreamSynchronize(h->stream));
+    prof_harvest(h);
+    if (name) *name = kClassNames[idx];
+    if (total_ms) *total_ms = h->prof.ms[idx];
+    if (count) *count = h->prof.n[idx];
+    return MPM_OK;
+}
+
+mpm_status mpm_active_nodes(mpm_handle h, int64_t* count) {
+    if (!h || !count) return MPM_ERR_INVALID_ARG;
+    if (h->phase < kForward) return fail(h, MPM_ERR_BAD_SEQUENCE, "active_nodes before forward");
+    const KParams k = kparams(h);
+    { KScope sc(h, KC_LAYOUT); launch_count_active(k, h->grid, h->com_part_count, h->stream); }
+    h->launches += 1;
+    int64_t c = 0;
+    CU(cudaMemcpyAsync(&c, h->com_part_count, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    *count = c;
     return MPM_OK;
 }
 

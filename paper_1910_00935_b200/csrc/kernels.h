@@ -42,6 +42,12 @@ int loss_blocks_per_episode(const KParams& p);
 void launch_loss(const KParams& p, const float* S, int loss_kind, float3 target, float* com_part,
                  float* loss, float* Sb, int* flags, cudaStream_t s);
 
+// ---- per-episode sum of the v-adjoint of the records: out[E][d] (fixed order)
+void launch_v_sum(const KParams& p, const float* Sb, float* part, float* out, cudaStream_t s);
+
+// ---- measurement: number of grid nodes with M > 0 (all episodes) -> *count (device)
+void launch_count_active(const KParams& p, const float4* grid, int64_t* count, cudaStream_t s);
+
 // ---- layout conversion (caller arrays <-> particle records) ------------------
 // pack: records[E*N][R] from x[E*N][d], v, C[E*N][d][d], F (any may be null -> zero / identity)
 void launch_pack(const KParams& p, const float* x, const float* v, const float* C, const float* F,

@@ -126,6 +126,47 @@ __global__ void k_com_partial(KParams p, const float* __restrict__ S, float* __r
         for (int k = 0; k < D; ++k) part[((int64_t)e * nb + blockIdx.x) * D + k] = red[k][0];
 }
 
+// partial sums of the v slot of adjoint records (same chunking as k_com_partial)
+template <int D>
+__global__ void k_vsum_partial(KParams p, const float* __restrict__ Sb, float* __restrict__ part) {
+    __shared__ float red[D][kLossThreads];
+    const int e = blockIdx.y, nb = gridDim.x;
+    const int64_t chunk = (p.N + nb - 1) / nb;
+    const int64_t lo = blockIdx.x * chunk, hi = min(p.N, lo + chunk);
+    float acc[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc[k] = 0.0f;
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const float* r = Sb + ((int64_t)e * p.N + i) * Rec<D>::R;
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc[k] += r[Rec<D>::V + k];
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) red[k][threadIdx.x] = acc[k];
+    __syncthreads();
+    for (int s = kLossThreads / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s)
+#pragma unroll
+            for (int k = 0; k < D; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < D; ++k) part[((int64_t)e * nb + blockIdx.x) * D + k] = red[k][0];
+}
+
+template <int D>
+__global__ void k_sum_parts(const float* __restrict__ part, int nb, float* __restrict__ out) {
+    const int e = blockIdx.x;
+    if (threadIdx.x != 0) return;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        float s = 0.0f;
+        for (int b = 0; b < nb; ++b) s += part[((int64_t)e * nb + b) * D + k];
+        out[e * D + k] = s;
+    }
+}
+
 // xbar = sum m x / sum m;  L = |xbar - x*|^2 or -xbar_0;  seed g = dL/dxbar * m / M
 template <int D>
 __global__ void k_loss_final(KParams p, const float* __restrict__ part, int nb, int kind,
@@ -211,6 +252,13 @@ __global__ void k_unpack(KParams p, const float* __restrict__ rec, float* __rest
     }
 }
 
+__global__ void k_count_active(int64_t n, const float4* __restrict__ grid, unsigned long long* count) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool act = i < n && grid[i].w > 0.0f;
+    const unsigned b = __ballot_sync(0xffffffffu, act);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, (unsigned long long)__popc(b));
+}
+
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -250,6 +298,20 @@ void launch_loss(const KParams& p, const float* S, int loss_kind, float3 target,
         k_com_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, S, com_part);
         k_loss_final<DIM><<<p.E, 32, 0, s>>>(p, com_part, nb, loss_kind, target, loss, seed, flags);
         k_seed<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, seed, Sb);
+    });
+}
+
+void launch_count_active(const KParams& p, const float4* grid, int64_t* count, cudaStream_t s) {
+    const int64_t n = p.nodes * p.E;
+    cudaMemsetAsync(count, 0, sizeof(int64_t), s);
+    k_count_active<<<nblk(n, 256), 256, 0, s>>>(n, grid, (unsigned long long*)count);
+}
+
+void launch_v_sum(const KParams& p, const float* Sb, float* part, float* out, cudaStream_t s) {
+    const int nb = loss_blocks_per_episode(p);
+    DISPATCH(p.dim, {
+        k_vsum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, Sb, part);
+        k_sum_parts<DIM><<<p.E, 32, 0, s>>>(part, nb, out);
     });
 }
 

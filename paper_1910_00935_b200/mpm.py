@@ -24,7 +24,8 @@ LOSS_COM_TARGET, LOSS_MOVE_FORWARD = 0, 1
 EXPORTS = ["mpm_create", "mpm_destroy", "mpm_last_error", "mpm_default_params", "mpm_get_params",
            "mpm_set_params", "mpm_set_stream", "mpm_workspace_bytes", "mpm_bind_workspace",
            "mpm_set_state", "mpm_n_theta", "mpm_set_controller", "mpm_forward", "mpm_loss",
-           "mpm_seed_adjoint", "mpm_backward", "mpm_grads", "mpm_get_state", "mpm_launch_count"]
+           "mpm_seed_adjoint", "mpm_backward", "mpm_grads", "mpm_get_state", "mpm_launch_count",
+           "mpm_grad_v0_sum", "mpm_set_profiling", "mpm_reset_kernel_stats", "mpm_kernel_stats", "mpm_active_nodes"]
 
 
 class MpmError(RuntimeError):
@@ -67,6 +68,10 @@ def load() -> ct.CDLL:
             "mpm_forward": [H, ct.c_int32], "mpm_loss": [H, P], "mpm_seed_adjoint": [H, P, P, P, P],
             "mpm_backward": [H, ct.c_int32], "mpm_grads": [H, P, P, P, P, P],
             "mpm_get_state": [H, P, P, P, P], "mpm_launch_count": [H, ct.POINTER(ct.c_int64)],
+            "mpm_grad_v0_sum": [H, P], "mpm_set_profiling": [H, ct.c_int32], "mpm_reset_kernel_stats": [H],
+            "mpm_kernel_stats": [H, ct.c_int32, ct.POINTER(ct.c_char_p), ct.POINTER(ct.c_double),
+                                 ct.POINTER(ct.c_int64)],
+            "mpm_active_nodes": [H, ct.POINTER(ct.c_int64)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -180,6 +185,13 @@ class Sim:
         self._check("mpm_grads", self.L.mpm_grads(self.h, *ptrs))
         return bufs
 
+    def grad_v0_sum(self, out=None):
+        """sum_p dL/dv0_p per episode: [E][d] (host numpy, or a given buffer)."""
+        out = np.zeros((self.E, self.dim), np.float32) if out is None else out
+        ptr, keep = _ptr(out)
+        self._check("mpm_grad_v0_sum", self.L.mpm_grad_v0_sum(self.h, ptr))
+        return out
+
     def get_state(self, out: str = "numpy"):
         d = self.dim
         shapes = {"x": (self.E, self.N, d), "v": (self.E, self.N, d),
@@ -191,6 +203,29 @@ class Sim:
     def launch_count(self) -> int:
         c = ct.c_int64()
         self._check("mpm_launch_count", self.L.mpm_launch_count(self.h, ct.byref(c)))
+        return int(c.value)
+
+    def set_profiling(self, on: bool):
+        self._check("mpm_set_profiling", self.L.mpm_set_profiling(self.h, int(bool(on))))
+
+    def reset_kernel_stats(self):
+        self._check("mpm_reset_kernel_stats", self.L.mpm_reset_kernel_stats(self.h))
+
+    def kernel_stats(self) -> dict:
+        """{kernel class: (total device ms, launches)} since the last reset."""
+        out, i = {}, 0
+        while True:
+            name, ms, n = ct.c_char_p(), ct.c_double(), ct.c_int64()
+            st = self.L.mpm_kernel_stats(self.h, i, ct.byref(name), ct.byref(ms), ct.byref(n))
+            if st != MPM_OK:
+                break
+            out[name.value.decode()] = (float(ms.value), int(n.value))
+            i += 1
+        return out
+
+    def active_nodes(self) -> int:
+        c = ct.c_int64()
+        self._check("mpm_active_nodes", self.L.mpm_active_nodes(self.h, ct.byref(c)))
         return int(c.value)
 
     def close(self):
