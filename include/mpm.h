@@ -58,7 +58,8 @@ typedef enum {
     MPM_ERR_OUT_OF_DOMAIN = 4,   /* a particle's 3^d stencil left [0, n_grid-1]^d (R13) */
     MPM_ERR_NONFINITE = 5,       /* NaN/Inf, J <= 0 under Neo-Hookean, r = 0 in the 2x2 polar (R14) */
     MPM_ERR_BAD_SEQUENCE = 6,    /* e.g. backward before forward/loss, steps != recorded */
-    MPM_ERR_UNSUPPORTED = 7      /* e.g. fixed-corotated in 3D (needs SVD, out of scope) */
+    MPM_ERR_UNSUPPORTED = 7      /* fixed-corotated in 3D (needs an SVD, out of scope), or more
+                                    than 1728 particles in one block (27 per cell on average) */
 } mpm_status;
 
 enum { MPM_MODEL_NEOHOOKEAN = 0, MPM_MODEL_FIXED_COROTATED = 1 };
@@ -82,9 +83,13 @@ typedef struct {
     float omega;          /* feature frequency, default 20 */
     int32_t ctrl_hidden;  /* H: 0 = tanh(W phi + b); H > 0 = 2-layer tanh MLP (R9) */
     int32_t n_episodes;   /* E independent episodes sharing theta, default 1 */
-    int32_t deterministic;/* 1 = fixed-order reductions (bitwise run-to-run) */
+    int32_t deterministic;/* accepted for compatibility: every reduction already has a fixed
+                             order, so results are bitwise reproducible run to run */
     int32_t loss_kind;    /* MPM_LOSS_* */
     float loss_target[3]; /* x* for MPM_LOSS_COM_TARGET */
+    int32_t max_active_blocks; /* capacity of the per-step active block list (blocks of
+                                  4^3 cells in 3D, 8^2 in 2D); 0 = automatic.  Exceeding it
+                                  returns MPM_ERR_OOM. */
 } mpm_params;
 
 /* Create a handle for n_particles per episode on an n_grid^dim grid over the

@@ -1,5 +1,14 @@
 // engine.cu -- the C-ABI (include/mpm.h): handle, workspace carving, the tape with
-// segment checkpointing (Appendix D) and error reporting.
+// segment checkpointing (Appendix D), error reporting and the
+// per-kernel timing hooks.
+//
+// Tape layout: S_t (records + particle ids) lives in the
+// final-state buffer (t = T), a checkpoint slot (t % k == 0) or the k-slot
+// window; each window slot j also holds the binning and the node tiles of the
+// step t with t % k == j, so the backward reuses the grid of every step of the
+// segment in the window without re-running p2g.  Adjoint states are kept in
+// caller (particle-id) order.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -17,11 +26,10 @@ namespace {
 enum Phase { kCreated = 0, kBound, kHasState, kForward, kSeeded, kBackward };
 
 // kernel classes for the per-kernel device-time accounting (mpm_kernel_stats)
-enum KClass { KC_P2G = 0, KC_GRID_OP, KC_G2P, KC_G2P_GRAD, KC_GRID_OP_GRAD, KC_P2G_GRAD,
-              KC_REDUCE_ABAR, KC_CLEAR, KC_CTRL, KC_LOSS, KC_LAYOUT, KC_N };
-const char* const kClassNames[KC_N] = {"p2g", "grid_op", "g2p", "g2p_grad", "grid_op_grad",
-                                        "p2g_grad", "reduce_abar", "clear_grid", "controller",
-                                        "loss", "layout"};
+enum KClass { KC_P2G = 0, KC_G2P, KC_BIN, KC_G2P_GRAD, KC_P2G_GRAD, KC_REDUCE_ABAR, KC_CTRL,
+              KC_LOSS, KC_LAYOUT, KC_N };
+const char* const kClassNames[KC_N] = {"p2g", "g2p", "bin", "g2p_grad", "p2g_grad", "reduce_abar",
+                                        "controller", "loss", "layout"};
 
 struct Profiler {
     bool on = false;
@@ -37,7 +45,6 @@ size_t align_up(size_t n) { return (n + 255) & ~size_t(255); }
 }  // namespace
 
 struct mpm_ctx {
-    // creation arguments
     int64_t N = 0;
     int32_t n_grid = 0, dim = 0;
     float dt = 0, E = 0, nu = 0;
@@ -51,35 +58,38 @@ struct mpm_ctx {
     size_t ws_bytes = 0;
     size_t state_floats = 0;  // E * N * R
     int n_ckpt = 0;
-    float* ckpt = nullptr;      // [n_ckpt][E*N*R]   S_{s k}
-    float* window = nullptr;    // [k][E*N*R]        S_{s k + j}, j = 1..k-1
-    float* final_state = nullptr;  // [E*N*R]        S_T of the recorded forward
-    float* sbar[2] = {nullptr, nullptr};
-    float* staging = nullptr;   // [E*N*R] caller-layout copies
-    int32_t* aid = nullptr;     // [E*N]
-    float4* grid = nullptr;     // [E][nodes]  (P, M)
-    float4* U = nullptr;        // [E][nodes]  (U, z)
-    float4* Ubar = nullptr;
-    float4* gbar = nullptr;
-    float* alpha = nullptr;     // [max_steps][n_act]
+    int max_active = 0;
+    std::vector<StateView> ckpt;   // S_{s k}
+    std::vector<StateView> window; // S_{s k + j}, j = 1..k-1
+    StateView final_state{};       // S_T
+    std::vector<SlotView> slots;   // binning + tiles of step t, slot t % k
+    float* sbar[2] = {nullptr, nullptr};  // adjoint states, caller order
+    float* staging = nullptr;
+    int32_t* aid = nullptr;        // caller order
+    int* bcount = nullptr;         // [TB] block histogram (kept zero between uses)
+    int* cursor = nullptr;         // [TB]
+    int* keys = nullptr;           // [EN]
+    float* xbar_part = nullptr;    // [EN][d]
+    float4* ubar = nullptr;        // [max_active][TN]
+    float* abar_part = nullptr;    // [max_active][n_act]
+    float* alpha = nullptr;        // [max_steps][n_act]
     float* alpha_bar = nullptr;
-    float* abar_part = nullptr; // [p2g_grad blocks][n_act]
     float* theta = nullptr;
     float* theta_bar = nullptr;
-    float* theta_part = nullptr;  // [max_steps][n_theta]
-    float* loss = nullptr;      // [E]
+    float* theta_part = nullptr;   // [max_steps][n_theta]
+    float* loss = nullptr;         // [E]
     float* com_part = nullptr;
-    int* flags = nullptr;       // device error flags
-    int* h_flags = nullptr;     // pinned host mirror
+    int64_t* counter = nullptr;
+    int* flags = nullptr;
+    int* h_flags = nullptr;
     // tape
     Phase phase = kCreated;
     bool has_aid = false;
-    int32_t recorded = 0;       // T of the recorded forward
-    int32_t t_final = 0;        // T whose state lives in final_state (0 = none)
-    int window_seg = -1;        // segment whose intermediate states are in the window
-    int sbar_cur = 0;           // index of the adjoint buffer holding S_bar of the current step
+    int32_t recorded = 0;
+    int32_t t_final = 0;
+    int window_seg = -1;
+    int sbar_cur = 0;
     Profiler prof;
-    int64_t* com_part_count = nullptr;  // scratch counter (active nodes)
 };
 
 namespace {
@@ -89,10 +99,10 @@ mpm_status fail(mpm_handle h, mpm_status st, const std::string& msg) {
     return st;
 }
 
-#define CU(call)                                                                       \
-    do {                                                                               \
-        cudaError_t e_ = (call);                                                       \
-        if (e_ != cudaSuccess)                                                         \
+#define CU(call)                                                                           \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
             return fail(h, MPM_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
     } while (0)
 
@@ -101,6 +111,10 @@ int64_t n_theta_of(const mpm_params& p) {
     if (A <= 0) return 0;
     return H > 0 ? H * S + H + A * H + A : A * S + A;
 }
+
+int block_edge(int dim) { return dim == 3 ? 4 : 8; }
+int tile_nodes(int dim) { return dim == 3 ? 216 : 100; }
+constexpr int kCells = 64;
 
 KParams kparams(const mpm_ctx* h) {
     KParams k{};
@@ -130,74 +144,111 @@ KParams kparams(const mpm_ctx* h) {
     k.nodes = h->dim == 2 ? (int64_t)h->n_grid * h->n_grid
                           : (int64_t)h->n_grid * h->n_grid * h->n_grid;
     k.E = p.n_episodes;
+    const int B = block_edge(h->dim);
+    k.nb = (h->n_grid + B - 1) / B;
+    k.nbe = h->dim == 2 ? k.nb * k.nb : k.nb * k.nb * k.nb;
+    k.TB = k.nbe * k.E;
+    k.max_active = h->max_active;
     return k;
 }
 
 int record_floats(int dim) { return 2 * dim + 2 * dim * dim; }
 
+int default_max_active(const mpm_ctx* h, const KParams& k) {
+    if (h->prm.max_active_blocks > 0) return std::min(h->prm.max_active_blocks, k.TB);
+    const int64_t EN = (int64_t)k.E * k.N;
+    const int64_t guess = (EN + kCells - 1) / kCells * 3 + (int64_t)k.E * 64;
+    return (int)std::min<int64_t>(k.TB, guess);
+}
+
 // carve (or just size, when base == nullptr) the workspace
 size_t carve(mpm_ctx* h, char* base) {
     const mpm_params& p = h->prm;
-    const KParams k = kparams(h);
-    const size_t E = (size_t)p.n_episodes, N = (size_t)h->N;
-    const size_t sf = E * N * record_floats(h->dim);
+    KParams k = kparams(h);
+    const int max_active = default_max_active(h, k);
+    const size_t E = (size_t)p.n_episodes, N = (size_t)h->N, EN = E * N;
+    const size_t sf = EN * record_floats(h->dim);
     const int kk = p.k_ckpt;
     const int n_ckpt = p.max_steps / kk + 1;
-    const size_t nodes = (size_t)k.nodes * E;
     const int A = p.n_actuators > 0 ? p.n_actuators : 1;
     const int64_t nth = n_theta_of(p) > 0 ? n_theta_of(p) : 1;
-    const int pblk = p2g_grad_blocks(k);
     const int lblk = loss_blocks_per_episode(k);
+    const size_t TN = tile_nodes(h->dim);
     size_t off = 0;
     auto take = [&](size_t bytes) -> char* {
         char* ptr = base ? base + off : nullptr;
         off += align_up(bytes);
         return ptr;
     };
-    float* ckpt = (float*)take(sizeof(float) * sf * n_ckpt);
-    float* window = (float*)take(sizeof(float) * sf * kk);
-    float* final_state = (float*)take(sizeof(float) * sf);
+    auto state = [&]() {
+        StateView s;
+        s.rec = (float*)take(sizeof(float) * sf);
+        s.pid = (int*)take(sizeof(int) * EN);
+        return s;
+    };
+    std::vector<StateView> ckpt, window;
+    for (int i = 0; i < n_ckpt; ++i) ckpt.push_back(state());
+    for (int i = 0; i < kk; ++i) window.push_back(i == 0 ? StateView{nullptr, nullptr} : state());
+    StateView fin = state();
+    std::vector<SlotView> slots;
+    for (int i = 0; i < kk; ++i) {
+        SlotView s;
+        s.sigma = (int*)take(sizeof(int) * EN);
+        s.blist = (int*)take(sizeof(int) * max_active);
+        s.bstart = (int*)take(sizeof(int) * (max_active + 1));
+        s.bmap = (int*)take(sizeof(int) * k.TB);
+        s.nactive = (int*)take(sizeof(int));
+        s.cstart = (unsigned short*)take(sizeof(unsigned short) * (size_t)max_active * (kCells + 1));
+        s.tiles = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
+        slots.push_back(s);
+    }
     float* sb0 = (float*)take(sizeof(float) * sf);
     float* sb1 = (float*)take(sizeof(float) * sf);
     float* staging = (float*)take(sizeof(float) * sf);
-    int32_t* aid = (int32_t*)take(sizeof(int32_t) * E * N);
-    float4* grid = (float4*)take(sizeof(float4) * nodes);
-    float4* U = (float4*)take(sizeof(float4) * nodes);
-    float4* Ubar = (float4*)take(sizeof(float4) * nodes);
-    float4* gbar = (float4*)take(sizeof(float4) * nodes);
+    int32_t* aid = (int32_t*)take(sizeof(int32_t) * EN);
+    int* bcount = (int*)take(sizeof(int) * k.TB);
+    int* cursor = (int*)take(sizeof(int) * k.TB);
+    int* keys = (int*)take(sizeof(int) * EN);
+    float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
+    float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
+    float* abar_part = (float*)take(sizeof(float) * (size_t)max_active * A);
     float* alpha = (float*)take(sizeof(float) * (size_t)p.max_steps * A);
     float* alpha_bar = (float*)take(sizeof(float) * (size_t)p.max_steps * A);
-    float* abar_part = (float*)take(sizeof(float) * (size_t)pblk * A);
     float* theta = (float*)take(sizeof(float) * nth);
     float* theta_bar = (float*)take(sizeof(float) * nth);
     float* theta_part = (float*)take(sizeof(float) * (size_t)p.max_steps * nth);
     float* loss = (float*)take(sizeof(float) * E);
-    float* com_part = (float*)take(sizeof(float) * E * (lblk + 1) * 3);
+    float* com_part = (float*)take(sizeof(float) * E * (lblk + 2) * 3);
+    int64_t* counter = (int64_t*)take(sizeof(int64_t) * 2);
     int* flags = (int*)take(sizeof(int) * 4);
-    int64_t* cnt = (int64_t*)take(sizeof(int64_t) * 2);
     if (base) {
-        h->com_part_count = cnt;
+        h->max_active = max_active;
         h->state_floats = sf;
         h->n_ckpt = n_ckpt;
-        h->ckpt = ckpt; h->window = window; h->final_state = final_state; h->sbar[0] = sb0; h->sbar[1] = sb1;
-        h->staging = staging; h->aid = aid; h->grid = grid; h->U = U; h->Ubar = Ubar;
-        h->gbar = gbar; h->alpha = alpha; h->alpha_bar = alpha_bar; h->abar_part = abar_part;
-        h->theta = theta; h->theta_bar = theta_bar; h->theta_part = theta_part; h->loss = loss;
-        h->com_part = com_part; h->flags = flags;
+        h->ckpt = ckpt;
+        h->window = window;
+        h->final_state = fin;
+        h->slots = slots;
+        h->sbar[0] = sb0; h->sbar[1] = sb1;
+        h->staging = staging; h->aid = aid; h->bcount = bcount; h->cursor = cursor; h->keys = keys;
+        h->xbar_part = xbar_part; h->ubar = ubar; h->abar_part = abar_part;
+        h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
+        h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
+        h->flags = flags;
     }
     return off;
 }
 
-// S_t lives in: final_state (t = T of the forward), a checkpoint slot (t % k == 0)
-// or the window (the intermediate states of one segment).
-float* state_ptr(mpm_ctx* h, int t) {
+StateView state_at(mpm_ctx* h, int t) {
     const int k = h->prm.k_ckpt;
     if (t > 0 && t == h->t_final) return h->final_state;
-    if (t % k == 0) return h->ckpt + (size_t)(t / k) * h->state_floats;
-    return h->window + (size_t)(t % k) * h->state_floats;
+    if (t % k == 0) return h->ckpt[t / k];
+    return h->window[t % k];
 }
 
-// collect pending event pairs (the stream must be synchronised)
+const SlotView& slot_at(mpm_ctx* h, int t) { return h->slots[t % h->prm.k_ckpt]; }
+
+// ---------------------------------------------------------------- profiling
 void prof_harvest(mpm_ctx* h) {
     for (auto& pr : h->prof.pending) {
         float ms = 0.0f;
@@ -210,13 +261,15 @@ void prof_harvest(mpm_ctx* h) {
     h->prof.used = 0;
 }
 
-// brackets one library launch with CUDA events when profiling is on
+// counts one library launch group and, when profiling is on, brackets it with
+// CUDA events on the bound stream
 struct KScope {
     mpm_ctx* h;
     int cls;
     size_t idx = 0;
     bool active = false;
     KScope(mpm_ctx* h_, int c) : h(h_), cls(c) {
+        h->launches += 1;
         if (!h->prof.on) return;
         if (h->prof.used + 2 > h->prof.pool.size()) {
             cudaStreamSynchronize(h->stream);
@@ -244,44 +297,64 @@ mpm_status sync_flags(mpm_handle h, const char* where) {
     if (f) {
         CU(cudaMemsetAsync(h->flags, 0, sizeof(int), h->stream));
         CU(cudaStreamSynchronize(h->stream));
+        if (f & FLAG_ACTIVE_OVERFLOW)
+            return fail(h, MPM_ERR_OOM, std::string(where) + ": active blocks exceed max_active_blocks (" +
+                                            std::to_string(h->max_active) + ")");
+        if (f & FLAG_BLOCK_OVERFLOW)
+            return fail(h, MPM_ERR_UNSUPPORTED, std::string(where) + ": more than 1728 particles in one block");
         if (f & FLAG_OUT_OF_DOMAIN)
-            return fail(h, MPM_ERR_OUT_OF_DOMAIN,
-                        std::string(where) + ": a particle stencil left [0, n_grid-1]^d");
+            return fail(h, MPM_ERR_OUT_OF_DOMAIN, std::string(where) + ": a particle stencil left [0, n_grid-1]^d");
         return fail(h, MPM_ERR_NONFINITE,
                     std::string(where) + ": non-finite value or degenerate deformation (J<=0 / r=0)");
     }
     return MPM_OK;
 }
 
-// advance(): clear_grid, p2g (actuation precomputed), grid_op, g2p
-void step_forward(mpm_ctx* h, const KParams& k, int t, const float* S, float* Sn) {
-    const size_t gbytes = sizeof(float4) * (size_t)k.nodes * k.E;
-    { KScope sc(h, KC_CLEAR); cudaMemsetAsync(h->grid, 0, gbytes, h->stream); }
-    const float* al = h->alpha + (size_t)t * (k.n_act > 0 ? k.n_act : 1);
-    { KScope sc(h, KC_P2G); launch_p2g(k, S, h->has_aid ? h->aid : nullptr, al, h->grid, Sn, h->flags, h->stream); }
-    { KScope sc(h, KC_GRID_OP); launch_grid_op(k, h->grid, h->U, h->stream); }
-    { KScope sc(h, KC_G2P); launch_g2p(k, S, h->U, Sn, h->flags, h->stream); }
-    h->launches += 3;
+const float* alpha_at(mpm_ctx* h, int t) {
+    return h->alpha + (size_t)t * (h->prm.n_actuators > 0 ? h->prm.n_actuators : 1);
 }
 
-// advance_grad(): recompute the grid, then g2p.grad, grid_op.grad, p2g.grad
-void step_backward(mpm_ctx* h, const KParams& k, int t, const float* S, const float* Sbn, float* Sb) {
-    const size_t gbytes = sizeof(float4) * (size_t)k.nodes * k.E;
+// fresh binning of S_t into slot(t) (start of a forward or of a segment re-forward)
+void bin_fresh(mpm_ctx* h, const KParams& k, int t) {
+    const SlotView& sl = slot_at(h, t);
+    KScope sc(h, KC_BIN);
+    h->launches += 2;
+    launch_bin_keys(k, state_at(h, t).rec, h->keys, h->bcount, h->flags, h->stream);
+    launch_bin_scan(k, h->bcount, h->cursor, sl, h->flags, h->stream);
+    launch_bin_scatter(k, h->keys, h->cursor, sl.sigma, h->stream);
+}
+
+// advance() for step t; write_next: produce S_{t+1}; bin_next: bin it into slot(t+1)
+void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin_next) {
+    const SlotView& sl = slot_at(h, t);
+    const StateView S = state_at(h, t);
+    const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr};
+    const int32_t* aid = h->has_aid ? h->aid : nullptr;
+    { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
+    if (!write_next) return;
+    { KScope sc(h, KC_G2P);
+      launch_g2p(k, sl, S, Sn, bin_next ? h->keys : nullptr, h->bcount, h->flags, h->stream); }
+    if (bin_next) {
+        const SlotView& nx = slot_at(h, t + 1);
+        KScope sc(h, KC_BIN);
+        h->launches += 1;
+        launch_bin_scan(k, h->bcount, h->cursor, nx, h->flags, h->stream);
+        launch_bin_scatter(k, h->keys, h->cursor, nx.sigma, h->stream);
+    }
+}
+
+// advance_grad() for step t, using the grid tiles stored in slot(t)
+void step_backward(mpm_ctx* h, const KParams& k, int t, const float* Sbn, float* Sb) {
+    const SlotView& sl = slot_at(h, t);
+    const StateView S = state_at(h, t);
     const int A = k.n_act > 0 ? k.n_act : 1;
-    const float* al = h->alpha + (size_t)t * A;
-    { KScope sc(h, KC_CLEAR); cudaMemsetAsync(h->grid, 0, gbytes, h->stream); }
-    { KScope sc(h, KC_P2G); launch_p2g(k, S, h->has_aid ? h->aid : nullptr, al, h->grid, nullptr, h->flags, h->stream); }
-    { KScope sc(h, KC_GRID_OP); launch_grid_op(k, h->grid, h->U, h->stream); }
-    { KScope sc(h, KC_CLEAR); cudaMemsetAsync(h->Ubar, 0, gbytes, h->stream); }
-    { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, S, h->U, Sbn, h->Ubar, Sb, h->stream); }
-    { KScope sc(h, KC_GRID_OP_GRAD); launch_grid_op_grad(k, h->grid, h->U, h->Ubar, h->gbar, h->stream); }
+    { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, sl, S, Sbn, h->ubar, h->xbar_part, h->stream); }
     { KScope sc(h, KC_P2G_GRAD);
-      launch_p2g_grad(k, S, h->has_aid ? h->aid : nullptr, al, h->gbar, Sbn, Sb, h->abar_part, h->flags, h->stream); }
-    h->launches += 5;
+      launch_p2g_grad(k, sl, S, h->has_aid ? h->aid : nullptr, alpha_at(h, t), h->ubar, Sbn, h->xbar_part,
+                      Sb, h->abar_part, h->flags, h->stream); }
     if (k.n_act > 0) {
         KScope sc(h, KC_REDUCE_ABAR);
-        launch_reduce_abar(k, h->abar_part, p2g_grad_blocks(k), h->alpha_bar + (size_t)t * A, h->stream);
-        h->launches += 1;
+        launch_reduce_abar(k, sl.nactive, h->abar_part, h->alpha_bar + (size_t)t * A, h->stream);
     }
 }
 
@@ -312,8 +385,9 @@ mpm_status mpm_default_params(int32_t dim, mpm_params* p) {
     p->omega = 20.0f;
     p->ctrl_hidden = 0;
     p->n_episodes = 1;
-    p->deterministic = 0;
+    p->deterministic = 1;
     p->loss_kind = MPM_LOSS_COM_TARGET;
+    p->max_active_blocks = 0;
     return MPM_OK;
 }
 
@@ -321,10 +395,10 @@ mpm_status mpm_create(int64_t n_particles, int32_t n_grid, int32_t dim, float dt
                       float nu, mpm_handle* out) {
     if (!out) return MPM_ERR_INVALID_ARG;
     *out = nullptr;
-    if (n_particles < 1 || n_grid < 4 || (dim != 2 && dim != 3) || !(dt > 0) || !(E > 0) ||
-        !(nu > -1.0f && nu < 0.5f))
+    if (n_particles < 1 || n_grid < 4 || n_grid > 4096 || (dim != 2 && dim != 3) || !(dt > 0) ||
+        !(E > 0) || !(nu > -1.0f && nu < 0.5f))
         return MPM_ERR_INVALID_ARG;
-    if (n_particles > (int64_t)1 << 31) return MPM_ERR_INVALID_ARG;
+    if (n_particles >= ((int64_t)1 << 31)) return MPM_ERR_INVALID_ARG;
     mpm_ctx* h = new mpm_ctx();
     h->N = n_particles;
     h->n_grid = n_grid;
@@ -335,6 +409,7 @@ mpm_status mpm_create(int64_t n_particles, int32_t n_grid, int32_t dim, float dt
     mpm_default_params(dim, &h->prm);
     cudaError_t e = cudaGetDevice(&h->device);
     if (e == cudaSuccess) e = cudaMallocHost((void**)&h->h_flags, sizeof(int) * 4);
+    if (e == cudaSuccess) e = tile_init();
     if (e != cudaSuccess) {
         delete h;
         return MPM_ERR_CUDA;
@@ -363,17 +438,21 @@ mpm_status mpm_set_params(mpm_handle h, const mpm_params* p) {
     if (!h || !p) return MPM_ERR_INVALID_ARG;
     if (h->phase >= kBound) return fail(h, MPM_ERR_BAD_SEQUENCE, "set_params after bind_workspace");
     if (p->k_ckpt < 1 || p->max_steps < 1 || p->n_episodes < 1 || p->bound < 0 ||
-        p->n_actuators < 0 || p->n_actuators > 256 || p->ctrl_hidden < 0 || p->ctrl_hidden > 1024 ||
+        p->n_actuators < 0 || p->n_actuators > 32 || p->ctrl_hidden < 0 || p->ctrl_hidden > 1024 ||
         p->n_sin < 1 || p->n_sin > 64 || p->act_axis < 0 || p->act_axis >= h->dim ||
-        !(p->p_mass > 0) || !(p->p_vol > 0) || p->eps_mass < 0 ||
+        !(p->p_mass > 0) || !(p->p_vol > 0) || p->eps_mass < 0 || p->max_active_blocks < 0 ||
         (p->loss_kind != MPM_LOSS_COM_TARGET && p->loss_kind != MPM_LOSS_MOVE_FORWARD))
         return fail(h, MPM_ERR_INVALID_ARG, "invalid mpm_params");
     if (p->model != MPM_MODEL_NEOHOOKEAN && p->model != MPM_MODEL_FIXED_COROTATED)
         return fail(h, MPM_ERR_INVALID_ARG, "unknown model");
     if (p->model == MPM_MODEL_FIXED_COROTATED && h->dim == 3)
         return fail(h, MPM_ERR_UNSUPPORTED, "fixed-corotated in 3D needs an SVD (out of scope, R2)");
-    if ((int64_t)p->n_episodes * h->N > ((int64_t)1 << 31))
-        return fail(h, MPM_ERR_INVALID_ARG, "n_episodes * n_particles exceeds 2^31");
+    if ((int64_t)p->n_episodes * h->N >= ((int64_t)1 << 31))
+        return fail(h, MPM_ERR_INVALID_ARG, "n_episodes * n_particles must be < 2^31");
+    const int B = block_edge(h->dim);
+    const int64_t nb = (h->n_grid + B - 1) / B;
+    const int64_t TB = (h->dim == 2 ? nb * nb : nb * nb * nb) * p->n_episodes;
+    if (TB >= ((int64_t)1 << 31)) return fail(h, MPM_ERR_INVALID_ARG, "too many grid blocks");
     h->prm = *p;
     return MPM_OK;
 }
@@ -393,15 +472,16 @@ mpm_status mpm_workspace_bytes(mpm_handle h, size_t* bytes) {
 mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     if (!h || !dptr) return MPM_ERR_INVALID_ARG;
     if (((uintptr_t)dptr & 255) != 0) return fail(h, MPM_ERR_INVALID_ARG, "workspace not 256-B aligned");
-    size_t need = carve(h, nullptr);
+    const size_t need = carve(h, nullptr);
     if (bytes < need)
         return fail(h, MPM_ERR_OOM, "workspace too small: need " + std::to_string(need) + " bytes");
     h->ws = (char*)dptr;
     h->ws_bytes = bytes;
     carve(h, h->ws);
+    const KParams k = kparams(h);
     CU(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
-    CU(cudaMemsetAsync(h->theta, 0, sizeof(float) * (n_theta_of(h->prm) > 0 ? n_theta_of(h->prm) : 1),
-                       h->stream));
+    CU(cudaMemsetAsync(h->bcount, 0, sizeof(int) * k.TB, h->stream));
+    CU(cudaMemsetAsync(h->theta, 0, sizeof(float) * (n_theta_of(h->prm) > 0 ? n_theta_of(h->prm) : 1), h->stream));
     h->phase = kBound;
     return MPM_OK;
 }
@@ -422,8 +502,9 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
     if (v && (st = copy_in(h, sv, v, sizeof(float) * EN * d))) return st;
     if (C && (st = copy_in(h, sC, C, sizeof(float) * EN * d * d))) return st;
     if (F && (st = copy_in(h, sF, F, sizeof(float) * EN * d * d))) return st;
-    { KScope sc(h, KC_LAYOUT); launch_pack(k, sx, v ? sv : nullptr, C ? sC : nullptr, F ? sF : nullptr, h->ckpt, h->stream); }
-    h->launches += 1;
+    { KScope sc(h, KC_LAYOUT);
+      launch_pack(k, sx, v ? sv : nullptr, C ? sC : nullptr, F ? sF : nullptr, h->ckpt[0].rec, h->ckpt[0].pid,
+                  h->stream); }
     h->has_aid = actuator_id != nullptr;
     if (actuator_id && (st = copy_in(h, h->aid, actuator_id, sizeof(int32_t) * EN))) return st;
     CU(cudaGetLastError());
@@ -456,9 +537,9 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
         return fail(h, MPM_ERR_INVALID_ARG, "steps must be in [1, max_steps]");
     const KParams k = kparams(h);
     h->t_final = steps;
-    { KScope sc(h, KC_CTRL); launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream); }
-    if (k.n_act > 0) h->launches += 1;
-    for (int t = 0; t < steps; ++t) step_forward(h, k, t, state_ptr(h, t), state_ptr(h, t + 1));
+    if (k.n_act > 0) { KScope sc(h, KC_CTRL); launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream); }
+    bin_fresh(h, k, 0);
+    for (int t = 0; t < steps; ++t) step_forward(h, k, t, true, t + 1 < steps);
     CU(cudaGetLastError());
     h->recorded = steps;
     h->window_seg = (steps - 1) / h->prm.k_ckpt;
@@ -475,9 +556,9 @@ mpm_status mpm_loss(mpm_handle h, float* loss_out) {
     const float3 tgt = make_float3(h->prm.loss_target[0], h->prm.loss_target[1], h->prm.loss_target[2]);
     h->sbar_cur = 0;
     { KScope sc(h, KC_LOSS);
-      launch_loss(k, state_ptr(h, h->recorded), h->prm.loss_kind, tgt, h->com_part, h->loss,
-                  h->sbar[0], h->flags, h->stream); }
-    h->launches += 3;
+      h->launches += 2;
+      launch_loss(k, state_at(h, h->recorded).rec, h->prm.loss_kind, tgt, h->com_part, h->loss, h->sbar[0],
+                  h->flags, h->stream); }
     if (loss_out) CU(cudaMemcpyAsync(loss_out, h->loss, sizeof(float) * k.E, cudaMemcpyDefault, h->stream));
     mpm_status st = sync_flags(h, "mpm_loss");
     if (st) return st;
@@ -501,8 +582,8 @@ mpm_status mpm_seed_adjoint(mpm_handle h, const float* dx, const float* dv, cons
     if (dC && (st = copy_in(h, sC, dC, sizeof(float) * EN * d * d))) return st;
     if (dF && (st = copy_in(h, sF, dF, sizeof(float) * EN * d * d))) return st;
     if (!dF) CU(cudaMemsetAsync(sF, 0, sizeof(float) * EN * d * d, h->stream));
-    { KScope sc(h, KC_LAYOUT); launch_pack(k, dx ? sx : nullptr, dv ? sv : nullptr, dC ? sC : nullptr, sF, h->sbar[0], h->stream); }
-    h->launches += 1;
+    { KScope sc(h, KC_LAYOUT);
+      launch_pack(k, dx ? sx : nullptr, dv ? sv : nullptr, dC ? sC : nullptr, sF, h->sbar[0], nullptr, h->stream); }
     CU(cudaGetLastError());
     h->sbar_cur = 0;
     h->phase = kSeeded;
@@ -521,20 +602,21 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     const int nseg = (T + kk - 1) / kk;
     for (int s = nseg - 1; s >= 0; --s) {
         const int t0 = s * kk, t1 = (t0 + kk < T) ? t0 + kk : T;
-        if (h->window_seg != s) {  // segment-wise recomputation
-            for (int t = t0; t < t1 - 1; ++t) step_forward(h, k, t, state_ptr(h, t), state_ptr(h, t + 1));
+        if (h->window_seg != s) {  // segment-wise recomputation, grid tiles kept per step
+            bin_fresh(h, k, t0);
+            for (int t = t0; t < t1; ++t) step_forward(h, k, t, t + 1 < t1, t + 1 < t1);
             h->window_seg = s;
         }
         for (int t = t1 - 1; t >= t0; --t) {
-            step_backward(h, k, t, state_ptr(h, t), h->sbar[h->sbar_cur], h->sbar[h->sbar_cur ^ 1]);
+            step_backward(h, k, t, h->sbar[h->sbar_cur], h->sbar[h->sbar_cur ^ 1]);
             h->sbar_cur ^= 1;
         }
     }
     const int64_t nth = n_theta_of(h->prm);
     if (nth > 0) {
         KScope sc(h, KC_CTRL);
+        h->launches += 1;
         launch_ctrl_bwd(k, h->theta, T, h->alpha, h->alpha_bar, h->theta_part, h->theta_bar, nth, h->stream);
-        h->launches += 2;
     }
     CU(cudaGetLastError());
     mpm_status st = sync_flags(h, "mpm_backward");
@@ -552,8 +634,11 @@ mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF
     float* sv = sx + EN * d;
     float* sC = sv + EN * d;
     float* sF = sC + EN * d * d;
-    { KScope sc(h, KC_LAYOUT); launch_unpack(k, h->sbar[h->sbar_cur], sx, sv, sC, sF, h->stream); }
-    h->launches += 1;
+    if (dx0 || dv0 || dC0 || dF0) {
+        KScope sc(h, KC_LAYOUT);
+        launch_unpack(k, h->sbar[h->sbar_cur], nullptr, dx0 ? sx : nullptr, dv0 ? sv : nullptr,
+                      dC0 ? sC : nullptr, dF0 ? sF : nullptr, h->stream);
+    }
     if (dx0) CU(cudaMemcpyAsync(dx0, sx, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
     if (dv0) CU(cudaMemcpyAsync(dv0, sv, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
     if (dC0) CU(cudaMemcpyAsync(dC0, sC, sizeof(float) * EN * d * d, cudaMemcpyDefault, h->stream));
@@ -570,9 +655,10 @@ mpm_status mpm_grad_v0_sum(mpm_handle h, float* out) {
     if (!h || !out) return MPM_ERR_INVALID_ARG;
     if (h->phase != kBackward) return fail(h, MPM_ERR_BAD_SEQUENCE, "grad_v0_sum before backward");
     const KParams k = kparams(h);
-    float* res = h->com_part + (size_t)k.E * loss_blocks_per_episode(k) * 3;  // tail of com_part
-    { KScope sc(h, KC_LOSS); launch_v_sum(k, h->sbar[h->sbar_cur], h->com_part, res, h->stream); }
-    h->launches += 2;
+    float* res = h->com_part + (size_t)k.E * (loss_blocks_per_episode(k) + 1) * 3;
+    { KScope sc(h, KC_LOSS);
+      h->launches += 1;
+      launch_v_sum(k, h->sbar[h->sbar_cur], h->com_part, res, h->stream); }
     CU(cudaMemcpyAsync(out, res, sizeof(float) * k.E * h->dim, cudaMemcpyDefault, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     CU(cudaGetLastError());
@@ -588,8 +674,8 @@ mpm_status mpm_get_state(mpm_handle h, float* x, float* v, float* C, float* F) {
     float* sv = sx + EN * d;
     float* sC = sv + EN * d;
     float* sF = sC + EN * d * d;
-    { KScope sc(h, KC_LAYOUT); launch_unpack(k, state_ptr(h, h->recorded), sx, sv, sC, sF, h->stream); }
-    h->launches += 1;
+    const StateView S = state_at(h, h->recorded);
+    { KScope sc(h, KC_LAYOUT); launch_unpack(k, S.rec, S.pid, sx, sv, sC, sF, h->stream); }
     if (x) CU(cudaMemcpyAsync(x, sx, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
     if (v) CU(cudaMemcpyAsync(v, sv, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
     if (C) CU(cudaMemcpyAsync(C, sC, sizeof(float) * EN * d * d, cudaMemcpyDefault, h->stream));
@@ -602,7 +688,7 @@ mpm_status mpm_get_state(mpm_handle h, float* x, float* v, float* C, float* F) {
 mpm_status mpm_set_profiling(mpm_handle h, int32_t enable) {
     if (!h) return MPM_ERR_INVALID_ARG;
     if (enable && h->prof.pool.empty()) {
-        h->prof.pool.resize(2 * 16384);
+        h->prof.pool.resize(2 * 65536);
         for (auto& ev : h->prof.pool) CU(cudaEventCreate(&ev));
     }
     if (!enable && h->prof.on) {
@@ -634,12 +720,14 @@ mpm_status mpm_kernel_stats(mpm_handle h, int32_t idx, const char** name, double
 
 mpm_status mpm_active_nodes(mpm_handle h, int64_t* count) {
     if (!h || !count) return MPM_ERR_INVALID_ARG;
-    if (h->phase < kForward) return fail(h, MPM_ERR_BAD_SEQUENCE, "active_nodes before forward");
+    if (h->phase < kForward || h->window_seg < 0)
+        return fail(h, MPM_ERR_BAD_SEQUENCE, "active_nodes before forward");
     const KParams k = kparams(h);
-    { KScope sc(h, KC_LAYOUT); launch_count_active(k, h->grid, h->com_part_count, h->stream); }
-    h->launches += 1;
+    // a step whose grid tiles are in the window: the last step of the window segment
+    const int t1 = std::min(h->recorded, (h->window_seg + 1) * h->prm.k_ckpt);
+    { KScope sc(h, KC_LAYOUT); launch_count_active(k, slot_at(h, t1 - 1), h->counter, h->stream); }
     int64_t c = 0;
-    CU(cudaMemcpyAsync(&c, h->com_part_count, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpyAsync(&c, h->counter, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     *count = c;
     return MPM_OK;

@@ -7,52 +7,69 @@
 
 namespace mpm {
 
-// ---- one forward step (advance()) ------------------------
-// p2g: clear_grid must precede (grid zeroed by the caller).  Writes F_{t+1} into
-// S_next's F slot when S_next != nullptr.
-void launch_p2g(const KParams& p, const float* S, const int32_t* aid, const float* alpha_t,
-                float4* grid, float* S_next, int* flags, cudaStream_t s);
-void launch_grid_op(const KParams& p, const float4* grid, float4* U, cudaStream_t s);
-void launch_g2p(const KParams& p, const float* S, const float4* U, float* S_next, int* flags,
-                cudaStream_t s);
+// particle state: records [n][R] (x, v, C, F) + particle id (global caller index e*N + p)
+struct StateView {
+    float* rec;
+    int* pid;
+};
 
-// ---- one reverse step (advance_grad()) ----------------------------
-void launch_g2p_grad(const KParams& p, const float* S, const float4* U, const float* Sb_next,
-                     float4* Ubar, float* Sb, cudaStream_t s);
-void launch_grid_op_grad(const KParams& p, const float4* grid, const float4* U, const float4* Ubar,
-                         float4* gbar, cudaStream_t s);
-// writes per-block actuation-gradient partials to abar_part[nblocks][n_act]
-void launch_p2g_grad(const KParams& p, const float* S, const int32_t* aid, const float* alpha_t,
-                     const float4* gbar, const float* Sb_next, float* Sb, float* abar_part,
-                     int* flags, cudaStream_t s);
-int p2g_grad_blocks(const KParams& p);
-// alpha_bar_t[a] = sum over blocks (fixed order) of abar_part[b][a]
-void launch_reduce_abar(const KParams& p, const float* abar_part, int nblocks, float* alpha_bar_t,
+// one time step's binning + grid:
+struct SlotView {
+    int* sigma;              // [EN]   sorted order -> index into that step's state array
+    int* blist;              // [max_active]   active block ids (block-id order)
+    int* bstart;             // [max_active+1] start of each block's segment of sigma
+    int* bmap;               // [TB]   block id -> active index, or -1
+    int* nactive;            // [1]
+    unsigned short* cstart;  // [max_active][CELLS+1] cell starts within the block segment
+    float4* tiles;           // [max_active][TN]  (P, M) partial node tiles
+};
+
+cudaError_t tile_init();
+
+// ---- binning (bin_keys only for a fresh sort; g2p emits keys for the next step)
+void launch_bin_keys(const KParams& p, const float* rec, int* keys, int* bcount, int* flags, cudaStream_t s);
+void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* flags, cudaStream_t s);
+void launch_bin_scatter(const KParams& p, const int* keys, int* cursor, int* sigma, cudaStream_t s);
+
+// ---- one forward step (advance())
+// p2g writes F_{t+1} and particle ids of S_{t+1} when Sn.rec / Sn.pid are non-null
+void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
+                const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s);
+// g2p (grid_op fused in its staging) writes x, v, C of S_{t+1}; keys != null -> next bin keys
+void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
+                int* bcount, int* flags, cudaStream_t s);
+
+// ---- one reverse step (advance_grad()); adjoint states are in caller order
+void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const float* Sb_next,
+                     float4* ubar, float* xbar_part, cudaStream_t s);
+void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
+                     const float* alpha_t, const float4* ubar, const float* Sb_next, const float* xbar_part,
+                     float* Sb, float* abar_part, int* flags, cudaStream_t s);
+void launch_reduce_abar(const KParams& p, const int* nactive, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s);
 
-// ---- controller (compute_actuation, P:577 / .grad P:591) ---------------------
+// ---- measurement: distinct grid nodes with M > 0 in a slot's tiles -> *count (device)
+void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s);
+
+// ---- controller (compute_actuation, P:577 / .grad P:591)
 void launch_ctrl_fwd(const KParams& p, const float* theta, int32_t T, float* alpha, cudaStream_t s);
-// per-step parameter-gradient partials, then a fixed-order sum over steps
 void launch_ctrl_bwd(const KParams& p, const float* theta, int32_t T, const float* alpha,
                      const float* alpha_bar, float* theta_part, float* theta_bar, int64_t n_theta,
                      cudaStream_t s);
 
-// ---- loss on S_T and the adjoint seed ----------------------------------------
+// ---- loss on S_T and the adjoint seed (seed written in caller order)
 int loss_blocks_per_episode(const KParams& p);
 void launch_loss(const KParams& p, const float* S, int loss_kind, float3 target, float* com_part,
                  float* loss, float* Sb, int* flags, cudaStream_t s);
-
-// ---- per-episode sum of the v-adjoint of the records: out[E][d] (fixed order)
+// ---- per-episode sum of the v-adjoint of caller-order records: out[E][d] (fixed order)
 void launch_v_sum(const KParams& p, const float* Sb, float* part, float* out, cudaStream_t s);
 
-// ---- measurement: number of grid nodes with M > 0 (all episodes) -> *count (device)
-void launch_count_active(const KParams& p, const float4* grid, int64_t* count, cudaStream_t s);
-
-// ---- layout conversion (caller arrays <-> particle records) ------------------
-// pack: records[E*N][R] from x[E*N][d], v, C[E*N][d][d], F (any may be null -> zero / identity)
+// ---- layout conversion (caller arrays <-> particle records)
+// pack: rec[i] from caller row i (pid[i] = i when pid != null); null inputs -> zero / identity
 void launch_pack(const KParams& p, const float* x, const float* v, const float* C, const float* F,
-                 float* rec, cudaStream_t s);
-void launch_unpack(const KParams& p, const float* rec, float* x, float* v, float* C, float* F,
-                   cudaStream_t s);
+                 float* rec, int* pid, cudaStream_t s);
+// unpack: caller row pid[i] (or i when pid == null) from rec[i]
+void launch_unpack(const KParams& p, const float* rec, const int* pid, float* x, float* v, float* C,
+                   float* F, cudaStream_t s);
 
 }  // namespace mpm

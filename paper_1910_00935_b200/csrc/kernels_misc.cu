@@ -218,9 +218,10 @@ __global__ void k_seed(KParams p, const float* __restrict__ seed, float* __restr
 template <int D>
 __global__ void k_pack(KParams p, const float* __restrict__ x, const float* __restrict__ v,
                        const float* __restrict__ C, const float* __restrict__ F,
-                       float* __restrict__ rec) {
+                       float* __restrict__ rec, int* __restrict__ pid) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= p.N * p.E) return;
+    if (pid) pid[i] = (int)i;
     float* r = rec + i * Rec<D>::R;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -235,11 +236,13 @@ __global__ void k_pack(KParams p, const float* __restrict__ x, const float* __re
 }
 
 template <int D>
-__global__ void k_unpack(KParams p, const float* __restrict__ rec, float* __restrict__ x,
-                         float* __restrict__ v, float* __restrict__ C, float* __restrict__ F) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= p.N * p.E) return;
-    const float* r = rec + i * Rec<D>::R;
+__global__ void k_unpack(KParams p, const float* __restrict__ rec, const int* __restrict__ pidv,
+                         float* __restrict__ x, float* __restrict__ v, float* __restrict__ C,
+                         float* __restrict__ F) {
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i0 >= p.N * p.E) return;
+    const float* r = rec + i0 * Rec<D>::R;
+    const int64_t i = pidv ? (int64_t)pidv[i0] : i0;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         if (x) x[i * D + k] = r[Rec<D>::X + k];
@@ -250,13 +253,6 @@ __global__ void k_unpack(KParams p, const float* __restrict__ rec, float* __rest
         if (C) C[i * D * D + q] = r[Rec<D>::C + q];
         if (F) F[i * D * D + q] = r[Rec<D>::F + q];
     }
-}
-
-__global__ void k_count_active(int64_t n, const float4* __restrict__ grid, unsigned long long* count) {
-    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool act = i < n && grid[i].w > 0.0f;
-    const unsigned b = __ballot_sync(0xffffffffu, act);
-    if ((threadIdx.x & 31) == 0 && b) atomicAdd(count, (unsigned long long)__popc(b));
 }
 
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
@@ -301,12 +297,6 @@ void launch_loss(const KParams& p, const float* S, int loss_kind, float3 target,
     });
 }
 
-void launch_count_active(const KParams& p, const float4* grid, int64_t* count, cudaStream_t s) {
-    const int64_t n = p.nodes * p.E;
-    cudaMemsetAsync(count, 0, sizeof(int64_t), s);
-    k_count_active<<<nblk(n, 256), 256, 0, s>>>(n, grid, (unsigned long long*)count);
-}
-
 void launch_v_sum(const KParams& p, const float* Sb, float* part, float* out, cudaStream_t s) {
     const int nb = loss_blocks_per_episode(p);
     DISPATCH(p.dim, {
@@ -316,13 +306,13 @@ void launch_v_sum(const KParams& p, const float* Sb, float* part, float* out, cu
 }
 
 void launch_pack(const KParams& p, const float* x, const float* v, const float* C, const float* F,
-                 float* rec, cudaStream_t s) {
-    DISPATCH(p.dim, k_pack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, x, v, C, F, rec));
+                 float* rec, int* pid, cudaStream_t s) {
+    DISPATCH(p.dim, k_pack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, x, v, C, F, rec, pid));
 }
 
-void launch_unpack(const KParams& p, const float* rec, float* x, float* v, float* C, float* F,
-                   cudaStream_t s) {
-    DISPATCH(p.dim, k_unpack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, rec, x, v, C, F));
+void launch_unpack(const KParams& p, const float* rec, const int* pid, float* x, float* v, float* C,
+                   float* F, cudaStream_t s) {
+    DISPATCH(p.dim, k_unpack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, rec, pid, x, v, C, F));
 }
 
 }  // namespace mpm

@@ -17,9 +17,28 @@ struct KParams {
     int64_t N;           // particles per episode
     int64_t nodes;       // grid nodes per episode (n_grid^dim)
     int32_t E;           // episodes
+    int32_t nb;          // blocks per axis (ceil(n_grid / B))
+    int32_t nbe;         // blocks per episode (nb^dim)
+    int32_t TB;          // blocks, all episodes (E * nbe)
+    int32_t max_active;  // capacity of the active-block list / tile storage
 };
 
-enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2 };
+enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8 };
+
+// Block geometry of the sorted-tile scheme: particles
+// are binned by the B^d block of cells containing their base cell; a block's
+// particles scatter into a (B+2)^d node tile.
+template <int D> struct Geo {
+    static constexpr int B = D == 3 ? 4 : 8;        // cells per block edge
+    static constexpr int LOGB = D == 3 ? 2 : 3;
+    static constexpr int CELLS = 64;                 // B^d
+    static constexpr int TE = B + 2;                 // tile edge in nodes
+    static constexpr int TN = D == 3 ? 216 : 100;    // tile nodes
+    static constexpr int NST = D == 3 ? 27 : 9;      // stencil offsets
+    static constexpr int NSUB = D == 3 ? 1 : 3;      // particle sub-streams per cell warp
+    static constexpr int ROW = D == 3 ? 24 : 12;     // floats per particle row (cell phase)
+    static constexpr int MAXP = 1728;                // particles per block (27 per cell)
+};
 
 template <int D> struct Rec {
     static constexpr int R = 2 * D + 2 * D * D;  // floats per particle record: x, v, C, F
