@@ -63,7 +63,7 @@ struct mpm_ctx {
     std::vector<StateView> window; // S_{s k + j}, j = 1..k-1
     StateView final_state{};       // S_T
     std::vector<SlotView> slots;   // binning + tiles of step t, slot t % k
-    float* sbar[2] = {nullptr, nullptr};  // adjoint states, caller order
+    AdjView sbar[2] = {};          // adjoint states, indexed like the primal state of their step
     float* staging = nullptr;
     int32_t* aid = nullptr;        // caller order
     int* bcount = nullptr;         // [TB] block histogram (kept zero between uses)
@@ -180,15 +180,25 @@ size_t carve(mpm_ctx* h, char* base) {
         off += align_up(bytes);
         return ptr;
     };
+    const size_t d = h->dim;
     auto state = [&]() {
         StateView s;
-        s.rec = (float*)take(sizeof(float) * sf);
+        s.x = (float*)take(sizeof(float) * EN * d);
+        s.vc = (float*)take(sizeof(float) * EN * (d + d * d));
+        s.f = (float*)take(sizeof(float) * EN * d * d);
         s.pid = (int*)take(sizeof(int) * EN);
+        return s;
+    };
+    auto adj = [&]() {
+        AdjView s;
+        s.x = (float*)take(sizeof(float) * EN * d);
+        s.vc = (float*)take(sizeof(float) * EN * (d + d * d));
+        s.f = (float*)take(sizeof(float) * EN * d * d);
         return s;
     };
     std::vector<StateView> ckpt, window;
     for (int i = 0; i < n_ckpt; ++i) ckpt.push_back(state());
-    for (int i = 0; i < kk; ++i) window.push_back(i == 0 ? StateView{nullptr, nullptr} : state());
+    for (int i = 0; i < kk; ++i) window.push_back(i == 0 ? StateView{nullptr, nullptr, nullptr, nullptr} : state());
     StateView fin = state();
     std::vector<SlotView> slots;
     for (int i = 0; i < kk; ++i) {
@@ -202,8 +212,8 @@ size_t carve(mpm_ctx* h, char* base) {
         s.tiles = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
         slots.push_back(s);
     }
-    float* sb0 = (float*)take(sizeof(float) * sf);
-    float* sb1 = (float*)take(sizeof(float) * sf);
+    AdjView sb0 = adj();
+    AdjView sb1 = adj();
     float* staging = (float*)take(sizeof(float) * sf);
     int32_t* aid = (int32_t*)take(sizeof(int32_t) * EN);
     int* bcount = (int*)take(sizeof(int) * k.TB);
@@ -319,7 +329,7 @@ void bin_fresh(mpm_ctx* h, const KParams& k, int t) {
     const SlotView& sl = slot_at(h, t);
     KScope sc(h, KC_BIN);
     h->launches += 2;
-    launch_bin_keys(k, state_at(h, t).rec, h->keys, h->bcount, h->flags, h->stream);
+    launch_bin_keys(k, state_at(h, t).x, h->keys, h->bcount, h->flags, h->stream);
     launch_bin_scan(k, h->bcount, h->cursor, sl, h->flags, h->stream);
     launch_bin_scatter(k, h->keys, h->cursor, sl.sigma, h->stream);
 }
@@ -328,7 +338,7 @@ void bin_fresh(mpm_ctx* h, const KParams& k, int t) {
 void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin_next) {
     const SlotView& sl = slot_at(h, t);
     const StateView S = state_at(h, t);
-    const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr};
+    const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr, nullptr, nullptr};
     const int32_t* aid = h->has_aid ? h->aid : nullptr;
     { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
     if (!write_next) return;
@@ -344,7 +354,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
 }
 
 // advance_grad() for step t, using the grid tiles stored in slot(t)
-void step_backward(mpm_ctx* h, const KParams& k, int t, const float* Sbn, float* Sb) {
+void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, const AdjView& Sb) {
     const SlotView& sl = slot_at(h, t);
     const StateView S = state_at(h, t);
     const int A = k.n_act > 0 ? k.n_act : 1;
@@ -503,8 +513,8 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
     if (C && (st = copy_in(h, sC, C, sizeof(float) * EN * d * d))) return st;
     if (F && (st = copy_in(h, sF, F, sizeof(float) * EN * d * d))) return st;
     { KScope sc(h, KC_LAYOUT);
-      launch_pack(k, sx, v ? sv : nullptr, C ? sC : nullptr, F ? sF : nullptr, h->ckpt[0].rec, h->ckpt[0].pid,
-                  h->stream); }
+      launch_pack(k, sx, v ? sv : nullptr, C ? sC : nullptr, F ? sF : nullptr, nullptr, h->ckpt[0].x,
+                  h->ckpt[0].vc, h->ckpt[0].f, h->ckpt[0].pid, false, h->stream); }
     h->has_aid = actuator_id != nullptr;
     if (actuator_id && (st = copy_in(h, h->aid, actuator_id, sizeof(int32_t) * EN))) return st;
     CU(cudaGetLastError());
@@ -557,7 +567,7 @@ mpm_status mpm_loss(mpm_handle h, float* loss_out) {
     h->sbar_cur = 0;
     { KScope sc(h, KC_LOSS);
       h->launches += 2;
-      launch_loss(k, state_at(h, h->recorded).rec, h->prm.loss_kind, tgt, h->com_part, h->loss, h->sbar[0],
+      launch_loss(k, state_at(h, h->recorded).x, h->prm.loss_kind, tgt, h->com_part, h->loss, h->sbar[0],
                   h->flags, h->stream); }
     if (loss_out) CU(cudaMemcpyAsync(loss_out, h->loss, sizeof(float) * k.E, cudaMemcpyDefault, h->stream));
     mpm_status st = sync_flags(h, "mpm_loss");
@@ -581,9 +591,11 @@ mpm_status mpm_seed_adjoint(mpm_handle h, const float* dx, const float* dv, cons
     if (dv && (st = copy_in(h, sv, dv, sizeof(float) * EN * d))) return st;
     if (dC && (st = copy_in(h, sC, dC, sizeof(float) * EN * d * d))) return st;
     if (dF && (st = copy_in(h, sF, dF, sizeof(float) * EN * d * d))) return st;
-    if (!dF) CU(cudaMemsetAsync(sF, 0, sizeof(float) * EN * d * d, h->stream));
+    // S_bar_T is indexed like S_T: row i takes the caller's row pid_T[i]
+    const StateView ST = state_at(h, h->recorded);
     { KScope sc(h, KC_LAYOUT);
-      launch_pack(k, dx ? sx : nullptr, dv ? sv : nullptr, dC ? sC : nullptr, sF, h->sbar[0], nullptr, h->stream); }
+      launch_pack(k, dx ? sx : nullptr, dv ? sv : nullptr, dC ? sC : nullptr, dF ? sF : nullptr, ST.pid,
+                  h->sbar[0].x, h->sbar[0].vc, h->sbar[0].f, nullptr, true, h->stream); }
     CU(cudaGetLastError());
     h->sbar_cur = 0;
     h->phase = kSeeded;
@@ -636,7 +648,9 @@ mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF
     float* sF = sC + EN * d * d;
     if (dx0 || dv0 || dC0 || dF0) {
         KScope sc(h, KC_LAYOUT);
-        launch_unpack(k, h->sbar[h->sbar_cur], nullptr, dx0 ? sx : nullptr, dv0 ? sv : nullptr,
+        // S_bar_0 is indexed like S_0, i.e. in caller order
+        const AdjView& B0 = h->sbar[h->sbar_cur];
+        launch_unpack(k, B0.x, B0.vc, B0.f, nullptr, dx0 ? sx : nullptr, dv0 ? sv : nullptr,
                       dC0 ? sC : nullptr, dF0 ? sF : nullptr, h->stream);
     }
     if (dx0) CU(cudaMemcpyAsync(dx0, sx, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
@@ -658,7 +672,7 @@ mpm_status mpm_grad_v0_sum(mpm_handle h, float* out) {
     float* res = h->com_part + (size_t)k.E * (loss_blocks_per_episode(k) + 1) * 3;
     { KScope sc(h, KC_LOSS);
       h->launches += 1;
-      launch_v_sum(k, h->sbar[h->sbar_cur], h->com_part, res, h->stream); }
+      launch_v_sum(k, h->sbar[h->sbar_cur].vc, h->com_part, res, h->stream); }
     CU(cudaMemcpyAsync(out, res, sizeof(float) * k.E * h->dim, cudaMemcpyDefault, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     CU(cudaGetLastError());
@@ -675,7 +689,7 @@ mpm_status mpm_get_state(mpm_handle h, float* x, float* v, float* C, float* F) {
     float* sC = sv + EN * d;
     float* sF = sC + EN * d * d;
     const StateView S = state_at(h, h->recorded);
-    { KScope sc(h, KC_LAYOUT); launch_unpack(k, S.rec, S.pid, sx, sv, sC, sF, h->stream); }
+    { KScope sc(h, KC_LAYOUT); launch_unpack(k, S.x, S.vc, S.f, S.pid, sx, sv, sC, sF, h->stream); }
     if (x) CU(cudaMemcpyAsync(x, sx, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
     if (v) CU(cudaMemcpyAsync(v, sv, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
     if (C) CU(cudaMemcpyAsync(C, sC, sizeof(float) * EN * d * d, cudaMemcpyDefault, h->stream));

@@ -7,10 +7,18 @@
 
 namespace mpm {
 
-// particle state: records [n][R] (x, v, C, F) + particle id (global caller index e*N + p)
+// particle state in split arrays (Lay<D>) + particle id (global caller index e*N + p)
 struct StateView {
-    float* rec;
+    float* x;
+    float* vc;
+    float* f;
     int* pid;
+};
+// adjoint state, same split layout, indexed like the primal state it belongs to
+struct AdjView {
+    float* x;
+    float* vc;
+    float* f;
 };
 
 // one time step's binning + grid:
@@ -27,7 +35,7 @@ struct SlotView {
 cudaError_t tile_init();
 
 // ---- binning (bin_keys only for a fresh sort; g2p emits keys for the next step)
-void launch_bin_keys(const KParams& p, const float* rec, int* keys, int* bcount, int* flags, cudaStream_t s);
+void launch_bin_keys(const KParams& p, const float* x, int* keys, int* bcount, int* flags, cudaStream_t s);
 void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* flags, cudaStream_t s);
 void launch_bin_scatter(const KParams& p, const int* keys, int* cursor, int* sigma, cudaStream_t s);
 
@@ -39,12 +47,12 @@ void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const 
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
                 int* bcount, int* flags, cudaStream_t s);
 
-// ---- one reverse step (advance_grad()); adjoint states are in caller order
-void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const float* Sb_next,
+// ---- one reverse step (advance_grad()); Sbn is indexed like S_{t+1}, Sb like S_t
+void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, float* xbar_part, cudaStream_t s);
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
-                     const float* alpha_t, const float4* ubar, const float* Sb_next, const float* xbar_part,
-                     float* Sb, float* abar_part, int* flags, cudaStream_t s);
+                     const float* alpha_t, const float4* ubar, const AdjView& Sbn, const float* xbar_part,
+                     const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s);
 void launch_reduce_abar(const KParams& p, const int* nactive, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s);
 
@@ -57,19 +65,21 @@ void launch_ctrl_bwd(const KParams& p, const float* theta, int32_t T, const floa
                      const float* alpha_bar, float* theta_part, float* theta_bar, int64_t n_theta,
                      cudaStream_t s);
 
-// ---- loss on S_T and the adjoint seed (seed written in caller order)
+// ---- loss on x_T and the adjoint seed (episodes occupy contiguous index ranges)
 int loss_blocks_per_episode(const KParams& p);
-void launch_loss(const KParams& p, const float* S, int loss_kind, float3 target, float* com_part,
-                 float* loss, float* Sb, int* flags, cudaStream_t s);
-// ---- per-episode sum of the v-adjoint of caller-order records: out[E][d] (fixed order)
-void launch_v_sum(const KParams& p, const float* Sb, float* part, float* out, cudaStream_t s);
+void launch_loss(const KParams& p, const float* x, int loss_kind, float3 target, float* com_part,
+                 float* loss, const AdjView& Sb, int* flags, cudaStream_t s);
+// ---- per-episode sum of the v-adjoint: out[E][d] (fixed order)
+void launch_v_sum(const KParams& p, const float* vc_bar, float* part, float* out, cudaStream_t s);
 
-// ---- layout conversion (caller arrays <-> particle records)
-// pack: rec[i] from caller row i (pid[i] = i when pid != null); null inputs -> zero / identity
+// ---- layout conversion (caller arrays <-> split state arrays)
+// pack: dst row i <- caller row src[i] (src == null: i); ident_pid != null -> ident_pid[i] = i;
+// null x / v / C -> zero, null F -> identity (zero when zero_f)
 void launch_pack(const KParams& p, const float* x, const float* v, const float* C, const float* F,
-                 float* rec, int* pid, cudaStream_t s);
-// unpack: caller row pid[i] (or i when pid == null) from rec[i]
-void launch_unpack(const KParams& p, const float* rec, const int* pid, float* x, float* v, float* C,
-                   float* F, cudaStream_t s);
+                 const int* src, float* dx, float* dvc, float* df, int* ident_pid, bool zero_f,
+                 cudaStream_t s);
+// unpack: caller row dst[i] (dst == null: i) <- row i
+void launch_unpack(const KParams& p, const float* sx, const float* svc, const float* sf, const int* dst,
+                   float* x, float* v, float* C, float* F, cudaStream_t s);
 
 }  // namespace mpm

@@ -97,9 +97,11 @@ __global__ void k_ctrl_reduce(const float* __restrict__ part, int T, int64_t n_t
 // ---------------------------------------------------------------- loss
 constexpr int kLossThreads = 256;
 
-// partial sums of m x over a contiguous particle chunk (fixed tree order)
+// partial sums of a d-vector field over a contiguous particle chunk (fixed tree order);
+// field row i = base[i * stride + k]
 template <int D>
-__global__ void k_com_partial(KParams p, const float* __restrict__ S, float* __restrict__ part) {
+__global__ void k_sum_partial(KParams p, const float* __restrict__ base, int stride,
+                              float* __restrict__ part) {
     __shared__ float red[D][kLossThreads];
     const int e = blockIdx.y, nb = gridDim.x;
     const int64_t chunk = (p.N + nb - 1) / nb;
@@ -108,38 +110,9 @@ __global__ void k_com_partial(KParams p, const float* __restrict__ S, float* __r
 #pragma unroll
     for (int k = 0; k < D; ++k) acc[k] = 0.0f;
     for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const float* r = S + ((int64_t)e * p.N + i) * Rec<D>::R;
+        const float* r = base + ((int64_t)e * p.N + i) * stride;
 #pragma unroll
-        for (int k = 0; k < D; ++k) acc[k] += r[Rec<D>::X + k];
-    }
-#pragma unroll
-    for (int k = 0; k < D; ++k) red[k][threadIdx.x] = acc[k];
-    __syncthreads();
-    for (int s = kLossThreads / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s)
-#pragma unroll
-            for (int k = 0; k < D; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0)
-#pragma unroll
-        for (int k = 0; k < D; ++k) part[((int64_t)e * nb + blockIdx.x) * D + k] = red[k][0];
-}
-
-// partial sums of the v slot of adjoint records (same chunking as k_com_partial)
-template <int D>
-__global__ void k_vsum_partial(KParams p, const float* __restrict__ Sb, float* __restrict__ part) {
-    __shared__ float red[D][kLossThreads];
-    const int e = blockIdx.y, nb = gridDim.x;
-    const int64_t chunk = (p.N + nb - 1) / nb;
-    const int64_t lo = blockIdx.x * chunk, hi = min(p.N, lo + chunk);
-    float acc[D];
-#pragma unroll
-    for (int k = 0; k < D; ++k) acc[k] = 0.0f;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const float* r = Sb + ((int64_t)e * p.N + i) * Rec<D>::R;
-#pragma unroll
-        for (int k = 0; k < D; ++k) acc[k] += r[Rec<D>::V + k];
+        for (int k = 0; k < D; ++k) acc[k] += r[k];
     }
 #pragma unroll
     for (int k = 0; k < D; ++k) red[k][threadIdx.x] = acc[k];
@@ -203,55 +176,57 @@ __global__ void k_loss_final(KParams p, const float* __restrict__ part, int nb, 
 }
 
 template <int D>
-__global__ void k_seed(KParams p, const float* __restrict__ seed, float* __restrict__ Sb) {
+__global__ void k_seed(KParams p, const float* __restrict__ seed, AdjView Sb) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= p.N * p.E) return;
     const int64_t e = i / p.N;
-    float* r = Sb + i * Rec<D>::R;
 #pragma unroll
-    for (int k = 0; k < D; ++k) r[Rec<D>::X + k] = seed[e * D + k];
+    for (int k = 0; k < D; ++k) Sb.x[i * D + k] = seed[e * D + k];
 #pragma unroll
-    for (int q = Rec<D>::V; q < Rec<D>::R; ++q) r[q] = 0.0f;
+    for (int q = 0; q < Lay<D>::VC; ++q) Sb.vc[i * Lay<D>::VC + q] = 0.0f;
+#pragma unroll
+    for (int q = 0; q < Lay<D>::FF; ++q) Sb.f[i * Lay<D>::FF + q] = 0.0f;
 }
 
 // ------------------------------------------------------------- layout
 template <int D>
 __global__ void k_pack(KParams p, const float* __restrict__ x, const float* __restrict__ v,
                        const float* __restrict__ C, const float* __restrict__ F,
-                       float* __restrict__ rec, int* __restrict__ pid) {
+                       const int* __restrict__ src, float* __restrict__ dx, float* __restrict__ dvc,
+                       float* __restrict__ df, int* __restrict__ ident_pid, bool zero_f) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= p.N * p.E) return;
-    if (pid) pid[i] = (int)i;
-    float* r = rec + i * Rec<D>::R;
+    if (ident_pid) ident_pid[i] = (int)i;
+    const int64_t s = src ? (int64_t)src[i] : i;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        r[Rec<D>::X + k] = x ? x[i * D + k] : 0.0f;
-        r[Rec<D>::V + k] = v ? v[i * D + k] : 0.0f;
+        dx[i * D + k] = x ? x[s * D + k] : 0.0f;
+        dvc[i * Lay<D>::VC + k] = v ? v[s * D + k] : 0.0f;
     }
 #pragma unroll
     for (int q = 0; q < D * D; ++q) {
-        r[Rec<D>::C + q] = C ? C[i * D * D + q] : 0.0f;
-        r[Rec<D>::F + q] = F ? F[i * D * D + q] : ((q % (D + 1)) == 0 ? 1.0f : 0.0f);
+        dvc[i * Lay<D>::VC + D + q] = C ? C[s * D * D + q] : 0.0f;
+        df[i * Lay<D>::FF + q] = F ? F[s * D * D + q] : ((!zero_f && (q % (D + 1)) == 0) ? 1.0f : 0.0f);
     }
 }
 
 template <int D>
-__global__ void k_unpack(KParams p, const float* __restrict__ rec, const int* __restrict__ pidv,
+__global__ void k_unpack(KParams p, const float* __restrict__ sx, const float* __restrict__ svc,
+                         const float* __restrict__ sf, const int* __restrict__ dst,
                          float* __restrict__ x, float* __restrict__ v, float* __restrict__ C,
                          float* __restrict__ F) {
-    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i0 >= p.N * p.E) return;
-    const float* r = rec + i0 * Rec<D>::R;
-    const int64_t i = pidv ? (int64_t)pidv[i0] : i0;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= p.N * p.E) return;
+    const int64_t o = dst ? (int64_t)dst[i] : i;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        if (x) x[i * D + k] = r[Rec<D>::X + k];
-        if (v) v[i * D + k] = r[Rec<D>::V + k];
+        if (x) x[o * D + k] = sx[i * D + k];
+        if (v) v[o * D + k] = svc[i * Lay<D>::VC + k];
     }
 #pragma unroll
     for (int q = 0; q < D * D; ++q) {
-        if (C) C[i * D * D + q] = r[Rec<D>::C + q];
-        if (F) F[i * D * D + q] = r[Rec<D>::F + q];
+        if (C) C[o * D * D + q] = svc[i * Lay<D>::VC + D + q];
+        if (F) F[o * D * D + q] = sf[i * Lay<D>::FF + q];
     }
 }
 
@@ -286,33 +261,35 @@ int loss_blocks_per_episode(const KParams& p) {
     return (int)(nb < 1 ? 1 : (nb > 512 ? 512 : nb));
 }
 
-void launch_loss(const KParams& p, const float* S, int loss_kind, float3 target, float* com_part,
-                 float* loss, float* Sb, int* flags, cudaStream_t s) {
+void launch_loss(const KParams& p, const float* x, int loss_kind, float3 target, float* com_part,
+                 float* loss, const AdjView& Sb, int* flags, cudaStream_t s) {
     const int nb = loss_blocks_per_episode(p);
     float* seed = com_part + (int64_t)p.E * nb * p.dim;
     DISPATCH(p.dim, {
-        k_com_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, S, com_part);
+        k_sum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, x, DIM, com_part);
         k_loss_final<DIM><<<p.E, 32, 0, s>>>(p, com_part, nb, loss_kind, target, loss, seed, flags);
         k_seed<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, seed, Sb);
     });
 }
 
-void launch_v_sum(const KParams& p, const float* Sb, float* part, float* out, cudaStream_t s) {
+void launch_v_sum(const KParams& p, const float* vc_bar, float* part, float* out, cudaStream_t s) {
     const int nb = loss_blocks_per_episode(p);
     DISPATCH(p.dim, {
-        k_vsum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, Sb, part);
+        k_sum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, vc_bar, Lay<DIM>::VC, part);
         k_sum_parts<DIM><<<p.E, 32, 0, s>>>(part, nb, out);
     });
 }
 
 void launch_pack(const KParams& p, const float* x, const float* v, const float* C, const float* F,
-                 float* rec, int* pid, cudaStream_t s) {
-    DISPATCH(p.dim, k_pack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, x, v, C, F, rec, pid));
+                 const int* src, float* dx, float* dvc, float* df, int* ident_pid, bool zero_f,
+                 cudaStream_t s) {
+    DISPATCH(p.dim, k_pack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, x, v, C, F, src, dx, dvc, df,
+                                                                     ident_pid, zero_f));
 }
 
-void launch_unpack(const KParams& p, const float* rec, const int* pid, float* x, float* v, float* C,
-                   float* F, cudaStream_t s) {
-    DISPATCH(p.dim, k_unpack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, rec, pid, x, v, C, F));
+void launch_unpack(const KParams& p, const float* sx, const float* svc, const float* sf, const int* dst,
+                   float* x, float* v, float* C, float* F, cudaStream_t s) {
+    DISPATCH(p.dim, k_unpack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, sx, svc, sf, dst, x, v, C, F));
 }
 
 }  // namespace mpm

@@ -5,36 +5,27 @@
 //
 // Layout:
 //  * particles are binned every step by the B^d block of cells that holds their
-//    base cell (bin_* kernels); the block's list sigma (indices into the state
-//    array) is put in canonical (cell, particle id) order by p2g, so every sum
-//    below has a fixed order -> bitwise run-to-run reproducible, no atomics in
-//    the hot loops;
-//  * p2g: one CTA per active block (persistent loop).  Thread-per-particle
-//    stress/affine math in registers, then a warp per cell with one lane per
-//    stencil offset o sums the cell's contributions to node (cell + o) (smem
-//    broadcast reads, no atomics), then a thread per tile node sums the <= 3^d
-//    (cell, o) partials and stores the block's (B+2)^d tile with plain stores;
-//  * g2p / g2p_grad / p2g_grad stage their node tile in shared memory by summing
-//    the <= 2^d overlapping block tiles, fusing grid_op (or grid_op_grad) into
-//    the staging; g2p_grad scatters U_bar with the same cell/offset scheme.
+//    base cell (bin_* kernels); p2g puts each block's list sigma in canonical
+//    (cell, particle id) order, so every sum below has a fixed order -> results are
+//    bitwise reproducible run to run, and there are no atomics in the hot loops;
+//  * p2g: one CTA per active block (persistent loop).  Thread per particle: the
+//    stress/affine math in registers, producing a 24-float row [wy*wz, c, A dx, wx]
+//    in shared memory; then a thread per (cell, o_x) walks the cell's rows and
+//    accumulates its 3^(d-1) nodes in registers (separable weights, incremental
+//    m = c + A dx o); a thread per tile node sums the <= 3^d (cell, o) partials and
+//    stores the block's (B+2)^d node tile with plain stores;
+//  * g2p / g2p_grad / p2g_grad stage their node tile in shared memory by summing the
+//    <= 2^d overlapping block tiles (grid_op / grid_op_grad fused into the staging);
+//    g2p uses nested separable sums for v and the first moments that give C;
+//    g2p_grad scatters U_bar with p2g's (cell, o_x) scheme.
 #include "kernels.h"
 
 namespace mpm {
 
 namespace {
 
-constexpr int kT = 256;             // threads per CTA (8 warps)
+constexpr int kT = 256;  // threads per CTA (8 warps)
 constexpr int kW = kT / 32;
-
-template <int D> __device__ __forceinline__ void load_rec(const float* __restrict__ src, float* r) {
-    constexpr int R = Rec<D>::R;
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-#pragma unroll
-    for (int q = 0; q < R / 4; ++q) {
-        float4 t = __ldg(s4 + q);
-        r[4 * q + 0] = t.x; r[4 * q + 1] = t.y; r[4 * q + 2] = t.z; r[4 * q + 3] = t.w;
-    }
-}
 
 // block id -> episode and first cell (c0 = block coords * B)
 template <int D>
@@ -71,6 +62,17 @@ template <int D> __device__ __forceinline__ int tile_lin(int a, int b, int c) {
     return D == 2 ? a * TE + b : (a * TE + b) * TE + c;
 }
 
+template <int D> __device__ __forceinline__ void local_node(int q, int n[3]) {
+    constexpr int TE = Geo<D>::TE;
+    if (D == 2) { n[0] = q / TE; n[1] = q % TE; n[2] = 0; }
+    else { n[0] = q / (TE * TE); n[1] = (q / TE) % TE; n[2] = q % TE; }
+}
+
+template <int D> __device__ __forceinline__ int cell_of(const int lb[3]) {
+    using G = Geo<D>;
+    return D == 2 ? lb[0] * G::B + lb[1] : (lb[0] * G::B + lb[1]) * G::B + lb[2];
+}
+
 // Sum of the <= 2^d block tiles that cover global node g (episode e): every
 // block whose cells [c0, c0 + B) satisfy c0 <= g < c0 + B + 2 holds a partial
 // of that node.  Fixed enumeration order -> deterministic.
@@ -79,25 +81,30 @@ __device__ __forceinline__ float4 covered_sum(const KParams& p, int e, const int
                                               const int* __restrict__ bmap,
                                               const float4* __restrict__ tiles) {
     using G = Geo<D>;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int blk[3][2], loc[3][2], cnt[3];
+    // per axis: option 0 = the block holding g (local l0), option 1 = the previous
+    // block (local l0 + B), valid when l0 < 2.  All 2^d combinations unrolled.
+    int b0[3], l0[3];
+    bool ok1[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        if (k >= D) { blk[k][0] = 0; loc[k][0] = 0; cnt[k] = 1; continue; }
-        const int b0 = g[k] >> G::LOGB, l0 = g[k] & (G::B - 1);
-        blk[k][0] = b0; loc[k][0] = l0; cnt[k] = 1;
-        if (l0 < 2 && b0 >= 1) { blk[k][1] = b0 - 1; loc[k][1] = l0 + G::B; cnt[k] = 2; }
-        else { blk[k][1] = b0; loc[k][1] = l0; }
-        if (b0 >= p.nb) cnt[k] = 0;  // node beyond the last block (never read)
+        b0[k] = k < D ? g[k] >> G::LOGB : 0;
+        l0[k] = k < D ? g[k] & (G::B - 1) : 0;
+        ok1[k] = k < D && l0[k] < 2 && b0[k] >= 1;
     }
-    for (int a = 0; a < cnt[0]; ++a)
-        for (int b = 0; b < cnt[1]; ++b)
-            for (int c = 0; c < cnt[2]; ++c) {
-                const int bb[3] = {blk[0][a], blk[1][b], blk[2][c]};
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < (D == 3 ? 2 : 1); ++c) {
+                if ((a && !ok1[0]) || (b && !ok1[1]) || (c && !ok1[2])) continue;
+                const int bb[3] = {b0[0] - a, b0[1] - b, b0[2] - c};
                 if (bb[0] >= p.nb || bb[1] >= p.nb || (D == 3 && bb[2] >= p.nb)) continue;
                 const int ti = __ldg(bmap + block_lin<D>(p, e, bb));
                 if (ti < 0) continue;
-                const float4 v = __ldg(tiles + (int64_t)ti * G::TN + tile_lin<D>(loc[0][a], loc[1][b], loc[2][c]));
+                const int lq = tile_lin<D>(l0[0] + a * G::B, l0[1] + b * G::B, l0[2] + c * G::B);
+                const float4 v = __ldg(tiles + (int64_t)ti * G::TN + lq);
                 acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
             }
     return acc;
@@ -119,12 +126,6 @@ __device__ __forceinline__ bool grid_velocity(const KParams& p, const int g[3], 
     return z;
 }
 
-template <int D> __device__ __forceinline__ void local_node(int q, int n[3]) {
-    constexpr int TE = Geo<D>::TE;
-    if (D == 2) { n[0] = q / TE; n[1] = q % TE; n[2] = 0; }
-    else { n[0] = q / (TE * TE); n[1] = (q / TE) % TE; n[2] = q % TE; }
-}
-
 // warp-aggregated histogram increment (keys in a warp are mostly equal)
 __device__ __forceinline__ void count_key(bool valid, int key, int* bcount) {
     const unsigned peers = __match_any_sync(0xffffffffu, valid ? key : -1);
@@ -132,79 +133,124 @@ __device__ __forceinline__ void count_key(bool valid, int key, int* bcount) {
     if (valid && (int)(threadIdx.x & 31) == leader) atomicAdd(&bcount[key], __popc(peers));
 }
 
+// weights and base of a particle relative to the block origin
+template <int D>
+__device__ __forceinline__ void particle_weights(const KParams& p, const float* x, const int c0[3], int lb[3],
+                                                 float fx[3], float w[3][3], float dw[3][3]) {
+    lb[2] = 0;
+    fx[2] = 0.f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const float xi = x[k] * p.inv_dx;
+        const float b = floorf(xi - 0.5f);
+        fx[k] = xi - b;
+        lb[k] = (int)b - c0[k];
+        bspline(fx[k], w[k], dw[k]);
+    }
+}
+
 // ---------------------------------------------------------------- binning
 template <int D>
-__global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restrict__ rec,
+__global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restrict__ X,
                                                  int* __restrict__ keys, int* __restrict__ bcount,
                                                  int* flags) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool in = i < p.N * p.E;
     int key = 0;
-    bool ok = false;
     if (in) {
         float x[3];
 #pragma unroll
-        for (int k = 0; k < D; ++k) x[k] = rec[i * Rec<D>::R + Rec<D>::X + k];
+        for (int k = 0; k < D; ++k) x[k] = X[i * D + k];
         int b[3];
-        ok = base_cell<D>(p, x, b);
+        const bool ok = base_cell<D>(p, x, b);
         const int e = (int)(i / p.N);
         int bb[3] = {b[0] >> Geo<D>::LOGB, b[1] >> Geo<D>::LOGB, b[2] >> Geo<D>::LOGB};
         key = block_lin<D>(p, e, bb);
-        if (!ok) { atomicOr(flags, FLAG_OUT_OF_DOMAIN); key = e * p.nbe; ok = true; }
+        if (!ok) { atomicOr(flags, FLAG_OUT_OF_DOMAIN); key = e * p.nbe; }
         keys[i] = key;
     }
-    count_key(in && ok, key, bcount);
+    count_key(in, key, bcount);
 }
 
 // single CTA: exclusive scan of the dense block histogram -> active block list
 // (block-id order), starts, block map, scatter cursors; clears the histogram.
+// Rounds of 1024 x 16 entries, loads issued together (latency, not bandwidth, bound).
 constexpr int kScanT = 1024;
+constexpr int kScanPer = 16;
 __global__ void __launch_bounds__(kScanT) k_bin_scan(KParams p, int* __restrict__ bcount,
                                                      int* __restrict__ cursor, SlotView sl, int* flags) {
-    __shared__ int s_part[kScanT], s_act[kScanT];
-    const int TB = p.TB, tid = threadIdx.x;
-    const int per = (TB + kScanT - 1) / kScanT;
-    const int lo = min(TB, tid * per), hi = min(TB, lo + per);
-    int tot = 0, act = 0;
-    for (int b = lo; b < hi; ++b) {
-        const int c = bcount[b];
-        tot += c;
-        act += c > 0;
-    }
-    s_part[tid] = tot;
-    s_act[tid] = act;
+    __shared__ int s_wt[32], s_wa[32];
+    __shared__ int s_carry[2];
+    const int TB = p.TB, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) { s_carry[0] = 0; s_carry[1] = 0; }
     __syncthreads();
-    for (int off = 1; off < kScanT; off <<= 1) {  // Hillis-Steele inclusive scan
-        int a = tid >= off ? s_part[tid - off] : 0, b = tid >= off ? s_act[tid - off] : 0;
+    for (int base = 0; base < TB; base += kScanT * kScanPer) {
+        const int i0 = base + tid * kScanPer;
+        int c[kScanPer];
+        if (i0 + kScanPer <= TB) {
+#pragma unroll
+            for (int q = 0; q < kScanPer / 4; ++q) {
+                const int4 v = *reinterpret_cast<const int4*>(bcount + i0 + 4 * q);
+                c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < kScanPer; ++q) c[q] = i0 + q < TB ? bcount[i0 + q] : 0;
+        }
+        int tot = 0, act = 0;
+#pragma unroll
+        for (int q = 0; q < kScanPer; ++q) { tot += c[q]; act += c[q] > 0; }
+        // block exclusive scan of (tot, act)
+        int it = tot, ia = act;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int a = __shfl_up_sync(0xffffffffu, it, off), b = __shfl_up_sync(0xffffffffu, ia, off);
+            if (lane >= off) { it += a; ia += b; }
+        }
+        if (lane == 31) { s_wt[warp] = it; s_wa[warp] = ia; }
         __syncthreads();
-        s_part[tid] += a;
-        s_act[tid] += b;
+        if (warp == 0) {
+            int wt = s_wt[lane], wa = s_wa[lane];
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int a = __shfl_up_sync(0xffffffffu, wt, off), b = __shfl_up_sync(0xffffffffu, wa, off);
+                if (lane >= off) { wt += a; wa += b; }
+            }
+            s_wt[lane] = wt;
+            s_wa[lane] = wa;
+        }
         __syncthreads();
-    }
-    int pos = s_part[tid] - tot, li = s_act[tid] - act;
-    for (int b = lo; b < hi; ++b) {
-        const int c = bcount[b];
-        if (c > 0) {
-            if (li < p.max_active) {
-                sl.blist[li] = b;
-                sl.bstart[li] = pos;
-                sl.bmap[b] = li;
+        int pos = s_carry[0] + (warp ? s_wt[warp - 1] : 0) + it - tot;
+        int li = s_carry[1] + (warp ? s_wa[warp - 1] : 0) + ia - act;
+#pragma unroll
+        for (int q = 0; q < kScanPer; ++q) {
+            const int b = i0 + q;
+            if (b >= TB) break;
+            if (c[q] > 0) {
+                if (li < p.max_active) {
+                    sl.blist[li] = b;
+                    sl.bstart[li] = pos;
+                    sl.bmap[b] = li;
+                } else {
+                    sl.bmap[b] = -1;
+                    atomicOr(flags, FLAG_ACTIVE_OVERFLOW);
+                }
+                cursor[b] = pos;
+                pos += c[q];
+                ++li;
+                bcount[b] = 0;
             } else {
                 sl.bmap[b] = -1;
-                atomicOr(flags, FLAG_ACTIVE_OVERFLOW);
             }
-            cursor[b] = pos;
-            pos += c;
-            ++li;
-        } else {
-            sl.bmap[b] = -1;
         }
-        bcount[b] = 0;
+        __syncthreads();
+        if (tid == kScanT - 1) { s_carry[0] = pos; s_carry[1] = li; }
+        __syncthreads();
     }
-    if (tid == kScanT - 1) {
-        const int n = min(li, p.max_active);
+    if (tid == 0) {
+        const int n = min(s_carry[1], p.max_active);
         *sl.nactive = n;
-        sl.bstart[n] = min(pos, (int)(p.N * p.E));
+        sl.bstart[n] = min(s_carry[0], (int)(p.N * p.E));
     }
 }
 
@@ -221,59 +267,53 @@ __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __rest
     if (in) sigma[base + __popc(peers & ((1u << lane) - 1u))] = (int)j;
 }
 
-// ---------------------------------------------------------------- P2G
-template <int D> constexpr int p2g_phase0_bytes() {
-    return Geo<D>::MAXP * 14 > kT * Geo<D>::ROW * 4 ? Geo<D>::MAXP * 14 : kT * Geo<D>::ROW * 4;
-}
-template <int D> constexpr int p2g_smem_bytes() {
-    return p2g_phase0_bytes<D>() + Geo<D>::CELLS * Geo<D>::NST * 16 + 2 * (Geo<D>::CELLS + 2) * 4;
-}
-
-// fold sub-streams: every lane of the warp must call (2D only)
-template <int D> __device__ __forceinline__ float4 fold_subs(float4 a) {
-    using G = Geo<D>;
-    if (G::NSUB == 1) return a;
-    float4 r = a;
+// ----------------------------------------------------- cell accumulation
+// A thread owns one cell and sums, over the cell's particles (canonical order), the
+// contributions W_o (c + A o) (and W_o when MASS) to the 3^d nodes cell + o, in
+// registers: separable weights W_o = wx[ox] wy[oy] wz[oz] and an incremental
+// m = c + A o.  (p2g: c = m v - A dx f, A = A dx;  g2p_grad: c = vh - B f, A = B.)
+template <int D, bool MASS> struct NodeAcc {
+    static constexpr int NN = Geo<D>::NST;
+    float4 a[NN];  // o = (ox*3 + oy)*3 + oz (3D) / ox*3 + oy (2D)
+    __device__ __forceinline__ void zero() {
 #pragma unroll
-    for (int s = 1; s < G::NSUB; ++s) {
-        r.x += __shfl_down_sync(0xffffffffu, a.x, s * G::NST);
-        r.y += __shfl_down_sync(0xffffffffu, a.y, s * G::NST);
-        r.z += __shfl_down_sync(0xffffffffu, a.z, s * G::NST);
-        r.w += __shfl_down_sync(0xffffffffu, a.w, s * G::NST);
+        for (int k = 0; k < NN; ++k) a[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    return r;
-}
-
-template <int D, bool MASS>
-__device__ __forceinline__ float4 cell_rows(const float* __restrict__ s_tab, int lo, int hi, int lane) {
-    using G = Geo<D>;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (lane < G::NST * G::NSUB) {
-        const int o = lane % G::NST, sub = lane / G::NST;
-        const int ox = D == 3 ? o / 9 : o / 3, oy = D == 3 ? (o / 3) % 3 : o % 3, oz = D == 3 ? o % 3 : 0;
-        const float fo[3] = {(float)ox, (float)oy, (float)oz};
-        for (int r = lo + sub; r < hi; r += G::NSUB) {
-            const float* row = s_tab + r * G::ROW;
-            float W = row[ox] * row[3 + oy];
-            if (D == 3) W *= row[6 + oz];
-            const float* c = row + 3 * D;
-            const float* A = c + D;
-            float m[3] = {0.f, 0.f, 0.f};
+    __device__ __forceinline__ void add(const float w[3][3], const float* c, const float* A) {
 #pragma unroll
-            for (int a = 0; a < D; ++a) {
-                float s = c[a];
+        for (int ox = 0; ox < 3; ++ox) {
+            float mx[3];
 #pragma unroll
-                for (int b = 0; b < D; ++b) s = fmaf(A[a * D + b], fo[b], s);
-                m[a] = s;
+            for (int q = 0; q < D; ++q) mx[q] = fmaf((float)ox, A[q * D], c[q]);
+#pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+                const float Wxy = w[0][ox] * w[1][oy];
+                float my[3];
+#pragma unroll
+                for (int q = 0; q < D; ++q) my[q] = fmaf((float)oy, A[q * D + 1], mx[q]);
+#pragma unroll
+                for (int oz = 0; oz < (D == 3 ? 3 : 1); ++oz) {
+                    const float W = D == 3 ? Wxy * w[2][oz] : Wxy;
+                    float4& acc = a[D == 3 ? (ox * 3 + oy) * 3 + oz : ox * 3 + oy];
+                    if (D == 3) {
+                        acc.x = fmaf(W, fmaf((float)oz, A[2], my[0]), acc.x);
+                        acc.y = fmaf(W, fmaf((float)oz, A[5], my[1]), acc.y);
+                        acc.z = fmaf(W, fmaf((float)oz, A[8], my[2]), acc.z);
+                    } else {
+                        acc.x = fmaf(W, my[0], acc.x);
+                        acc.y = fmaf(W, my[1], acc.y);
+                    }
+                    if (MASS) acc.w += W;
+                }
             }
-            acc.x = fmaf(W, m[0], acc.x);
-            acc.y = fmaf(W, m[1], acc.y);
-            if (D == 3) acc.z = fmaf(W, m[2], acc.z);
-            if (MASS) acc.w += W;
         }
     }
-    return fold_subs<D>(acc);
-}
+    __device__ __forceinline__ void store(float4* cellbuf, int cell) const {
+        float4* dst = cellbuf + cell * NN;
+#pragma unroll
+        for (int k = 0; k < NN; ++k) dst[k] = a[k];
+    }
+};
 
 // thread per tile node: sum the (cell, o) partials with cell + o = node (fixed order)
 template <int D>
@@ -300,30 +340,67 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
     return s;
 }
 
-template <int D> __device__ __forceinline__ int cell_of(const int lb[3]) {
-    using G = Geo<D>;
-    return D == 2 ? lb[0] * G::B + lb[1] : (lb[0] * G::B + lb[1]) * G::B + lb[2];
+constexpr int kTC = 64;  // thread-per-cell kernels: one thread per cell of a block (CELLS = 64)
+
+template <int D> constexpr int p2g_union_bytes() {
+    return Geo<D>::MAXP * 14 > Geo<D>::CELLS * Geo<D>::NST * 16 ? Geo<D>::MAXP * 14
+                                                                 : Geo<D>::CELLS * Geo<D>::NST * 16;
+}
+template <int D> constexpr int p2g_smem_bytes() { return p2g_union_bytes<D>() + 2 * (Geo<D>::CELLS + 2) * 4; }
+
+// per-particle p2g math: returns c = m v - A dx f and A dx (for NodeAcc) and Ft
+template <int D>
+__device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, const float* vc, const float* F,
+                                             float act, const int c0[3], float w[3][3], float* c, float* Adx,
+                                             float* Ft) {
+    const float* v = vc;
+    const float* C = vc + D;
+    int lb[3];
+    float fx[3], dw[3][3];
+    particle_weights<D>(p, x, c0, lb, fx, w, dw);
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+            float s = 0.0f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fmaf(C[a * D + k], F[k * D + b], s);
+            Ft[a * D + b] = fmaf(p.dt, s, F[a * D + b]);
+        }
+    float tau[D * D];
+    const bool ok = kirchhoff<D>(p, Ft, act, tau);
+#pragma unroll
+    for (int q = 0; q < D * D; ++q) Adx[q] = p.dx * fmaf(p.stress_scale, tau[q], p.p_mass * C[q]);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        float s = p.p_mass * v[a];
+#pragma unroll
+        for (int b = 0; b < D; ++b) s = fmaf(-Adx[a * D + b], fx[b], s);
+        c[a] = s;
+    }
+    return ok;
 }
 
+// ---------------------------------------------------------------- P2G
 // p2g: canonicalise the block list, then per particle
 // Ft = (I + dt C) F; tau = tau(Ft) [+ actuation]; A = -dt V 4/dx^2 tau + m C;
 // node b+o receives W_o (m v + A (o - f) dx) and W_o m.  F_{t+1} = Ft.
+// CTA = 64 threads = one thread per cell of the block (persistent over blocks).
 template <int D>
-__global__ void __launch_bounds__(kT) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
-                                            const int32_t* __restrict__ aid,
-                                            const float* __restrict__ alpha, int* flags) {
+__global__ void __launch_bounds__(kTC, 6) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
+                                               const int32_t* __restrict__ aid,
+                                               const float* __restrict__ alpha, int* flags) {
     using G = Geo<D>;
-    using RC = Rec<D>;
+    using L = Lay<D>;
     extern __shared__ __align__(16) unsigned char smem[];
-    float* s_tab = reinterpret_cast<float*>(smem);
     int* s_idx = reinterpret_cast<int*>(smem);
     int* s_pid = s_idx + G::MAXP;
     int* s_tmp = s_pid + G::MAXP;
     short* s_cell = reinterpret_cast<short*>(s_tmp + G::MAXP);
-    float4* s_cb = reinterpret_cast<float4*>(smem + p2g_phase0_bytes<D>());
-    int* s_cnt = reinterpret_cast<int*>(s_cb + G::CELLS * G::NST);
+    float4* s_cb = reinterpret_cast<float4*>(smem);  // aliases the phase-0 arrays
+    int* s_cnt = reinterpret_cast<int*>(smem + p2g_union_bytes<D>());
     int* s_cst = s_cnt + G::CELLS + 2;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
     const int nact = *sl.nactive;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         const int bid = sl.blist[bi];
@@ -335,9 +412,9 @@ __global__ void __launch_bounds__(kT) k_p2g(KParams p, SlotView sl, StateView S,
             continue;
         }
         // ---- phase 0: cells, then canonical (cell, particle id) order
-        for (int q = tid; q < G::CELLS + 2; q += kT) s_cnt[q] = 0;
+        for (int q = tid; q < G::CELLS + 2; q += kTC) s_cnt[q] = 0;
         __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kT) {
+        for (int q0 = 0; q0 < n; q0 += kTC) {
             const int q = q0 + tid;
             const bool in = q < n;
             int cell = G::CELLS;
@@ -345,7 +422,7 @@ __global__ void __launch_bounds__(kT) k_p2g(KParams p, SlotView sl, StateView S,
                 const int i = sl.sigma[start + q];
                 float x[3];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = S.rec[(int64_t)i * RC::R + RC::X + k];
+                for (int k = 0; k < D; ++k) x[k] = S.x[(int64_t)i * D + k];
                 int b[3];
                 bool ok = base_cell<D>(p, x, b);
                 int lb[3] = {0, 0, 0};
@@ -364,18 +441,24 @@ __global__ void __launch_bounds__(kT) k_p2g(KParams p, SlotView sl, StateView S,
             if (in && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[cell], __popc(peers));
         }
         __syncthreads();
-        if (tid == 0) {
-            int run = 0;
-            for (int c = 0; c <= G::CELLS; ++c) {
-                s_cst[c] = run;
-                const int k = s_cnt[c];
-                s_cnt[c] = run;  // becomes the bucket cursor
-                run += k;
+        if (tid < 32) {  // exclusive scan of the 65 bucket counts (one warp)
+            int carry = 0;
+            for (int b0 = 0; b0 <= G::CELLS; b0 += 32) {
+                const int c = b0 + lane;
+                const int v = c <= G::CELLS ? s_cnt[c] : 0;
+                int inc = v;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, inc, off);
+                    if (lane >= off) inc += t;
+                }
+                if (c <= G::CELLS) { s_cst[c] = carry + inc - v; s_cnt[c] = carry + inc - v; }
+                carry += __shfl_sync(0xffffffffu, inc, 31);
             }
-            s_cst[G::CELLS + 1] = run;
+            if (lane == 0) s_cst[G::CELLS + 1] = carry;
         }
         __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kT) {  // bucket by cell (order inside a cell arbitrary)
+        for (int q0 = 0; q0 < n; q0 += kTC) {  // bucket by cell (order inside a cell arbitrary)
             const int q = q0 + tid;
             const bool in = q < n;
             const int cell = in ? s_cell[q] : -1;
@@ -387,7 +470,7 @@ __global__ void __launch_bounds__(kT) k_p2g(KParams p, SlotView sl, StateView S,
             if (in) s_tmp[base + __popc(peers & ((1u << lane) - 1u))] = q;
         }
         __syncthreads();
-        for (int r = tid; r < n; r += kT) {  // rank by particle id inside the cell
+        for (int r = tid; r < n; r += kTC) {  // rank by particle id inside the cell
             const int q = s_tmp[r];
             const int cell = s_cell[q], pq = s_pid[q];
             int rank = 0;
@@ -396,82 +479,42 @@ __global__ void __launch_bounds__(kT) k_p2g(KParams p, SlotView sl, StateView S,
             sl.sigma[fpos] = s_idx[q];
             if (Sn.pid) Sn.pid[fpos] = pq;
         }
-        for (int c = tid; c <= G::CELLS; c += kT) sl.cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
-        for (int q = tid; q < G::CELLS * G::NST; q += kT) s_cb[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int c = tid; c <= G::CELLS; c += kTC) sl.cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
         __syncthreads();
-        const int nvalid = s_cst[G::CELLS];
-        // ---- phases 1 + 2 over chunks of kT particles in canonical order
-        for (int ch = 0; ch < nvalid; ch += kT) {
-            const int r = ch + tid;
-            if (r < nvalid) {
-                const int i = sl.sigma[start + r];
-                float rr[RC::R];
-                load_rec<D>(S.rec + (int64_t)i * RC::R, rr);
-                const float* x = rr + RC::X;
-                const float* v = rr + RC::V;
-                const float* C = rr + RC::C;
-                const float* F = rr + RC::F;
-                float fx[3], w[3][3], dw[3][3];
+        // ---- phase 1: thread = cell, particles of the cell in canonical order
+        {
+            NodeAcc<D, true> acc;
+            acc.zero();
+            const int lo = start + s_cst[tid], hi = start + s_cst[tid + 1];
+            for (int j = lo; j < hi; ++j) {
+                const int i = sl.sigma[j];
+                float x[3], vc[L::VC], F[L::FF];
 #pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    float xi = x[k] * p.inv_dx;
-                    fx[k] = xi - floorf(xi - 0.5f);
-                    bspline(fx[k], w[k], dw[k]);
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
+#pragma unroll
+                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + (int64_t)i * L::VC + q);
+#pragma unroll
+                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + (int64_t)i * L::FF + q);
+                float act = 0.0f;
+                if (aid) {
+                    const int a_id = aid[S.pid[i]];
+                    act = a_id >= 0 ? alpha[a_id] : 0.0f;
                 }
-                float Ft[D * D];
-#pragma unroll
-                for (int a = 0; a < D; ++a)
-#pragma unroll
-                    for (int b = 0; b < D; ++b) {
-                        float s = 0.0f;
-#pragma unroll
-                        for (int k = 0; k < D; ++k) s = fmaf(C[a * D + k], F[k * D + b], s);
-                        Ft[a * D + b] = fmaf(p.dt, s, F[a * D + b]);
-                    }
-                const int pid = S.pid[i];
-                const int a_id = aid ? aid[pid] : -1;
-                const float act = a_id >= 0 ? alpha[a_id] : 0.0f;
-                float tau[D * D];
-                if (!kirchhoff<D>(p, Ft, act, tau)) atomicOr(flags, FLAG_NONFINITE);
-                float* row = s_tab + tid * G::ROW;
-#pragma unroll
-                for (int k = 0; k < D; ++k)
-#pragma unroll
-                    for (int o = 0; o < 3; ++o) row[3 * k + o] = w[k][o];
-                // contribution W_o (c + Adx o), c = m v - Adx f, Adx = A dx
-                float Adx[D * D];
-#pragma unroll
-                for (int q = 0; q < D * D; ++q) Adx[q] = p.dx * fmaf(p.stress_scale, tau[q], p.p_mass * C[q]);
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    float s = p.p_mass * v[a];
-#pragma unroll
-                    for (int b = 0; b < D; ++b) s = fmaf(-Adx[a * D + b], fx[b], s);
-                    row[3 * D + a] = s;
-                }
-#pragma unroll
-                for (int q = 0; q < D * D; ++q) row[4 * D + q] = Adx[q];
-                if (Sn.rec) {
-                    float* dst = Sn.rec + (int64_t)(start + r) * RC::R + RC::F;
+                float w[3][3], c[3], Adx[D * D], Ft[D * D];
+                if (!p2g_particle<D>(p, x, vc, F, act, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
+                acc.add(w, c, Adx);
+                if (Sn.f) {
+                    float* dst = Sn.f + (int64_t)j * L::FF;
 #pragma unroll
                     for (int q = 0; q < D * D; ++q) dst[q] = Ft[q];
                 }
             }
-            __syncthreads();
-            for (int c = warp; c < G::CELLS; c += kW) {
-                const int lo = max(s_cst[c], ch), hi = min(s_cst[c + 1], ch + kT);
-                if (lo >= hi) continue;
-                const float4 acc = cell_rows<D, true>(s_tab - ch * G::ROW, lo, hi, lane);
-                if (lane < G::NST) {
-                    float4& dst = s_cb[c * G::NST + lane];
-                    dst.x += acc.x; dst.y += acc.y; dst.z += acc.z; dst.w += acc.w;
-                }
-            }
-            __syncthreads();
+            acc.store(s_cb, tid);  // the phase-0 arrays are dead after the barrier above
         }
-        // ---- phase 3: node tile (plain stores)
+        __syncthreads();
+        // ---- phase 2: node tile (plain stores)
         float4* tile = sl.tiles + (int64_t)bi * G::TN;
-        for (int q = tid; q < G::TN; q += kT) {
+        for (int q = tid; q < G::TN; q += kTC) {
             float4 s = node_gather<D>(s_cb, q);
             s.w *= p.p_mass;
             tile[q] = s;
@@ -480,7 +523,7 @@ __global__ void __launch_bounds__(kT) k_p2g(KParams p, SlotView sl, StateView S,
     }
 }
 
-// stage U = grid_op(sum of covering tiles) for the CTA's tile; returns #active owned nodes
+// stage U = grid_op(sum of covering tiles) for the CTA's tile
 template <int D>
 __device__ __forceinline__ void stage_velocity(const KParams& p, const SlotView& sl, int e, const int c0[3],
                                                float4* sU) {
@@ -489,7 +532,7 @@ __device__ __forceinline__ void stage_velocity(const KParams& p, const SlotView&
         int n[3];
         local_node<D>(q, n);
         const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-        bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
+        const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
         float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
         if (inside) {
             const float4 pm = covered_sum<D>(p, e, g, sl.bmap, sl.tiles);
@@ -501,15 +544,64 @@ __device__ __forceinline__ void stage_velocity(const KParams& p, const SlotView&
     }
 }
 
+// nested separable gather: S0 = sum W U, Sb[b] = sum W U o_b (first moments)
+template <int D>
+__device__ __forceinline__ void gather_moments(const float4* __restrict__ sU, const int lb[3],
+                                               const float w[3][3], float S0[3], float Sb[3][3]) {
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        S0[a] = 0.f;
+        Sb[0][a] = Sb[1][a] = Sb[2][a] = 0.f;
+    }
+#pragma unroll
+    for (int ox = 0; ox < 3; ++ox) {
+        float u0[3] = {0.f, 0.f, 0.f}, uy[3] = {0.f, 0.f, 0.f}, uz[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int oy = 0; oy < 3; ++oy) {
+            float t0[3] = {0.f, 0.f, 0.f}, tz[3] = {0.f, 0.f, 0.f};
+            if (D == 3) {
+#pragma unroll
+                for (int oz = 0; oz < 3; ++oz) {
+                    const float4 U = sU[tile_lin<D>(lb[0] + ox, lb[1] + oy, lb[2] + oz)];
+                    const float wz = w[2][oz];
+                    t0[0] = fmaf(wz, U.x, t0[0]); t0[1] = fmaf(wz, U.y, t0[1]); t0[2] = fmaf(wz, U.z, t0[2]);
+                    if (oz) {
+                        const float wzo = wz * (float)oz;
+                        tz[0] = fmaf(wzo, U.x, tz[0]); tz[1] = fmaf(wzo, U.y, tz[1]); tz[2] = fmaf(wzo, U.z, tz[2]);
+                    }
+                }
+            } else {
+                const float4 U = sU[tile_lin<D>(lb[0] + ox, lb[1] + oy, 0)];
+                t0[0] = U.x; t0[1] = U.y;
+            }
+            const float wy = w[1][oy];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                u0[a] = fmaf(wy, t0[a], u0[a]);
+                if (D == 3) uz[a] = fmaf(wy, tz[a], uz[a]);
+                if (oy) uy[a] = fmaf(wy * (float)oy, t0[a], uy[a]);
+            }
+        }
+        const float wx = w[0][ox];
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            S0[a] = fmaf(wx, u0[a], S0[a]);
+            Sb[1][a] = fmaf(wx, uy[a], Sb[1][a]);
+            if (D == 3) Sb[2][a] = fmaf(wx, uz[a], Sb[2][a]);
+            if (ox) Sb[0][a] = fmaf(wx * (float)ox, u0[a], Sb[0][a]);
+        }
+    }
+}
+
 // ----------------------------------------------------------------- G2P
-// v' = sum W U; C' = 4/dx sum W U (o - f)^T; x' = x + dt v'; key of x' for the next bin
+// v' = sum W U; C' = 4/dx sum W U (o - f)^T = 4/dx (Sb - v' f^T); x' = x + dt v'
 template <int D>
 __global__ void __launch_bounds__(kT) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
                                             int* __restrict__ keys, int* __restrict__ bcount, int* flags) {
     using G = Geo<D>;
-    using RC = Rec<D>;
+    using L = Lay<D>;
     __shared__ float4 sU[G::TN];
-    __shared__ unsigned short s_cst[G::CELLS + 1];
+    __shared__ int s_nv;
     const int tid = threadIdx.x;
     const int nact = *sl.nactive;
     const float c4 = 4.0f * p.inv_dx;
@@ -519,9 +611,9 @@ __global__ void __launch_bounds__(kT) k_g2p(KParams p, SlotView sl, StateView S,
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         stage_velocity<D>(p, sl, e, c0, sU);
-        if (tid == 0) s_cst[G::CELLS] = sl.cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
+        if (tid == 0) s_nv = sl.cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         __syncthreads();
-        const int nvalid = s_cst[G::CELLS];
+        const int nvalid = s_nv;
         for (int r0 = 0; r0 < nvalid; r0 += kT) {
             const int r = r0 + tid;
             const bool in = r < nvalid;
@@ -531,52 +623,24 @@ __global__ void __launch_bounds__(kT) k_g2p(KParams p, SlotView sl, StateView S,
                 const int i = sl.sigma[j];
                 float x[3];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.rec + (int64_t)i * RC::R + RC::X + k);
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
+                int lb[3];
                 float fx[3], w[3][3], dw[3][3];
-                int lb[3] = {0, 0, 0};
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const float xi = x[k] * p.inv_dx;
-                    const float b = floorf(xi - 0.5f);
-                    fx[k] = xi - b;
-                    lb[k] = (int)b - c0[k];
-                    bspline(fx[k], w[k], dw[k]);
-                }
-                float nv[3] = {0.f, 0.f, 0.f}, nC[D * D];
-#pragma unroll
-                for (int q = 0; q < D * D; ++q) nC[q] = 0.f;
-#pragma unroll
-                for (int o0 = 0; o0 < 3; ++o0)
-#pragma unroll
-                    for (int o1 = 0; o1 < 3; ++o1)
-#pragma unroll
-                        for (int o2 = 0; o2 < (D == 3 ? 3 : 1); ++o2) {
-                            const int o[3] = {o0, o1, o2};
-                            float W = w[0][o0] * w[1][o1];
-                            if (D == 3) W *= w[2][o2];
-                            const float4 u4 = sU[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
-                            const float u[3] = {u4.x, u4.y, u4.z};
-#pragma unroll
-                            for (int a = 0; a < D; ++a) {
-                                const float wu = W * u[a];
-                                nv[a] += wu;
-                                const float cw = c4 * wu;
-#pragma unroll
-                                for (int b = 0; b < D; ++b) nC[a * D + b] = fmaf(cw, (float)o[b] - fx[b], nC[a * D + b]);
-                            }
-                        }
-                float* dst = Sn.rec + (int64_t)j * RC::R;
+                particle_weights<D>(p, x, c0, lb, fx, w, dw);
+                float S0[3], Sb[3][3];
+                gather_moments<D>(sU, lb, w, S0, Sb);
                 float xn[3];
                 bool fin = true;
+                float* dvc = Sn.vc + (int64_t)j * L::VC;
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
-                    xn[a] = fmaf(p.dt, nv[a], x[a]);
-                    dst[RC::X + a] = xn[a];
-                    dst[RC::V + a] = nv[a];
-                    fin = fin && isfinite(nv[a]);
-                }
+                    xn[a] = fmaf(p.dt, S0[a], x[a]);
+                    Sn.x[(int64_t)j * D + a] = xn[a];
+                    dvc[a] = S0[a];
+                    fin = fin && isfinite(S0[a]);
 #pragma unroll
-                for (int q = 0; q < D * D; ++q) dst[RC::C + q] = nC[q];
+                    for (int b = 0; b < D; ++b) dvc[D + a * D + b] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
+                }
                 if (!fin) atomicOr(flags, FLAG_NONFINITE);
                 if (keys) {
                     int b[3];
@@ -599,22 +663,21 @@ __global__ void __launch_bounds__(kT) k_g2p(KParams p, SlotView sl, StateView S,
 // ------------------------------------------------------------ g2p_grad
 // vh = vb' + dt xb';  Ub[b+o] += W (vh + 4/dx Cb' (o - f));  Wb = U.(vh + 4/dx Cb'(o - f));
 // fb += Wb dW/df - 4/dx W Cb'^T U;  xb_t (partial) = xb' + fb/dx.
+// CTA = 64 threads = one thread per cell; U_bar accumulated like p2g's momentum.
 template <int D> constexpr int g2pg_smem_bytes() {
-    return kT * Geo<D>::ROW * 4 + Geo<D>::CELLS * Geo<D>::NST * 16 + Geo<D>::TN * 16 + (Geo<D>::CELLS + 2) * 4;
+    return Geo<D>::CELLS * Geo<D>::NST * 16 + Geo<D>::TN * 16 + (Geo<D>::CELLS + 2) * 4;
 }
 
 template <int D>
-__global__ void __launch_bounds__(kT) k_g2p_grad(KParams p, SlotView sl, StateView S,
-                                                 const float* __restrict__ Sbn, float4* __restrict__ ubar,
-                                                 float* __restrict__ xbp) {
+__global__ void __launch_bounds__(kTC, 4) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
+                                                    float4* __restrict__ ubar, float* __restrict__ xbp) {
     using G = Geo<D>;
-    using RC = Rec<D>;
+    using L = Lay<D>;
     extern __shared__ __align__(16) unsigned char smem[];
-    float* s_tab = reinterpret_cast<float*>(smem);
-    float4* s_cb = reinterpret_cast<float4*>(smem + kT * G::ROW * 4);
+    float4* s_cb = reinterpret_cast<float4*>(smem);
     float4* sU = s_cb + G::CELLS * G::NST;
     int* s_cst = reinterpret_cast<int*>(sU + G::TN);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     const int nact = *sl.nactive;
     const float c4 = 4.0f * p.inv_dx;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
@@ -622,40 +685,43 @@ __global__ void __launch_bounds__(kT) k_g2p_grad(KParams p, SlotView sl, StateVi
         const int start = sl.bstart[bi];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        stage_velocity<D>(p, sl, e, c0, sU);
-        for (int c = tid; c <= G::CELLS; c += kT) s_cst[c] = sl.cstart[(int64_t)bi * (G::CELLS + 1) + c];
-        for (int q = tid; q < G::CELLS * G::NST; q += kT) s_cb[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = threadIdx.x; q < G::TN; q += kTC) {
+            int n[3];
+            local_node<D>(q, n);
+            const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
+            const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
+            float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (inside) {
+                const float4 pm = covered_sum<D>(p, e, g, sl.bmap, sl.tiles);
+                float u0[3], u1[3];
+                const bool z = grid_velocity<D>(p, g, pm, u0, u1);
+                out = z ? make_float4(0.f, 0.f, 0.f, 1.f) : make_float4(u1[0], u1[1], u1[2], 0.f);
+            }
+            sU[q] = out;
+        }
+        for (int c = tid; c <= G::CELLS; c += kTC) s_cst[c] = sl.cstart[(int64_t)bi * (G::CELLS + 1) + c];
         __syncthreads();
-        const int nvalid = s_cst[G::CELLS];
-        for (int ch = 0; ch < nvalid; ch += kT) {
-            const int r = ch + tid;
-            if (r < nvalid) {
-                const int j = start + r;
+        {
+            NodeAcc<D, false> acc;
+            acc.zero();
+            const int lo = start + s_cst[tid], hi = start + s_cst[tid + 1];
+            for (int j = lo; j < hi; ++j) {
                 const int i = sl.sigma[j];
-                const int pid = S.pid[i];
                 float x[3];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.rec + (int64_t)i * RC::R + RC::X + k);
-                const float* bn = Sbn + (int64_t)pid * RC::R;
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
                 float xb[3], vh[3], B[D * D];
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
-                    xb[a] = __ldg(bn + RC::X + a);
-                    vh[a] = fmaf(p.dt, xb[a], __ldg(bn + RC::V + a));
+                    xb[a] = __ldg(Sbn.x + (int64_t)j * D + a);
+                    vh[a] = fmaf(p.dt, xb[a], __ldg(Sbn.vc + (int64_t)j * L::VC + a));
                 }
 #pragma unroll
-                for (int q = 0; q < D * D; ++q) B[q] = c4 * __ldg(bn + RC::C + q);
+                for (int q = 0; q < D * D; ++q) B[q] = c4 * __ldg(Sbn.vc + (int64_t)j * L::VC + D + q);
+                int lb[3];
                 float fx[3], w[3][3], dw[3][3];
-                int lb[3] = {0, 0, 0};
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const float xi = x[k] * p.inv_dx;
-                    const float b = floorf(xi - 0.5f);
-                    fx[k] = xi - b;
-                    lb[k] = (int)b - c0[k];
-                    bspline(fx[k], w[k], dw[k]);
-                }
-                float cp[3];  // c' = vh - B f
+                particle_weights<D>(p, x, c0, lb, fx, w, dw);
+                float cp[3];  // c' = vh - B f ; t_o = c' + B o
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
                     float s = vh[a];
@@ -663,64 +729,55 @@ __global__ void __launch_bounds__(kT) k_g2p_grad(KParams p, SlotView sl, StateVi
                     for (int b = 0; b < D; ++b) s = fmaf(-B[a * D + b], fx[b], s);
                     cp[a] = s;
                 }
-                float fb[3] = {0.f, 0.f, 0.f};
+                float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-                for (int o0 = 0; o0 < 3; ++o0)
+                for (int o0 = 0; o0 < 3; ++o0) {
+                    float tx[3];
 #pragma unroll
-                    for (int o1 = 0; o1 < 3; ++o1)
+                    for (int a = 0; a < D; ++a) tx[a] = fmaf((float)o0, B[a * D], cp[a]);
+#pragma unroll
+                    for (int o1 = 0; o1 < 3; ++o1) {
+                        float ty[3];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) ty[a] = fmaf((float)o1, B[a * D + 1], tx[a]);
 #pragma unroll
                         for (int o2 = 0; o2 < (D == 3 ? 3 : 1); ++o2) {
-                            const int o[3] = {o0, o1, o2};
-                            float wo[3] = {w[0][o0], w[1][o1], D == 3 ? w[2][o2] : 1.0f};
-                            const float W = wo[0] * wo[1] * wo[2];
+                            float t[3];
+#pragma unroll
+                            for (int a = 0; a < D; ++a) t[a] = D == 3 ? fmaf((float)o2, B[a * D + 2], ty[a]) : ty[a];
+                            const float wyz = D == 3 ? w[1][o1] * w[2][o2] : w[1][o1];
+                            const float W = w[0][o0] * wyz;
                             float gW[3];
-                            gW[0] = dw[0][o0] * wo[1] * wo[2];
-                            gW[1] = wo[0] * dw[1][o1] * wo[2];
-                            if (D == 3) gW[2] = wo[0] * wo[1] * dw[2][o2];
+                            gW[0] = dw[0][o0] * wyz;
+                            gW[1] = D == 3 ? w[0][o0] * dw[1][o1] * w[2][o2] : w[0][o0] * dw[1][o1];
+                            if (D == 3) gW[2] = w[0][o0] * w[1][o1] * dw[2][o2];
                             const float4 u4 = sU[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
                             const float u[3] = {u4.x, u4.y, u4.z};
                             float Wb = 0.0f;
 #pragma unroll
                             for (int a = 0; a < D; ++a) {
-                                float t = cp[a];
-#pragma unroll
-                                for (int b = 0; b < D; ++b) t = fmaf(B[a * D + b], (float)o[b], t);
-                                Wb = fmaf(u[a], t, Wb);
+                                Wb = fmaf(u[a], t[a], Wb);
+                                S0[a] = fmaf(W, u[a], S0[a]);
                             }
 #pragma unroll
-                            for (int k = 0; k < D; ++k) {
-                                float btu = 0.0f;
-#pragma unroll
-                                for (int a = 0; a < D; ++a) btu = fmaf(B[a * D + k], u[a], btu);
-                                fb[k] = fmaf(Wb, gW[k], fb[k]) - W * btu;
-                            }
+                            for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
                         }
-#pragma unroll
-                for (int k = 0; k < D; ++k) xbp[(int64_t)j * D + k] = fmaf(p.inv_dx, fb[k], xb[k]);
-                float* row = s_tab + tid * G::ROW;
-#pragma unroll
-                for (int k = 0; k < D; ++k)
-#pragma unroll
-                    for (int o = 0; o < 3; ++o) row[3 * k + o] = w[k][o];
-#pragma unroll
-                for (int a = 0; a < D; ++a) row[3 * D + a] = cp[a];
-#pragma unroll
-                for (int q = 0; q < D * D; ++q) row[4 * D + q] = B[q];
-            }
-            __syncthreads();
-            for (int c = warp; c < G::CELLS; c += kW) {
-                const int lo = max(s_cst[c], ch), hi = min(s_cst[c + 1], ch + kT);
-                if (lo >= hi) continue;
-                const float4 acc = cell_rows<D, false>(s_tab - ch * G::ROW, lo, hi, lane);
-                if (lane < G::NST) {
-                    float4& dst = s_cb[c * G::NST + lane];
-                    dst.x += acc.x; dst.y += acc.y; dst.z += acc.z;
+                    }
                 }
+#pragma unroll
+                for (int k = 0; k < D; ++k) {  // fb_k -= (B^T S0)_k
+                    float s = 0.0f;
+#pragma unroll
+                    for (int a = 0; a < D; ++a) s = fmaf(B[a * D + k], S0[a], s);
+                    xbp[(int64_t)j * D + k] = fmaf(p.inv_dx, fb[k] - s, xb[k]);
+                }
+                acc.add(w, cp, B);
             }
-            __syncthreads();
+            acc.store(s_cb, tid);
         }
+        __syncthreads();
         float4* tile = ubar + (int64_t)bi * G::TN;
-        for (int q = tid; q < G::TN; q += kT) tile[q] = node_gather<D>(s_cb, q);
+        for (int q = tid; q < G::TN; q += kTC) tile[q] = node_gather<D>(s_cb, q);
         __syncthreads();
     }
 }
@@ -735,13 +792,11 @@ template <int D>
 __global__ void __launch_bounds__(kT) k_p2g_grad(KParams p, SlotView sl, StateView S,
                                                  const int32_t* __restrict__ aid,
                                                  const float* __restrict__ alpha,
-                                                 const float4* __restrict__ ubar,
-                                                 const float* __restrict__ Sbn,
-                                                 const float* __restrict__ xbp,
-                                                 float* __restrict__ Sb, float* __restrict__ abar_part,
-                                                 int* flags) {
+                                                 const float4* __restrict__ ubar, AdjView Sbn,
+                                                 const float* __restrict__ xbp, AdjView Sb,
+                                                 float* __restrict__ abar_part, int* flags) {
     using G = Geo<D>;
-    using RC = Rec<D>;
+    using L = Lay<D>;
     __shared__ float4 sG[G::TN];
     __shared__ float s_ab[kW][32];
     __shared__ int s_nvalid;
@@ -784,22 +839,18 @@ __global__ void __launch_bounds__(kT) k_p2g_grad(KParams p, SlotView sl, StateVi
                 const int j = start + r;
                 const int i = sl.sigma[j];
                 const int pid = S.pid[i];
-                float rr[RC::R];
-                load_rec<D>(S.rec + (int64_t)i * RC::R, rr);
-                const float* x = rr + RC::X;
-                const float* v = rr + RC::V;
-                const float* C = rr + RC::C;
-                const float* F = rr + RC::F;
-                float fx[3], w[3][3], dw[3][3];
-                int lb[3] = {0, 0, 0};
+                float x[3], vc[L::VC], F[L::FF];
 #pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    const float xi = x[k] * p.inv_dx;
-                    const float b = floorf(xi - 0.5f);
-                    fx[k] = xi - b;
-                    lb[k] = (int)b - c0[k];
-                    bspline(fx[k], w[k], dw[k]);
-                }
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
+#pragma unroll
+                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + (int64_t)i * L::VC + q);
+#pragma unroll
+                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + (int64_t)i * L::FF + q);
+                const float* v = vc;
+                const float* C = vc + D;
+                int lb[3];
+                float fx[3], w[3][3], dw[3][3];
+                particle_weights<D>(p, x, c0, lb, fx, w, dw);
                 float Ft[D * D];
 #pragma unroll
                 for (int a = 0; a < D; ++a)
@@ -812,61 +863,80 @@ __global__ void __launch_bounds__(kT) k_p2g_grad(KParams p, SlotView sl, StateVi
                     }
                 a_id = aid ? aid[pid] : -1;
                 const float act = a_id >= 0 ? alpha[a_id] : 0.0f;
-                float tau[D * D], A[D * D];
+                float tau[D * D], Adx[D * D], c[3];
                 kirchhoff<D>(p, Ft, act, tau);
 #pragma unroll
-                for (int q = 0; q < D * D; ++q) A[q] = fmaf(p.stress_scale, tau[q], p.p_mass * C[q]);
-                float vb[3] = {0.f, 0.f, 0.f}, fb[3] = {0.f, 0.f, 0.f}, Ab[D * D];
+                for (int q = 0; q < D * D; ++q) Adx[q] = p.dx * fmaf(p.stress_scale, tau[q], p.p_mass * C[q]);
 #pragma unroll
-                for (int q = 0; q < D * D; ++q) Ab[q] = 0.0f;
+                for (int a = 0; a < D; ++a) {  // m v + A dpos = c + Adx o
+                    float s = p.p_mass * v[a];
 #pragma unroll
-                for (int o0 = 0; o0 < 3; ++o0)
+                    for (int b = 0; b < D; ++b) s = fmaf(-Adx[a * D + b], fx[b], s);
+                    c[a] = s;
+                }
+                float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f}, Sm[3][3];
 #pragma unroll
-                    for (int o1 = 0; o1 < 3; ++o1)
+                for (int q = 0; q < 9; ++q) (&Sm[0][0])[q] = 0.f;
+#pragma unroll
+                for (int o0 = 0; o0 < 3; ++o0) {
+                    float mx[3];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) mx[a] = fmaf((float)o0, Adx[a * D], c[a]);
+#pragma unroll
+                    for (int o1 = 0; o1 < 3; ++o1) {
+                        float my[3];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) my[a] = fmaf((float)o1, Adx[a * D + 1], mx[a]);
 #pragma unroll
                         for (int o2 = 0; o2 < (D == 3 ? 3 : 1); ++o2) {
-                            const int o[3] = {o0, o1, o2};
-                            float wo[3] = {w[0][o0], w[1][o1], D == 3 ? w[2][o2] : 1.0f};
-                            const float W = wo[0] * wo[1] * wo[2];
-                            float gW[3];
-                            gW[0] = dw[0][o0] * wo[1] * wo[2];
-                            gW[1] = wo[0] * dw[1][o1] * wo[2];
-                            if (D == 3) gW[2] = wo[0] * wo[1] * dw[2][o2];
-                            float dpos[3];
+                            float m[3];
 #pragma unroll
-                            for (int k = 0; k < D; ++k) dpos[k] = ((float)o[k] - fx[k]) * p.dx;
+                            for (int a = 0; a < D; ++a) m[a] = D == 3 ? fmaf((float)o2, Adx[a * D + 2], my[a]) : my[a];
+                            const float wyz = D == 3 ? w[1][o1] * w[2][o2] : w[1][o1];
+                            const float W = w[0][o0] * wyz;
+                            float gW[3];
+                            gW[0] = dw[0][o0] * wyz;
+                            gW[1] = D == 3 ? w[0][o0] * dw[1][o1] * w[2][o2] : w[0][o0] * dw[1][o1];
+                            if (D == 3) gW[2] = w[0][o0] * w[1][o1] * dw[2][o2];
                             const float4 g4 = sG[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
                             const float gP[3] = {g4.x, g4.y, g4.z};
                             float Wb = g4.w * p.p_mass;
+                            const int o[3] = {o0, o1, o2};
 #pragma unroll
                             for (int a = 0; a < D; ++a) {
-                                vb[a] = fmaf(W * p.p_mass, gP[a], vb[a]);
-                                float mom = p.p_mass * v[a];
+                                Wb = fmaf(gP[a], m[a], Wb);
                                 const float wg = W * gP[a];
+                                S0[a] += wg;
 #pragma unroll
-                                for (int b = 0; b < D; ++b) {
-                                    Ab[a * D + b] = fmaf(wg, dpos[b], Ab[a * D + b]);
-                                    mom = fmaf(A[a * D + b], dpos[b], mom);
-                                }
-                                Wb = fmaf(gP[a], mom, Wb);
+                                for (int b = 0; b < D; ++b)
+                                    if (o[b]) Sm[b][a] = fmaf((float)o[b], wg, Sm[b][a]);
                             }
 #pragma unroll
-                            for (int k = 0; k < D; ++k) {
-                                float s = 0.0f;
-#pragma unroll
-                                for (int a = 0; a < D; ++a) s = fmaf(A[a * D + k], gP[a], s);
-                                fb[k] = fmaf(Wb, gW[k], fb[k]) - p.dx * W * s;
-                            }
+                            for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
                         }
-                float taub[D * D], Ftb[D * D];
-                const float* bn = Sbn + (int64_t)pid * RC::R;
+                    }
+                }
+                // Ab[a][b] = dx (Sm[b][a] - S0[a] f[b]);  fb_k -= (Adx^T S0)_k
+                float Ab[D * D], taub[D * D], Ftb[D * D];
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+#pragma unroll
+                    for (int b = 0; b < D; ++b) Ab[a * D + b] = p.dx * fmaf(-S0[a], fx[b], Sm[b][a]);
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    float s = 0.0f;
+#pragma unroll
+                    for (int a = 0; a < D; ++a) s = fmaf(Adx[a * D + k], S0[a], s);
+                    fb[k] -= s;
+                }
 #pragma unroll
                 for (int q = 0; q < D * D; ++q) {
                     taub[q] = p.stress_scale * Ab[q];
-                    Ftb[q] = __ldg(bn + RC::F + q);
+                    Ftb[q] = __ldg(Sbn.f + (int64_t)j * L::FF + q);
                 }
                 abar = kirchhoff_adj<D>(p, Ft, a_id >= 0, act, taub, Ftb);
-                float* dst = Sb + (int64_t)pid * RC::R;
+                float* dvc = Sb.vc + (int64_t)i * L::VC;
+                float* dF = Sb.f + (int64_t)i * L::FF;
                 bool fin = true;
 #pragma unroll
                 for (int a = 0; a < D; ++a)
@@ -878,14 +948,14 @@ __global__ void __launch_bounds__(kT) k_p2g_grad(KParams p, SlotView sl, StateVi
                             sF = fmaf(p.dt * C[k * D + a], Ftb[k * D + b], sF);
                             sC = fmaf(Ftb[a * D + k], F[b * D + k], sC);
                         }
-                        dst[RC::F + a * D + b] = sF;
-                        dst[RC::C + a * D + b] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
+                        dF[a * D + b] = sF;
+                        dvc[D + a * D + b] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
                         fin = fin && isfinite(sF);
                     }
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
-                    dst[RC::X + a] = fmaf(p.inv_dx, fb[a], xbp[(int64_t)j * D + a]);
-                    dst[RC::V + a] = vb[a];
+                    Sb.x[(int64_t)i * D + a] = fmaf(p.inv_dx, fb[a], xbp[(int64_t)j * D + a]);
+                    dvc[a] = p.p_mass * S0[a];
                 }
                 if (!fin) atomicOr(flags, FLAG_NONFINITE);
             }
@@ -976,11 +1046,11 @@ int g_grid[4][2];  // persistent grid size per kernel kind and dimension (set by
         }                \
     } while (0)
 
-static int occupancy_grid(const void* fn, int smem) {
+static int occupancy_grid(const void* fn, int smem, int threads = kT) {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kT, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
     return sms * (per > 0 ? per : 1);
 }
 
@@ -993,9 +1063,9 @@ cudaError_t tile_init() {
         if (e) return e;
         e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
         if (e) return e;
-        g_grid[0][0] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>());
+        g_grid[0][0] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTC);
         g_grid[1][0] = occupancy_grid((const void*)k_g2p<DIM>, 0);
-        g_grid[2][0] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>());
+        g_grid[2][0] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTC);
         g_grid[3][0] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0);
     });
     DISPATCH(3, {
@@ -1003,9 +1073,9 @@ cudaError_t tile_init() {
         if (e) return e;
         e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
         if (e) return e;
-        g_grid[0][1] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>());
+        g_grid[0][1] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTC);
         g_grid[1][1] = occupancy_grid((const void*)k_g2p<DIM>, 0);
-        g_grid[2][1] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>());
+        g_grid[2][1] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTC);
         g_grid[3][1] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0);
     });
     done = true;
@@ -1017,8 +1087,8 @@ static unsigned pgrid(const KParams& p, int kind) {
     return (unsigned)(p.max_active < g ? p.max_active : g);
 }
 
-void launch_bin_keys(const KParams& p, const float* rec, int* keys, int* bcount, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_bin_keys<DIM><<<nblk(p.N * p.E), kT, 0, s>>>(p, rec, keys, bcount, flags));
+void launch_bin_keys(const KParams& p, const float* x, int* keys, int* bcount, int* flags, cudaStream_t s) {
+    DISPATCH(p.dim, k_bin_keys<DIM><<<nblk(p.N * p.E), kT, 0, s>>>(p, x, keys, bcount, flags));
 }
 void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* flags, cudaStream_t s) {
     k_bin_scan<<<1, kScanT, 0, s>>>(p, bcount, cursor, sl, flags);
@@ -1028,19 +1098,19 @@ void launch_bin_scatter(const KParams& p, const int* keys, int* cursor, int* sig
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_p2g<DIM><<<pgrid(p, 0), kT, p2g_smem_bytes<DIM>(), s>>>(p, sl, S, Sn, aid, alpha_t, flags));
+    DISPATCH(p.dim, k_p2g<DIM><<<pgrid(p, 0), kTC, p2g_smem_bytes<DIM>(), s>>>(p, sl, S, Sn, aid, alpha_t, flags));
 }
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
                 int* bcount, int* flags, cudaStream_t s) {
     DISPATCH(p.dim, k_g2p<DIM><<<pgrid(p, 1), kT, 0, s>>>(p, sl, S, Sn, keys, bcount, flags));
 }
-void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const float* Sbn,
+void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, float* xbp, cudaStream_t s) {
-    DISPATCH(p.dim, k_g2p_grad<DIM><<<pgrid(p, 2), kT, g2pg_smem_bytes<DIM>(), s>>>(p, sl, S, Sbn, ubar, xbp));
+    DISPATCH(p.dim, k_g2p_grad<DIM><<<pgrid(p, 2), kTC, g2pg_smem_bytes<DIM>(), s>>>(p, sl, S, Sbn, ubar, xbp));
 }
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
-                     const float* alpha_t, const float4* ubar, const float* Sbn, const float* xbp,
-                     float* Sb, float* abar_part, int* flags, cudaStream_t s) {
+                     const float* alpha_t, const float4* ubar, const AdjView& Sbn, const float* xbp,
+                     const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s) {
     DISPATCH(p.dim, k_p2g_grad<DIM><<<pgrid(p, 3), kT, 0, s>>>(p, sl, S, aid, alpha_t, ubar, Sbn, xbp, Sb, abar_part, flags));
 }
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s) {

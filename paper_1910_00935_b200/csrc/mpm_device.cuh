@@ -36,14 +36,18 @@ template <int D> struct Geo {
     static constexpr int TN = D == 3 ? 216 : 100;    // tile nodes
     static constexpr int NST = D == 3 ? 27 : 9;      // stencil offsets
     static constexpr int NSUB = D == 3 ? 1 : 3;      // particle sub-streams per cell warp
-    static constexpr int ROW = D == 3 ? 24 : 12;     // floats per particle row (cell phase)
+    static constexpr int ROW = D == 3 ? 24 : 12;     // floats per particle row (cell phase):
+                                                     // 3D [wy*wz (9), c (3), A dx (9), wx (3)]
+                                                     // 2D [wy (3), c (2), A dx (4), wx (3)]
     static constexpr int MAXP = 1728;                // particles per block (27 per cell)
 };
 
-template <int D> struct Rec {
-    static constexpr int R = 2 * D + 2 * D * D;  // floats per particle record: x, v, C, F
-    static constexpr int X = 0, V = D, C = 2 * D, F = 2 * D + D * D;
-    static constexpr int NST = D == 2 ? 9 : 27;  // stencil nodes
+// State layout: three dense arrays per state, so a kernel
+// that needs only x (g2p, g2p_grad, binning, loss) reads 4d bytes per particle.
+template <int D> struct Lay {
+    static constexpr int X = D;           // x        [n][d]
+    static constexpr int VC = D + D * D;  // (v, C)   [n][d + d^2]   (v first, C row-major)
+    static constexpr int FF = D * D;      // F        [n][d^2]       row-major
 };
 
 // quadratic B-spline N_0..N_2 at f in [1/2, 3/2) and derivatives (R1)
