@@ -68,6 +68,7 @@ struct mpm_ctx {
     int32_t* aid = nullptr;        // caller order
     int* bcount = nullptr;         // [TB] block histogram (kept zero between uses)
     int* cursor = nullptr;         // [TB]
+    int* scan_part = nullptr;      // [scan chunks] int2
     int* keys = nullptr;           // [EN]
     float* xbar_part = nullptr;    // [EN][d]
     float4* ubar = nullptr;        // [max_active][TN]
@@ -204,6 +205,8 @@ size_t carve(mpm_ctx* h, char* base) {
     for (int i = 0; i < kk; ++i) {
         SlotView s;
         s.sigma = (int*)take(sizeof(int) * EN);
+        s.scell = (unsigned char*)take(EN);
+        s.spid = (int*)take(sizeof(int) * EN);
         s.blist = (int*)take(sizeof(int) * max_active);
         s.bstart = (int*)take(sizeof(int) * (max_active + 1));
         s.bmap = (int*)take(sizeof(int) * k.TB);
@@ -218,6 +221,7 @@ size_t carve(mpm_ctx* h, char* base) {
     int32_t* aid = (int32_t*)take(sizeof(int32_t) * EN);
     int* bcount = (int*)take(sizeof(int) * k.TB);
     int* cursor = (int*)take(sizeof(int) * k.TB);
+    int* scan_part = (int*)take(sizeof(int) * 2 * (scan_chunks(k) + 1));
     int* keys = (int*)take(sizeof(int) * EN);
     float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
     float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
@@ -240,7 +244,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->final_state = fin;
         h->slots = slots;
         h->sbar[0] = sb0; h->sbar[1] = sb1;
-        h->staging = staging; h->aid = aid; h->bcount = bcount; h->cursor = cursor; h->keys = keys;
+        h->staging = staging; h->aid = aid; h->bcount = bcount; h->cursor = cursor; h->scan_part = scan_part; h->keys = keys;
         h->xbar_part = xbar_part; h->ubar = ubar; h->abar_part = abar_part;
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
         h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
@@ -328,10 +332,10 @@ const float* alpha_at(mpm_ctx* h, int t) {
 void bin_fresh(mpm_ctx* h, const KParams& k, int t) {
     const SlotView& sl = slot_at(h, t);
     KScope sc(h, KC_BIN);
-    h->launches += 2;
+    h->launches += 3;
     launch_bin_keys(k, state_at(h, t).x, h->keys, h->bcount, h->flags, h->stream);
-    launch_bin_scan(k, h->bcount, h->cursor, sl, h->flags, h->stream);
-    launch_bin_scatter(k, h->keys, h->cursor, sl.sigma, h->stream);
+    launch_bin_scan(k, h->bcount, h->cursor, sl, h->scan_part, h->flags, h->stream);
+    launch_bin_scatter(k, h->keys, state_at(h, t).pid, h->cursor, sl, h->stream);
 }
 
 // advance() for step t; write_next: produce S_{t+1}; bin_next: bin it into slot(t+1)
@@ -347,9 +351,9 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     if (bin_next) {
         const SlotView& nx = slot_at(h, t + 1);
         KScope sc(h, KC_BIN);
-        h->launches += 1;
-        launch_bin_scan(k, h->bcount, h->cursor, nx, h->flags, h->stream);
-        launch_bin_scatter(k, h->keys, h->cursor, nx.sigma, h->stream);
+        h->launches += 2;
+        launch_bin_scan(k, h->bcount, h->cursor, nx, h->scan_part, h->flags, h->stream);
+        launch_bin_scatter(k, h->keys, Sn.pid, h->cursor, nx, h->stream);
     }
 }
 
@@ -515,8 +519,8 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
     { KScope sc(h, KC_LAYOUT);
       launch_pack(k, sx, v ? sv : nullptr, C ? sC : nullptr, F ? sF : nullptr, nullptr, h->ckpt[0].x,
                   h->ckpt[0].vc, h->ckpt[0].f, h->ckpt[0].pid, false, h->stream); }
-    h->has_aid = actuator_id != nullptr;
-    if (actuator_id && (st = copy_in(h, h->aid, actuator_id, sizeof(int32_t) * EN))) return st;
+    h->has_aid = actuator_id != nullptr && h->prm.n_actuators > 0;  // ids are meaningless without actuators
+    if (h->has_aid && (st = copy_in(h, h->aid, actuator_id, sizeof(int32_t) * EN))) return st;
     CU(cudaGetLastError());
     h->phase = kHasState;
     h->recorded = 0;

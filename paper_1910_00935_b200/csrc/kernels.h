@@ -24,6 +24,8 @@ struct AdjView {
 // one time step's binning + grid:
 struct SlotView {
     int* sigma;              // [EN]   sorted order -> index into that step's state array
+    unsigned char* scell;    // [EN]   cell (0..63, 64 = junk) of the sorted entry (set by bin_scatter)
+    int* spid;               // [EN]   particle id of the sorted entry (set by bin_scatter)
     int* blist;              // [max_active]   active block ids (block-id order)
     int* bstart;             // [max_active+1] start of each block's segment of sigma
     int* bmap;               // [TB]   block id -> active index, or -1
@@ -36,8 +38,12 @@ cudaError_t tile_init();
 
 // ---- binning (bin_keys only for a fresh sort; g2p emits keys for the next step)
 void launch_bin_keys(const KParams& p, const float* x, int* keys, int* bcount, int* flags, cudaStream_t s);
-void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* flags, cudaStream_t s);
-void launch_bin_scatter(const KParams& p, const int* keys, int* cursor, int* sigma, cudaStream_t s);
+int scan_chunks(const KParams& p);  // entries of `part` (int2) the scan needs
+void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
+                     cudaStream_t s);
+// keys[j] = block * 128 + cell of entry j; pid[j] its particle id
+void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
+                        cudaStream_t s);
 
 // ---- one forward step (advance())
 // p2g writes F_{t+1} and particle ids of S_{t+1} when Sn.rec / Sn.pid are non-null

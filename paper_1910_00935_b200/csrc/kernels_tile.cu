@@ -165,106 +165,118 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
         const bool ok = base_cell<D>(p, x, b);
         const int e = (int)(i / p.N);
         int bb[3] = {b[0] >> Geo<D>::LOGB, b[1] >> Geo<D>::LOGB, b[2] >> Geo<D>::LOGB};
+        int lb[3] = {b[0] & (Geo<D>::B - 1), b[1] & (Geo<D>::B - 1), b[2] & (Geo<D>::B - 1)};
         key = block_lin<D>(p, e, bb);
-        if (!ok) { atomicOr(flags, FLAG_OUT_OF_DOMAIN); key = e * p.nbe; }
-        keys[i] = key;
+        int cell = cell_of<D>(lb);
+        if (!ok) { atomicOr(flags, FLAG_OUT_OF_DOMAIN); key = e * p.nbe; cell = Geo<D>::CELLS; }
+        keys[i] = key * 128 + cell;
     }
     count_key(in, key, bcount);
 }
 
-// single CTA: exclusive scan of the dense block histogram -> active block list
-// (block-id order), starts, block map, scatter cursors; clears the histogram.
-// Rounds of 1024 x 16 entries, loads issued together (latency, not bandwidth, bound).
-constexpr int kScanT = 1024;
+// Exclusive scan of the dense block histogram -> active block list (block-id order),
+// starts, block map, scatter cursors; clears the histogram.  Two launches over chunks of
+// 256 x 16 entries: k_bin_scan<0> writes per-chunk totals, k_bin_scan<1> adds the totals
+// of the earlier chunks (fixed order) and writes the outputs.
 constexpr int kScanPer = 16;
-__global__ void __launch_bounds__(kScanT) k_bin_scan(KParams p, int* __restrict__ bcount,
-                                                     int* __restrict__ cursor, SlotView sl, int* flags) {
-    __shared__ int s_wt[32], s_wa[32];
-    __shared__ int s_carry[2];
+constexpr int kScanChunk = kT * kScanPer;
+template <int MODE>
+__global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bcount, int* __restrict__ cursor,
+                                                SlotView sl, int2* __restrict__ part, int* flags) {
+    __shared__ int s_wt[kW], s_wa[kW];
+    __shared__ int s_base[2];
     const int TB = p.TB, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) { s_carry[0] = 0; s_carry[1] = 0; }
-    __syncthreads();
-    for (int base = 0; base < TB; base += kScanT * kScanPer) {
-        const int i0 = base + tid * kScanPer;
-        int c[kScanPer];
-        if (i0 + kScanPer <= TB) {
+    const int i0 = blockIdx.x * kScanChunk + tid * kScanPer;
+    int c[kScanPer];
+    if (i0 + kScanPer <= TB) {
 #pragma unroll
-            for (int q = 0; q < kScanPer / 4; ++q) {
-                const int4 v = *reinterpret_cast<const int4*>(bcount + i0 + 4 * q);
-                c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < kScanPer; ++q) c[q] = i0 + q < TB ? bcount[i0 + q] : 0;
+        for (int q = 0; q < kScanPer / 4; ++q) {
+            const int4 v = *reinterpret_cast<const int4*>(bcount + i0 + 4 * q);
+            c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
         }
-        int tot = 0, act = 0;
+    } else {
 #pragma unroll
-        for (int q = 0; q < kScanPer; ++q) { tot += c[q]; act += c[q] > 0; }
-        // block exclusive scan of (tot, act)
-        int it = tot, ia = act;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int a = __shfl_up_sync(0xffffffffu, it, off), b = __shfl_up_sync(0xffffffffu, ia, off);
-            if (lane >= off) { it += a; ia += b; }
-        }
-        if (lane == 31) { s_wt[warp] = it; s_wa[warp] = ia; }
-        __syncthreads();
-        if (warp == 0) {
-            int wt = s_wt[lane], wa = s_wa[lane];
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int a = __shfl_up_sync(0xffffffffu, wt, off), b = __shfl_up_sync(0xffffffffu, wa, off);
-                if (lane >= off) { wt += a; wa += b; }
-            }
-            s_wt[lane] = wt;
-            s_wa[lane] = wa;
-        }
-        __syncthreads();
-        int pos = s_carry[0] + (warp ? s_wt[warp - 1] : 0) + it - tot;
-        int li = s_carry[1] + (warp ? s_wa[warp - 1] : 0) + ia - act;
-#pragma unroll
-        for (int q = 0; q < kScanPer; ++q) {
-            const int b = i0 + q;
-            if (b >= TB) break;
-            if (c[q] > 0) {
-                if (li < p.max_active) {
-                    sl.blist[li] = b;
-                    sl.bstart[li] = pos;
-                    sl.bmap[b] = li;
-                } else {
-                    sl.bmap[b] = -1;
-                    atomicOr(flags, FLAG_ACTIVE_OVERFLOW);
-                }
-                cursor[b] = pos;
-                pos += c[q];
-                ++li;
-                bcount[b] = 0;
-            } else {
-                sl.bmap[b] = -1;
-            }
-        }
-        __syncthreads();
-        if (tid == kScanT - 1) { s_carry[0] = pos; s_carry[1] = li; }
-        __syncthreads();
+        for (int q = 0; q < kScanPer; ++q) c[q] = i0 + q < TB ? bcount[i0 + q] : 0;
     }
-    if (tid == 0) {
-        const int n = min(s_carry[1], p.max_active);
+    int tot = 0, act = 0;
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q) { tot += c[q]; act += c[q] > 0; }
+    int it = tot, ia = act;  // inclusive warp scan
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int a = __shfl_up_sync(0xffffffffu, it, off), b = __shfl_up_sync(0xffffffffu, ia, off);
+        if (lane >= off) { it += a; ia += b; }
+    }
+    if (lane == 31) { s_wt[warp] = it; s_wa[warp] = ia; }
+    if (MODE == 1 && warp == kW - 1) {  // sum of the earlier chunks' totals (fixed order)
+        int bt = 0, ba = 0;
+        for (int k = lane; k < (int)blockIdx.x; k += 32) { bt += part[k].x; ba += part[k].y; }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            bt += __shfl_xor_sync(0xffffffffu, bt, off);
+            ba += __shfl_xor_sync(0xffffffffu, ba, off);
+        }
+        if (lane == 0) { s_base[0] = bt; s_base[1] = ba; }
+    }
+    __syncthreads();
+    if (MODE == 0) {
+        if (tid == 0) {
+            int bt = 0, ba = 0;
+            for (int w = 0; w < kW; ++w) { bt += s_wt[w]; ba += s_wa[w]; }
+            part[blockIdx.x] = make_int2(bt, ba);
+        }
+        return;
+    }
+    int pos = s_base[0] + it - tot, li = s_base[1] + ia - act;
+    for (int w = 0; w < warp; ++w) { pos += s_wt[w]; li += s_wa[w]; }
+#pragma unroll
+    for (int q = 0; q < kScanPer; ++q) {
+        const int b = i0 + q;
+        if (b >= TB) break;
+        if (c[q] > 0) {
+            if (li < p.max_active) {
+                sl.blist[li] = b;
+                sl.bstart[li] = pos;
+                sl.bmap[b] = li;
+            } else {
+                // capacity exceeded: the list ends before this block (error is reported)
+                if (li == p.max_active) sl.bstart[li] = pos;
+                sl.bmap[b] = -1;
+                atomicOr(flags, FLAG_ACTIVE_OVERFLOW);
+            }
+            cursor[b] = pos;
+            pos += c[q];
+            ++li;
+            bcount[b] = 0;
+        } else {
+            sl.bmap[b] = -1;
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1 && tid == kT - 1) {  // grand totals
+        const int n = min(li, p.max_active);
         *sl.nactive = n;
-        sl.bstart[n] = min(s_carry[0], (int)(p.N * p.E));
+        if (li <= p.max_active) sl.bstart[n] = pos;
     }
 }
 
 __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __restrict__ keys,
-                                                    int* __restrict__ cursor, int* __restrict__ sigma) {
+                                                    const int* __restrict__ pid, int* __restrict__ cursor,
+                                                    SlotView sl) {
     const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool in = j < p.N * p.E;
-    const int key = in ? keys[j] : -1;
+    const int kc = in ? keys[j] : -1;
+    const int key = in ? kc >> 7 : -1;
     const unsigned peers = __match_any_sync(0xffffffffu, key);
     const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
     int base = 0;
     if (in && lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (in) sigma[base + __popc(peers & ((1u << lane) - 1u))] = (int)j;
+    if (in) {
+        const int pos = base + __popc(peers & ((1u << lane) - 1u));
+        sl.sigma[pos] = (int)j;
+        sl.scell[pos] = (unsigned char)(kc & 127);
+        sl.spid[pos] = pid[j];
+    }
 }
 
 // ----------------------------------------------------- cell accumulation
@@ -343,10 +355,12 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
 constexpr int kTC = 64;  // thread-per-cell kernels: one thread per cell of a block (CELLS = 64)
 
 template <int D> constexpr int p2g_union_bytes() {
-    return Geo<D>::MAXP * 14 > Geo<D>::CELLS * Geo<D>::NST * 16 ? Geo<D>::MAXP * 14
+    return Geo<D>::MAXP * 11 > Geo<D>::CELLS * Geo<D>::NST * 16 ? Geo<D>::MAXP * 11
                                                                  : Geo<D>::CELLS * Geo<D>::NST * 16;
 }
-template <int D> constexpr int p2g_smem_bytes() { return p2g_union_bytes<D>() + 2 * (Geo<D>::CELLS + 2) * 4; }
+template <int D> constexpr int p2g_smem_bytes() {
+    return p2g_union_bytes<D>() + Geo<D>::MAXP * 4 + 2 * (Geo<D>::CELLS + 2) * 4;
+}
 
 // per-particle p2g math: returns c = m v - A dx f and A dx (for NodeAcc) and Ft
 template <int D>
@@ -387,18 +401,19 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
 // node b+o receives W_o (m v + A (o - f) dx) and W_o m.  F_{t+1} = Ft.
 // CTA = 64 threads = one thread per cell of the block (persistent over blocks).
 template <int D>
-__global__ void __launch_bounds__(kTC, 6) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
+__global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
                                                const int32_t* __restrict__ aid,
                                                const float* __restrict__ alpha, int* flags) {
     using G = Geo<D>;
     using L = Lay<D>;
     extern __shared__ __align__(16) unsigned char smem[];
-    int* s_idx = reinterpret_cast<int*>(smem);
+    int* s_idx = reinterpret_cast<int*>(smem);                       // phase 0 ...
     int* s_pid = s_idx + G::MAXP;
-    int* s_tmp = s_pid + G::MAXP;
-    short* s_cell = reinterpret_cast<short*>(s_tmp + G::MAXP);
-    float4* s_cb = reinterpret_cast<float4*>(smem);  // aliases the phase-0 arrays
-    int* s_cnt = reinterpret_cast<int*>(smem + p2g_union_bytes<D>());
+    short* s_tmp = reinterpret_cast<short*>(s_pid + G::MAXP);
+    unsigned char* s_cell = reinterpret_cast<unsigned char*>(s_tmp + G::MAXP);
+    float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... aliased by phase 2
+    int* s_ci = reinterpret_cast<int*>(smem + p2g_union_bytes<D>());  // canonical state index
+    int* s_cnt = s_ci + G::MAXP;
     int* s_cst = s_cnt + G::CELLS + 2;
     const int tid = threadIdx.x, lane = tid & 31;
     const int nact = *sl.nactive;
@@ -411,33 +426,21 @@ __global__ void __launch_bounds__(kTC, 6) k_p2g(KParams p, SlotView sl, StateVie
             if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
             continue;
         }
-        // ---- phase 0: cells, then canonical (cell, particle id) order
+        // ---- phase 0: canonical (cell, particle id) order of the block's list.  The
+        // scatter wrote each entry's cell and particle id next to it: coalesced loads only.
         for (int q = tid; q < G::CELLS + 2; q += kTC) s_cnt[q] = 0;
+#pragma unroll 4
+        for (int q = tid; q < n; q += kTC) {
+            s_idx[q] = sl.sigma[start + q];
+            s_pid[q] = sl.spid[start + q];
+            s_cell[q] = sl.scell[start + q];
+        }
         __syncthreads();
         for (int q0 = 0; q0 < n; q0 += kTC) {
             const int q = q0 + tid;
             const bool in = q < n;
-            int cell = G::CELLS;
-            if (in) {
-                const int i = sl.sigma[start + q];
-                float x[3];
-#pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = S.x[(int64_t)i * D + k];
-                int b[3];
-                bool ok = base_cell<D>(p, x, b);
-                int lb[3] = {0, 0, 0};
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    lb[k] = b[k] - c0[k];
-                    ok = ok && lb[k] >= 0 && lb[k] < G::B;
-                }
-                if (ok) cell = cell_of<D>(lb);
-                else atomicOr(flags, FLAG_OUT_OF_DOMAIN);
-                s_idx[q] = i;
-                s_pid[q] = S.pid[i];
-                s_cell[q] = (short)cell;
-            }
-            const unsigned peers = __match_any_sync(0xffffffffu, in ? cell : -1);
+            const int cell = in ? (int)s_cell[q] : -1;
+            const unsigned peers = __match_any_sync(0xffffffffu, cell);
             if (in && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[cell], __popc(peers));
         }
         __syncthreads();
@@ -461,13 +464,13 @@ __global__ void __launch_bounds__(kTC, 6) k_p2g(KParams p, SlotView sl, StateVie
         for (int q0 = 0; q0 < n; q0 += kTC) {  // bucket by cell (order inside a cell arbitrary)
             const int q = q0 + tid;
             const bool in = q < n;
-            const int cell = in ? s_cell[q] : -1;
+            const int cell = in ? (int)s_cell[q] : -1;
             const unsigned peers = __match_any_sync(0xffffffffu, cell);
             const int leader = __ffs(peers) - 1;
             int base = 0;
             if (in && lane == leader) base = atomicAdd(&s_cnt[cell], __popc(peers));
             base = __shfl_sync(0xffffffffu, base, leader);
-            if (in) s_tmp[base + __popc(peers & ((1u << lane) - 1u))] = q;
+            if (in) s_tmp[base + __popc(peers & ((1u << lane) - 1u))] = (short)q;
         }
         __syncthreads();
         for (int r = tid; r < n; r += kTC) {  // rank by particle id inside the cell
@@ -475,41 +478,53 @@ __global__ void __launch_bounds__(kTC, 6) k_p2g(KParams p, SlotView sl, StateVie
             const int cell = s_cell[q], pq = s_pid[q];
             int rank = 0;
             for (int m = s_cst[cell]; m < s_cst[cell + 1]; ++m) rank += s_pid[s_tmp[m]] < pq;
-            const int fpos = start + s_cst[cell] + rank;
-            sl.sigma[fpos] = s_idx[q];
-            if (Sn.pid) Sn.pid[fpos] = pq;
+            const int fl = s_cst[cell] + rank;
+            s_ci[fl] = s_idx[q];
+            sl.sigma[start + fl] = s_idx[q];
+            if (Sn.pid) Sn.pid[start + fl] = pq;
         }
         for (int c = tid; c <= G::CELLS; c += kTC) sl.cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
+        if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
         __syncthreads();
-        // ---- phase 1: thread = cell, particles of the cell in canonical order
+        // ---- phase 1: thread = cell, particles of the cell in canonical order, next one prefetched
         {
             NodeAcc<D, true> acc;
             acc.zero();
-            const int lo = start + s_cst[tid], hi = start + s_cst[tid + 1];
-            for (int j = lo; j < hi; ++j) {
-                const int i = sl.sigma[j];
+            const int lo = s_cst[tid], hi = s_cst[tid + 1];
+            float nx[3], nvc[L::VC], nF[L::FF];
+            int npid = 0;
+#define MPM_P2G_FETCH(R)                                                                  \
+    do {                                                                                  \
+        const int i_ = s_ci[(R)];                                                          \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) nx[k] = __ldg(S.x + (int64_t)i_ * D + k); \
+        _Pragma("unroll") for (int q = 0; q < L::VC; ++q) nvc[q] = __ldg(S.vc + (int64_t)i_ * L::VC + q); \
+        _Pragma("unroll") for (int q = 0; q < L::FF; ++q) nF[q] = __ldg(S.f + (int64_t)i_ * L::FF + q); \
+        if (aid) npid = __ldg(aid + __ldg(S.pid + i_));                                    \
+    } while (0)
+            if (lo < hi) MPM_P2G_FETCH(lo);
+            for (int r = lo; r < hi; ++r) {
                 float x[3], vc[L::VC], F[L::FF];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
+                for (int k = 0; k < D; ++k) x[k] = nx[k];
 #pragma unroll
-                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + (int64_t)i * L::VC + q);
+                for (int q = 0; q < L::VC; ++q) vc[q] = nvc[q];
 #pragma unroll
-                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + (int64_t)i * L::FF + q);
-                float act = 0.0f;
-                if (aid) {
-                    const int a_id = aid[S.pid[i]];
-                    act = a_id >= 0 ? alpha[a_id] : 0.0f;
-                }
+                for (int q = 0; q < L::FF; ++q) F[q] = nF[q];
+                const int a_id = npid;  // actuator id (prefetched), valid when aid != null
+                if (r + 1 < hi) MPM_P2G_FETCH(r + 1);
+#undef MPM_P2G_FETCH
+                const float act = (aid && a_id >= 0) ? alpha[a_id] : 0.0f;
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
                 if (!p2g_particle<D>(p, x, vc, F, act, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
                 acc.add(w, c, Adx);
                 if (Sn.f) {
-                    float* dst = Sn.f + (int64_t)j * L::FF;
+                    float* dst = Sn.f + (int64_t)(start + r) * L::FF;
 #pragma unroll
                     for (int q = 0; q < D * D; ++q) dst[q] = Ft[q];
                 }
             }
-            acc.store(s_cb, tid);  // the phase-0 arrays are dead after the barrier above
+            __syncthreads();  // everybody is done with the phase-0 arrays the buffer aliases
+            acc.store(s_cb, tid);
         }
         __syncthreads();
         // ---- phase 2: node tile (plain stores)
@@ -644,14 +659,17 @@ __global__ void __launch_bounds__(kT) k_g2p(KParams p, SlotView sl, StateView S,
                 if (!fin) atomicOr(flags, FLAG_NONFINITE);
                 if (keys) {
                     int b[3];
+                    int cell = G::CELLS;
                     if (base_cell<D>(p, xn, b)) {
                         int bb[3] = {b[0] >> G::LOGB, b[1] >> G::LOGB, b[2] >> G::LOGB};
+                        int lc[3] = {b[0] & (G::B - 1), b[1] & (G::B - 1), b[2] & (G::B - 1)};
                         key = block_lin<D>(p, e, bb);
+                        cell = cell_of<D>(lc);
                     } else {
                         atomicOr(flags, FLAG_OUT_OF_DOMAIN);
                         key = bid;  // p2g of the next step drops it into the junk bucket
                     }
-                    keys[j] = key;
+                    keys[j] = key * 128 + cell;
                 }
             }
             if (keys) count_key(in, key, bcount);
@@ -1090,11 +1108,16 @@ static unsigned pgrid(const KParams& p, int kind) {
 void launch_bin_keys(const KParams& p, const float* x, int* keys, int* bcount, int* flags, cudaStream_t s) {
     DISPATCH(p.dim, k_bin_keys<DIM><<<nblk(p.N * p.E), kT, 0, s>>>(p, x, keys, bcount, flags));
 }
-void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* flags, cudaStream_t s) {
-    k_bin_scan<<<1, kScanT, 0, s>>>(p, bcount, cursor, sl, flags);
+int scan_chunks(const KParams& p) { return (p.TB + kScanChunk - 1) / kScanChunk; }
+void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
+                     cudaStream_t s) {
+    const int nc = scan_chunks(p);
+    k_bin_scan<0><<<nc, kT, 0, s>>>(p, bcount, cursor, sl, (int2*)part, flags);
+    k_bin_scan<1><<<nc, kT, 0, s>>>(p, bcount, cursor, sl, (int2*)part, flags);
 }
-void launch_bin_scatter(const KParams& p, const int* keys, int* cursor, int* sigma, cudaStream_t s) {
-    k_bin_scatter<<<nblk(p.N * p.E), kT, 0, s>>>(p, keys, cursor, sigma);
+void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
+                        cudaStream_t s) {
+    k_bin_scatter<<<nblk(p.N * p.E), kT, 0, s>>>(p, keys, pid, cursor, sl);
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {

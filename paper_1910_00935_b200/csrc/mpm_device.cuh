@@ -107,6 +107,15 @@ template <int D> __device__ __forceinline__ void cof(const float* F, float* K) {
     }
 }
 
+// element (i, e) of a row-major d x d matrix for a runtime column e, without
+// dynamic register indexing (which would spill the matrix to local memory)
+template <int D> __device__ __forceinline__ float column(const float* M, int i, int e) {
+    float v = M[i * D];
+#pragma unroll
+    for (int k = 1; k < D; ++k) v = e == k ? M[i * D + k] : v;
+    return v;
+}
+
 // Kirchhoff stress tau(Ft) of the material (R2) plus actuation (R8).
 // NH : tau = mu (F F^T - I) + lambda ln J I
 // FCR: tau = 2 mu (F - R) F^T + lambda (J - 1) J I   (2D closed-form polar R)
@@ -141,12 +150,15 @@ __device__ __forceinline__ bool kirchhoff(const KParams& p, const float* Fm, flo
         tau[3] = 2.0f * p.mu * (M2 * Fm[2] + M3 * Fm[3]) + iso;
     }
     if (act != 0.0f) {
-        const int e = p.act_axis;
+        // q = F e (column act_axis); selects keep F in registers (no dynamic indexing)
+        float q[D];
+#pragma unroll
+        for (int i = 0; i < D; ++i) q[i] = column<D>(Fm, i, p.act_axis);
         float s = p.kappa * act;
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
-            for (int j = 0; j < D; ++j) tau[i * D + j] = fmaf(s * Fm[i * D + e], Fm[j * D + e], tau[i * D + j]);
+            for (int j = 0; j < D; ++j) tau[i * D + j] = fmaf(s * q[i], q[j], tau[i * D + j]);
     }
     return ok;
 }
@@ -203,7 +215,7 @@ __device__ __forceinline__ float kirchhoff_adj(const KParams& p, const float* Fm
         const int e = p.act_axis;
         float q[D], sq[D];
 #pragma unroll
-        for (int i = 0; i < D; ++i) q[i] = Fm[i * D + e];
+        for (int i = 0; i < D; ++i) q[i] = column<D>(Fm, i, e);
 #pragma unroll
         for (int i = 0; i < D; ++i) {
             float s = 0.0f;
@@ -215,7 +227,10 @@ __device__ __forceinline__ float kirchhoff_adj(const KParams& p, const float* Fm
         abar *= 0.5f * p.kappa;  // q^T tb q = 1/2 q^T (tb + tb^T) q
         float s = p.kappa * act;
 #pragma unroll
-        for (int i = 0; i < D; ++i) Fb[i * D + e] = fmaf(s, sq[i], Fb[i * D + e]);
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int k = 0; k < D; ++k)
+                if (k == e) Fb[i * D + k] = fmaf(s, sq[i], Fb[i * D + k]);
     }
     return abar;
 }
