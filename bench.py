@@ -49,17 +49,15 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
-def _workload(name: str, world: int):
+def _workload(name: str, world: int, rank: int = 0):
+    """config, this rank's episode indices, scaling kind.  C4: 64 episodes split over
+    the ranks (strong scaling); others: one episode per rank (weak scaling)."""
     from paper_1910_00935_b200 import workloads as W
+    from paper_1910_00935_b200.dist import episode_shard
     p = W.config(name)
     if name == "c4":
-        total = int(p["episodes"])
-        per = max(1, total // world)
-        scaling = "strong"
-    else:
-        per = 1
-        scaling = "weak"
-    return p, per, scaling
+        return p, episode_shard(int(p["episodes"]), rank, world), "strong"
+    return p, range(rank, rank + 1), "weak"
 
 
 def _describe(p, n_particles, episodes, world, k):
@@ -166,7 +164,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     from paper_1910_00935_b200 import workloads as W
-    p, per, scaling = _workload(args.config, 1)
+    p, _, scaling = _workload(args.config, 1)
     inp = W.make_inputs(p)
     steps = 1
     for _ in range(args.warmup):
@@ -200,15 +198,24 @@ def run_ours(args):
     from paper_1910_00935_b200 import mpm, workloads as W
 
     rank, world, local = _env_int("RANK", 0), _env_int("WORLD_SIZE", 1), _env_int("LOCAL_RANK", 0)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    p, per, scaling = _workload(args.config, world)
+        # NCCL over NVLink/NVSwitch; BENCH_DIST_BACKEND=gloo only for exercising the
+        # multi-rank code path with several ranks on one GPU (NCCL rejects that)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    from paper_1910_00935_b200.dist import allreduce_shared_grad, max_over_ranks
+    p, shard, scaling = _workload(args.config, world, rank)
+    per = len(shard)
     k = int(args.k_ckpt or p["k_ckpt"])
     T = int(p["steps"])
     if args.config == "c4":
-        inps = [W.make_inputs(p, episode=rank * per + e) for e in range(per)]
+        inps = [W.make_inputs(p, episode=e) for e in shard]
     else:
         inps = [W.make_inputs(p, rank=rank)]
     N = len(inps[0]["x"])
@@ -245,10 +252,10 @@ def run_ours(args):
         if world > 1:
             # the one exchange of the path: sum of the shared-parameter gradient over ranks
             if shared_buf.is_cuda:
-                dist.all_reduce(shared_buf)
+                allreduce_shared_grad(shared_buf)
             else:
                 t = shared_buf.to(dev)
-                dist.all_reduce(t)
+                allreduce_shared_grad(t)
                 shared_buf.copy_(t)
 
     def timed(K, fn):
@@ -263,12 +270,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ms = s.elapsed_time(e)
-        if world > 1:
-            t = torch.tensor([ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
-        return ms
+        return max_over_ranks(s.elapsed_time(e), dev)
 
     dev_step = lambda: step(devin, loss_d, shared_d, gdev)  # noqa: E731
     host_step = lambda: step(host, loss_h, shared_h, None)  # noqa: E731
@@ -297,7 +299,13 @@ def run_ours(args):
     sim.set_profiling(False)
     ms_e2e = timed(args.steps, host_step)
 
-    particle_steps = float(N) * per * T * world * args.steps
+    # units of all ranks (C4 shards may differ by one episode: count them exactly)
+    if world > 1:
+        tot = torch.tensor([float(N) * per * T * args.steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot)
+        particle_steps = float(tot.item())
+    else:
+        particle_steps = float(N) * per * T * args.steps
     value = particle_steps / (ms / 1e3)
     e2e_value = particle_steps / (ms_e2e / 1e3)
     h2d = sum(int(t.numel() * t.element_size()) for t in host.values())
