@@ -190,6 +190,23 @@ def run_reference(args):
     return 0
 
 
+def _pick_k(p, N, per, T, dev):
+    """Smallest checkpoint interval whose tape fits in 90% of free HBM (Appendix D.2:
+    k trades re-forward work for memory; on a 180 GB B200 the 1M-particle cube fits k = 2)."""
+    import torch
+    from paper_1910_00935_b200 import mpm
+    free, _ = torch.cuda.mem_get_info(dev)
+    for k in (1, 2, 4, 8, 16, 32, 64, 128):
+        if k > T:
+            break
+        probe = mpm.sim_from_config(p, N, episodes=per, max_steps=T, k_ckpt=k, probe_only=True)
+        need = probe.workspace_bytes
+        probe.close()
+        if need < 0.9 * free:
+            return k
+    return int(p.get("k_ckpt", 32))
+
+
 # -------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -212,7 +229,6 @@ def run_ours(args):
     from paper_1910_00935_b200.dist import allreduce_shared_grad, max_over_ranks
     p, shard, scaling = _workload(args.config, world, rank)
     per = len(shard)
-    k = int(args.k_ckpt or p["k_ckpt"])
     T = int(p["steps"])
     if args.config == "c4":
         inps = [W.make_inputs(p, episode=e) for e in shard]
@@ -224,6 +240,7 @@ def run_ours(args):
     host["theta"] = torch.from_numpy(inps[0]["theta"]).pin_memory()
     devin = {key: t.to(dev) for key, t in host.items()}
 
+    k = int(args.k_ckpt) if args.k_ckpt else _pick_k(p, N, per, T, dev)
     sim = mpm.sim_from_config(p, N, episodes=per, max_steps=T, k_ckpt=k)
     nth = sim.n_theta
     shared_len = nth if nth > 0 else per * p["dim"]

@@ -539,11 +539,11 @@ __global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateVie
 }
 
 // stage U = grid_op(sum of covering tiles) for the CTA's tile
-template <int D>
+template <int D, int NT = kT>
 __device__ __forceinline__ void stage_velocity(const KParams& p, const SlotView& sl, int e, const int c0[3],
                                                float4* sU) {
     using G = Geo<D>;
-    for (int q = threadIdx.x; q < G::TN; q += kT) {
+    for (int q = threadIdx.x; q < G::TN; q += NT) {
         int n[3];
         local_node<D>(q, n);
         const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
@@ -609,68 +609,95 @@ __device__ __forceinline__ void gather_moments(const float4* __restrict__ sU, co
 }
 
 // ----------------------------------------------------------------- G2P
+constexpr int kTG = 128;  // g2p CTA: smaller CTAs -> more independent blocks in flight per SM
 // v' = sum W U; C' = 4/dx sum W U (o - f)^T = 4/dx (Sb - v' f^T); x' = x + dt v'
 template <int D>
-__global__ void __launch_bounds__(kT) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
-                                            int* __restrict__ keys, int* __restrict__ bcount, int* flags) {
+__device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __restrict__ sU, const float* x,
+                                            const int c0[3], int j, int e, int bid, const StateView& Sn,
+                                            int* __restrict__ keys, int* flags) {
     using G = Geo<D>;
     using L = Lay<D>;
+    const float c4 = 4.0f * p.inv_dx;
+    int lb[3];
+    float fx[3], w[3][3], dw[3][3];
+    particle_weights<D>(p, x, c0, lb, fx, w, dw);
+    float S0[3], Sb[3][3];
+    gather_moments<D>(sU, lb, w, S0, Sb);
+    float xn[3];
+    bool fin = true;
+    float* dvc = Sn.vc + (int64_t)j * L::VC;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        xn[a] = fmaf(p.dt, S0[a], x[a]);
+        Sn.x[(int64_t)j * D + a] = xn[a];
+        dvc[a] = S0[a];
+        fin = fin && isfinite(S0[a]);
+#pragma unroll
+        for (int b = 0; b < D; ++b) dvc[D + a * D + b] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
+    }
+    if (!fin) atomicOr(flags, FLAG_NONFINITE);
+    int key = -1;
+    if (keys) {
+        int b[3];
+        int cell = G::CELLS;
+        if (base_cell<D>(p, xn, b)) {
+            int bb[3] = {b[0] >> G::LOGB, b[1] >> G::LOGB, b[2] >> G::LOGB};
+            int lc[3] = {b[0] & (G::B - 1), b[1] & (G::B - 1), b[2] & (G::B - 1)};
+            key = block_lin<D>(p, e, bb);
+            cell = cell_of<D>(lc);
+        } else {
+            atomicOr(flags, FLAG_OUT_OF_DOMAIN);
+            key = bid;  // p2g of the next step drops it into the junk bucket
+        }
+        keys[j] = key * 128 + cell;
+    }
+    return key;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
+                                            int* __restrict__ keys, int* __restrict__ bcount, int* flags) {
+    using G = Geo<D>;
     __shared__ float4 sU[G::TN];
-    __shared__ int s_nv;
     const int tid = threadIdx.x;
     const int nact = *sl.nactive;
-    const float c4 = 4.0f * p.inv_dx;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         const int bid = sl.blist[bi];
         const int start = sl.bstart[bi];
+        const int nvalid = sl.cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        stage_velocity<D>(p, sl, e, c0, sU);
-        if (tid == 0) s_nv = sl.cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
+        // particle loads of the first two passes go out before the tile staging
+        float xa[3], xb[3];
+        const bool va = tid < nvalid, vb = tid + kTG < nvalid;
+        if (va) {
+            const int i = sl.sigma[start + tid];
+#pragma unroll
+            for (int k = 0; k < D; ++k) xa[k] = __ldg(S.x + (int64_t)i * D + k);
+        }
+        if (vb) {
+            const int i = sl.sigma[start + tid + kTG];
+#pragma unroll
+            for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + (int64_t)i * D + k);
+        }
+        stage_velocity<D, kTG>(p, sl, e, c0, sU);
         __syncthreads();
-        const int nvalid = s_nv;
-        for (int r0 = 0; r0 < nvalid; r0 += kT) {
+        int key = -1;
+        if (va) key = g2p_particle<D>(p, sU, xa, c0, start + tid, e, bid, Sn, keys, flags);
+        if (keys) count_key(va, key, bcount);
+        key = -1;
+        if (vb) key = g2p_particle<D>(p, sU, xb, c0, start + tid + kTG, e, bid, Sn, keys, flags);
+        if (keys) count_key(vb, key, bcount);
+        for (int r0 = 2 * kTG; r0 < nvalid; r0 += kTG) {
             const int r = r0 + tid;
             const bool in = r < nvalid;
-            int key = -1;
+            key = -1;
             if (in) {
-                const int j = start + r;
-                const int i = sl.sigma[j];
+                const int i = sl.sigma[start + r];
                 float x[3];
 #pragma unroll
                 for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
-                int lb[3];
-                float fx[3], w[3][3], dw[3][3];
-                particle_weights<D>(p, x, c0, lb, fx, w, dw);
-                float S0[3], Sb[3][3];
-                gather_moments<D>(sU, lb, w, S0, Sb);
-                float xn[3];
-                bool fin = true;
-                float* dvc = Sn.vc + (int64_t)j * L::VC;
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    xn[a] = fmaf(p.dt, S0[a], x[a]);
-                    Sn.x[(int64_t)j * D + a] = xn[a];
-                    dvc[a] = S0[a];
-                    fin = fin && isfinite(S0[a]);
-#pragma unroll
-                    for (int b = 0; b < D; ++b) dvc[D + a * D + b] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
-                }
-                if (!fin) atomicOr(flags, FLAG_NONFINITE);
-                if (keys) {
-                    int b[3];
-                    int cell = G::CELLS;
-                    if (base_cell<D>(p, xn, b)) {
-                        int bb[3] = {b[0] >> G::LOGB, b[1] >> G::LOGB, b[2] >> G::LOGB};
-                        int lc[3] = {b[0] & (G::B - 1), b[1] & (G::B - 1), b[2] & (G::B - 1)};
-                        key = block_lin<D>(p, e, bb);
-                        cell = cell_of<D>(lc);
-                    } else {
-                        atomicOr(flags, FLAG_OUT_OF_DOMAIN);
-                        key = bid;  // p2g of the next step drops it into the junk bucket
-                    }
-                    keys[j] = key * 128 + cell;
-                }
+                key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags);
             }
             if (keys) count_key(in, key, bcount);
         }
@@ -687,7 +714,7 @@ template <int D> constexpr int g2pg_smem_bytes() {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kTC, 4) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
+__global__ void __launch_bounds__(kTC, 6) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
                                                     float4* __restrict__ ubar, float* __restrict__ xbp) {
     using G = Geo<D>;
     using L = Lay<D>;
@@ -719,75 +746,99 @@ __global__ void __launch_bounds__(kTC, 4) k_g2p_grad(KParams p, SlotView sl, Sta
         }
         for (int c = tid; c <= G::CELLS; c += kTC) s_cst[c] = sl.cstart[(int64_t)bi * (G::CELLS + 1) + c];
         __syncthreads();
+        const int lo = start + s_cst[tid], hi = start + s_cst[tid + 1];
+        // pass 1: gather part (W_bar, f_bar -> partial x_bar), one particle at a time
+        for (int j = lo; j < hi; ++j) {
+            const int i = sl.sigma[j];
+            float x[3];
+#pragma unroll
+            for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
+            float xb[3], vh[3], B[D * D];
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                xb[a] = __ldg(Sbn.x + (int64_t)j * D + a);
+                vh[a] = fmaf(p.dt, xb[a], __ldg(Sbn.vc + (int64_t)j * L::VC + a));
+            }
+#pragma unroll
+            for (int q = 0; q < D * D; ++q) B[q] = c4 * __ldg(Sbn.vc + (int64_t)j * L::VC + D + q);
+            int lb[3];
+            float fx[3], w[3][3], dw[3][3];
+            particle_weights<D>(p, x, c0, lb, fx, w, dw);
+            float cp[3];  // c' = vh - B f ; t_o = c' + B o
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                float s = vh[a];
+#pragma unroll
+                for (int b = 0; b < D; ++b) s = fmaf(-B[a * D + b], fx[b], s);
+                cp[a] = s;
+            }
+            float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int o0 = 0; o0 < 3; ++o0) {
+                float tx[3];
+#pragma unroll
+                for (int a = 0; a < D; ++a) tx[a] = fmaf((float)o0, B[a * D], cp[a]);
+#pragma unroll
+                for (int o1 = 0; o1 < 3; ++o1) {
+                    float ty[3];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) ty[a] = fmaf((float)o1, B[a * D + 1], tx[a]);
+#pragma unroll
+                    for (int o2 = 0; o2 < (D == 3 ? 3 : 1); ++o2) {
+                        float t[3];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) t[a] = D == 3 ? fmaf((float)o2, B[a * D + 2], ty[a]) : ty[a];
+                        const float wyz = D == 3 ? w[1][o1] * w[2][o2] : w[1][o1];
+                        const float W = w[0][o0] * wyz;
+                        float gW[3];
+                        gW[0] = dw[0][o0] * wyz;
+                        gW[1] = D == 3 ? w[0][o0] * dw[1][o1] * w[2][o2] : w[0][o0] * dw[1][o1];
+                        if (D == 3) gW[2] = w[0][o0] * w[1][o1] * dw[2][o2];
+                        const float4 u4 = sU[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
+                        const float u[3] = {u4.x, u4.y, u4.z};
+                        float Wb = 0.0f;
+#pragma unroll
+                        for (int a = 0; a < D; ++a) {
+                            Wb = fmaf(u[a], t[a], Wb);
+                            S0[a] = fmaf(W, u[a], S0[a]);
+                        }
+#pragma unroll
+                        for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < D; ++k) {  // fb_k -= (B^T S0)_k
+                float s = 0.0f;
+#pragma unroll
+                for (int a = 0; a < D; ++a) s = fmaf(B[a * D + k], S0[a], s);
+                xbp[(int64_t)j * D + k] = fmaf(p.inv_dx, fb[k] - s, xb[k]);
+            }
+        }
+        // pass 2: U_bar scatter of the cell, accumulated in registers (inputs re-read, L1/L2 hits)
         {
             NodeAcc<D, false> acc;
             acc.zero();
-            const int lo = start + s_cst[tid], hi = start + s_cst[tid + 1];
             for (int j = lo; j < hi; ++j) {
                 const int i = sl.sigma[j];
-                float x[3];
+                float x[3], vh[3], B[D * D];
 #pragma unroll
                 for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
-                float xb[3], vh[3], B[D * D];
 #pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    xb[a] = __ldg(Sbn.x + (int64_t)j * D + a);
-                    vh[a] = fmaf(p.dt, xb[a], __ldg(Sbn.vc + (int64_t)j * L::VC + a));
-                }
+                for (int a = 0; a < D; ++a)
+                    vh[a] = fmaf(p.dt, __ldg(Sbn.x + (int64_t)j * D + a), __ldg(Sbn.vc + (int64_t)j * L::VC + a));
 #pragma unroll
                 for (int q = 0; q < D * D; ++q) B[q] = c4 * __ldg(Sbn.vc + (int64_t)j * L::VC + D + q);
                 int lb[3];
                 float fx[3], w[3][3], dw[3][3];
                 particle_weights<D>(p, x, c0, lb, fx, w, dw);
-                float cp[3];  // c' = vh - B f ; t_o = c' + B o
+                float cp[3];
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
                     float s = vh[a];
 #pragma unroll
                     for (int b = 0; b < D; ++b) s = fmaf(-B[a * D + b], fx[b], s);
                     cp[a] = s;
-                }
-                float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-                for (int o0 = 0; o0 < 3; ++o0) {
-                    float tx[3];
-#pragma unroll
-                    for (int a = 0; a < D; ++a) tx[a] = fmaf((float)o0, B[a * D], cp[a]);
-#pragma unroll
-                    for (int o1 = 0; o1 < 3; ++o1) {
-                        float ty[3];
-#pragma unroll
-                        for (int a = 0; a < D; ++a) ty[a] = fmaf((float)o1, B[a * D + 1], tx[a]);
-#pragma unroll
-                        for (int o2 = 0; o2 < (D == 3 ? 3 : 1); ++o2) {
-                            float t[3];
-#pragma unroll
-                            for (int a = 0; a < D; ++a) t[a] = D == 3 ? fmaf((float)o2, B[a * D + 2], ty[a]) : ty[a];
-                            const float wyz = D == 3 ? w[1][o1] * w[2][o2] : w[1][o1];
-                            const float W = w[0][o0] * wyz;
-                            float gW[3];
-                            gW[0] = dw[0][o0] * wyz;
-                            gW[1] = D == 3 ? w[0][o0] * dw[1][o1] * w[2][o2] : w[0][o0] * dw[1][o1];
-                            if (D == 3) gW[2] = w[0][o0] * w[1][o1] * dw[2][o2];
-                            const float4 u4 = sU[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
-                            const float u[3] = {u4.x, u4.y, u4.z};
-                            float Wb = 0.0f;
-#pragma unroll
-                            for (int a = 0; a < D; ++a) {
-                                Wb = fmaf(u[a], t[a], Wb);
-                                S0[a] = fmaf(W, u[a], S0[a]);
-                            }
-#pragma unroll
-                            for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
-                        }
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < D; ++k) {  // fb_k -= (B^T S0)_k
-                    float s = 0.0f;
-#pragma unroll
-                    for (int a = 0; a < D; ++a) s = fmaf(B[a * D + k], S0[a], s);
-                    xbp[(int64_t)j * D + k] = fmaf(p.inv_dx, fb[k] - s, xb[k]);
                 }
                 acc.add(w, cp, B);
             }
@@ -806,8 +857,131 @@ __global__ void __launch_bounds__(kTC, 4) k_g2p_grad(KParams p, SlotView sl, Sta
 // vb = sum W m Pb; Ab = sum W Pb dpos^T; Wb = Pb.(m v + A dpos) + Mb m;
 // fb += Wb dW/df - dx W A^T Pb; Cb = m Ab + dt Ftb F^T; taub = -dt V 4/dx^2 Ab;
 // Ftb = Fb' + stress/actuation adjoint; Fb = (I + dt C)^T Ftb; xb += fb/dx.
+// per-particle p2g_grad; returns the actuation-gradient contribution kappa q^T taub q
 template <int D>
-__global__ void __launch_bounds__(kT) k_p2g_grad(KParams p, SlotView sl, StateView S,
+__device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float4* __restrict__ sG,
+                                                   const float* x, const float* vc, const float* F,
+                                                   const float* Fbn, const float* xbp, bool has_act,
+                                                   float act, const int c0[3], int64_t i, const AdjView& Sb,
+                                                   int* flags) {
+    using L = Lay<D>;
+    const float* v = vc;
+    const float* C = vc + D;
+    int lb[3];
+    float fx[3], w[3][3], dw[3][3];
+    particle_weights<D>(p, x, c0, lb, fx, w, dw);
+    float Ft[D * D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+            float s = 0.0f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fmaf(C[a * D + k], F[k * D + b], s);
+            Ft[a * D + b] = fmaf(p.dt, s, F[a * D + b]);
+        }
+    float tau[D * D], Adx[D * D], c[3];
+    kirchhoff<D>(p, Ft, act, tau);
+#pragma unroll
+    for (int q = 0; q < D * D; ++q) Adx[q] = p.dx * fmaf(p.stress_scale, tau[q], p.p_mass * C[q]);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {  // m v + A dpos = c + Adx o
+        float s = p.p_mass * v[a];
+#pragma unroll
+        for (int b = 0; b < D; ++b) s = fmaf(-Adx[a * D + b], fx[b], s);
+        c[a] = s;
+    }
+    float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f}, Sm[3][3];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) (&Sm[0][0])[q] = 0.f;
+#pragma unroll
+    for (int o0 = 0; o0 < 3; ++o0) {
+        float mx[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) mx[a] = fmaf((float)o0, Adx[a * D], c[a]);
+#pragma unroll
+        for (int o1 = 0; o1 < 3; ++o1) {
+            float my[3];
+#pragma unroll
+            for (int a = 0; a < D; ++a) my[a] = fmaf((float)o1, Adx[a * D + 1], mx[a]);
+#pragma unroll
+            for (int o2 = 0; o2 < (D == 3 ? 3 : 1); ++o2) {
+                float m[3];
+#pragma unroll
+                for (int a = 0; a < D; ++a) m[a] = D == 3 ? fmaf((float)o2, Adx[a * D + 2], my[a]) : my[a];
+                const float wyz = D == 3 ? w[1][o1] * w[2][o2] : w[1][o1];
+                const float W = w[0][o0] * wyz;
+                float gW[3];
+                gW[0] = dw[0][o0] * wyz;
+                gW[1] = D == 3 ? w[0][o0] * dw[1][o1] * w[2][o2] : w[0][o0] * dw[1][o1];
+                if (D == 3) gW[2] = w[0][o0] * w[1][o1] * dw[2][o2];
+                const float4 g4 = sG[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
+                const float gP[3] = {g4.x, g4.y, g4.z};
+                float Wb = g4.w * p.p_mass;
+                const int o[3] = {o0, o1, o2};
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    Wb = fmaf(gP[a], m[a], Wb);
+                    const float wg = W * gP[a];
+                    S0[a] += wg;
+#pragma unroll
+                    for (int b = 0; b < D; ++b)
+                        if (o[b]) Sm[b][a] = fmaf((float)o[b], wg, Sm[b][a]);
+                }
+#pragma unroll
+                for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
+            }
+        }
+    }
+    // Ab[a][b] = dx (Sm[b][a] - S0[a] f[b]);  fb_k -= (Adx^T S0)_k
+    float Ab[D * D], taub[D * D], Ftb[D * D];
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) Ab[a * D + b] = p.dx * fmaf(-S0[a], fx[b], Sm[b][a]);
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        float s = 0.0f;
+#pragma unroll
+        for (int a = 0; a < D; ++a) s = fmaf(Adx[a * D + k], S0[a], s);
+        fb[k] -= s;
+    }
+#pragma unroll
+    for (int q = 0; q < D * D; ++q) {
+        taub[q] = p.stress_scale * Ab[q];
+        Ftb[q] = Fbn[q];
+    }
+    const float abar = kirchhoff_adj<D>(p, Ft, has_act, act, taub, Ftb);
+    float* dvc = Sb.vc + i * L::VC;
+    float* dF = Sb.f + i * L::FF;
+    bool fin = true;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+            float sF = Ftb[a * D + b], sC = 0.0f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                sF = fmaf(p.dt * C[k * D + a], Ftb[k * D + b], sF);
+                sC = fmaf(Ftb[a * D + k], F[b * D + k], sC);
+            }
+            dF[a * D + b] = sF;
+            dvc[D + a * D + b] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
+            fin = fin && isfinite(sF);
+        }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        Sb.x[i * D + a] = fmaf(p.inv_dx, fb[a], xbp[a]);
+        dvc[a] = p.p_mass * S0[a];
+    }
+    if (!fin) atomicOr(flags, FLAG_NONFINITE);
+    return abar;
+}
+
+constexpr int kTP = 128;  // p2g_grad CTA
+
+template <int D>
+__global__ void __launch_bounds__(kTP, 4) k_p2g_grad(KParams p, SlotView sl, StateView S,
                                                  const int32_t* __restrict__ aid,
                                                  const float* __restrict__ alpha,
                                                  const float4* __restrict__ ubar, AdjView Sbn,
@@ -816,166 +990,66 @@ __global__ void __launch_bounds__(kT) k_p2g_grad(KParams p, SlotView sl, StateVi
     using G = Geo<D>;
     using L = Lay<D>;
     __shared__ float4 sG[G::TN];
-    __shared__ float s_ab[kW][32];
-    __shared__ int s_nvalid;
+    __shared__ float s_ab[kTP / 32][32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nact = *sl.nactive;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         const int bid = sl.blist[bi];
         const int start = sl.bstart[bi];
+        const int nvalid = sl.cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        for (int q = tid; q < G::TN; q += kT) {
-            int n[3];
-            local_node<D>(q, n);
-            const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-            const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
-            float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (inside) {
-                const float4 pm = covered_sum<D>(p, e, g, sl.bmap, sl.tiles);
-                const float4 ub = covered_sum<D>(p, e, g, sl.bmap, ubar);
-                float u0[3], u1[3];
-                const bool z = grid_velocity<D>(p, g, pm, u0, u1);
-                if (!z) {
-                    const float denom = pm.w + p.eps_mass;
-                    const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
-                    out = make_float4(ub.x / denom, ub.y / denom, D == 3 ? ub.z / denom : 0.0f, -dot / denom);
-                }
-            }
-            sG[q] = out;
-        }
-        for (int q = tid; q < kW * 32; q += kT) (&s_ab[0][0])[q] = 0.0f;
-        if (tid == 0) s_nvalid = sl.cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
-        __syncthreads();
-        const int nvalid = s_nvalid;
-        for (int r0 = 0; r0 < nvalid; r0 += kT) {
+        for (int r0 = 0; r0 < nvalid; r0 += kTP) {
             const int r = r0 + tid;
             const bool in = r < nvalid;
+            // particle loads go out before the (first pass's) tile staging
+            float x[3], vc[L::VC], F[L::FF], Fbn[L::FF], xb[3];
+            int64_t i = 0;
             int a_id = -1;
-            float abar = 0.0f;
             if (in) {
                 const int j = start + r;
-                const int i = sl.sigma[j];
-                const int pid = S.pid[i];
-                float x[3], vc[L::VC], F[L::FF];
+                i = sl.sigma[j];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + i * D + k);
 #pragma unroll
-                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + (int64_t)i * L::VC + q);
+                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + i * L::VC + q);
 #pragma unroll
-                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + (int64_t)i * L::FF + q);
-                const float* v = vc;
-                const float* C = vc + D;
-                int lb[3];
-                float fx[3], w[3][3], dw[3][3];
-                particle_weights<D>(p, x, c0, lb, fx, w, dw);
-                float Ft[D * D];
+                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + i * L::FF + q);
 #pragma unroll
-                for (int a = 0; a < D; ++a)
+                for (int q = 0; q < L::FF; ++q) Fbn[q] = __ldg(Sbn.f + (int64_t)j * L::FF + q);
 #pragma unroll
-                    for (int b = 0; b < D; ++b) {
-                        float s = 0.0f;
-#pragma unroll
-                        for (int k = 0; k < D; ++k) s = fmaf(C[a * D + k], F[k * D + b], s);
-                        Ft[a * D + b] = fmaf(p.dt, s, F[a * D + b]);
-                    }
-                a_id = aid ? aid[pid] : -1;
-                const float act = a_id >= 0 ? alpha[a_id] : 0.0f;
-                float tau[D * D], Adx[D * D], c[3];
-                kirchhoff<D>(p, Ft, act, tau);
-#pragma unroll
-                for (int q = 0; q < D * D; ++q) Adx[q] = p.dx * fmaf(p.stress_scale, tau[q], p.p_mass * C[q]);
-#pragma unroll
-                for (int a = 0; a < D; ++a) {  // m v + A dpos = c + Adx o
-                    float s = p.p_mass * v[a];
-#pragma unroll
-                    for (int b = 0; b < D; ++b) s = fmaf(-Adx[a * D + b], fx[b], s);
-                    c[a] = s;
-                }
-                float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f}, Sm[3][3];
-#pragma unroll
-                for (int q = 0; q < 9; ++q) (&Sm[0][0])[q] = 0.f;
-#pragma unroll
-                for (int o0 = 0; o0 < 3; ++o0) {
-                    float mx[3];
-#pragma unroll
-                    for (int a = 0; a < D; ++a) mx[a] = fmaf((float)o0, Adx[a * D], c[a]);
-#pragma unroll
-                    for (int o1 = 0; o1 < 3; ++o1) {
-                        float my[3];
-#pragma unroll
-                        for (int a = 0; a < D; ++a) my[a] = fmaf((float)o1, Adx[a * D + 1], mx[a]);
-#pragma unroll
-                        for (int o2 = 0; o2 < (D == 3 ? 3 : 1); ++o2) {
-                            float m[3];
-#pragma unroll
-                            for (int a = 0; a < D; ++a) m[a] = D == 3 ? fmaf((float)o2, Adx[a * D + 2], my[a]) : my[a];
-                            const float wyz = D == 3 ? w[1][o1] * w[2][o2] : w[1][o1];
-                            const float W = w[0][o0] * wyz;
-                            float gW[3];
-                            gW[0] = dw[0][o0] * wyz;
-                            gW[1] = D == 3 ? w[0][o0] * dw[1][o1] * w[2][o2] : w[0][o0] * dw[1][o1];
-                            if (D == 3) gW[2] = w[0][o0] * w[1][o1] * dw[2][o2];
-                            const float4 g4 = sG[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
-                            const float gP[3] = {g4.x, g4.y, g4.z};
-                            float Wb = g4.w * p.p_mass;
-                            const int o[3] = {o0, o1, o2};
-#pragma unroll
-                            for (int a = 0; a < D; ++a) {
-                                Wb = fmaf(gP[a], m[a], Wb);
-                                const float wg = W * gP[a];
-                                S0[a] += wg;
-#pragma unroll
-                                for (int b = 0; b < D; ++b)
-                                    if (o[b]) Sm[b][a] = fmaf((float)o[b], wg, Sm[b][a]);
-                            }
-#pragma unroll
-                            for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
+                for (int k = 0; k < D; ++k) xb[k] = __ldg(xbp + (int64_t)j * D + k);
+                if (aid) a_id = __ldg(aid + __ldg(S.pid + i));
+            }
+            if (r0 == 0) {
+                for (int q = tid; q < G::TN; q += kTP) {
+                    int n[3];
+                    local_node<D>(q, n);
+                    const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
+                    const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
+                    float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (inside) {
+                        const float4 pm = covered_sum<D>(p, e, g, sl.bmap, sl.tiles);
+                        const float4 ub = covered_sum<D>(p, e, g, sl.bmap, ubar);
+                        float u0[3], u1[3];
+                        const bool z = grid_velocity<D>(p, g, pm, u0, u1);
+                        if (!z) {
+                            const float denom = pm.w + p.eps_mass;
+                            const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
+                            out = make_float4(ub.x / denom, ub.y / denom, D == 3 ? ub.z / denom : 0.0f, -dot / denom);
                         }
                     }
+                    sG[q] = out;
                 }
-                // Ab[a][b] = dx (Sm[b][a] - S0[a] f[b]);  fb_k -= (Adx^T S0)_k
-                float Ab[D * D], taub[D * D], Ftb[D * D];
-#pragma unroll
-                for (int a = 0; a < D; ++a)
-#pragma unroll
-                    for (int b = 0; b < D; ++b) Ab[a * D + b] = p.dx * fmaf(-S0[a], fx[b], Sm[b][a]);
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    float s = 0.0f;
-#pragma unroll
-                    for (int a = 0; a < D; ++a) s = fmaf(Adx[a * D + k], S0[a], s);
-                    fb[k] -= s;
-                }
-#pragma unroll
-                for (int q = 0; q < D * D; ++q) {
-                    taub[q] = p.stress_scale * Ab[q];
-                    Ftb[q] = __ldg(Sbn.f + (int64_t)j * L::FF + q);
-                }
-                abar = kirchhoff_adj<D>(p, Ft, a_id >= 0, act, taub, Ftb);
-                float* dvc = Sb.vc + (int64_t)i * L::VC;
-                float* dF = Sb.f + (int64_t)i * L::FF;
-                bool fin = true;
-#pragma unroll
-                for (int a = 0; a < D; ++a)
-#pragma unroll
-                    for (int b = 0; b < D; ++b) {
-                        float sF = Ftb[a * D + b], sC = 0.0f;
-#pragma unroll
-                        for (int k = 0; k < D; ++k) {
-                            sF = fmaf(p.dt * C[k * D + a], Ftb[k * D + b], sF);
-                            sC = fmaf(Ftb[a * D + k], F[b * D + k], sC);
-                        }
-                        dF[a * D + b] = sF;
-                        dvc[D + a * D + b] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
-                        fin = fin && isfinite(sF);
-                    }
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    Sb.x[(int64_t)i * D + a] = fmaf(p.inv_dx, fb[a], xbp[(int64_t)j * D + a]);
-                    dvc[a] = p.p_mass * S0[a];
-                }
-                if (!fin) atomicOr(flags, FLAG_NONFINITE);
+                for (int q = tid; q < (kTP / 32) * 32; q += kTP) (&s_ab[0][0])[q] = 0.0f;
+                __syncthreads();
+            }
+            float abar = 0.0f;
+            if (in) {
+                const bool has_act = aid && a_id >= 0;
+                abar = p2g_grad_particle<D>(p, sG, x, vc, F, Fbn, xb, has_act, has_act ? alpha[a_id] : 0.0f, c0,
+                                            i, Sb, flags);
+                if (!has_act) a_id = -1;
             }
             if (p.n_act > 0) {  // per-actuator warp sums (fixed butterfly) into the warp's slot
                 unsigned rem = __ballot_sync(0xffffffffu, a_id >= 0);
@@ -989,10 +1063,14 @@ __global__ void __launch_bounds__(kT) k_p2g_grad(KParams p, SlotView sl, StateVi
                 }
             }
         }
+        if (nvalid == 0) {  // keep the staging barrier structure uniform
+            for (int q = tid; q < (kTP / 32) * 32; q += kTP) (&s_ab[0][0])[q] = 0.0f;
+            __syncthreads();
+        }
         __syncthreads();
         if (p.n_act > 0 && tid < p.n_act) {
             float s = 0.0f;
-            for (int wv = 0; wv < kW; ++wv) s += s_ab[wv][tid];
+            for (int wv = 0; wv < kTP / 32; ++wv) s += s_ab[wv][tid];
             abar_part[(int64_t)bi * p.n_act + tid] = s;
         }
         __syncthreads();
@@ -1082,9 +1160,9 @@ cudaError_t tile_init() {
         e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
         if (e) return e;
         g_grid[0][0] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTC);
-        g_grid[1][0] = occupancy_grid((const void*)k_g2p<DIM>, 0);
+        g_grid[1][0] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
         g_grid[2][0] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTC);
-        g_grid[3][0] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0);
+        g_grid[3][0] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
     });
     DISPATCH(3, {
         e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>());
@@ -1092,9 +1170,9 @@ cudaError_t tile_init() {
         e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
         if (e) return e;
         g_grid[0][1] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTC);
-        g_grid[1][1] = occupancy_grid((const void*)k_g2p<DIM>, 0);
+        g_grid[1][1] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
         g_grid[2][1] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTC);
-        g_grid[3][1] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0);
+        g_grid[3][1] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
     });
     done = true;
     return cudaGetLastError();
@@ -1125,7 +1203,7 @@ void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const 
 }
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
                 int* bcount, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_g2p<DIM><<<pgrid(p, 1), kT, 0, s>>>(p, sl, S, Sn, keys, bcount, flags));
+    DISPATCH(p.dim, k_g2p<DIM><<<pgrid(p, 1), kTG, 0, s>>>(p, sl, S, Sn, keys, bcount, flags));
 }
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, float* xbp, cudaStream_t s) {
@@ -1134,7 +1212,7 @@ void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, c
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
                      const float* alpha_t, const float4* ubar, const AdjView& Sbn, const float* xbp,
                      const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_p2g_grad<DIM><<<pgrid(p, 3), kT, 0, s>>>(p, sl, S, aid, alpha_t, ubar, Sbn, xbp, Sb, abar_part, flags));
+    DISPATCH(p.dim, k_p2g_grad<DIM><<<pgrid(p, 3), kTP, 0, s>>>(p, sl, S, aid, alpha_t, ubar, Sbn, xbp, Sb, abar_part, flags));
 }
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s) {
     cudaMemsetAsync(count, 0, sizeof(int64_t), s);

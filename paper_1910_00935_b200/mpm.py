@@ -100,7 +100,7 @@ class Sim:
     """One mpm handle with a torch-owned workspace on the current CUDA device."""
 
     def __init__(self, n_particles: int, n_grid: int, dim: int, dt: float, E: float, nu: float,
-                 params: dict | None = None, stream=None):
+                 params: dict | None = None, stream=None, probe_only: bool = False):
         import torch
         self.L = load()
         self.h = ct.c_void_p()
@@ -124,6 +124,9 @@ class Sim:
         nbytes = ct.c_size_t()
         self._check("mpm_workspace_bytes", self.L.mpm_workspace_bytes(self.h, ct.byref(nbytes)))
         self.workspace_bytes = int(nbytes.value)
+        self.n_theta = 0
+        if probe_only:  # size query only: no workspace
+            return
         self.workspace = torch.empty(self.workspace_bytes + 256, dtype=torch.uint8, device="cuda")
         base = self.workspace.data_ptr()
         aligned = (base + 255) & ~255
@@ -241,7 +244,8 @@ class Sim:
 
 
 def sim_from_config(p: dict, n_particles: int, episodes: int | None = None,
-                    max_steps: int | None = None, k_ckpt: int | None = None, **overrides) -> Sim:
+                    max_steps: int | None = None, k_ckpt: int | None = None, probe_only: bool = False,
+                    **overrides) -> Sim:
     """Build a Sim from a workload config dict (paper_1910_00935_b200.workloads)."""
     dim = int(p["dim"])
     model = p.get("model", "neohookean")
@@ -260,4 +264,4 @@ def sim_from_config(p: dict, n_particles: int, episodes: int | None = None,
                   loss_target=list(p.get("target", [0, 0, 0])))
     params.update(overrides)
     return Sim(int(n_particles), int(p["n_grid"]), dim, float(p["dt"]), float(p["E"]),
-               float(p["nu"]), params)
+               float(p["nu"]), params, probe_only=probe_only)
