@@ -87,9 +87,12 @@ typedef struct {
                              order, so results are bitwise reproducible run to run */
     int32_t loss_kind;    /* MPM_LOSS_* */
     float loss_target[3]; /* x* for MPM_LOSS_COM_TARGET */
-    int32_t max_active_blocks; /* capacity of the per-step active block list (blocks of
+    int32_t max_active_blocks; /* capacity of one step's active block list (blocks of
                                   4^3 cells in 3D, 8^2 in 2D); 0 = automatic.  Exceeding it
                                   returns MPM_ERR_OOM. */
+    int64_t grid_store_blocks; /* capacity of the grid store that keeps every step's node tiles
+                                  for the reverse pass (blocks summed over all steps);
+                                  0 = automatic (about 3x a dense body).  MPM_ERR_OOM if exceeded. */
 } mpm_params;
 
 /* Create a handle for n_particles per episode on an n_grid^dim grid over the

@@ -62,7 +62,20 @@ struct mpm_ctx {
     std::vector<StateView> ckpt;   // S_{s k}
     std::vector<StateView> window; // S_{s k + j}, j = 1..k-1
     StateView final_state{};       // S_T
-    std::vector<SlotView> slots;   // binning + tiles of step t, slot t % k
+    // grid store (all steps): sorted lists, block maps, and a pool of block lists /
+    // cell starts / node tiles addressed by a per-step device-side base
+    int* sigma_store = nullptr;    // [T_max][EN]
+    unsigned char* scell_ring[2] = {nullptr, nullptr};  // [EN] (consumed by the next p2g only)
+    int* spid_ring[2] = {nullptr, nullptr};
+    int* bmap_store = nullptr;     // [T_max][TB]
+    int* nactive_arr = nullptr;    // [T_max]
+    int* base_arr = nullptr;       // [T_max]
+    int* blist_pool = nullptr;     // [P]
+    int* bstart_pool = nullptr;    // [P + T_max + 1]
+    unsigned short* cstart_pool = nullptr;  // [P][65]
+    float4* tiles_pool = nullptr;  // [P][TN]
+    int pool_blocks = 0;           // P
+    int step_blocks = 0;           // per-step capacity of block-local buffers
     AdjView sbar[2] = {};          // adjoint states, indexed like the primal state of their step
     float* staging = nullptr;
     int32_t* aid = nullptr;        // caller order
@@ -149,7 +162,8 @@ KParams kparams(const mpm_ctx* h) {
     k.nb = (h->n_grid + B - 1) / B;
     k.nbe = h->dim == 2 ? k.nb * k.nb : k.nb * k.nb * k.nb;
     k.TB = k.nbe * k.E;
-    k.max_active = h->max_active;
+    k.max_active = h->pool_blocks;
+    k.step_blocks = h->step_blocks;
     return k;
 }
 
@@ -162,11 +176,21 @@ int default_max_active(const mpm_ctx* h, const KParams& k) {
     return (int)std::min<int64_t>(k.TB, guess);
 }
 
+// grid-store pool capacity (blocks over all steps): grid_store_blocks, or an estimate of
+// ~3x the active blocks of a dense body (8 particles per cell) per step
+int64_t pool_capacity(const mpm_ctx* h, const KParams& k, int step_cap) {
+    if (h->prm.grid_store_blocks > 0) return h->prm.grid_store_blocks;
+    const int64_t EN = (int64_t)k.E * k.N;
+    const int64_t per = std::min<int64_t>(step_cap, 3 * ((EN + 511) / 512) + (int64_t)k.E * 64 + 64);
+    return per * h->prm.max_steps;
+}
+
 // carve (or just size, when base == nullptr) the workspace
 size_t carve(mpm_ctx* h, char* base) {
     const mpm_params& p = h->prm;
     KParams k = kparams(h);
-    const int max_active = default_max_active(h, k);
+    const int max_active = default_max_active(h, k);   // per-step block capacity
+    const int64_t pool = pool_capacity(h, k, max_active);
     const size_t E = (size_t)p.n_episodes, N = (size_t)h->N, EN = E * N;
     const size_t sf = EN * record_floats(h->dim);
     const int kk = p.k_ckpt;
@@ -201,20 +225,19 @@ size_t carve(mpm_ctx* h, char* base) {
     for (int i = 0; i < n_ckpt; ++i) ckpt.push_back(state());
     for (int i = 0; i < kk; ++i) window.push_back(i == 0 ? StateView{nullptr, nullptr, nullptr, nullptr} : state());
     StateView fin = state();
-    std::vector<SlotView> slots;
-    for (int i = 0; i < kk; ++i) {
-        SlotView s;
-        s.sigma = (int*)take(sizeof(int) * EN);
-        s.scell = (unsigned char*)take(EN);
-        s.spid = (int*)take(sizeof(int) * EN);
-        s.blist = (int*)take(sizeof(int) * max_active);
-        s.bstart = (int*)take(sizeof(int) * (max_active + 1));
-        s.bmap = (int*)take(sizeof(int) * k.TB);
-        s.nactive = (int*)take(sizeof(int));
-        s.cstart = (unsigned short*)take(sizeof(unsigned short) * (size_t)max_active * (kCells + 1));
-        s.tiles = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
-        slots.push_back(s);
-    }
+    const int Tm = p.max_steps;
+    int* sigma_store = (int*)take(sizeof(int) * EN * Tm);
+    unsigned char* scell0 = (unsigned char*)take(EN);
+    unsigned char* scell1 = (unsigned char*)take(EN);
+    int* spid0 = (int*)take(sizeof(int) * EN);
+    int* spid1 = (int*)take(sizeof(int) * EN);
+    int* bmap_store = (int*)take(sizeof(int) * (size_t)k.TB * Tm);
+    int* nactive_arr = (int*)take(sizeof(int) * Tm);
+    int* base_arr = (int*)take(sizeof(int) * Tm);
+    int* blist_pool = (int*)take(sizeof(int) * (size_t)pool);
+    int* bstart_pool = (int*)take(sizeof(int) * ((size_t)pool + Tm + 1));
+    unsigned short* cstart_pool = (unsigned short*)take(sizeof(unsigned short) * (size_t)pool * (kCells + 1));
+    float4* tiles_pool = (float4*)take(sizeof(float4) * (size_t)pool * TN);
     AdjView sb0 = adj();
     AdjView sb1 = adj();
     float* staging = (float*)take(sizeof(float) * sf);
@@ -225,7 +248,7 @@ size_t carve(mpm_ctx* h, char* base) {
     int* keys = (int*)take(sizeof(int) * EN);
     float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
     float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
-    float* abar_part = (float*)take(sizeof(float) * (size_t)max_active * A);
+    float* abar_part = (float*)take(sizeof(float) * (size_t)max_active * A);  // per-step buffers
     float* alpha = (float*)take(sizeof(float) * (size_t)p.max_steps * A);
     float* alpha_bar = (float*)take(sizeof(float) * (size_t)p.max_steps * A);
     float* theta = (float*)take(sizeof(float) * nth);
@@ -237,12 +260,17 @@ size_t carve(mpm_ctx* h, char* base) {
     int* flags = (int*)take(sizeof(int) * 4);
     if (base) {
         h->max_active = max_active;
+        h->step_blocks = max_active;
+        h->pool_blocks = pool;
+        h->sigma_store = sigma_store; h->scell_ring[0] = scell0; h->scell_ring[1] = scell1;
+        h->spid_ring[0] = spid0; h->spid_ring[1] = spid1; h->bmap_store = bmap_store;
+        h->nactive_arr = nactive_arr; h->base_arr = base_arr; h->blist_pool = blist_pool;
+        h->bstart_pool = bstart_pool; h->cstart_pool = cstart_pool; h->tiles_pool = tiles_pool;
         h->state_floats = sf;
         h->n_ckpt = n_ckpt;
         h->ckpt = ckpt;
         h->window = window;
         h->final_state = fin;
-        h->slots = slots;
         h->sbar[0] = sb0; h->sbar[1] = sb1;
         h->staging = staging; h->aid = aid; h->bcount = bcount; h->cursor = cursor; h->scan_part = scan_part; h->keys = keys;
         h->xbar_part = xbar_part; h->ubar = ubar; h->abar_part = abar_part;
@@ -260,7 +288,23 @@ StateView state_at(mpm_ctx* h, int t) {
     return h->window[t % k];
 }
 
-const SlotView& slot_at(mpm_ctx* h, int t) { return h->slots[t % h->prm.k_ckpt]; }
+SlotView slot_at(mpm_ctx* h, int t) {
+    const KParams k = kparams(h);
+    const size_t EN = (size_t)k.E * k.N;
+    SlotView s;
+    s.sigma = h->sigma_store + EN * t;
+    s.scell = h->scell_ring[t & 1];
+    s.spid = h->spid_ring[t & 1];
+    s.blist = h->blist_pool;
+    s.bstart = h->bstart_pool;
+    s.bmap = h->bmap_store + (size_t)k.TB * t;
+    s.nactive = h->nactive_arr + t;
+    s.base = h->base_arr + t;
+    s.cstart = h->cstart_pool;
+    s.tiles = h->tiles_pool;
+    s.step = t;
+    return s;
+}
 
 // ---------------------------------------------------------------- profiling
 void prof_harvest(mpm_ctx* h) {
@@ -330,7 +374,7 @@ const float* alpha_at(mpm_ctx* h, int t) {
 
 // fresh binning of S_t into slot(t) (start of a forward or of a segment re-forward)
 void bin_fresh(mpm_ctx* h, const KParams& k, int t) {
-    const SlotView& sl = slot_at(h, t);
+    const SlotView sl = slot_at(h, t);
     KScope sc(h, KC_BIN);
     h->launches += 3;
     launch_bin_keys(k, state_at(h, t).x, h->keys, h->bcount, h->flags, h->stream);
@@ -340,16 +384,16 @@ void bin_fresh(mpm_ctx* h, const KParams& k, int t) {
 
 // advance() for step t; write_next: produce S_{t+1}; bin_next: bin it into slot(t+1)
 void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin_next) {
-    const SlotView& sl = slot_at(h, t);
+    const SlotView sl = slot_at(h, t);
     const StateView S = state_at(h, t);
     const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr, nullptr, nullptr};
     const int32_t* aid = h->has_aid ? h->aid : nullptr;
     { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
     if (!write_next) return;
     { KScope sc(h, KC_G2P);
-      launch_g2p(k, sl, S, Sn, bin_next ? h->keys : nullptr, h->bcount, h->flags, h->stream); }
+      launch_g2p(k, sl, S, Sn, bin_next ? h->keys : nullptr, h->bcount, h->flags, false, h->stream); }
     if (bin_next) {
-        const SlotView& nx = slot_at(h, t + 1);
+        const SlotView nx = slot_at(h, t + 1);
         KScope sc(h, KC_BIN);
         h->launches += 2;
         launch_bin_scan(k, h->bcount, h->cursor, nx, h->scan_part, h->flags, h->stream);
@@ -357,9 +401,16 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     }
 }
 
-// advance_grad() for step t, using the grid tiles stored in slot(t)
+// re-forward of step t inside a segment: the grid of step t is in the grid
+// store, so only g2p runs (plus F_{t+1} = (I + dt C) F and the particle ids)
+void step_reforward(mpm_ctx* h, const KParams& k, int t) {
+    KScope sc(h, KC_G2P);
+    launch_g2p(k, slot_at(h, t), state_at(h, t), state_at(h, t + 1), nullptr, h->bcount, h->flags, true, h->stream);
+}
+
+// advance_grad() for step t, using the grid tiles stored for step t
 void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, const AdjView& Sb) {
-    const SlotView& sl = slot_at(h, t);
+    const SlotView sl = slot_at(h, t);
     const StateView S = state_at(h, t);
     const int A = k.n_act > 0 ? k.n_act : 1;
     { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, sl, S, Sbn, h->ubar, h->xbar_part, h->stream); }
@@ -618,9 +669,8 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     const int nseg = (T + kk - 1) / kk;
     for (int s = nseg - 1; s >= 0; --s) {
         const int t0 = s * kk, t1 = (t0 + kk < T) ? t0 + kk : T;
-        if (h->window_seg != s) {  // segment-wise recomputation, grid tiles kept per step
-            bin_fresh(h, k, t0);
-            for (int t = t0; t < t1; ++t) step_forward(h, k, t, t + 1 < t1, t + 1 < t1);
+        if (h->window_seg != s) {  // segment-wise recomputation of the states
+            for (int t = t0; t < t1 - 1; ++t) step_reforward(h, k, t);
             h->window_seg = s;
         }
         for (int t = t1 - 1; t >= t0; --t) {
@@ -742,8 +792,7 @@ mpm_status mpm_active_nodes(mpm_handle h, int64_t* count) {
         return fail(h, MPM_ERR_BAD_SEQUENCE, "active_nodes before forward");
     const KParams k = kparams(h);
     // a step whose grid tiles are in the window: the last step of the window segment
-    const int t1 = std::min(h->recorded, (h->window_seg + 1) * h->prm.k_ckpt);
-    { KScope sc(h, KC_LAYOUT); launch_count_active(k, slot_at(h, t1 - 1), h->counter, h->stream); }
+    { KScope sc(h, KC_LAYOUT); launch_count_active(k, slot_at(h, h->recorded - 1), h->counter, h->stream); }
     int64_t c = 0;
     CU(cudaMemcpyAsync(&c, h->counter, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));

@@ -21,17 +21,22 @@ struct AdjView {
     float* f;
 };
 
-// one time step's binning + grid:
+// one time step's binning + grid.  The block lists, cell
+// starts and node tiles of all steps live in one pool; step t's entries start at pool
+// index *base (set on the device by the step's scan), so only the active blocks of
+// each step take space.  bmap holds pool (global) tile indices.
 struct SlotView {
     int* sigma;              // [EN]   sorted order -> index into that step's state array
     unsigned char* scell;    // [EN]   cell (0..63, 64 = junk) of the sorted entry (set by bin_scatter)
     int* spid;               // [EN]   particle id of the sorted entry (set by bin_scatter)
-    int* blist;              // [max_active]   active block ids (block-id order)
-    int* bstart;             // [max_active+1] start of each block's segment of sigma
-    int* bmap;               // [TB]   block id -> active index, or -1
-    int* nactive;            // [1]
-    unsigned short* cstart;  // [max_active][CELLS+1] cell starts within the block segment
-    float4* tiles;           // [max_active][TN]  (P, M) partial node tiles
+    int* blist;              // pool [P]          active block ids of a step (block-id order)
+    int* bstart;             // pool [P + T + 1]  segment starts; step t uses [base + t, base + t + n]
+    int* bmap;               // [TB]   block id -> pool tile index, or -1
+    int* nactive;            // [1]    active blocks of this step
+    int* base;               // [1]    pool offset of this step (nactive[-1], base[-1]: previous step)
+    unsigned short* cstart;  // pool [P][CELLS+1] cell starts within the block segment
+    float4* tiles;           // pool [P][TN]      (P, M) partial node tiles
+    int step;                // t
 };
 
 cudaError_t tile_init();
@@ -49,9 +54,10 @@ void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* 
 // p2g writes F_{t+1} and particle ids of S_{t+1} when Sn.rec / Sn.pid are non-null
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s);
-// g2p (grid_op fused in its staging) writes x, v, C of S_{t+1}; keys != null -> next bin keys
+// g2p (grid_op fused in its staging) writes x, v, C of S_{t+1}; keys != null -> next bin keys;
+// refwd: segment re-forward from stored tiles -- also writes F_{t+1} = (I + dt C) F and the ids
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
-                int* bcount, int* flags, cudaStream_t s);
+                int* bcount, int* flags, bool refwd, cudaStream_t s);
 
 // ---- one reverse step (advance_grad()); Sbn is indexed like S_{t+1}, Sb like S_t
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,

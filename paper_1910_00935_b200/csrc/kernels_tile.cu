@@ -227,20 +227,23 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
         }
         return;
     }
+    // pool offset of this step: right after the previous step's blocks
+    const int b0 = sl.step > 0 ? sl.base[-1] + sl.nactive[-1] : 0;
     int pos = s_base[0] + it - tot, li = s_base[1] + ia - act;
     for (int w = 0; w < warp; ++w) { pos += s_wt[w]; li += s_wa[w]; }
+    const int cap = min(p.max_active - b0, p.step_blocks);  // blocks this step may take
 #pragma unroll
     for (int q = 0; q < kScanPer; ++q) {
         const int b = i0 + q;
         if (b >= TB) break;
         if (c[q] > 0) {
-            if (li < p.max_active) {
-                sl.blist[li] = b;
-                sl.bstart[li] = pos;
-                sl.bmap[b] = li;
+            if (li < cap) {
+                sl.blist[b0 + li] = b;
+                sl.bstart[b0 + sl.step + li] = pos;
+                sl.bmap[b] = b0 + li;
             } else {
                 // capacity exceeded: the list ends before this block (error is reported)
-                if (li == p.max_active) sl.bstart[li] = pos;
+                if (li == cap) sl.bstart[b0 + sl.step + li] = pos;
                 sl.bmap[b] = -1;
                 atomicOr(flags, FLAG_ACTIVE_OVERFLOW);
             }
@@ -253,9 +256,10 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
         }
     }
     if (blockIdx.x == gridDim.x - 1 && tid == kT - 1) {  // grand totals
-        const int n = min(li, p.max_active);
+        const int n = max(0, min(li, cap));
         *sl.nactive = n;
-        if (li <= p.max_active) sl.bstart[n] = pos;
+        *sl.base = b0;
+        if (li <= cap) sl.bstart[b0 + sl.step + n] = pos;
     }
 }
 
@@ -372,15 +376,7 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
     int lb[3];
     float fx[3], dw[3][3];
     particle_weights<D>(p, x, c0, lb, fx, w, dw);
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-        for (int b = 0; b < D; ++b) {
-            float s = 0.0f;
-#pragma unroll
-            for (int k = 0; k < D; ++k) s = fmaf(C[a * D + k], F[k * D + b], s);
-            Ft[a * D + b] = fmaf(p.dt, s, F[a * D + b]);
-        }
+    deform_update<D>(p.dt, C, F, Ft);
     float tau[D * D];
     const bool ok = kirchhoff<D>(p, Ft, act, tau);
 #pragma unroll
@@ -417,9 +413,14 @@ __global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateVie
     int* s_cst = s_cnt + G::CELLS + 2;
     const int tid = threadIdx.x, lane = tid & 31;
     const int nact = *sl.nactive;
+    const int b0 = *sl.base;  // this step's offset in the grid-store pool
+    const int* blist = sl.blist + b0;
+    const int* bstart = sl.bstart + b0 + sl.step;
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
+    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
-        const int bid = sl.blist[bi];
-        const int start = sl.bstart[bi], n = sl.bstart[bi + 1] - start;
+        const int bid = blist[bi];
+        const int start = bstart[bi], n = bstart[bi + 1] - start;
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         if (n > G::MAXP) {
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateVie
             sl.sigma[start + fl] = s_idx[q];
             if (Sn.pid) Sn.pid[start + fl] = pq;
         }
-        for (int c = tid; c <= G::CELLS; c += kTC) sl.cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
+        for (int c = tid; c <= G::CELLS; c += kTC) cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
         if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
         __syncthreads();
         // ---- phase 1: thread = cell, particles of the cell in canonical order, next one prefetched
@@ -528,7 +529,7 @@ __global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateVie
         }
         __syncthreads();
         // ---- phase 2: node tile (plain stores)
-        float4* tile = sl.tiles + (int64_t)bi * G::TN;
+        float4* tile = tiles_l + (int64_t)bi * G::TN;
         for (int q = tid; q < G::TN; q += kTC) {
             float4 s = node_gather<D>(s_cb, q);
             s.w *= p.p_mass;
@@ -614,7 +615,8 @@ constexpr int kTG = 128;  // g2p CTA: smaller CTAs -> more independent blocks in
 template <int D>
 __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __restrict__ sU, const float* x,
                                             const int c0[3], int j, int e, int bid, const StateView& Sn,
-                                            int* __restrict__ keys, int* flags) {
+                                            int* __restrict__ keys, int* flags, bool refwd,
+                                            const StateView& S, int64_t i) {
     using G = Geo<D>;
     using L = Lay<D>;
     const float c4 = 4.0f * p.inv_dx;
@@ -636,6 +638,18 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
         for (int b = 0; b < D; ++b) dvc[D + a * D + b] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
     }
     if (!fin) atomicOr(flags, FLAG_NONFINITE);
+    if (refwd) {  // re-forward from stored tiles: F_{t+1} and the particle id too
+        float C[D * D], F[D * D], Ft[D * D];
+#pragma unroll
+        for (int q = 0; q < D * D; ++q) {
+            C[q] = __ldg(S.vc + i * L::VC + D + q);
+            F[q] = __ldg(S.f + i * L::FF + q);
+        }
+        deform_update<D>(p.dt, C, F, Ft);
+#pragma unroll
+        for (int q = 0; q < D * D; ++q) Sn.f[(int64_t)j * L::FF + q] = Ft[q];
+        Sn.pid[j] = __ldg(S.pid + i);
+    }
     int key = -1;
     if (keys) {
         int b[3];
@@ -656,37 +670,44 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
 
 template <int D>
 __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
-                                            int* __restrict__ keys, int* __restrict__ bcount, int* flags) {
+                                            int* __restrict__ keys, int* __restrict__ bcount, int* flags,
+                                            bool refwd) {
     using G = Geo<D>;
     __shared__ float4 sU[G::TN];
     const int tid = threadIdx.x;
     const int nact = *sl.nactive;
+    const int b0 = *sl.base;  // this step's offset in the grid-store pool
+    const int* blist = sl.blist + b0;
+    const int* bstart = sl.bstart + b0 + sl.step;
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
+    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
-        const int bid = sl.blist[bi];
-        const int start = sl.bstart[bi];
-        const int nvalid = sl.cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
+        const int bid = blist[bi];
+        const int start = bstart[bi];
+        const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         // particle loads of the first two passes go out before the tile staging
         float xa[3], xb[3];
         const bool va = tid < nvalid, vb = tid + kTG < nvalid;
+        int ia = 0, ib = 0;
         if (va) {
-            const int i = sl.sigma[start + tid];
+            ia = sl.sigma[start + tid];
 #pragma unroll
-            for (int k = 0; k < D; ++k) xa[k] = __ldg(S.x + (int64_t)i * D + k);
+            for (int k = 0; k < D; ++k) xa[k] = __ldg(S.x + (int64_t)ia * D + k);
         }
         if (vb) {
-            const int i = sl.sigma[start + tid + kTG];
+            ib = sl.sigma[start + tid + kTG];
 #pragma unroll
-            for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + (int64_t)i * D + k);
+            for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + (int64_t)ib * D + k);
         }
         stage_velocity<D, kTG>(p, sl, e, c0, sU);
         __syncthreads();
         int key = -1;
-        if (va) key = g2p_particle<D>(p, sU, xa, c0, start + tid, e, bid, Sn, keys, flags);
+        if (va) key = g2p_particle<D>(p, sU, xa, c0, start + tid, e, bid, Sn, keys, flags, refwd, S, ia);
         if (keys) count_key(va, key, bcount);
         key = -1;
-        if (vb) key = g2p_particle<D>(p, sU, xb, c0, start + tid + kTG, e, bid, Sn, keys, flags);
+        if (vb) key = g2p_particle<D>(p, sU, xb, c0, start + tid + kTG, e, bid, Sn, keys, flags, refwd, S, ib);
         if (keys) count_key(vb, key, bcount);
         for (int r0 = 2 * kTG; r0 < nvalid; r0 += kTG) {
             const int r = r0 + tid;
@@ -697,7 +718,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
                 float x[3];
 #pragma unroll
                 for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
-                key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags);
+                key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags, refwd, S, i);
             }
             if (keys) count_key(in, key, bcount);
         }
@@ -724,10 +745,15 @@ __global__ void __launch_bounds__(kTC, 6) k_g2p_grad(KParams p, SlotView sl, Sta
     int* s_cst = reinterpret_cast<int*>(sU + G::TN);
     const int tid = threadIdx.x;
     const int nact = *sl.nactive;
+    const int b0 = *sl.base;  // this step's offset in the grid-store pool
+    const int* blist = sl.blist + b0;
+    const int* bstart = sl.bstart + b0 + sl.step;
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
+    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
     const float c4 = 4.0f * p.inv_dx;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
-        const int bid = sl.blist[bi];
-        const int start = sl.bstart[bi];
+        const int bid = blist[bi];
+        const int start = bstart[bi];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         for (int q = threadIdx.x; q < G::TN; q += kTC) {
@@ -744,7 +770,7 @@ __global__ void __launch_bounds__(kTC, 6) k_g2p_grad(KParams p, SlotView sl, Sta
             }
             sU[q] = out;
         }
-        for (int c = tid; c <= G::CELLS; c += kTC) s_cst[c] = sl.cstart[(int64_t)bi * (G::CELLS + 1) + c];
+        for (int c = tid; c <= G::CELLS; c += kTC) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
         __syncthreads();
         const int lo = start + s_cst[tid], hi = start + s_cst[tid + 1];
         // pass 1: gather part (W_bar, f_bar -> partial x_bar), one particle at a time
@@ -993,10 +1019,15 @@ __global__ void __launch_bounds__(kTP, 4) k_p2g_grad(KParams p, SlotView sl, Sta
     __shared__ float s_ab[kTP / 32][32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nact = *sl.nactive;
+    const int b0 = *sl.base;  // this step's offset in the grid-store pool
+    const int* blist = sl.blist + b0;
+    const int* bstart = sl.bstart + b0 + sl.step;
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
+    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
-        const int bid = sl.blist[bi];
-        const int start = sl.bstart[bi];
-        const int nvalid = sl.cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
+        const int bid = blist[bi];
+        const int start = bstart[bi];
+        const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         for (int r0 = 0; r0 < nvalid; r0 += kTP) {
@@ -1030,7 +1061,7 @@ __global__ void __launch_bounds__(kTP, 4) k_p2g_grad(KParams p, SlotView sl, Sta
                     float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (inside) {
                         const float4 pm = covered_sum<D>(p, e, g, sl.bmap, sl.tiles);
-                        const float4 ub = covered_sum<D>(p, e, g, sl.bmap, ubar);
+                        const float4 ub = covered_sum<D>(p, e, g, sl.bmap, ubar - (int64_t)b0 * G::TN);
                         float u0[3], u1[3];
                         const bool z = grid_velocity<D>(p, g, pm, u0, u1);
                         if (!z) {
@@ -1095,9 +1126,14 @@ template <int D>
 __global__ void __launch_bounds__(kT) k_count_active(KParams p, SlotView sl, unsigned long long* count) {
     using G = Geo<D>;
     const int nact = *sl.nactive;
+    const int b0 = *sl.base;  // this step's offset in the grid-store pool
+    const int* blist = sl.blist + b0;
+    const int* bstart = sl.bstart + b0 + sl.step;
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
+    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         int e, c0[3];
-        block_origin<D>(p, sl.blist[bi], e, c0);
+        block_origin<D>(p, blist[bi], e, c0);
         for (int q = threadIdx.x; q < G::TN; q += kT) {
             int n[3];
             local_node<D>(q, n);
@@ -1122,7 +1158,7 @@ __global__ void __launch_bounds__(kT) k_count_active(KParams p, SlotView sl, uns
                         const int ti = sl.bmap[block_lin<D>(p, e, bb)];
                         if (ti >= 0) first = ti;
                     }
-            if (first == bi) atomicAdd(count, 1ull);
+            if (first == b0 + bi) atomicAdd(count, 1ull);
         }
     }
 }
@@ -1180,7 +1216,7 @@ cudaError_t tile_init() {
 
 static unsigned pgrid(const KParams& p, int kind) {
     const int g = g_grid[kind][p.dim == 3 ? 1 : 0];
-    return (unsigned)(p.max_active < g ? p.max_active : g);
+    return (unsigned)(p.step_blocks < g ? p.step_blocks : g);
 }
 
 void launch_bin_keys(const KParams& p, const float* x, int* keys, int* bcount, int* flags, cudaStream_t s) {
@@ -1202,8 +1238,8 @@ void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const 
     DISPATCH(p.dim, k_p2g<DIM><<<pgrid(p, 0), kTC, p2g_smem_bytes<DIM>(), s>>>(p, sl, S, Sn, aid, alpha_t, flags));
 }
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
-                int* bcount, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_g2p<DIM><<<pgrid(p, 1), kTG, 0, s>>>(p, sl, S, Sn, keys, bcount, flags));
+                int* bcount, int* flags, bool refwd, cudaStream_t s) {
+    DISPATCH(p.dim, k_g2p<DIM><<<pgrid(p, 1), kTG, 0, s>>>(p, sl, S, Sn, keys, bcount, flags, refwd));
 }
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, float* xbp, cudaStream_t s) {

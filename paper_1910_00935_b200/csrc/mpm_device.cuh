@@ -20,7 +20,8 @@ struct KParams {
     int32_t nb;          // blocks per axis (ceil(n_grid / B))
     int32_t nbe;         // blocks per episode (nb^dim)
     int32_t TB;          // blocks, all episodes (E * nbe)
-    int32_t max_active;  // capacity of the active-block list / tile storage
+    int32_t max_active;  // capacity (blocks) of the grid-store pool shared by all steps
+    int32_t step_blocks; // capacity of one step's block-local buffers (U_bar tiles, partials)
 };
 
 enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8 };
@@ -114,6 +115,19 @@ template <int D> __device__ __forceinline__ float column(const float* M, int i, 
 #pragma unroll
     for (int k = 1; k < D; ++k) v = e == k ? M[i * D + k] : v;
     return v;
+}
+
+// F_{t+1} = (I + dt C) F (shared by p2g and the re-forward so both produce the same bits)
+template <int D> __device__ __forceinline__ void deform_update(float dt, const float* C, const float* F, float* Ft) {
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = 0; b < D; ++b) {
+            float s = 0.0f;
+#pragma unroll
+            for (int k = 0; k < D; ++k) s = fmaf(C[a * D + k], F[k * D + b], s);
+            Ft[a * D + b] = fmaf(dt, s, F[a * D + b]);
+        }
 }
 
 // Kirchhoff stress tau(Ft) of the material (R2) plus actuation (R8).

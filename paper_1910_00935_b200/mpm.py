@@ -41,7 +41,8 @@ class mpm_params(ct.Structure):
                 ("act_strength", ct.c_float), ("act_axis", ct.c_int32), ("n_sin", ct.c_int32),
                 ("omega", ct.c_float), ("ctrl_hidden", ct.c_int32), ("n_episodes", ct.c_int32),
                 ("deterministic", ct.c_int32), ("loss_kind", ct.c_int32),
-                ("loss_target", ct.c_float * 3), ("max_active_blocks", ct.c_int32)]
+                ("loss_target", ct.c_float * 3), ("max_active_blocks", ct.c_int32),
+                ("grid_store_blocks", ct.c_int64)]
 
 
 _lib = None

@@ -53,13 +53,23 @@ def test_default_params_host_only(lib):
     assert lib.mpm_default_params(4, ct.byref(p)) == 1  # MPM_ERR_INVALID_ARG
 
 
-def test_params_struct_matches_header():
-    """the ctypes mirror has the header's field order and size"""
+def test_params_struct_matches_header(tmp_path):
+    """the ctypes mirror has the header's field order, offsets and size (checked
+    against the C compiler's layout of include/mpm.h)"""
     src = open(os.path.join(ROOT, "include", "mpm.h")).read()
     body = src[src.index("typedef struct {", src.index("enum { MPM_LOSS_COM_TARGET")):src.index("} mpm_params;")]
-    fields = re.findall(r"\b(?:float|int32_t)\s+(\w+)", body)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"\b(?:float|int32_t|int64_t)\s+(\w+)", body)
     assert fields == [f[0] for f in mpm.mpm_params._fields_]
-    assert ct.sizeof(mpm.mpm_params) == 4 * (len(fields) + 2)
+    prog = tmp_path / "layout.c"
+    prog.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "mpm.h"\nint main(void){'
+                    + "".join(f'printf("%zu ", offsetof(mpm_params, {f}));' for f in fields)
+                    + 'printf("%zu", sizeof(mpm_params)); return 0;}\n')
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(prog)])
+    got = list(map(int, subprocess.check_output([str(exe)]).split()))
+    want = [getattr(mpm.mpm_params, f).offset for f in fields] + [ct.sizeof(mpm.mpm_params)]
+    assert got == want
 
 
 def test_product_never_imports_oracle():
