@@ -358,12 +358,98 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
 
 constexpr int kTC = 64;  // thread-per-cell kernels: one thread per cell of a block (CELLS = 64)
 
+constexpr int kTQ = 192;  // p2g CTA: 3 threads per cell (64 cells) in the accumulation phase
+
+template <int D> struct RowL {  // particle row in shared memory (floats); stride avoids STS.128 conflicts
+    static constexpr int STRIDE = D == 3 ? 28 : 12;
+};
 template <int D> constexpr int p2g_union_bytes() {
-    return Geo<D>::MAXP * 11 > Geo<D>::CELLS * Geo<D>::NST * 16 ? Geo<D>::MAXP * 11
-                                                                 : Geo<D>::CELLS * Geo<D>::NST * 16;
+    constexpr int a = Geo<D>::MAXP * 11, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kTQ * RowL<D>::STRIDE * 4;
+    return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 template <int D> constexpr int p2g_smem_bytes() {
     return p2g_union_bytes<D>() + Geo<D>::MAXP * 4 + 2 * (Geo<D>::CELLS + 2) * 4;
+}
+
+// Thread (cell, o_x): sums over the cell's rows W_o (c + A o) (and W_o) for the
+// 3^(d-1) nodes o = (o_x, .) in registers.  Row: [wy*wz (9) | c (3) | A dx (9) | wx (3)] (3D),
+// [wy (3) | c (2) | A dx (4) | wx (3)] (2D).
+template <int D, bool MASS> struct SliceAcc {
+    static constexpr int NN = D == 3 ? 9 : 3;
+    float4 a[NN];
+    __device__ __forceinline__ void zero() {
+#pragma unroll
+        for (int k = 0; k < NN; ++k) a[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __device__ __forceinline__ void row(const float* __restrict__ rw, int ox) {
+        const float4* r4 = reinterpret_cast<const float4*>(rw);
+        const float fox = (float)ox;
+        if (D == 3) {
+            const float4 r0 = r4[0], r1 = r4[1], r2 = r4[2], r3 = r4[3], r4_ = r4[4], r5 = r4[5];
+            const float wyz[9] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x};
+            const float A[9] = {r3.x, r3.y, r3.z, r3.w, r4_.x, r4_.y, r4_.z, r4_.w, r5.x};
+            const float W0 = ox == 0 ? r5.y : (ox == 1 ? r5.z : r5.w);
+            float mx[3] = {fmaf(fox, A[0], r2.y), fmaf(fox, A[3], r2.z), fmaf(fox, A[6], r2.w)};
+#pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+                float m[3] = {fmaf((float)oy, A[1], mx[0]), fmaf((float)oy, A[4], mx[1]), fmaf((float)oy, A[7], mx[2])};
+#pragma unroll
+                for (int oz = 0; oz < 3; ++oz) {
+                    const float W = W0 * wyz[oy * 3 + oz];
+                    float4& acc = a[oy * 3 + oz];
+                    acc.x = fmaf(W, m[0], acc.x);
+                    acc.y = fmaf(W, m[1], acc.y);
+                    acc.z = fmaf(W, m[2], acc.z);
+                    if (MASS) acc.w += W;
+                    m[0] += A[2]; m[1] += A[5]; m[2] += A[8];
+                }
+            }
+        } else {
+            const float4 r0 = r4[0], r1 = r4[1], r2 = r4[2];
+            // [wy0 wy1 wy2 c0][c1 A00 A01 A10][A11 wx0 wx1 wx2]
+            const float W0 = ox == 0 ? r2.y : (ox == 1 ? r2.z : r2.w);
+            const float wy[3] = {r0.x, r0.y, r0.z};
+            float m[2] = {fmaf(fox, r1.y, r0.w), fmaf(fox, r1.w, r1.x)};
+#pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+                const float W = W0 * wy[oy];
+                float4& acc = a[oy];
+                acc.x = fmaf(W, m[0], acc.x);
+                acc.y = fmaf(W, m[1], acc.y);
+                if (MASS) acc.w += W;
+                m[0] += r1.z; m[1] += r2.x;
+            }
+        }
+    }
+    // cellbuf[c][o], o = (ox*3 + oy)*3 + oz (3D) / ox*3 + oy (2D)
+    __device__ __forceinline__ void store(float4* cellbuf, int c, int ox) const {
+        float4* dst = cellbuf + c * Geo<D>::NST + ox * NN;
+#pragma unroll
+        for (int k = 0; k < NN; ++k) dst[k] = a[k];
+    }
+};
+
+// row writer (vector stores): layouts as SliceAcc::row
+template <int D>
+__device__ __forceinline__ void write_row(float* row, const float w[3][3], const float* c, const float* Adx) {
+    float4* r4 = reinterpret_cast<float4*>(row);
+    if (D == 3) {
+        float wyz[9];
+#pragma unroll
+        for (int oy = 0; oy < 3; ++oy)
+#pragma unroll
+            for (int oz = 0; oz < 3; ++oz) wyz[oy * 3 + oz] = w[1][oy] * w[2][oz];
+        r4[0] = make_float4(wyz[0], wyz[1], wyz[2], wyz[3]);
+        r4[1] = make_float4(wyz[4], wyz[5], wyz[6], wyz[7]);
+        r4[2] = make_float4(wyz[8], c[0], c[1], c[2]);
+        r4[3] = make_float4(Adx[0], Adx[1], Adx[2], Adx[3]);
+        r4[4] = make_float4(Adx[4], Adx[5], Adx[6], Adx[7]);
+        r4[5] = make_float4(Adx[8], w[0][0], w[0][1], w[0][2]);
+    } else {
+        r4[0] = make_float4(w[1][0], w[1][1], w[1][2], c[0]);
+        r4[1] = make_float4(c[1], Adx[0], Adx[1], Adx[2]);
+        r4[2] = make_float4(Adx[3], w[0][0], w[0][1], w[0][2]);
+    }
 }
 
 // per-particle p2g math: returns c = m v - A dx f and A dx (for NodeAcc) and Ft
@@ -395,29 +481,32 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
 // p2g: canonicalise the block list, then per particle
 // Ft = (I + dt C) F; tau = tau(Ft) [+ actuation]; A = -dt V 4/dx^2 tau + m C;
 // node b+o receives W_o (m v + A (o - f) dx) and W_o m.  F_{t+1} = Ft.
-// CTA = 64 threads = one thread per cell of the block (persistent over blocks).
+// CTA = 192 threads: phase 1 thread per particle (rows in smem), phase 2 thread per (cell, o_x).
 template <int D>
-__global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
+__global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
                                                const int32_t* __restrict__ aid,
                                                const float* __restrict__ alpha, int* flags) {
     using G = Geo<D>;
     using L = Lay<D>;
+    constexpr int RS = RowL<D>::STRIDE;
     extern __shared__ __align__(16) unsigned char smem[];
     int* s_idx = reinterpret_cast<int*>(smem);                       // phase 0 ...
     int* s_pid = s_idx + G::MAXP;
     short* s_tmp = reinterpret_cast<short*>(s_pid + G::MAXP);
     unsigned char* s_cell = reinterpret_cast<unsigned char*>(s_tmp + G::MAXP);
-    float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... aliased by phase 2
+    float* s_row = reinterpret_cast<float*>(smem);                   // ... phase 1/2 rows ...
+    float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... node partials
     int* s_ci = reinterpret_cast<int*>(smem + p2g_union_bytes<D>());  // canonical state index
     int* s_cnt = s_ci + G::MAXP;
     int* s_cst = s_cnt + G::CELLS + 2;
     const int tid = threadIdx.x, lane = tid & 31;
+    const int my_cell = tid / 3, my_ox = tid - 3 * (tid / 3);
     const int nact = *sl.nactive;
     const int b0 = *sl.base;  // this step's offset in the grid-store pool
     const int* blist = sl.blist + b0;
     const int* bstart = sl.bstart + b0 + sl.step;
-    unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
-    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
+    float4* tiles_l = sl.tiles + (int64_t)b0 * G::TN;
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         const int bid = blist[bi];
         const int start = bstart[bi], n = bstart[bi + 1] - start;
@@ -429,15 +518,15 @@ __global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateVie
         }
         // ---- phase 0: canonical (cell, particle id) order of the block's list.  The
         // scatter wrote each entry's cell and particle id next to it: coalesced loads only.
-        for (int q = tid; q < G::CELLS + 2; q += kTC) s_cnt[q] = 0;
+        for (int q = tid; q < G::CELLS + 2; q += kTQ) s_cnt[q] = 0;
 #pragma unroll 4
-        for (int q = tid; q < n; q += kTC) {
+        for (int q = tid; q < n; q += kTQ) {
             s_idx[q] = sl.sigma[start + q];
             s_pid[q] = sl.spid[start + q];
             s_cell[q] = sl.scell[start + q];
         }
         __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kTC) {
+        for (int q0 = 0; q0 < n; q0 += kTQ) {
             const int q = q0 + tid;
             const bool in = q < n;
             const int cell = in ? (int)s_cell[q] : -1;
@@ -447,8 +536,7 @@ __global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateVie
         __syncthreads();
         if (tid < 32) {  // exclusive scan of the 65 bucket counts (one warp)
             int carry = 0;
-            for (int b0 = 0; b0 <= G::CELLS; b0 += 32) {
-                const int c = b0 + lane;
+            for (int c = lane; c - lane <= G::CELLS; c += 32) {
                 const int v = c <= G::CELLS ? s_cnt[c] : 0;
                 int inc = v;
 #pragma unroll
@@ -462,7 +550,7 @@ __global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateVie
             if (lane == 0) s_cst[G::CELLS + 1] = carry;
         }
         __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kTC) {  // bucket by cell (order inside a cell arbitrary)
+        for (int q0 = 0; q0 < n; q0 += kTQ) {  // bucket by cell (order inside a cell arbitrary)
             const int q = q0 + tid;
             const bool in = q < n;
             const int cell = in ? (int)s_cell[q] : -1;
@@ -474,7 +562,7 @@ __global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateVie
             if (in) s_tmp[base + __popc(peers & ((1u << lane) - 1u))] = (short)q;
         }
         __syncthreads();
-        for (int r = tid; r < n; r += kTC) {  // rank by particle id inside the cell
+        for (int r = tid; r < n; r += kTQ) {  // rank by particle id inside the cell
             const int q = s_tmp[r];
             const int cell = s_cell[q], pq = s_pid[q];
             int rank = 0;
@@ -484,56 +572,53 @@ __global__ void __launch_bounds__(kTC, 4) k_p2g(KParams p, SlotView sl, StateVie
             sl.sigma[start + fl] = s_idx[q];
             if (Sn.pid) Sn.pid[start + fl] = pq;
         }
-        for (int c = tid; c <= G::CELLS; c += kTC) cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
+        for (int c = tid; c <= G::CELLS; c += kTQ) cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
         if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
         __syncthreads();
-        // ---- phase 1: thread = cell, particles of the cell in canonical order, next one prefetched
-        {
-            NodeAcc<D, true> acc;
-            acc.zero();
-            const int lo = s_cst[tid], hi = s_cst[tid + 1];
-            float nx[3], nvc[L::VC], nF[L::FF];
-            int npid = 0;
-#define MPM_P2G_FETCH(R)                                                                  \
-    do {                                                                                  \
-        const int i_ = s_ci[(R)];                                                          \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) nx[k] = __ldg(S.x + (int64_t)i_ * D + k); \
-        _Pragma("unroll") for (int q = 0; q < L::VC; ++q) nvc[q] = __ldg(S.vc + (int64_t)i_ * L::VC + q); \
-        _Pragma("unroll") for (int q = 0; q < L::FF; ++q) nF[q] = __ldg(S.f + (int64_t)i_ * L::FF + q); \
-        if (aid) npid = __ldg(aid + __ldg(S.pid + i_));                                    \
-    } while (0)
-            if (lo < hi) MPM_P2G_FETCH(lo);
-            for (int r = lo; r < hi; ++r) {
+        const int nvalid = s_cst[G::CELLS];
+        // ---- phases 1 + 2 over chunks of kTQ particles in canonical order
+        SliceAcc<D, true> acc;
+        acc.zero();
+        for (int ch = 0; ch < nvalid; ch += kTQ) {
+            const int r = ch + tid;
+            if (r < nvalid) {
+                const int i = s_ci[r];
                 float x[3], vc[L::VC], F[L::FF];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = nx[k];
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
 #pragma unroll
-                for (int q = 0; q < L::VC; ++q) vc[q] = nvc[q];
+                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + (int64_t)i * L::VC + q);
 #pragma unroll
-                for (int q = 0; q < L::FF; ++q) F[q] = nF[q];
-                const int a_id = npid;  // actuator id (prefetched), valid when aid != null
-                if (r + 1 < hi) MPM_P2G_FETCH(r + 1);
-#undef MPM_P2G_FETCH
-                const float act = (aid && a_id >= 0) ? alpha[a_id] : 0.0f;
+                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + (int64_t)i * L::FF + q);
+                float act = 0.0f;
+                if (aid) {
+                    const int a_id = __ldg(aid + __ldg(S.pid + i));
+                    act = a_id >= 0 ? alpha[a_id] : 0.0f;
+                }
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
                 if (!p2g_particle<D>(p, x, vc, F, act, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
-                acc.add(w, c, Adx);
+                write_row<D>(s_row + tid * RS, w, c, Adx);
                 if (Sn.f) {
                     float* dst = Sn.f + (int64_t)(start + r) * L::FF;
 #pragma unroll
                     for (int q = 0; q < D * D; ++q) dst[q] = Ft[q];
                 }
             }
-            __syncthreads();  // everybody is done with the phase-0 arrays the buffer aliases
-            acc.store(s_cb, tid);
+            __syncthreads();
+            {
+                const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], ch + kTQ);
+                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
+            }
+            __syncthreads();
         }
+        acc.store(s_cb, my_cell, my_ox);  // the rows are dead after the last barrier
         __syncthreads();
-        // ---- phase 2: node tile (plain stores)
+        // ---- phase 3: node tile (plain stores)
         float4* tile = tiles_l + (int64_t)bi * G::TN;
-        for (int q = tid; q < G::TN; q += kTC) {
-            float4 s = node_gather<D>(s_cb, q);
-            s.w *= p.p_mass;
-            tile[q] = s;
+        for (int q = tid; q < G::TN; q += kTQ) {
+            float4 s4 = node_gather<D>(s_cb, q);
+            s4.w *= p.p_mass;
+            tile[q] = s4;
         }
         __syncthreads();
     }
@@ -1195,7 +1280,7 @@ cudaError_t tile_init() {
         if (e) return e;
         e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
         if (e) return e;
-        g_grid[0][0] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTC);
+        g_grid[0][0] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);
         g_grid[1][0] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
         g_grid[2][0] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTC);
         g_grid[3][0] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
@@ -1205,7 +1290,7 @@ cudaError_t tile_init() {
         if (e) return e;
         e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
         if (e) return e;
-        g_grid[0][1] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTC);
+        g_grid[0][1] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);
         g_grid[1][1] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
         g_grid[2][1] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTC);
         g_grid[3][1] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
@@ -1235,7 +1320,7 @@ void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* 
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_p2g<DIM><<<pgrid(p, 0), kTC, p2g_smem_bytes<DIM>(), s>>>(p, sl, S, Sn, aid, alpha_t, flags));
+    DISPATCH(p.dim, k_p2g<DIM><<<pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s>>>(p, sl, S, Sn, aid, alpha_t, flags));
 }
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
                 int* bcount, int* flags, bool refwd, cudaStream_t s) {
