@@ -305,22 +305,22 @@ def run_ours(args):
     A_start = sim.active_nodes()
     A = 0.5 * (A_end + A_start) / per
 
-    sim.reset_kernel_stats()
-    sim.set_profiling(True)
+    # timed region (CUDA graphs replayed; no per-kernel events so nothing perturbs it)
     l0 = sim.launch_count()
     clocks = ClockSampler(local)
     with clocks:
         ms = timed(args.steps, dev_step)
     launches = sim.launch_count() - l0
+    # per-kernel device time: a second timed region with CUDA events bracketing every
+    # library launch on the library's stream (eager launches; graphs are off while profiling)
+    sim.reset_kernel_stats()
+    sim.set_profiling(True)
+    ms_prof = timed(args.steps, dev_step)
     stats = sim.kernel_stats()
     sim.set_profiling(False)
     ms_e2e = timed(args.steps, host_step)
 
-    # units of all ranks (C4 shards may differ by one episode: count them exactly)
-    if world > 1:
-        tot = torch.tensor([float(N) * per * T * args.steps], dtype=torch.float64, device=dev)
-        dist.all_reduce(tot)
-        particle_steps = float(tot.item())
+    particle_steps = float(tot.item())
     else:
         particle_steps = float(N) * per * T * args.steps
     value = particle_steps / (ms / 1e3)
@@ -342,6 +342,7 @@ def run_ours(args):
                 "share_of_kernel_time": dom_ms / total_ms if total_ms else None,
                 "active_nodes_per_episode": A,
                 "kernel_ms": {kk: round(v[0] / args.steps, 3) for kk, v in stats.items() if v[1]},
+                "profiled_ms_per_step": ms_prof / args.steps,
                 "kernel_launches_per_step": {kk: v[1] // args.steps for kk, v in stats.items() if v[1]}}
     # whole-step effective bandwidth against the SURVEY 8(d) byte model
     s_rec = 4 * (2 * p["dim"] + 2 * p["dim"] ** 2)
@@ -376,6 +377,16 @@ def run_ours(args):
     return 0
 
 
+def run_ours_on_stream(args):
+    """the library captures its forward/backward tapes as CUDA graphs, which needs a
+    non-default stream: run the whole arm on a dedicated torch stream."""
+    import torch
+    local = _env_int("LOCAL_RANK", 0) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    with torch.cuda.stream(torch.cuda.Stream()):
+        return run_ours(args)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -388,7 +399,7 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
-    return run_ours(args)
+    return run_ours_on_stream(args)
 
 
 if __name__ == "__main__":

@@ -9,6 +9,10 @@
 // segment in the window without re-running p2g.  Adjoint states are kept in
 // caller (particle-id) order.
 #include <algorithm>
+#include <cstdlib>
+#include <functional>
+#include <map>
+#include <tuple>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -104,6 +108,15 @@ struct mpm_ctx {
     int window_seg = -1;
     int sbar_cur = 0;
     Profiler prof;
+    // CUDA graphs of whole forward / backward tapes, keyed by (kind, T, has_aid, window
+    // segment at entry); replayed instead of re-enqueueing thousands of launches
+    struct GraphRec {
+        cudaGraphExec_t exec = nullptr;
+        int64_t launches = 0;
+        int window_seg = -1, sbar_cur = 0;
+    };
+    std::map<std::tuple<int, int, int, int>, GraphRec> graphs;
+    bool use_graphs = true;
 };
 
 namespace {
@@ -423,6 +436,38 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
     }
 }
 
+// Enqueue `body` through a cached CUDA graph (captured on first use).  body may update
+// h->window_seg / h->sbar_cur; their values after the captured run are replayed.
+mpm_status run_graphed(mpm_handle h, std::tuple<int, int, int, int> key, const std::function<void()>& body) {
+    const bool graphs = h->use_graphs && !h->prof.on && h->stream != 0;
+    if (!graphs) {
+        body();
+        return MPM_OK;
+    }
+    auto it = h->graphs.find(key);
+    if (it == h->graphs.end()) {
+        const int64_t l0 = h->launches;
+        CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+        body();
+        cudaGraph_t g = nullptr;
+        CU(cudaStreamEndCapture(h->stream, &g));
+        mpm_ctx::GraphRec rec;
+        const cudaError_t ie = cudaGraphInstantiate(&rec.exec, g, 0);
+        cudaGraphDestroy(g);
+        CU(ie);
+        rec.launches = h->launches - l0;
+        rec.window_seg = h->window_seg;
+        rec.sbar_cur = h->sbar_cur;
+        h->launches = l0;
+        it = h->graphs.emplace(key, rec).first;
+    }
+    CU(cudaGraphLaunch(it->second.exec, h->stream));
+    h->launches += it->second.launches;
+    h->window_seg = it->second.window_seg;
+    h->sbar_cur = it->second.sbar_cur;
+    return MPM_OK;
+}
+
 mpm_status copy_in(mpm_handle h, void* dst, const void* src, size_t bytes) {
     CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, h->stream));
     return MPM_OK;
@@ -475,6 +520,8 @@ mpm_status mpm_create(int64_t n_particles, int32_t n_grid, int32_t dim, float dt
     cudaError_t e = cudaGetDevice(&h->device);
     if (e == cudaSuccess) e = cudaMallocHost((void**)&h->h_flags, sizeof(int) * 4);
     if (e == cudaSuccess) e = tile_init();
+    const char* ng = std::getenv("MPM_NO_GRAPHS");
+    h->use_graphs = !(ng && ng[0] == '1');
     if (e != cudaSuccess) {
         delete h;
         return MPM_ERR_CUDA;
@@ -487,6 +534,7 @@ mpm_status mpm_destroy(mpm_handle h) {
     if (!h) return MPM_ERR_INVALID_ARG;
     if (h->h_flags) cudaFreeHost(h->h_flags);
     for (auto ev : h->prof.pool) cudaEventDestroy(ev);
+    for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
     delete h;
     return MPM_OK;
 }
@@ -602,9 +650,12 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
         return fail(h, MPM_ERR_INVALID_ARG, "steps must be in [1, max_steps]");
     const KParams k = kparams(h);
     h->t_final = steps;
-    if (k.n_act > 0) { KScope sc(h, KC_CTRL); launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream); }
-    bin_fresh(h, k, 0);
-    for (int t = 0; t < steps; ++t) step_forward(h, k, t, true, t + 1 < steps);
+    mpm_status gs = run_graphed(h, std::make_tuple(0, steps, (int)h->has_aid, -1), [&]() {
+        if (k.n_act > 0) { KScope sc(h, KC_CTRL); launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream); }
+        bin_fresh(h, k, 0);
+        for (int t = 0; t < steps; ++t) step_forward(h, k, t, true, t + 1 < steps);
+    });
+    if (gs) return gs;
     CU(cudaGetLastError());
     h->recorded = steps;
     h->window_seg = (steps - 1) / h->prm.k_ckpt;
@@ -665,25 +716,28 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     const KParams k = kparams(h);
     const int kk = h->prm.k_ckpt, T = steps;
     const int A = k.n_act > 0 ? k.n_act : 1;
-    if (k.n_act > 0) CU(cudaMemsetAsync(h->alpha_bar, 0, sizeof(float) * (size_t)T * A, h->stream));
-    const int nseg = (T + kk - 1) / kk;
-    for (int s = nseg - 1; s >= 0; --s) {
-        const int t0 = s * kk, t1 = (t0 + kk < T) ? t0 + kk : T;
-        if (h->window_seg != s) {  // segment-wise recomputation of the states
-            for (int t = t0; t < t1 - 1; ++t) step_reforward(h, k, t);
-            h->window_seg = s;
+    mpm_status gs = run_graphed(h, std::make_tuple(1, T, (int)h->has_aid, h->window_seg * 2 + h->sbar_cur), [&]() {
+        if (k.n_act > 0) cudaMemsetAsync(h->alpha_bar, 0, sizeof(float) * (size_t)T * A, h->stream);
+        const int nseg = (T + kk - 1) / kk;
+        for (int s = nseg - 1; s >= 0; --s) {
+            const int t0 = s * kk, t1 = (t0 + kk < T) ? t0 + kk : T;
+            if (h->window_seg != s) {  // segment-wise recomputation of the states
+                for (int t = t0; t < t1 - 1; ++t) step_reforward(h, k, t);
+                h->window_seg = s;
+            }
+            for (int t = t1 - 1; t >= t0; --t) {
+                step_backward(h, k, t, h->sbar[h->sbar_cur], h->sbar[h->sbar_cur ^ 1]);
+                h->sbar_cur ^= 1;
+            }
         }
-        for (int t = t1 - 1; t >= t0; --t) {
-            step_backward(h, k, t, h->sbar[h->sbar_cur], h->sbar[h->sbar_cur ^ 1]);
-            h->sbar_cur ^= 1;
+        const int64_t nth = n_theta_of(h->prm);
+        if (nth > 0) {
+            KScope sc(h, KC_CTRL);
+            h->launches += 1;
+            launch_ctrl_bwd(k, h->theta, T, h->alpha, h->alpha_bar, h->theta_part, h->theta_bar, nth, h->stream);
         }
-    }
-    const int64_t nth = n_theta_of(h->prm);
-    if (nth > 0) {
-        KScope sc(h, KC_CTRL);
-        h->launches += 1;
-        launch_ctrl_bwd(k, h->theta, T, h->alpha, h->alpha_bar, h->theta_part, h->theta_bar, nth, h->stream);
-    }
+    });
+    if (gs) return gs;
     CU(cudaGetLastError());
     mpm_status st = sync_flags(h, "mpm_backward");
     if (st) return st;

@@ -576,25 +576,25 @@ __global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateVie
         if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
         __syncthreads();
         const int nvalid = s_cst[G::CELLS];
-        // ---- phases 1 + 2 over chunks of kTQ particles in canonical order
+        // ---- phases 1 + 2 over chunks of kTQ particles in canonical order; the particle
+        // loads of chunk k+1 are issued before the accumulation of chunk k (same registers)
         SliceAcc<D, true> acc;
         acc.zero();
+        float x[3], vc[L::VC], F[L::FF];
+        int a_id = -1;
+#define MPM_P2G_LOAD(R)                                                                          \
+    do {                                                                                         \
+        const int i_ = s_ci[(R)];                                                                 \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i_ * D + k);   \
+        _Pragma("unroll") for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + (int64_t)i_ * L::VC + q); \
+        _Pragma("unroll") for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + (int64_t)i_ * L::FF + q); \
+        if (aid) a_id = __ldg(aid + __ldg(S.pid + i_));                                           \
+    } while (0)
+        if (tid < nvalid) MPM_P2G_LOAD(tid);
         for (int ch = 0; ch < nvalid; ch += kTQ) {
             const int r = ch + tid;
             if (r < nvalid) {
-                const int i = s_ci[r];
-                float x[3], vc[L::VC], F[L::FF];
-#pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
-#pragma unroll
-                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + (int64_t)i * L::VC + q);
-#pragma unroll
-                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + (int64_t)i * L::FF + q);
-                float act = 0.0f;
-                if (aid) {
-                    const int a_id = __ldg(aid + __ldg(S.pid + i));
-                    act = a_id >= 0 ? alpha[a_id] : 0.0f;
-                }
+                const float act = (aid && a_id >= 0) ? alpha[a_id] : 0.0f;
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
                 if (!p2g_particle<D>(p, x, vc, F, act, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
                 write_row<D>(s_row + tid * RS, w, c, Adx);
@@ -605,12 +605,14 @@ __global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateVie
                 }
             }
             __syncthreads();
+            if (r + kTQ < nvalid) MPM_P2G_LOAD(r + kTQ);
             {
                 const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], ch + kTQ);
                 for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
             }
             __syncthreads();
         }
+#undef MPM_P2G_LOAD
         acc.store(s_cb, my_cell, my_ox);  // the rows are dead after the last barrier
         __syncthreads();
         // ---- phase 3: node tile (plain stores)

@@ -253,6 +253,36 @@ def test_active_block_capacity_is_an_error():
     sim.close()
 
 
+def test_cuda_graph_replay_is_bitwise_identical():
+    """forward/backward tapes captured as CUDA graphs on a side stream (and replayed on
+    the second iteration) give the same bytes as eager launches on the default stream"""
+    import torch
+    p = W.config("c4", steps=40)
+    inps = [W.make_inputs(p, episode=e) for e in range(2)]
+    eager = gpu_run(p, inps, k_ckpt=8)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g1 = gpu_run(p, inps, k_ckpt=8)
+    for key in ("x", "v", "C", "F", "dx0", "dv0", "dC0", "dF0", "dtheta", "loss"):
+        assert np.array_equal(eager[key], g1[key]), key
+    from paper_1910_00935_b200 import mpm
+    with torch.cuda.stream(s):  # same handle twice: the second iteration replays the graphs
+        N = len(inps[0]["x"])
+        sim = mpm.sim_from_config(p, N, episodes=2, max_steps=40, k_ckpt=8)
+        cat = lambda k: np.ascontiguousarray(np.stack([i[k] for i in inps]))  # noqa: E731
+        outs = []
+        for _ in range(2):
+            sim.set_state(cat("x"), cat("v"), cat("C"), cat("F"), cat("aid"))
+            sim.set_controller(inps[0]["theta"])
+            sim.forward(40)
+            sim.loss()
+            sim.backward(40)
+            outs.append(sim.grads())
+        sim.close()
+    for key in ("dx0", "dv0", "dtheta"):
+        assert np.array_equal(outs[0][key], outs[1][key]) and np.array_equal(outs[0][key], eager[key]), key
+
+
 def test_native_library_is_what_runs():
     """the kernels launched are ours (launch counter of libmpm_b200.so)"""
     p, inp = inputs("c1a", steps=8)
