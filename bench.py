@@ -320,7 +320,11 @@ def run_ours(args):
     sim.set_profiling(False)
     ms_e2e = timed(args.steps, host_step)
 
-    particle_steps = float(tot.item())
+    # units of all ranks (C4 shards may differ by one episode: count them exactly)
+    if world > 1:
+        tot = torch.tensor([float(N) * per * T * args.steps], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot)
+        particle_steps = float(tot.item())
     else:
         particle_steps = float(N) * per * T * args.steps
     value = particle_steps / (ms / 1e3)
