@@ -359,9 +359,9 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v_cpu, dt_cpu = oracle_sample(p, inps[0], steps=1)
+        v_cpu, dt_cpu = oracle_sample(p, inps[0], steps=4)
         cpu = {"value": v_cpu, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{p['name']} episode 0, all {N:,} particles, 1 time step of forward + "
+               "sample": f"{p['name']} episode 0, all {N:,} particles, 4 time steps of forward + "
                          f"loss + backward, fp64, single thread ({dt_cpu:.1f} s)"}
 
     if rank == 0:

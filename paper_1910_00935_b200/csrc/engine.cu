@@ -31,9 +31,9 @@ enum Phase { kCreated = 0, kBound, kHasState, kForward, kSeeded, kBackward };
 
 // kernel classes for the per-kernel device-time accounting (mpm_kernel_stats)
 enum KClass { KC_P2G = 0, KC_G2P, KC_BIN, KC_G2P_GRAD, KC_P2G_GRAD, KC_REDUCE_ABAR, KC_CTRL,
-              KC_LOSS, KC_LAYOUT, KC_N };
+              KC_LOSS, KC_LAYOUT, KC_GRID_OP, KC_GRID_OP_GRAD, KC_N };
 const char* const kClassNames[KC_N] = {"p2g", "g2p", "bin", "g2p_grad", "p2g_grad", "reduce_abar",
-                                        "controller", "loss", "layout"};
+                                        "controller", "loss", "layout", "grid_op", "grid_op_grad"};
 
 struct Profiler {
     bool on = false;
@@ -88,7 +88,8 @@ struct mpm_ctx {
     int* scan_part = nullptr;      // [scan chunks] int2
     int* keys = nullptr;           // [EN]
     float* xbar_part = nullptr;    // [EN][d]
-    float4* ubar = nullptr;        // [max_active][TN]
+    float4* ubar = nullptr;        // [max_active][TN]  U_bar partial tiles of the current step
+    float4* part = nullptr;        // [max_active][TN]  p2g partial tiles / (Pb, Mb) tiles
     float* abar_part = nullptr;    // [max_active][n_act]
     float* alpha = nullptr;        // [max_steps][n_act]
     float* alpha_bar = nullptr;
@@ -261,6 +262,7 @@ size_t carve(mpm_ctx* h, char* base) {
     int* keys = (int*)take(sizeof(int) * EN);
     float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
     float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
+    float4* part = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
     float* abar_part = (float*)take(sizeof(float) * (size_t)max_active * A);  // per-step buffers
     float* alpha = (float*)take(sizeof(float) * (size_t)p.max_steps * A);
     float* alpha_bar = (float*)take(sizeof(float) * (size_t)p.max_steps * A);
@@ -286,7 +288,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->final_state = fin;
         h->sbar[0] = sb0; h->sbar[1] = sb1;
         h->staging = staging; h->aid = aid; h->bcount = bcount; h->cursor = cursor; h->scan_part = scan_part; h->keys = keys;
-        h->xbar_part = xbar_part; h->ubar = ubar; h->abar_part = abar_part;
+        h->xbar_part = xbar_part; h->ubar = ubar; h->part = part; h->abar_part = abar_part;
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
         h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
         h->flags = flags;
@@ -315,6 +317,7 @@ SlotView slot_at(mpm_ctx* h, int t) {
     s.base = h->base_arr + t;
     s.cstart = h->cstart_pool;
     s.tiles = h->tiles_pool;
+    s.part = h->part;
     s.step = t;
     return s;
 }
@@ -402,6 +405,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr, nullptr, nullptr};
     const int32_t* aid = h->has_aid ? h->aid : nullptr;
     { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
+    { KScope sc(h, KC_GRID_OP); launch_grid_op(k, sl, h->stream); }
     if (!write_next) return;
     { KScope sc(h, KC_G2P);
       launch_g2p(k, sl, S, Sn, bin_next ? h->keys : nullptr, h->bcount, h->flags, false, h->stream); }
@@ -427,8 +431,9 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
     const StateView S = state_at(h, t);
     const int A = k.n_act > 0 ? k.n_act : 1;
     { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, sl, S, Sbn, h->ubar, h->xbar_part, h->stream); }
+    { KScope sc(h, KC_GRID_OP_GRAD); launch_grid_op_grad(k, sl, h->ubar, h->stream); }
     { KScope sc(h, KC_P2G_GRAD);
-      launch_p2g_grad(k, sl, S, h->has_aid ? h->aid : nullptr, alpha_at(h, t), h->ubar, Sbn, h->xbar_part,
+      launch_p2g_grad(k, sl, S, h->has_aid ? h->aid : nullptr, alpha_at(h, t), Sbn, h->xbar_part,
                       Sb, h->abar_part, h->flags, h->stream); }
     if (k.n_act > 0) {
         KScope sc(h, KC_REDUCE_ABAR);

@@ -35,7 +35,9 @@ struct SlotView {
     int* nactive;            // [1]    active blocks of this step
     int* base;               // [1]    pool offset of this step (nactive[-1], base[-1]: previous step)
     unsigned short* cstart;  // pool [P][CELLS+1] cell starts within the block segment
-    float4* tiles;           // pool [P][TN]      (P, M) partial node tiles
+    float4* tiles;           // pool [P][TN]      resolved node tiles (u1, M or -1 = sticky)
+    float4* part;            // [max_active][TN]  per-step scratch: p2g partial (P, M) tiles,
+                             //                   backward: grid_op_grad output (Pb, Mb)
     int step;                // t
 };
 
@@ -54,7 +56,9 @@ void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* 
 // p2g writes F_{t+1} and particle ids of S_{t+1} when Sn.rec / Sn.pid are non-null
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s);
-// g2p (grid_op fused in its staging) writes x, v, C of S_{t+1}; keys != null -> next bin keys;
+// grid_op: sum of the covering partial tiles -> resolved tile of every active block
+void launch_grid_op(const KParams& p, const SlotView& sl, cudaStream_t s);
+// g2p writes x, v, C of S_{t+1}; keys != null -> next bin keys;
 // refwd: segment re-forward from stored tiles -- also writes F_{t+1} = (I + dt C) F and the ids
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
                 int* bcount, int* flags, bool refwd, cudaStream_t s);
@@ -62,8 +66,10 @@ void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const 
 // ---- one reverse step (advance_grad()); Sbn is indexed like S_{t+1}, Sb like S_t
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, float* xbar_part, cudaStream_t s);
+// grid_op_grad: covering sums of the U_bar partial tiles -> (P_bar, M_bar) tiles in sl.part
+void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* ubar, cudaStream_t s);
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
-                     const float* alpha_t, const float4* ubar, const AdjView& Sbn, const float* xbar_part,
+                     const float* alpha_t, const AdjView& Sbn, const float* xbar_part,
                      const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s);
 void launch_reduce_abar(const KParams& p, const int* nactive, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s);

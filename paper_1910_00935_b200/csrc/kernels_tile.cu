@@ -126,6 +126,70 @@ __device__ __forceinline__ bool grid_velocity(const KParams& p, const int g[3], 
     return z;
 }
 
+// ---- bulk async copy (TMA engine, cp.async.bulk) of a contiguous node tile into
+// shared memory, completion tracked by an mbarrier (transaction bytes)
+__device__ __forceinline__ uint32_t smem_u32(const void* ptr) {
+    return (uint32_t)__cvta_generic_to_shared(ptr);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// generic-proxy accesses of the buffer (earlier reads) before the async-proxy write
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+// Double-buffered node-tile pipeline of a persistent CTA: tile(bi) of `src` is copied
+// into buf[it & 1] while the CTA works on the previous block.  Call init() once
+// (before a __syncthreads), start() before the loop, next() at the top of iteration
+// `it` (after the previous iteration's closing __syncthreads) and wait() before use.
+template <int D> struct TilePipe {
+    static constexpr uint32_t BYTES = Geo<D>::TN * sizeof(float4);
+    float4* buf;     // [2][TN]
+    uint64_t* bar;   // [2]
+    __device__ void init() {
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            mbar_init(bar + 1, 1);
+            fence_mbar_init();
+        }
+    }
+    __device__ void start(const float4* src, int bi, int nact) {
+        if (threadIdx.x == 0 && bi < nact) bulk_load(buf, src + (int64_t)bi * Geo<D>::TN, BYTES, bar);
+    }
+    __device__ void next(const float4* src, int bi_next, int nact, int it) {
+        if (threadIdx.x == 0 && bi_next < nact) {
+            fence_proxy_async();
+            const int nb = (it + 1) & 1;
+            bulk_load(buf + nb * Geo<D>::TN, src + (int64_t)bi_next * Geo<D>::TN, BYTES, bar + nb);
+        }
+    }
+    __device__ float4* wait(int it) {
+        const int cb = it & 1;
+        mbar_wait(bar + cb, (uint32_t)((it >> 1) & 1));
+        return buf + cb * Geo<D>::TN;
+    }
+};
+
 // warp-aggregated histogram increment (keys in a warp are mostly equal)
 __device__ __forceinline__ void count_key(bool valid, int key, int* bcount) {
     const unsigned peers = __match_any_sync(0xffffffffu, valid ? key : -1);
@@ -506,7 +570,7 @@ __global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateVie
     const int* blist = sl.blist + b0;
     const int* bstart = sl.bstart + b0 + sl.step;
     unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
-    float4* tiles_l = sl.tiles + (int64_t)b0 * G::TN;
+    float4* tiles_l = sl.part;  // partial tiles of this step (local block index)
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         const int bid = blist[bi];
         const int start = bstart[bi], n = bstart[bi + 1] - start;
@@ -626,24 +690,67 @@ __global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateVie
     }
 }
 
-// stage U = grid_op(sum of covering tiles) for the CTA's tile
-template <int D, int NT = kT>
-__device__ __forceinline__ void stage_velocity(const KParams& p, const SlotView& sl, int e, const int c0[3],
-                                               float4* sU) {
+// ------------------------------------------------------------- grid_op
+// P:579 (R5-R7): thread per node of every active block's (B+2)^d tile:
+// (P, M) = sum of the covering partial tiles; u1 = P/(M + eps) - dt g e_y; sticky walls.
+// Resolved tile entry: (u1, M), or (0, 0, 0, -M) where the wall zeroed the velocity
+// (sign bit set, also for M = 0: -0.0f; nodes outside the grid: (0, 0, 0, -0)).  Stored per step: g2p / g2p_grad / grid_op_grad read it.
+template <int D>
+__global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
     using G = Geo<D>;
-    for (int q = threadIdx.x; q < G::TN; q += NT) {
-        int n[3];
+    const int nact = *sl.nactive;
+    const int b0 = *sl.base;
+    const int* blist = sl.blist + b0;
+    const float4* part_g = sl.part - (int64_t)b0 * G::TN;  // bmap holds pool indices
+    float4* rt = sl.tiles + (int64_t)b0 * G::TN;
+    const int64_t total = (int64_t)nact * G::TN;
+    for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
+        const int bi = (int)(idx / G::TN), q = (int)(idx - (int64_t)bi * G::TN);
+        int e, c0[3], n[3];
+        block_origin<D>(p, __ldg(blist + bi), e, c0);
         local_node<D>(q, n);
         const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
         const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
-        float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 out = make_float4(0.f, 0.f, 0.f, -0.0f);
         if (inside) {
-            const float4 pm = covered_sum<D>(p, e, g, sl.bmap, sl.tiles);
+            const float4 pm = covered_sum<D>(p, e, g, sl.bmap, part_g);
             float u0[3], u1[3];
-            const bool z = grid_velocity<D>(p, g, pm, u0, u1);
-            out = z ? make_float4(0.f, 0.f, 0.f, 1.f) : make_float4(u1[0], u1[1], u1[2], 0.f);
+            out = grid_velocity<D>(p, g, pm, u0, u1) ? make_float4(0.f, 0.f, 0.f, -pm.w)
+                                                      : make_float4(u1[0], u1[1], u1[2], pm.w);
         }
-        sU[q] = out;
+        rt[idx] = out;
+    }
+}
+
+// --------------------------------------------------------- grid_op_grad
+// P:589 (select rule): per node, ub = sum of the covering U_bar partial tiles;
+// sticky (sign bit of w): Pb = Mb = 0; else u0 = u1 + dt g e_y, Pb = ub/(M + eps),
+// Mb = -(ub . u0)/(M + eps).  Output tile (Pb, Mb) -> sl.part (local block index).
+template <int D>
+__global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, const float4* __restrict__ ubar) {
+    using G = Geo<D>;
+    const int nact = *sl.nactive;
+    const int b0 = *sl.base;
+    const int* blist = sl.blist + b0;
+    const float4* ub_g = ubar - (int64_t)b0 * G::TN;
+    const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
+    const int64_t total = (int64_t)nact * G::TN;
+    for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
+        const float4 r = __ldg(rt + idx);
+        float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!signbit(r.w)) {
+            const int bi = (int)(idx / G::TN), q = (int)(idx - (int64_t)bi * G::TN);
+            int e, c0[3], n[3];
+            block_origin<D>(p, __ldg(blist + bi), e, c0);
+            local_node<D>(q, n);
+            const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
+            const float4 ub = covered_sum<D>(p, e, g, sl.bmap, ub_g);
+            const float u0[3] = {r.x, r.y + p.dt * p.gravity, r.z};
+            const float denom = r.w + p.eps_mass;
+            const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
+            out = make_float4(ub.x / denom, ub.y / denom, D == 3 ? ub.z / denom : 0.0f, -dot / denom);
+        }
+        sl.part[idx] = out;
     }
 }
 
@@ -760,21 +867,28 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
                                             int* __restrict__ keys, int* __restrict__ bcount, int* flags,
                                             bool refwd) {
     using G = Geo<D>;
-    __shared__ float4 sU[G::TN];
+    __shared__ __align__(128) float4 s_buf[2 * G::TN];
+    __shared__ __align__(8) uint64_t s_bar[2];
     const int tid = threadIdx.x;
     const int nact = *sl.nactive;
     const int b0 = *sl.base;  // this step's offset in the grid-store pool
     const int* blist = sl.blist + b0;
     const int* bstart = sl.bstart + b0 + sl.step;
     unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
-    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
+    const float4* rt = sl.tiles + (int64_t)b0 * Geo<D>::TN;
+    TilePipe<D> pipe{s_buf, s_bar};
+    pipe.init();
+    __syncthreads();
+    pipe.start(rt, blockIdx.x, nact);
+    int it = 0;
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
+        pipe.next(rt, bi + gridDim.x, nact, it);
         const int bid = blist[bi];
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        // particle loads of the first two passes go out before the tile staging
+        // particle loads of the first two passes go out before waiting for the tile
         float xa[3], xb[3];
         const bool va = tid < nvalid, vb = tid + kTG < nvalid;
         int ia = 0, ib = 0;
@@ -788,8 +902,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
 #pragma unroll
             for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + (int64_t)ib * D + k);
         }
-        stage_velocity<D, kTG>(p, sl, e, c0, sU);
-        __syncthreads();
+        const float4* sU = pipe.wait(it);
         int key = -1;
         if (va) key = g2p_particle<D>(p, sU, xa, c0, start + tid, e, bid, Sn, keys, flags, refwd, S, ia);
         if (keys) count_key(va, key, bcount);
@@ -816,150 +929,154 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
 // ------------------------------------------------------------ g2p_grad
 // vh = vb' + dt xb';  Ub[b+o] += W (vh + 4/dx Cb' (o - f));  Wb = U.(vh + 4/dx Cb'(o - f));
 // fb += Wb dW/df - 4/dx W Cb'^T U;  xb_t (partial) = xb' + fb/dx.
-// CTA = 64 threads = one thread per cell; U_bar accumulated like p2g's momentum.
+// CTA = 192 threads: phase 1 thread per particle (gather part, rows in smem),
+// phase 2 thread per (cell, o_x) accumulating U_bar like p2g's momentum.
+template <int D> constexpr int g2pg_union_bytes() {
+    constexpr int a = Geo<D>::CELLS * Geo<D>::NST * 16, c = kTQ * RowL<D>::STRIDE * 4;
+    return a > c ? a : c;
+}
 template <int D> constexpr int g2pg_smem_bytes() {
-    return Geo<D>::CELLS * Geo<D>::NST * 16 + Geo<D>::TN * 16 + (Geo<D>::CELLS + 2) * 4;
+    return g2pg_union_bytes<D>() + 2 * Geo<D>::TN * 16 + 16 + (Geo<D>::CELLS + 2) * 4;
+}
+
+// per-particle gather part; returns c' = vh - B f and B (row inputs), weights in w
+template <int D>
+__device__ __forceinline__ void g2pg_particle(const KParams& p, const float4* __restrict__ sU, const float* x,
+                                              const float* xb, const float* vbn, const float* Cbn, const int c0[3],
+                                              float w[3][3], float* cp, float* B, float* xbp_out) {
+    const float c4 = 4.0f * p.inv_dx;
+    float vh[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) vh[a] = fmaf(p.dt, xb[a], vbn[a]);
+#pragma unroll
+    for (int q = 0; q < D * D; ++q) B[q] = c4 * Cbn[q];
+    int lb[3];
+    float fx[3], dw[3][3];
+    particle_weights<D>(p, x, c0, lb, fx, w, dw);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        float s = vh[a];
+#pragma unroll
+        for (int b = 0; b < D; ++b) s = fmaf(-B[a * D + b], fx[b], s);
+        cp[a] = s;
+    }
+    float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f};
+#pragma unroll 1
+    for (int o0 = 0; o0 < 3; ++o0) {  // rolled: keeps 9 (not 27) node loads in flight
+        const float w0 = o0 == 0 ? w[0][0] : (o0 == 1 ? w[0][1] : w[0][2]);
+        const float d0 = o0 == 0 ? dw[0][0] : (o0 == 1 ? dw[0][1] : dw[0][2]);
+        float tx[3];
+#pragma unroll
+        for (int a = 0; a < D; ++a) tx[a] = fmaf((float)o0, B[a * D], cp[a]);
+#pragma unroll
+        for (int o1 = 0; o1 < 3; ++o1) {
+            float ty[3];
+#pragma unroll
+            for (int a = 0; a < D; ++a) ty[a] = fmaf((float)o1, B[a * D + 1], tx[a]);
+#pragma unroll
+            for (int o2 = 0; o2 < (D == 3 ? 3 : 1); ++o2) {
+                float t[3];
+#pragma unroll
+                for (int a = 0; a < D; ++a) t[a] = D == 3 ? fmaf((float)o2, B[a * D + 2], ty[a]) : ty[a];
+                const float wyz = D == 3 ? w[1][o1] * w[2][o2] : w[1][o1];
+                const float W = w0 * wyz;
+                float gW[3];
+                gW[0] = d0 * wyz;
+                gW[1] = D == 3 ? w0 * dw[1][o1] * w[2][o2] : w0 * dw[1][o1];
+                if (D == 3) gW[2] = w0 * w[1][o1] * dw[2][o2];
+                const float4 u4 = sU[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
+                const float u[3] = {u4.x, u4.y, u4.z};
+                float Wb = 0.0f;
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    Wb = fmaf(u[a], t[a], Wb);
+                    S0[a] = fmaf(W, u[a], S0[a]);
+                }
+#pragma unroll
+                for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) {  // fb_k -= (B^T S0)_k
+        float s = 0.0f;
+#pragma unroll
+        for (int a = 0; a < D; ++a) s = fmaf(B[a * D + k], S0[a], s);
+        xbp_out[k] = fmaf(p.inv_dx, fb[k] - s, xb[k]);
+    }
 }
 
 template <int D>
-__global__ void __launch_bounds__(kTC, 6) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
+__global__ void __maxnreg__(112) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
                                                     float4* __restrict__ ubar, float* __restrict__ xbp) {
     using G = Geo<D>;
     using L = Lay<D>;
+    constexpr int RS = RowL<D>::STRIDE;
     extern __shared__ __align__(16) unsigned char smem[];
-    float4* s_cb = reinterpret_cast<float4*>(smem);
-    float4* sU = s_cb + G::CELLS * G::NST;
-    int* s_cst = reinterpret_cast<int*>(sU + G::TN);
+    float* s_row = reinterpret_cast<float*>(smem);   // rows, then ...
+    float4* s_cb = reinterpret_cast<float4*>(smem);  // ... node partials
+    float4* s_buf = reinterpret_cast<float4*>(smem + g2pg_union_bytes<D>());  // [2][TN]
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_buf + 2 * G::TN);
+    int* s_cst = reinterpret_cast<int*>(s_bar + 2);
     const int tid = threadIdx.x;
+    const int my_cell = tid / 3, my_ox = tid - 3 * (tid / 3);
     const int nact = *sl.nactive;
-    const int b0 = *sl.base;  // this step's offset in the grid-store pool
+    const int b0 = *sl.base;
     const int* blist = sl.blist + b0;
     const int* bstart = sl.bstart + b0 + sl.step;
-    unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
-    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
-    const float c4 = 4.0f * p.inv_dx;
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
+    const unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
+    const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
+    TilePipe<D> pipe{s_buf, s_bar};
+    pipe.init();
+    __syncthreads();
+    pipe.start(rt, blockIdx.x, nact);
+    int it = 0;
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
+        pipe.next(rt, bi + gridDim.x, nact, it);
         const int bid = blist[bi];
         const int start = bstart[bi];
+        const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        for (int q = threadIdx.x; q < G::TN; q += kTC) {
-            int n[3];
-            local_node<D>(q, n);
-            const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-            const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
-            float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (inside) {
-                const float4 pm = covered_sum<D>(p, e, g, sl.bmap, sl.tiles);
-                float u0[3], u1[3];
-                const bool z = grid_velocity<D>(p, g, pm, u0, u1);
-                out = z ? make_float4(0.f, 0.f, 0.f, 1.f) : make_float4(u1[0], u1[1], u1[2], 0.f);
-            }
-            sU[q] = out;
-        }
-        for (int c = tid; c <= G::CELLS; c += kTC) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
+        // particle loads of the first chunk go out before the tile staging
+        float x[3], xb[3], vbn[3], Cbn[D * D];
+#define MPM_G2PG_LOAD(R)                                                                      \
+    do {                                                                                      \
+        const int j_ = start + (R);                                                           \
+        const int i_ = sl.sigma[j_];                                                          \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i_ * D + k); \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) xb[k] = __ldg(Sbn.x + (int64_t)j_ * D + k); \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) vbn[k] = __ldg(Sbn.vc + (int64_t)j_ * L::VC + k); \
+        _Pragma("unroll") for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + (int64_t)j_ * L::VC + D + q); \
+    } while (0)
+        if (tid < nvalid) MPM_G2PG_LOAD(tid);
+        for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
+        const float4* sU = pipe.wait(it);
         __syncthreads();
-        const int lo = start + s_cst[tid], hi = start + s_cst[tid + 1];
-        // pass 1: gather part (W_bar, f_bar -> partial x_bar), one particle at a time
-        for (int j = lo; j < hi; ++j) {
-            const int i = sl.sigma[j];
-            float x[3];
+        SliceAcc<D, false> acc;
+        acc.zero();
+        for (int ch = 0; ch < nvalid; ch += kTQ) {
+            const int r = ch + tid;
+            if (r < nvalid) {
+                float w[3][3], cp[3], B[D * D], xo[3];
+                g2pg_particle<D>(p, sU, x, xb, vbn, Cbn, c0, w, cp, B, xo);
 #pragma unroll
-            for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
-            float xb[3], vh[3], B[D * D];
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                xb[a] = __ldg(Sbn.x + (int64_t)j * D + a);
-                vh[a] = fmaf(p.dt, xb[a], __ldg(Sbn.vc + (int64_t)j * L::VC + a));
+                for (int k = 0; k < D; ++k) xbp[(int64_t)(start + r) * D + k] = xo[k];
+                write_row<D>(s_row + tid * RS, w, cp, B);
             }
-#pragma unroll
-            for (int q = 0; q < D * D; ++q) B[q] = c4 * __ldg(Sbn.vc + (int64_t)j * L::VC + D + q);
-            int lb[3];
-            float fx[3], w[3][3], dw[3][3];
-            particle_weights<D>(p, x, c0, lb, fx, w, dw);
-            float cp[3];  // c' = vh - B f ; t_o = c' + B o
-#pragma unroll
-            for (int a = 0; a < D; ++a) {
-                float s = vh[a];
-#pragma unroll
-                for (int b = 0; b < D; ++b) s = fmaf(-B[a * D + b], fx[b], s);
-                cp[a] = s;
+            __syncthreads();
+            if (r + kTQ < nvalid) MPM_G2PG_LOAD(r + kTQ);
+            {
+                const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], ch + kTQ);
+                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
             }
-            float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-            for (int o0 = 0; o0 < 3; ++o0) {
-                float tx[3];
-#pragma unroll
-                for (int a = 0; a < D; ++a) tx[a] = fmaf((float)o0, B[a * D], cp[a]);
-#pragma unroll
-                for (int o1 = 0; o1 < 3; ++o1) {
-                    float ty[3];
-#pragma unroll
-                    for (int a = 0; a < D; ++a) ty[a] = fmaf((float)o1, B[a * D + 1], tx[a]);
-#pragma unroll
-                    for (int o2 = 0; o2 < (D == 3 ? 3 : 1); ++o2) {
-                        float t[3];
-#pragma unroll
-                        for (int a = 0; a < D; ++a) t[a] = D == 3 ? fmaf((float)o2, B[a * D + 2], ty[a]) : ty[a];
-                        const float wyz = D == 3 ? w[1][o1] * w[2][o2] : w[1][o1];
-                        const float W = w[0][o0] * wyz;
-                        float gW[3];
-                        gW[0] = dw[0][o0] * wyz;
-                        gW[1] = D == 3 ? w[0][o0] * dw[1][o1] * w[2][o2] : w[0][o0] * dw[1][o1];
-                        if (D == 3) gW[2] = w[0][o0] * w[1][o1] * dw[2][o2];
-                        const float4 u4 = sU[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
-                        const float u[3] = {u4.x, u4.y, u4.z};
-                        float Wb = 0.0f;
-#pragma unroll
-                        for (int a = 0; a < D; ++a) {
-                            Wb = fmaf(u[a], t[a], Wb);
-                            S0[a] = fmaf(W, u[a], S0[a]);
-                        }
-#pragma unroll
-                        for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
-                    }
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < D; ++k) {  // fb_k -= (B^T S0)_k
-                float s = 0.0f;
-#pragma unroll
-                for (int a = 0; a < D; ++a) s = fmaf(B[a * D + k], S0[a], s);
-                xbp[(int64_t)j * D + k] = fmaf(p.inv_dx, fb[k] - s, xb[k]);
-            }
+            __syncthreads();
         }
-        // pass 2: U_bar scatter of the cell, accumulated in registers (inputs re-read, L1/L2 hits)
-        {
-            NodeAcc<D, false> acc;
-            acc.zero();
-            for (int j = lo; j < hi; ++j) {
-                const int i = sl.sigma[j];
-                float x[3], vh[3], B[D * D];
-#pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
-#pragma unroll
-                for (int a = 0; a < D; ++a)
-                    vh[a] = fmaf(p.dt, __ldg(Sbn.x + (int64_t)j * D + a), __ldg(Sbn.vc + (int64_t)j * L::VC + a));
-#pragma unroll
-                for (int q = 0; q < D * D; ++q) B[q] = c4 * __ldg(Sbn.vc + (int64_t)j * L::VC + D + q);
-                int lb[3];
-                float fx[3], w[3][3], dw[3][3];
-                particle_weights<D>(p, x, c0, lb, fx, w, dw);
-                float cp[3];
-#pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    float s = vh[a];
-#pragma unroll
-                    for (int b = 0; b < D; ++b) s = fmaf(-B[a * D + b], fx[b], s);
-                    cp[a] = s;
-                }
-                acc.add(w, cp, B);
-            }
-            acc.store(s_cb, tid);
-        }
+#undef MPM_G2PG_LOAD
+        acc.store(s_cb, my_cell, my_ox);
         __syncthreads();
         float4* tile = ubar + (int64_t)bi * G::TN;
-        for (int q = tid; q < G::TN; q += kTC) tile[q] = node_gather<D>(s_cb, q);
+        for (int q = tid; q < G::TN; q += kTQ) tile[q] = node_gather<D>(s_cb, q);
         __syncthreads();
     }
 }
@@ -1096,13 +1213,13 @@ constexpr int kTP = 128;  // p2g_grad CTA
 template <int D>
 __global__ void __launch_bounds__(kTP, 4) k_p2g_grad(KParams p, SlotView sl, StateView S,
                                                  const int32_t* __restrict__ aid,
-                                                 const float* __restrict__ alpha,
-                                                 const float4* __restrict__ ubar, AdjView Sbn,
+                                                 const float* __restrict__ alpha, AdjView Sbn,
                                                  const float* __restrict__ xbp, AdjView Sb,
                                                  float* __restrict__ abar_part, int* flags) {
     using G = Geo<D>;
     using L = Lay<D>;
-    __shared__ float4 sG[G::TN];
+    __shared__ __align__(128) float4 s_buf[2 * G::TN];
+    __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ float s_ab[kTP / 32][32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nact = *sl.nactive;
@@ -1110,13 +1227,23 @@ __global__ void __launch_bounds__(kTP, 4) k_p2g_grad(KParams p, SlotView sl, Sta
     const int* blist = sl.blist + b0;
     const int* bstart = sl.bstart + b0 + sl.step;
     unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
-    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
+    const float4* gt = sl.part;  // (Pb, Mb) tiles from grid_op_grad (local block index)
+    TilePipe<D> pipe{s_buf, s_bar};
+    pipe.init();
+    __syncthreads();
+    pipe.start(gt, blockIdx.x, nact);
+    int it = 0;
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
+        pipe.next(gt, bi + gridDim.x, nact, it);
         const int bid = blist[bi];
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
+        s_ab[warp][lane] = 0.0f;  // each warp owns its row
+        __syncwarp();
+        const float4* sG = nullptr;
+        if (nvalid == 0) pipe.wait(it);
         for (int r0 = 0; r0 < nvalid; r0 += kTP) {
             const int r = r0 + tid;
             const bool in = r < nvalid;
@@ -1139,29 +1266,7 @@ __global__ void __launch_bounds__(kTP, 4) k_p2g_grad(KParams p, SlotView sl, Sta
                 for (int k = 0; k < D; ++k) xb[k] = __ldg(xbp + (int64_t)j * D + k);
                 if (aid) a_id = __ldg(aid + __ldg(S.pid + i));
             }
-            if (r0 == 0) {
-                for (int q = tid; q < G::TN; q += kTP) {
-                    int n[3];
-                    local_node<D>(q, n);
-                    const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-                    const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
-                    float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (inside) {
-                        const float4 pm = covered_sum<D>(p, e, g, sl.bmap, sl.tiles);
-                        const float4 ub = covered_sum<D>(p, e, g, sl.bmap, ubar - (int64_t)b0 * G::TN);
-                        float u0[3], u1[3];
-                        const bool z = grid_velocity<D>(p, g, pm, u0, u1);
-                        if (!z) {
-                            const float denom = pm.w + p.eps_mass;
-                            const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
-                            out = make_float4(ub.x / denom, ub.y / denom, D == 3 ? ub.z / denom : 0.0f, -dot / denom);
-                        }
-                    }
-                    sG[q] = out;
-                }
-                for (int q = tid; q < (kTP / 32) * 32; q += kTP) (&s_ab[0][0])[q] = 0.0f;
-                __syncthreads();
-            }
+            if (r0 == 0) sG = pipe.wait(it);
             float abar = 0.0f;
             if (in) {
                 const bool has_act = aid && a_id >= 0;
@@ -1180,10 +1285,6 @@ __global__ void __launch_bounds__(kTP, 4) k_p2g_grad(KParams p, SlotView sl, Sta
                     rem &= ~__ballot_sync(0xffffffffu, a_id == target);
                 }
             }
-        }
-        if (nvalid == 0) {  // keep the staging barrier structure uniform
-            for (int q = tid; q < (kTP / 32) * 32; q += kTP) (&s_ab[0][0])[q] = 0.0f;
-            __syncthreads();
         }
         __syncthreads();
         if (p.n_act > 0 && tid < p.n_act) {
@@ -1207,52 +1308,30 @@ __global__ void k_reduce_abar(const int* __restrict__ nactive, const float* __re
     if (threadIdx.x == 0) out[a] = s;
 }
 
-// measurement: number of distinct grid nodes with M > 0 in a slot's tiles.  Each
-// node is counted once, by the first active block in covered_sum's order.
+// measurement: number of distinct grid nodes with M > 0 in a step's resolved tiles.
+// Each node is counted once, in the tile of the block that owns it (local n < B).
 template <int D>
 __global__ void __launch_bounds__(kT) k_count_active(KParams p, SlotView sl, unsigned long long* count) {
     using G = Geo<D>;
     const int nact = *sl.nactive;
-    const int b0 = *sl.base;  // this step's offset in the grid-store pool
-    const int* blist = sl.blist + b0;
-    const int* bstart = sl.bstart + b0 + sl.step;
-    unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
-    float4* tiles_l = sl.tiles + (int64_t)b0 * Geo<D>::TN;
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
-        int e, c0[3];
-        block_origin<D>(p, blist[bi], e, c0);
-        for (int q = threadIdx.x; q < G::TN; q += kT) {
-            int n[3];
-            local_node<D>(q, n);
-            const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-            if (g[0] >= p.n_grid || g[1] >= p.n_grid || (D == 3 && g[2] >= p.n_grid)) continue;
-            if (covered_sum<D>(p, e, g, sl.bmap, sl.tiles).w <= 0.0f) continue;
-            // first active covering block (same enumeration as covered_sum)
-            int first = -1;
-            for (int a = 0; a < 2 && first < 0; ++a)
-                for (int b = 0; b < 2 && first < 0; ++b)
-                    for (int c = 0; c < (D == 3 ? 2 : 1) && first < 0; ++c) {
-                        const int off[3] = {a, b, c};
-                        int bb[3] = {0, 0, 0};
-                        bool ok = true;
-                        for (int k = 0; k < D; ++k) {
-                            const int b0 = g[k] >> G::LOGB, l0 = g[k] & (G::B - 1);
-                            if (off[k] == 1 && !(l0 < 2 && b0 >= 1)) ok = false;
-                            bb[k] = b0 - off[k];
-                            if (bb[k] >= p.nb) ok = false;
-                        }
-                        if (!ok) continue;
-                        const int ti = sl.bmap[block_lin<D>(p, e, bb)];
-                        if (ti >= 0) first = ti;
-                    }
-            if (first == b0 + bi) atomicAdd(count, 1ull);
-        }
+    const int b0 = *sl.base;
+    const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
+    const int64_t total = (int64_t)nact * G::TN;
+    unsigned long long c = 0;
+    for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
+        int n[3];
+        local_node<D>((int)(idx % G::TN), n);
+        if (n[0] >= G::B || n[1] >= G::B || (D == 3 && n[2] >= G::B)) continue;
+        if (fabsf(rt[idx].w) > 0.0f) ++c;  // |w| = M (sign bit = sticky)
     }
+    for (int off = 16; off > 0; off >>= 1) c += __shfl_xor_sync(0xffffffffu, c, off);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
 inline unsigned nblk(int64_t n) { return (unsigned)((n + kT - 1) / kT); }
 
 int g_grid[4][2];  // persistent grid size per kernel kind and dimension (set by tile_init)
+int g_sms = 148;
 
 }  // namespace
 
@@ -1277,6 +1356,11 @@ cudaError_t tile_init() {
     static bool done = false;
     if (done) return cudaSuccess;
     cudaError_t e = cudaSuccess;
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
     DISPATCH(2, {
         e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>());
         if (e) return e;
@@ -1284,7 +1368,7 @@ cudaError_t tile_init() {
         if (e) return e;
         g_grid[0][0] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);
         g_grid[1][0] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
-        g_grid[2][0] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTC);
+        g_grid[2][0] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTQ);
         g_grid[3][0] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
     });
     DISPATCH(3, {
@@ -1294,7 +1378,7 @@ cudaError_t tile_init() {
         if (e) return e;
         g_grid[0][1] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);
         g_grid[1][1] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
-        g_grid[2][1] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTC);
+        g_grid[2][1] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTQ);
         g_grid[3][1] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
     });
     done = true;
@@ -1324,22 +1408,33 @@ void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const 
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
     DISPATCH(p.dim, k_p2g<DIM><<<pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s>>>(p, sl, S, Sn, aid, alpha_t, flags));
 }
+static unsigned node_grid(const KParams& p) {
+    const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? Geo<3>::TN : Geo<2>::TN) + kT - 1) / kT;
+    const int64_t cap = (int64_t)g_sms * 8;
+    return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
+}
+void launch_grid_op(const KParams& p, const SlotView& sl, cudaStream_t s) {
+    DISPATCH(p.dim, k_grid_op<DIM><<<node_grid(p), kT, 0, s>>>(p, sl));
+}
+void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* ubar, cudaStream_t s) {
+    DISPATCH(p.dim, k_grid_op_grad<DIM><<<node_grid(p), kT, 0, s>>>(p, sl, ubar));
+}
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
                 int* bcount, int* flags, bool refwd, cudaStream_t s) {
     DISPATCH(p.dim, k_g2p<DIM><<<pgrid(p, 1), kTG, 0, s>>>(p, sl, S, Sn, keys, bcount, flags, refwd));
 }
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, float* xbp, cudaStream_t s) {
-    DISPATCH(p.dim, k_g2p_grad<DIM><<<pgrid(p, 2), kTC, g2pg_smem_bytes<DIM>(), s>>>(p, sl, S, Sbn, ubar, xbp));
+    DISPATCH(p.dim, k_g2p_grad<DIM><<<pgrid(p, 2), kTQ, g2pg_smem_bytes<DIM>(), s>>>(p, sl, S, Sbn, ubar, xbp));
 }
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
-                     const float* alpha_t, const float4* ubar, const AdjView& Sbn, const float* xbp,
+                     const float* alpha_t, const AdjView& Sbn, const float* xbp,
                      const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_p2g_grad<DIM><<<pgrid(p, 3), kTP, 0, s>>>(p, sl, S, aid, alpha_t, ubar, Sbn, xbp, Sb, abar_part, flags));
+    DISPATCH(p.dim, k_p2g_grad<DIM><<<pgrid(p, 3), kTP, 0, s>>>(p, sl, S, aid, alpha_t, Sbn, xbp, Sb, abar_part, flags));
 }
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s) {
     cudaMemsetAsync(count, 0, sizeof(int64_t), s);
-    DISPATCH(p.dim, k_count_active<DIM><<<pgrid(p, 1), kT, 0, s>>>(p, sl, (unsigned long long*)count));
+    DISPATCH(p.dim, k_count_active<DIM><<<node_grid(p), kT, 0, s>>>(p, sl, (unsigned long long*)count));
 }
 void launch_reduce_abar(const KParams& p, const int* nactive, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s) {
