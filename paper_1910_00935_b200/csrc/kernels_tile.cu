@@ -423,12 +423,13 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
 constexpr int kTC = 64;  // thread-per-cell kernels: one thread per cell of a block (CELLS = 64)
 
 constexpr int kTQ = 192;  // p2g CTA: 3 threads per cell (64 cells) in the accumulation phase
+constexpr int kCH = 3 * kTQ;  // rows per chunk: most blocks fit one chunk -> all 64 cells busy in phase 2
 
 template <int D> struct RowL {  // particle row in shared memory (floats); stride avoids STS.128 conflicts
     static constexpr int STRIDE = D == 3 ? 28 : 12;
 };
 template <int D> constexpr int p2g_union_bytes() {
-    constexpr int a = Geo<D>::MAXP * 11, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kTQ * RowL<D>::STRIDE * 4;
+    constexpr int a = Geo<D>::MAXP * 11, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 template <int D> constexpr int p2g_smem_bytes() {
@@ -655,23 +656,23 @@ __global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateVie
         if (aid) a_id = __ldg(aid + __ldg(S.pid + i_));                                           \
     } while (0)
         if (tid < nvalid) MPM_P2G_LOAD(tid);
-        for (int ch = 0; ch < nvalid; ch += kTQ) {
-            const int r = ch + tid;
-            if (r < nvalid) {
+        for (int ch = 0; ch < nvalid; ch += kCH) {
+            const int cend = min(nvalid, ch + kCH);
+            for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
                 const float act = (aid && a_id >= 0) ? alpha[a_id] : 0.0f;
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
                 if (!p2g_particle<D>(p, x, vc, F, act, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
-                write_row<D>(s_row + tid * RS, w, c, Adx);
+                write_row<D>(s_row + (r - ch) * RS, w, c, Adx);
                 if (Sn.f) {
                     float* dst = Sn.f + (int64_t)(start + r) * L::FF;
 #pragma unroll
                     for (int q = 0; q < D * D; ++q) dst[q] = Ft[q];
                 }
+                if (r + kTQ < nvalid) MPM_P2G_LOAD(r + kTQ);  // this thread's next particle
             }
             __syncthreads();
-            if (r + kTQ < nvalid) MPM_P2G_LOAD(r + kTQ);
             {
-                const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], ch + kTQ);
+                const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], cend);
                 for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
             }
             __syncthreads();
@@ -932,7 +933,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
 // CTA = 192 threads: phase 1 thread per particle (gather part, rows in smem),
 // phase 2 thread per (cell, o_x) accumulating U_bar like p2g's momentum.
 template <int D> constexpr int g2pg_union_bytes() {
-    constexpr int a = Geo<D>::CELLS * Geo<D>::NST * 16, c = kTQ * RowL<D>::STRIDE * 4;
+    constexpr int a = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
     return a > c ? a : c;
 }
 template <int D> constexpr int g2pg_smem_bytes() {
@@ -1055,19 +1056,19 @@ __global__ void __maxnreg__(112) k_g2p_grad(KParams p, SlotView sl, StateView S,
         __syncthreads();
         SliceAcc<D, false> acc;
         acc.zero();
-        for (int ch = 0; ch < nvalid; ch += kTQ) {
-            const int r = ch + tid;
-            if (r < nvalid) {
+        for (int ch = 0; ch < nvalid; ch += kCH) {
+            const int cend = min(nvalid, ch + kCH);
+            for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
                 float w[3][3], cp[3], B[D * D], xo[3];
                 g2pg_particle<D>(p, sU, x, xb, vbn, Cbn, c0, w, cp, B, xo);
 #pragma unroll
                 for (int k = 0; k < D; ++k) xbp[(int64_t)(start + r) * D + k] = xo[k];
-                write_row<D>(s_row + tid * RS, w, cp, B);
+                write_row<D>(s_row + (r - ch) * RS, w, cp, B);
+                if (r + kTQ < nvalid) MPM_G2PG_LOAD(r + kTQ);  // this thread's next particle
             }
             __syncthreads();
-            if (r + kTQ < nvalid) MPM_G2PG_LOAD(r + kTQ);
             {
-                const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], ch + kTQ);
+                const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], cend);
                 for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
             }
             __syncthreads();
@@ -1364,6 +1365,10 @@ cudaError_t tile_init() {
     DISPATCH(2, {
         e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>());
         if (e) return e;
+        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e) return e;
+        e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e) return e;
         e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
         if (e) return e;
         g_grid[0][0] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);
@@ -1373,6 +1378,10 @@ cudaError_t tile_init() {
     });
     DISPATCH(3, {
         e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>());
+        if (e) return e;
+        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        if (e) return e;
+        e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         if (e) return e;
         e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
         if (e) return e;

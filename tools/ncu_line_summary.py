@@ -29,6 +29,12 @@ for row in csv.reader(io.StringIO(out)):
     except ValueError:  # SASS rows and '-' cells
         continue
     stats.append((s, e, f"{fname}:{row[0]}", row[1].strip()[:90]))
+merged = {}
+for s_, e_, where, src in stats:  # several launches of the kernel: merge per line
+    m = merged.setdefault(where, [0, 0, src])
+    m[0] += s_
+    m[1] += e_
+stats = [(v[0], v[1], k, v[2]) for k, v in merged.items()]
 tot_s = sum(s for s, *_ in stats) or 1
 tot_e = sum(e for _, e, *_ in stats) or 1
 print(f"stall samples {tot_s}, warp-instr {tot_e}")
