@@ -172,6 +172,7 @@ KParams kparams(const mpm_ctx* h) {
     k.nodes = h->dim == 2 ? (int64_t)h->n_grid * h->n_grid
                           : (int64_t)h->n_grid * h->n_grid * h->n_grid;
     k.E = p.n_episodes;
+    k.EN = (int64_t)h->N * p.n_episodes;
     const int B = block_edge(h->dim);
     k.nb = (h->n_grid + B - 1) / B;
     k.nbe = h->dim == 2 ? k.nb * k.nb : k.nb * k.nb * k.nb;

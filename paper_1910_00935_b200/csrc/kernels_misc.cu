@@ -98,10 +98,9 @@ __global__ void k_ctrl_reduce(const float* __restrict__ part, int T, int64_t n_t
 constexpr int kLossThreads = 256;
 
 // partial sums of a d-vector field over a contiguous particle chunk (fixed tree order);
-// field row i = base[i * stride + k]
+// component k of particle i = base[k * EN + i] (the first d components of a state array)
 template <int D>
-__global__ void k_sum_partial(KParams p, const float* __restrict__ base, int stride,
-                              float* __restrict__ part) {
+__global__ void k_sum_partial(KParams p, const float* __restrict__ base, float* __restrict__ part) {
     __shared__ float red[D][kLossThreads];
     const int e = blockIdx.y, nb = gridDim.x;
     const int64_t chunk = (p.N + nb - 1) / nb;
@@ -110,9 +109,8 @@ __global__ void k_sum_partial(KParams p, const float* __restrict__ base, int str
 #pragma unroll
     for (int k = 0; k < D; ++k) acc[k] = 0.0f;
     for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const float* r = base + ((int64_t)e * p.N + i) * stride;
 #pragma unroll
-        for (int k = 0; k < D; ++k) acc[k] += r[k];
+        for (int k = 0; k < D; ++k) acc[k] += base[soa(p.EN, k, (int64_t)e * p.N + i)];
     }
 #pragma unroll
     for (int k = 0; k < D; ++k) red[k][threadIdx.x] = acc[k];
@@ -181,11 +179,11 @@ __global__ void k_seed(KParams p, const float* __restrict__ seed, AdjView Sb) {
     if (i >= p.N * p.E) return;
     const int64_t e = i / p.N;
 #pragma unroll
-    for (int k = 0; k < D; ++k) Sb.x[i * D + k] = seed[e * D + k];
+    for (int k = 0; k < D; ++k) Sb.x[soa(p.EN, k, i)] = seed[e * D + k];
 #pragma unroll
-    for (int q = 0; q < Lay<D>::VC; ++q) Sb.vc[i * Lay<D>::VC + q] = 0.0f;
+    for (int q = 0; q < Lay<D>::VC; ++q) Sb.vc[soa(p.EN, q, i)] = 0.0f;
 #pragma unroll
-    for (int q = 0; q < Lay<D>::FF; ++q) Sb.f[i * Lay<D>::FF + q] = 0.0f;
+    for (int q = 0; q < Lay<D>::FF; ++q) Sb.f[soa(p.EN, q, i)] = 0.0f;
 }
 
 // ------------------------------------------------------------- layout
@@ -200,13 +198,13 @@ __global__ void k_pack(KParams p, const float* __restrict__ x, const float* __re
     const int64_t s = src ? (int64_t)src[i] : i;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        dx[i * D + k] = x ? x[s * D + k] : 0.0f;
-        dvc[i * Lay<D>::VC + k] = v ? v[s * D + k] : 0.0f;
+        dx[soa(p.EN, k, i)] = x ? x[s * D + k] : 0.0f;
+        dvc[soa(p.EN, k, i)] = v ? v[s * D + k] : 0.0f;
     }
 #pragma unroll
     for (int q = 0; q < D * D; ++q) {
-        dvc[i * Lay<D>::VC + D + q] = C ? C[s * D * D + q] : 0.0f;
-        df[i * Lay<D>::FF + q] = F ? F[s * D * D + q] : ((!zero_f && (q % (D + 1)) == 0) ? 1.0f : 0.0f);
+        dvc[soa(p.EN, D + q, i)] = C ? C[s * D * D + q] : 0.0f;
+        df[soa(p.EN, q, i)] = F ? F[s * D * D + q] : ((!zero_f && (q % (D + 1)) == 0) ? 1.0f : 0.0f);
     }
 }
 
@@ -220,13 +218,13 @@ __global__ void k_unpack(KParams p, const float* __restrict__ sx, const float* _
     const int64_t o = dst ? (int64_t)dst[i] : i;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        if (x) x[o * D + k] = sx[i * D + k];
-        if (v) v[o * D + k] = svc[i * Lay<D>::VC + k];
+        if (x) x[o * D + k] = sx[soa(p.EN, k, i)];
+        if (v) v[o * D + k] = svc[soa(p.EN, k, i)];
     }
 #pragma unroll
     for (int q = 0; q < D * D; ++q) {
-        if (C) C[o * D * D + q] = svc[i * Lay<D>::VC + D + q];
-        if (F) F[o * D * D + q] = sf[i * Lay<D>::FF + q];
+        if (C) C[o * D * D + q] = svc[soa(p.EN, D + q, i)];
+        if (F) F[o * D * D + q] = sf[soa(p.EN, q, i)];
     }
 }
 
@@ -266,7 +264,7 @@ void launch_loss(const KParams& p, const float* x, int loss_kind, float3 target,
     const int nb = loss_blocks_per_episode(p);
     float* seed = com_part + (int64_t)p.E * nb * p.dim;
     DISPATCH(p.dim, {
-        k_sum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, x, DIM, com_part);
+        k_sum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, x, com_part);
         k_loss_final<DIM><<<p.E, 32, 0, s>>>(p, com_part, nb, loss_kind, target, loss, seed, flags);
         k_seed<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, seed, Sb);
     });
@@ -275,7 +273,7 @@ void launch_loss(const KParams& p, const float* x, int loss_kind, float3 target,
 void launch_v_sum(const KParams& p, const float* vc_bar, float* part, float* out, cudaStream_t s) {
     const int nb = loss_blocks_per_episode(p);
     DISPATCH(p.dim, {
-        k_sum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, vc_bar, Lay<DIM>::VC, part);
+        k_sum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, vc_bar, part);
         k_sum_parts<DIM><<<p.E, 32, 0, s>>>(part, nb, out);
     });
 }

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
     if (in) {
         float x[3];
 #pragma unroll
-        for (int k = 0; k < D; ++k) x[k] = X[i * D + k];
+        for (int k = 0; k < D; ++k) x[k] = X[soa(p.EN, k, i)];
         int b[3];
         const bool ok = base_cell<D>(p, x, b);
         const int e = (int)(i / p.N);
@@ -650,9 +650,9 @@ __global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateVie
 #define MPM_P2G_LOAD(R)                                                                          \
     do {                                                                                         \
         const int i_ = s_ci[(R)];                                                                 \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i_ * D + k);   \
-        _Pragma("unroll") for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + (int64_t)i_ * L::VC + q); \
-        _Pragma("unroll") for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + (int64_t)i_ * L::FF + q); \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i_));      \
+        _Pragma("unroll") for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + soa(p.EN, q, i_)); \
+        _Pragma("unroll") for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + soa(p.EN, q, i_));  \
         if (aid) a_id = __ldg(aid + __ldg(S.pid + i_));                                           \
     } while (0)
         if (tid < nvalid) MPM_P2G_LOAD(tid);
@@ -664,9 +664,8 @@ __global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateVie
                 if (!p2g_particle<D>(p, x, vc, F, act, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
                 write_row<D>(s_row + (r - ch) * RS, w, c, Adx);
                 if (Sn.f) {
-                    float* dst = Sn.f + (int64_t)(start + r) * L::FF;
 #pragma unroll
-                    for (int q = 0; q < D * D; ++q) dst[q] = Ft[q];
+                    for (int q = 0; q < D * D; ++q) Sn.f[soa(p.EN, q, start + r)] = Ft[q];
                 }
                 if (r + kTQ < nvalid) MPM_P2G_LOAD(r + kTQ);  // this thread's next particle
             }
@@ -822,27 +821,26 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
     gather_moments<D>(sU, lb, w, S0, Sb);
     float xn[3];
     bool fin = true;
-    float* dvc = Sn.vc + (int64_t)j * L::VC;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         xn[a] = fmaf(p.dt, S0[a], x[a]);
-        Sn.x[(int64_t)j * D + a] = xn[a];
-        dvc[a] = S0[a];
+        Sn.x[soa(p.EN, a, j)] = xn[a];
+        Sn.vc[soa(p.EN, a, j)] = S0[a];
         fin = fin && isfinite(S0[a]);
 #pragma unroll
-        for (int b = 0; b < D; ++b) dvc[D + a * D + b] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
+        for (int b = 0; b < D; ++b) Sn.vc[soa(p.EN, D + a * D + b, j)] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
     }
     if (!fin) atomicOr(flags, FLAG_NONFINITE);
     if (refwd) {  // re-forward from stored tiles: F_{t+1} and the particle id too
         float C[D * D], F[D * D], Ft[D * D];
 #pragma unroll
         for (int q = 0; q < D * D; ++q) {
-            C[q] = __ldg(S.vc + i * L::VC + D + q);
-            F[q] = __ldg(S.f + i * L::FF + q);
+            C[q] = __ldg(S.vc + soa(p.EN, D + q, i));
+            F[q] = __ldg(S.f + soa(p.EN, q, i));
         }
         deform_update<D>(p.dt, C, F, Ft);
 #pragma unroll
-        for (int q = 0; q < D * D; ++q) Sn.f[(int64_t)j * L::FF + q] = Ft[q];
+        for (int q = 0; q < D * D; ++q) Sn.f[soa(p.EN, q, j)] = Ft[q];
         Sn.pid[j] = __ldg(S.pid + i);
     }
     int key = -1;
@@ -896,12 +894,12 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
         if (va) {
             ia = sl.sigma[start + tid];
 #pragma unroll
-            for (int k = 0; k < D; ++k) xa[k] = __ldg(S.x + (int64_t)ia * D + k);
+            for (int k = 0; k < D; ++k) xa[k] = __ldg(S.x + soa(p.EN, k, ia));
         }
         if (vb) {
             ib = sl.sigma[start + tid + kTG];
 #pragma unroll
-            for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + (int64_t)ib * D + k);
+            for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + soa(p.EN, k, ib));
         }
         const float4* sU = pipe.wait(it);
         int key = -1;
@@ -918,7 +916,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
                 const int i = sl.sigma[start + r];
                 float x[3];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i * D + k);
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i));
                 key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags, refwd, S, i);
             }
             if (keys) count_key(in, key, bcount);
@@ -1045,10 +1043,10 @@ __global__ void __maxnreg__(112) k_g2p_grad(KParams p, SlotView sl, StateView S,
     do {                                                                                      \
         const int j_ = start + (R);                                                           \
         const int i_ = sl.sigma[j_];                                                          \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + (int64_t)i_ * D + k); \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) xb[k] = __ldg(Sbn.x + (int64_t)j_ * D + k); \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) vbn[k] = __ldg(Sbn.vc + (int64_t)j_ * L::VC + k); \
-        _Pragma("unroll") for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + (int64_t)j_ * L::VC + D + q); \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i_));   \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) xb[k] = __ldg(Sbn.x + soa(p.EN, k, j_)); \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) vbn[k] = __ldg(Sbn.vc + soa(p.EN, k, j_)); \
+        _Pragma("unroll") for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + soa(p.EN, D + q, j_)); \
     } while (0)
         if (tid < nvalid) MPM_G2PG_LOAD(tid);
         for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
@@ -1062,7 +1060,7 @@ __global__ void __maxnreg__(112) k_g2p_grad(KParams p, SlotView sl, StateView S,
                 float w[3][3], cp[3], B[D * D], xo[3];
                 g2pg_particle<D>(p, sU, x, xb, vbn, Cbn, c0, w, cp, B, xo);
 #pragma unroll
-                for (int k = 0; k < D; ++k) xbp[(int64_t)(start + r) * D + k] = xo[k];
+                for (int k = 0; k < D; ++k) xbp[soa(p.EN, k, start + r)] = xo[k];
                 write_row<D>(s_row + (r - ch) * RS, w, cp, B);
                 if (r + kTQ < nvalid) MPM_G2PG_LOAD(r + kTQ);  // this thread's next particle
             }
@@ -1183,8 +1181,6 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
         Ftb[q] = Fbn[q];
     }
     const float abar = kirchhoff_adj<D>(p, Ft, has_act, act, taub, Ftb);
-    float* dvc = Sb.vc + i * L::VC;
-    float* dF = Sb.f + i * L::FF;
     bool fin = true;
 #pragma unroll
     for (int a = 0; a < D; ++a)
@@ -1196,14 +1192,14 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
                 sF = fmaf(p.dt * C[k * D + a], Ftb[k * D + b], sF);
                 sC = fmaf(Ftb[a * D + k], F[b * D + k], sC);
             }
-            dF[a * D + b] = sF;
-            dvc[D + a * D + b] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
+            Sb.f[soa(p.EN, a * D + b, i)] = sF;
+            Sb.vc[soa(p.EN, D + a * D + b, i)] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
             fin = fin && isfinite(sF);
         }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        Sb.x[i * D + a] = fmaf(p.inv_dx, fb[a], xbp[a]);
-        dvc[a] = p.p_mass * S0[a];
+        Sb.x[soa(p.EN, a, i)] = fmaf(p.inv_dx, fb[a], xbp[a]);
+        Sb.vc[soa(p.EN, a, i)] = p.p_mass * S0[a];
     }
     if (!fin) atomicOr(flags, FLAG_NONFINITE);
     return abar;
@@ -1256,15 +1252,15 @@ __global__ void __launch_bounds__(kTP, 4) k_p2g_grad(KParams p, SlotView sl, Sta
                 const int j = start + r;
                 i = sl.sigma[j];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + i * D + k);
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i));
 #pragma unroll
-                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + i * L::VC + q);
+                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + soa(p.EN, q, i));
 #pragma unroll
-                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + i * L::FF + q);
+                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + soa(p.EN, q, i));
 #pragma unroll
-                for (int q = 0; q < L::FF; ++q) Fbn[q] = __ldg(Sbn.f + (int64_t)j * L::FF + q);
+                for (int q = 0; q < L::FF; ++q) Fbn[q] = __ldg(Sbn.f + soa(p.EN, q, j));
 #pragma unroll
-                for (int k = 0; k < D; ++k) xb[k] = __ldg(xbp + (int64_t)j * D + k);
+                for (int k = 0; k < D; ++k) xb[k] = __ldg(xbp + soa(p.EN, k, j));
                 if (aid) a_id = __ldg(aid + __ldg(S.pid + i));
             }
             if (r0 == 0) sG = pipe.wait(it);

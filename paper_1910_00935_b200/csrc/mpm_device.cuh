@@ -22,6 +22,7 @@ struct KParams {
     int32_t TB;          // blocks, all episodes (E * nbe)
     int32_t max_active;  // capacity (blocks) of the grid-store pool shared by all steps
     int32_t step_blocks; // capacity of one step's block-local buffers (U_bar tiles, partials)
+    int64_t EN;          // particles, all episodes (N * E): component stride of the state arrays
 };
 
 enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8 };
@@ -43,13 +44,17 @@ template <int D> struct Geo {
     static constexpr int MAXP = 1728;                // particles per block (27 per cell)
 };
 
-// State layout: three dense arrays per state, so a kernel
-// that needs only x (g2p, g2p_grad, binning, loss) reads 4d bytes per particle.
+// State layout: three component-major (SoA) arrays per
+// state -- component k of particle i at ptr[k * EN + i] -- so a warp's access to one
+// component of consecutive particles is one contiguous segment, and a kernel that
+// needs only x (g2p, g2p_grad, binning, loss) reads 4d bytes per particle.
 template <int D> struct Lay {
-    static constexpr int X = D;           // x        [n][d]
-    static constexpr int VC = D + D * D;  // (v, C)   [n][d + d^2]   (v first, C row-major)
-    static constexpr int FF = D * D;      // F        [n][d^2]       row-major
+    static constexpr int X = D;           // x        [d][n]
+    static constexpr int VC = D + D * D;  // (v, C)   [d + d^2][n]   (v first, C row-major)
+    static constexpr int FF = D * D;      // F        [d^2][n]       row-major
 };
+// element (component k, particle i) of a component-major array with n particles
+__device__ __forceinline__ int64_t soa(int64_t n, int k, int64_t i) { return (int64_t)k * n + i; }
 
 // quadratic B-spline N_0..N_2 at f in [1/2, 3/2) and derivatives (R1)
 __device__ __forceinline__ void bspline(float f, float w[3], float dw[3]) {

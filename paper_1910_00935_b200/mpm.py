@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpm_b200.so")
+# MPM_B200_LIB: an alternative build of the same library (A/B kernel experiments)
+LIB_PATH = os.environ.get("MPM_B200_LIB") or os.path.join(_HERE, "libmpm_b200.so")
 
 MPM_OK = 0
 STATUS_NAMES = {0: "MPM_OK", 1: "MPM_ERR_INVALID_ARG", 2: "MPM_ERR_OOM", 3: "MPM_ERR_CUDA",
