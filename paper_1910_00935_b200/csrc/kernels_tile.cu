@@ -429,7 +429,7 @@ template <int D> struct RowL {  // particle row in shared memory (floats); strid
     static constexpr int STRIDE = D == 3 ? 28 : 12;
 };
 template <int D> constexpr int p2g_union_bytes() {
-    constexpr int a = Geo<D>::MAXP * 11, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
+    constexpr int a = Geo<D>::MAXP * 15, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 template <int D> constexpr int p2g_smem_bytes() {
@@ -557,7 +557,8 @@ __global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateVie
     extern __shared__ __align__(16) unsigned char smem[];
     int* s_idx = reinterpret_cast<int*>(smem);                       // phase 0 ...
     int* s_pid = s_idx + G::MAXP;
-    short* s_tmp = reinterpret_cast<short*>(s_pid + G::MAXP);
+    int* s_bpid = s_pid + G::MAXP;                                   // pid in bucketed order
+    short* s_tmp = reinterpret_cast<short*>(s_bpid + G::MAXP);
     unsigned char* s_cell = reinterpret_cast<unsigned char*>(s_tmp + G::MAXP);
     float* s_row = reinterpret_cast<float*>(smem);                   // ... phase 1/2 rows ...
     float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... node partials
@@ -624,14 +625,19 @@ __global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateVie
             int base = 0;
             if (in && lane == leader) base = atomicAdd(&s_cnt[cell], __popc(peers));
             base = __shfl_sync(0xffffffffu, base, leader);
-            if (in) s_tmp[base + __popc(peers & ((1u << lane) - 1u))] = (short)q;
+            if (in) {
+                const int pos = base + __popc(peers & ((1u << lane) - 1u));
+                s_tmp[pos] = (short)q;
+                s_bpid[pos] = s_pid[q];
+            }
         }
         __syncthreads();
         for (int r = tid; r < n; r += kTQ) {  // rank by particle id inside the cell
             const int q = s_tmp[r];
-            const int cell = s_cell[q], pq = s_pid[q];
+            const int cell = s_cell[q], pq = s_bpid[r];
             int rank = 0;
-            for (int m = s_cst[cell]; m < s_cst[cell + 1]; ++m) rank += s_pid[s_tmp[m]] < pq;
+            const int m1 = s_cst[cell + 1];
+            for (int m = s_cst[cell]; m < m1; ++m) rank += s_bpid[m] < pq;
             const int fl = s_cst[cell] + rank;
             s_ci[fl] = s_idx[q];
             sl.sigma[start + fl] = s_idx[q];

@@ -7,6 +7,7 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 40
+by_instr = len(sys.argv) > 4 and sys.argv[4] == "instr"  # sort by executed instructions
 # (ncu prints this page only into a pipe; regexes must avoid '<')
 out = subprocess.run(f"ncu -i {rep} --page source --csv --print-source cuda,sass -k regex:{kern} 2>&1 | cat",
                      shell=True, capture_output=True, text=True).stdout
@@ -38,5 +39,6 @@ stats = [(v[0], v[1], k, v[2]) for k, v in merged.items()]
 tot_s = sum(s for s, *_ in stats) or 1
 tot_e = sum(e for _, e, *_ in stats) or 1
 print(f"stall samples {tot_s}, warp-instr {tot_e}")
-for s, e, where, src in sorted(stats, reverse=True)[:top]:
+key = (lambda t: t[1]) if by_instr else (lambda t: t[0])
+for s, e, where, src in sorted(stats, key=key, reverse=True)[:top]:
     print(f"{100*s/tot_s:5.1f}% {100*e/tot_e:5.1f}%  {where:22s} {src}")
