@@ -242,7 +242,10 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
 // starts, block map, scatter cursors; clears the histogram.  Two launches over chunks of
 // 256 x 16 entries: k_bin_scan<0> writes per-chunk totals, k_bin_scan<1> adds the totals
 // of the earlier chunks (fixed order) and writes the outputs.
-constexpr int kScanPer = 16;
+#ifndef MPM_SCAN_PER
+#define MPM_SCAN_PER 4
+#endif
+constexpr int kScanPer = MPM_SCAN_PER;
 constexpr int kScanChunk = kT * kScanPer;
 template <int MODE>
 __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bcount, int* __restrict__ cursor,
@@ -327,23 +330,42 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
     }
 }
 
+// stable-free scatter of particle indices by block key (position inside a block is
+// arbitrary; p2g canonicalises).  kScatterPer particles per thread, all loads and
+// cursor atomics issued before any result is used (memory-level parallelism).
+constexpr int kScatterPer = 4;
 __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __restrict__ keys,
                                                     const int* __restrict__ pid, int* __restrict__ cursor,
                                                     SlotView sl) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool in = j < p.N * p.E;
-    const int kc = in ? keys[j] : -1;
-    const int key = in ? kc >> 7 : -1;
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
-    int base = 0;
-    if (in && lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (in) {
-        const int pos = base + __popc(peers & ((1u << lane) - 1u));
-        sl.sigma[pos] = (int)j;
-        sl.scell[pos] = (unsigned char)(kc & 127);
-        sl.spid[pos] = pid[j];
+    const int64_t n = p.N * p.E;
+    const int lane = threadIdx.x & 31;
+    int64_t j[kScatterPer];
+    int kc[kScatterPer], pj[kScatterPer], base[kScatterPer];
+    unsigned peers[kScatterPer];
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u) {
+        j[u] = ((int64_t)blockIdx.x * kScatterPer + u) * kT + threadIdx.x;
+        const bool in = j[u] < n;
+        kc[u] = in ? __ldg(keys + j[u]) : -1;
+        pj[u] = in ? __ldg(pid + j[u]) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u) {
+        const int key = kc[u] >= 0 ? kc[u] >> 7 : -1;
+        peers[u] = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(peers[u]) - 1;
+        base[u] = 0;
+        if (kc[u] >= 0 && lane == leader) base[u] = atomicAdd(&cursor[key], __popc(peers[u]));
+    }
+#pragma unroll
+    for (int u = 0; u < kScatterPer; ++u) {
+        const int b = __shfl_sync(0xffffffffu, base[u], __ffs(peers[u]) - 1);
+        if (kc[u] >= 0) {
+            const int pos = b + __popc(peers[u] & ((1u << lane) - 1u));
+            sl.sigma[pos] = (int)j[u];
+            sl.scell[pos] = (unsigned char)(kc[u] & 127);
+            sl.spid[pos] = pj[u];
+        }
     }
 }
 
@@ -422,8 +444,24 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
 
 constexpr int kTC = 64;  // thread-per-cell kernels: one thread per cell of a block (CELLS = 64)
 
+// Tuning knobs (overridable with -D for A/B builds, tools/build_variant.py)
+#ifndef MPM_P2G_CHUNK
+#define MPM_P2G_CHUNK 576
+#endif
+#ifndef MPM_P2G_MINB
+#define MPM_P2G_MINB 3
+#endif
+#ifndef MPM_G2PG_MAXREG
+#define MPM_G2PG_MAXREG 112
+#endif
+#ifndef MPM_P2GG_MINB
+#define MPM_P2GG_MINB 4
+#endif
+#ifndef MPM_G2P_THREADS
+#define MPM_G2P_THREADS 128
+#endif
 constexpr int kTQ = 192;  // p2g CTA: 3 threads per cell (64 cells) in the accumulation phase
-constexpr int kCH = 3 * kTQ;  // rows per chunk: most blocks fit one chunk -> all 64 cells busy in phase 2
+constexpr int kCH = MPM_P2G_CHUNK;  // rows per chunk: most blocks fit one chunk -> all 64 cells busy in phase 2
 
 template <int D> struct RowL {  // particle row in shared memory (floats); stride avoids STS.128 conflicts
     static constexpr int STRIDE = D == 3 ? 28 : 12;
@@ -548,7 +586,7 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
 // node b+o receives W_o (m v + A (o - f) dx) and W_o m.  F_{t+1} = Ft.
 // CTA = 192 threads: phase 1 thread per particle (rows in smem), phase 2 thread per (cell, o_x).
 template <int D>
-__global__ void __launch_bounds__(kTQ, 3) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
+__global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
                                                const int32_t* __restrict__ aid,
                                                const float* __restrict__ alpha, int* flags) {
     using G = Geo<D>;
@@ -810,7 +848,7 @@ __device__ __forceinline__ void gather_moments(const float4* __restrict__ sU, co
 }
 
 // ----------------------------------------------------------------- G2P
-constexpr int kTG = 128;  // g2p CTA: smaller CTAs -> more independent blocks in flight per SM
+constexpr int kTG = MPM_G2P_THREADS;  // g2p CTA: smaller CTAs -> more independent blocks in flight per SM
 // v' = sum W U; C' = 4/dx sum W U (o - f)^T = 4/dx (Sb - v' f^T); x' = x + dt v'
 template <int D>
 __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __restrict__ sU, const float* x,
@@ -1012,7 +1050,7 @@ __device__ __forceinline__ void g2pg_particle(const KParams& p, const float4* __
 }
 
 template <int D>
-__global__ void __maxnreg__(112) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
+__global__ void __maxnreg__(MPM_G2PG_MAXREG) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
                                                     float4* __restrict__ ubar, float* __restrict__ xbp) {
     using G = Geo<D>;
     using L = Lay<D>;
@@ -1214,7 +1252,7 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
 constexpr int kTP = 128;  // p2g_grad CTA
 
 template <int D>
-__global__ void __launch_bounds__(kTP, 4) k_p2g_grad(KParams p, SlotView sl, StateView S,
+__global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, SlotView sl, StateView S,
                                                  const int32_t* __restrict__ aid,
                                                  const float* __restrict__ alpha, AdjView Sbn,
                                                  const float* __restrict__ xbp, AdjView Sb,
@@ -1413,7 +1451,7 @@ void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView&
 }
 void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
                         cudaStream_t s) {
-    k_bin_scatter<<<nblk(p.N * p.E), kT, 0, s>>>(p, keys, pid, cursor, sl);
+    k_bin_scatter<<<(unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s>>>(p, keys, pid, cursor, sl);
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
