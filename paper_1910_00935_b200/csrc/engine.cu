@@ -54,6 +54,9 @@ struct mpm_ctx {
     float dt = 0, E = 0, nu = 0;
     mpm_params prm{};
     cudaStream_t stream = 0;
+    cudaStream_t side = nullptr;             // second stream (g2p_grad gather || U_bar scatter)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    float* xbar_part = nullptr;    // [d][EN] xb_t partial from g2p_grad's gather part
     int device = 0;
     std::string err;
     int64_t launches = 0;
@@ -87,7 +90,6 @@ struct mpm_ctx {
     int* cursor = nullptr;         // [TB]
     int* scan_part = nullptr;      // [scan chunks] int2
     int* keys = nullptr;           // [EN]
-    float* xbar_part = nullptr;    // [EN][d]
     float4* ubar = nullptr;        // [max_active][TN]  U_bar partial tiles of the current step
     float4* part = nullptr;        // [max_active][TN]  p2g partial tiles / (Pb, Mb) tiles
     float* abar_part = nullptr;    // [max_active][n_act]
@@ -257,11 +259,11 @@ size_t carve(mpm_ctx* h, char* base) {
     AdjView sb1 = adj();
     float* staging = (float*)take(sizeof(float) * sf);
     int32_t* aid = (int32_t*)take(sizeof(int32_t) * EN);
+    float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
     int* bcount = (int*)take(sizeof(int) * k.TB);
     int* cursor = (int*)take(sizeof(int) * k.TB);
     int* scan_part = (int*)take(sizeof(int) * 2 * (scan_chunks(k) + 1));
     int* keys = (int*)take(sizeof(int) * EN);
-    float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
     float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
     float4* part = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
     float* abar_part = (float*)take(sizeof(float) * (size_t)max_active * A);  // per-step buffers
@@ -288,8 +290,9 @@ size_t carve(mpm_ctx* h, char* base) {
         h->window = window;
         h->final_state = fin;
         h->sbar[0] = sb0; h->sbar[1] = sb1;
+        h->xbar_part = xbar_part;
         h->staging = staging; h->aid = aid; h->bcount = bcount; h->cursor = cursor; h->scan_part = scan_part; h->keys = keys;
-        h->xbar_part = xbar_part; h->ubar = ubar; h->part = part; h->abar_part = abar_part;
+        h->ubar = ubar; h->part = part; h->abar_part = abar_part;
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
         h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
         h->flags = flags;
@@ -431,8 +434,24 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
     const SlotView sl = slot_at(h, t);
     const StateView S = state_at(h, t);
     const int A = k.n_act > 0 ? k.n_act : 1;
-    { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, sl, S, Sbn, h->ubar, h->xbar_part, h->stream); }
+    // g2p_grad's gather part is independent of its U_bar scatter and of grid_op_grad:
+    // it runs on the side stream (fork/join by events; captured into the graphs as a
+    // parallel branch).  Profiling keeps everything on one stream so the per-kernel
+    // CUDA-event times stay exclusive.
+    const bool fork = !h->prof.on && h->side != nullptr;
+    if (fork) {
+        cudaEventRecord(h->ev_fork, h->stream);
+        cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+        launch_g2p_grad_gather(k, sl, S, Sbn, h->xbar_part, h->side);
+        cudaEventRecord(h->ev_join, h->side);
+        h->launches += 1;
+    } else {
+        KScope sc(h, KC_G2P_GRAD);
+        launch_g2p_grad_gather(k, sl, S, Sbn, h->xbar_part, h->stream);
+    }
+    { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, sl, S, Sbn, h->ubar, h->stream); }
     { KScope sc(h, KC_GRID_OP_GRAD); launch_grid_op_grad(k, sl, h->ubar, h->stream); }
+    if (fork) cudaStreamWaitEvent(h->stream, h->ev_join, 0);
     { KScope sc(h, KC_P2G_GRAD);
       launch_p2g_grad(k, sl, S, h->has_aid ? h->aid : nullptr, alpha_at(h, t), Sbn, h->xbar_part,
                       Sb, h->abar_part, h->flags, h->stream); }
@@ -541,6 +560,9 @@ mpm_status mpm_destroy(mpm_handle h) {
     if (h->h_flags) cudaFreeHost(h->h_flags);
     for (auto ev : h->prof.pool) cudaEventDestroy(ev);
     for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
+    if (h->side) cudaStreamDestroy(h->side);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     delete h;
     return MPM_OK;
 }
@@ -579,6 +601,11 @@ mpm_status mpm_set_params(mpm_handle h, const mpm_params* p) {
 mpm_status mpm_set_stream(mpm_handle h, void* s) {
     if (!h) return MPM_ERR_INVALID_ARG;
     h->stream = (cudaStream_t)s;
+    if (!h->side) {  // the side stream of the backward's parallel branch (see step_backward)
+        CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    }
     return MPM_OK;
 }
 

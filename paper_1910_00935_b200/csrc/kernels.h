@@ -64,8 +64,12 @@ void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const 
                 int* bcount, int* flags, bool refwd, cudaStream_t s);
 
 // ---- one reverse step (advance_grad()); Sbn is indexed like S_{t+1}, Sb like S_t
+// g2p_grad in two independent passes over step t's blocks: the U_bar scatter and
+// the gather part (xb_t partial = xb_{t+1} + fb/dx); they may run on two streams
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
-                     float4* ubar, float* xbar_part, cudaStream_t s);
+                     float4* ubar, cudaStream_t s);
+void launch_g2p_grad_gather(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
+                            float* xbar_part, cudaStream_t s);
 // grid_op_grad: covering sums of the U_bar partial tiles -> (P_bar, M_bar) tiles in sl.part
 void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* ubar, cudaStream_t s);
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,

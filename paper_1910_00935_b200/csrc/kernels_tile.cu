@@ -451,8 +451,8 @@ constexpr int kTC = 64;  // thread-per-cell kernels: one thread per cell of a bl
 #ifndef MPM_P2G_MINB
 #define MPM_P2G_MINB 3
 #endif
-#ifndef MPM_G2PG_MAXREG
-#define MPM_G2PG_MAXREG 112
+#ifndef MPM_G2PG_MINB
+#define MPM_G2PG_MINB 3
 #endif
 #ifndef MPM_P2GG_MINB
 #define MPM_P2GG_MINB 4
@@ -970,23 +970,22 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
 }
 
 // ------------------------------------------------------------ g2p_grad
-// vh = vb' + dt xb';  Ub[b+o] += W (vh + 4/dx Cb' (o - f));  Wb = U.(vh + 4/dx Cb'(o - f));
-// fb += Wb dW/df - 4/dx W Cb'^T U;  xb_t (partial) = xb' + fb/dx.
-// CTA = 192 threads: phase 1 thread per particle (gather part, rows in smem),
-// phase 2 thread per (cell, o_x) accumulating U_bar like p2g's momentum.
+// vh = vb' + dt xb';  Ub[b+o] += W (vh + 4/dx Cb' (o - f))  (the scatter part; the gather
+// part Wb = U.(vh + 4/dx Cb'(o - f)), fb += Wb dW/df - 4/dx W Cb'^T U, xb_t = xb' + fb/dx
+// runs in p2g_grad's pass over the same block, g2pg_gather).
+// CTA = 192 threads: phase 1 thread per particle (rows in smem), phase 2 thread per
+// (cell, o_x) accumulating U_bar like p2g's momentum.
 template <int D> constexpr int g2pg_union_bytes() {
     constexpr int a = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
     return a > c ? a : c;
 }
-template <int D> constexpr int g2pg_smem_bytes() {
-    return g2pg_union_bytes<D>() + 2 * Geo<D>::TN * 16 + 16 + (Geo<D>::CELLS + 2) * 4;
-}
+template <int D> constexpr int g2pg_smem_bytes() { return g2pg_union_bytes<D>() + (Geo<D>::CELLS + 2) * 4; }
 
-// per-particle gather part; returns c' = vh - B f and B (row inputs), weights in w
+// per-particle row inputs of the U_bar scatter: vh = vb' + dt xb'; B = 4/dx Cb';
+// c' = vh - B f (weights in w)
 template <int D>
-__device__ __forceinline__ void g2pg_particle(const KParams& p, const float4* __restrict__ sU, const float* x,
-                                              const float* xb, const float* vbn, const float* Cbn, const int c0[3],
-                                              float w[3][3], float* cp, float* B, float* xbp_out) {
+__device__ __forceinline__ void g2pg_row(const KParams& p, const float* x, const float* xb, const float* vbn,
+                                         const float* Cbn, const int c0[3], float w[3][3], float* cp, float* B) {
     const float c4 = 4.0f * p.inv_dx;
     float vh[3];
 #pragma unroll
@@ -996,6 +995,29 @@ __device__ __forceinline__ void g2pg_particle(const KParams& p, const float4* __
     int lb[3];
     float fx[3], dw[3][3];
     particle_weights<D>(p, x, c0, lb, fx, w, dw);
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        float s = vh[a];
+#pragma unroll
+        for (int b = 0; b < D; ++b) s = fmaf(-B[a * D + b], fx[b], s);
+        cp[a] = s;
+    }
+}
+
+// g2p_grad's gather part, evaluated inside p2g_grad's pass over the same step-t
+// block (same binning, same weights): Wb_o = U_o . (vh + B (o - f));
+// fb = sum_o Wb_o grad W_o - B^T sum_o W_o U_o;  returns xb_t (partial) = xb' + fb/dx.
+template <int D>
+__device__ __forceinline__ void g2pg_gather(const KParams& p, const float4* __restrict__ sU, const int lb[3],
+                                            const float fx[3], const float w[3][3], const float dw[3][3],
+                                            const float* xb, const float* vbn, const float* Cbn,
+                                            float* xbp_out) {
+    const float c4 = 4.0f * p.inv_dx;
+    float vh[3], B[D * D], cp[3];
+#pragma unroll
+    for (int a = 0; a < D; ++a) vh[a] = fmaf(p.dt, xb[a], vbn[a]);
+#pragma unroll
+    for (int q = 0; q < D * D; ++q) B[q] = c4 * Cbn[q];
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         float s = vh[a];
@@ -1050,17 +1072,14 @@ __device__ __forceinline__ void g2pg_particle(const KParams& p, const float4* __
 }
 
 template <int D>
-__global__ void __maxnreg__(MPM_G2PG_MAXREG) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
-                                                    float4* __restrict__ ubar, float* __restrict__ xbp) {
+__global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
+                                                            float4* __restrict__ ubar) {
     using G = Geo<D>;
-    using L = Lay<D>;
     constexpr int RS = RowL<D>::STRIDE;
     extern __shared__ __align__(16) unsigned char smem[];
     float* s_row = reinterpret_cast<float*>(smem);   // rows, then ...
     float4* s_cb = reinterpret_cast<float4*>(smem);  // ... node partials
-    float4* s_buf = reinterpret_cast<float4*>(smem + g2pg_union_bytes<D>());  // [2][TN]
-    uint64_t* s_bar = reinterpret_cast<uint64_t*>(s_buf + 2 * G::TN);
-    int* s_cst = reinterpret_cast<int*>(s_bar + 2);
+    int* s_cst = reinterpret_cast<int*>(smem + g2pg_union_bytes<D>());
     const int tid = threadIdx.x;
     const int my_cell = tid / 3, my_ox = tid - 3 * (tid / 3);
     const int nact = *sl.nactive;
@@ -1068,20 +1087,12 @@ __global__ void __maxnreg__(MPM_G2PG_MAXREG) k_g2p_grad(KParams p, SlotView sl, 
     const int* blist = sl.blist + b0;
     const int* bstart = sl.bstart + b0 + sl.step;
     const unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
-    const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
-    TilePipe<D> pipe{s_buf, s_bar};
-    pipe.init();
-    __syncthreads();
-    pipe.start(rt, blockIdx.x, nact);
-    int it = 0;
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
-        pipe.next(rt, bi + gridDim.x, nact, it);
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         const int bid = blist[bi];
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        // particle loads of the first chunk go out before the tile staging
         float x[3], xb[3], vbn[3], Cbn[D * D];
 #define MPM_G2PG_LOAD(R)                                                                      \
     do {                                                                                      \
@@ -1094,17 +1105,14 @@ __global__ void __maxnreg__(MPM_G2PG_MAXREG) k_g2p_grad(KParams p, SlotView sl, 
     } while (0)
         if (tid < nvalid) MPM_G2PG_LOAD(tid);
         for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
-        const float4* sU = pipe.wait(it);
         __syncthreads();
         SliceAcc<D, false> acc;
         acc.zero();
         for (int ch = 0; ch < nvalid; ch += kCH) {
             const int cend = min(nvalid, ch + kCH);
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
-                float w[3][3], cp[3], B[D * D], xo[3];
-                g2pg_particle<D>(p, sU, x, xb, vbn, Cbn, c0, w, cp, B, xo);
-#pragma unroll
-                for (int k = 0; k < D; ++k) xbp[soa(p.EN, k, start + r)] = xo[k];
+                float w[3][3], cp[3], B[D * D];
+                g2pg_row<D>(p, x, xb, vbn, Cbn, c0, w, cp, B);
                 write_row<D>(s_row + (r - ch) * RS, w, cp, B);
                 if (r + kTQ < nvalid) MPM_G2PG_LOAD(r + kTQ);  // this thread's next particle
             }
@@ -1120,6 +1128,65 @@ __global__ void __maxnreg__(MPM_G2PG_MAXREG) k_g2p_grad(KParams p, SlotView sl, 
         __syncthreads();
         float4* tile = ubar + (int64_t)bi * G::TN;
         for (int q = tid; q < G::TN; q += kTQ) tile[q] = node_gather<D>(s_cb, q);
+        __syncthreads();
+    }
+}
+
+// g2p_grad's gather part as its own pass: thread per particle of a block,
+// U tile staged like g2p.  Runs on a second stream, concurrently with the U_bar scatter
+// (k_g2p_grad) and grid_op_grad; writes xb_t (partial) for p2g_grad.
+template <int D>
+__global__ void __launch_bounds__(kTG) k_g2p_grad_gather(KParams p, SlotView sl, StateView S, AdjView Sbn,
+                                                        float* __restrict__ xbp) {
+    using G = Geo<D>;
+    __shared__ __align__(128) float4 s_buf[2 * G::TN];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const int tid = threadIdx.x;
+    const int nact = *sl.nactive;
+    const int b0 = *sl.base;
+    const int* blist = sl.blist + b0;
+    const int* bstart = sl.bstart + b0 + sl.step;
+    const unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
+    const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
+    TilePipe<D> pipe{s_buf, s_bar};
+    pipe.init();
+    __syncthreads();
+    pipe.start(rt, blockIdx.x, nact);
+    int it = 0;
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
+        pipe.next(rt, bi + gridDim.x, nact, it);
+        const int start = bstart[bi];
+        const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
+        int e, c0[3];
+        block_origin<D>(p, blist[bi], e, c0);
+        const float4* sU = nullptr;
+        if (nvalid == 0) pipe.wait(it);
+        for (int r0 = 0; r0 < nvalid; r0 += kTG) {
+            const int r = r0 + tid;
+            const bool in = r < nvalid;
+            float x[3], xb[3], vbn[3], Cbn[D * D];
+            const int j = start + r;
+            if (in) {
+                const int i = sl.sigma[j];
+#pragma unroll
+                for (int k = 0; k < D; ++k) {
+                    x[k] = __ldg(S.x + soa(p.EN, k, i));
+                    xb[k] = __ldg(Sbn.x + soa(p.EN, k, j));
+                    vbn[k] = __ldg(Sbn.vc + soa(p.EN, k, j));
+                }
+#pragma unroll
+                for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + soa(p.EN, D + q, j));
+            }
+            if (r0 == 0) sU = pipe.wait(it);
+            if (in) {
+                int lb[3];
+                float fx[3], w[3][3], dw[3][3], xo[3];
+                particle_weights<D>(p, x, c0, lb, fx, w, dw);
+                g2pg_gather<D>(p, sU, lb, fx, w, dw, xb, vbn, Cbn, xo);
+#pragma unroll
+                for (int k = 0; k < D; ++k) xbp[soa(p.EN, k, j)] = xo[k];
+            }
+        }
         __syncthreads();
     }
 }
@@ -1371,7 +1438,7 @@ __global__ void __launch_bounds__(kT) k_count_active(KParams p, SlotView sl, uns
 
 inline unsigned nblk(int64_t n) { return (unsigned)((n + kT - 1) / kT); }
 
-int g_grid[4][2];  // persistent grid size per kernel kind and dimension (set by tile_init)
+int g_grid[5][2];  // persistent grid size per kernel kind and dimension (set by tile_init)
 int g_sms = 148;
 
 }  // namespace
@@ -1415,6 +1482,7 @@ cudaError_t tile_init() {
         g_grid[1][0] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
         g_grid[2][0] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTQ);
         g_grid[3][0] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
+        g_grid[4][0] = occupancy_grid((const void*)k_g2p_grad_gather<DIM>, 0, kTG);
     });
     DISPATCH(3, {
         e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>());
@@ -1429,13 +1497,22 @@ cudaError_t tile_init() {
         g_grid[1][1] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
         g_grid[2][1] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTQ);
         g_grid[3][1] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
+        g_grid[4][1] = occupancy_grid((const void*)k_g2p_grad_gather<DIM>, 0, kTG);
     });
     done = true;
     return cudaGetLastError();
 }
 
+#ifndef MPM_CAP_G2PG
+#define MPM_CAP_G2PG 0  // CTAs per SM of the U_bar scatter (0: occupancy limit)
+#endif
+#ifndef MPM_CAP_GATHER
+#define MPM_CAP_GATHER 0  // CTAs per SM of g2p_grad's gather part (0: occupancy limit)
+#endif
 static unsigned pgrid(const KParams& p, int kind) {
-    const int g = g_grid[kind][p.dim == 3 ? 1 : 0];
+    int g = g_grid[kind][p.dim == 3 ? 1 : 0];
+    if (kind == 2 && MPM_CAP_G2PG > 0) g = min(g, g_sms * MPM_CAP_G2PG);
+    if (kind == 4 && MPM_CAP_GATHER > 0) g = min(g, g_sms * MPM_CAP_GATHER);
     return (unsigned)(p.step_blocks < g ? p.step_blocks : g);
 }
 
@@ -1473,8 +1550,12 @@ void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const 
     DISPATCH(p.dim, k_g2p<DIM><<<pgrid(p, 1), kTG, 0, s>>>(p, sl, S, Sn, keys, bcount, flags, refwd));
 }
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
-                     float4* ubar, float* xbp, cudaStream_t s) {
-    DISPATCH(p.dim, k_g2p_grad<DIM><<<pgrid(p, 2), kTQ, g2pg_smem_bytes<DIM>(), s>>>(p, sl, S, Sbn, ubar, xbp));
+                     float4* ubar, cudaStream_t s) {
+    DISPATCH(p.dim, k_g2p_grad<DIM><<<pgrid(p, 2), kTQ, g2pg_smem_bytes<DIM>(), s>>>(p, sl, S, Sbn, ubar));
+}
+void launch_g2p_grad_gather(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
+                            float* xbp, cudaStream_t s) {
+    DISPATCH(p.dim, k_g2p_grad_gather<DIM><<<pgrid(p, 4), kTG, 0, s>>>(p, sl, S, Sbn, xbp));
 }
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
                      const float* alpha_t, const AdjView& Sbn, const float* xbp,
