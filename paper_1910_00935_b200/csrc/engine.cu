@@ -56,6 +56,8 @@ struct mpm_ctx {
     cudaStream_t stream = 0;
     cudaStream_t side = nullptr;             // second stream (g2p_grad gather || U_bar scatter)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t side2 = nullptr;            // third stream: segment re-forward ahead of the reverse
+    cudaEvent_t ev_seg = nullptr, ev_refwd = nullptr;
     float* xbar_part = nullptr;    // [d][EN] xb_t partial from g2p_grad's gather part
     int device = 0;
     std::string err;
@@ -67,7 +69,8 @@ struct mpm_ctx {
     int n_ckpt = 0;
     int max_active = 0;
     std::vector<StateView> ckpt;   // S_{s k}
-    std::vector<StateView> window; // S_{s k + j}, j = 1..k-1
+    std::vector<StateView> window; // [2][k]: S_{s k + j}, j = 1..k-1, in half (s & 1) (double-buffered so
+                                   // the re-forward of segment s-1 overlaps the reverse of segment s)
     StateView final_state{};       // S_T
     // grid store (all steps): sorted lists, block maps, and a pool of block lists /
     // cell starts / node tiles addressed by a per-step device-side base
@@ -240,7 +243,7 @@ size_t carve(mpm_ctx* h, char* base) {
     };
     std::vector<StateView> ckpt, window;
     for (int i = 0; i < n_ckpt; ++i) ckpt.push_back(state());
-    for (int i = 0; i < kk; ++i) window.push_back(i == 0 ? StateView{nullptr, nullptr, nullptr, nullptr} : state());
+    for (int i = 0; i < 2 * kk; ++i) window.push_back(i % kk == 0 ? StateView{nullptr, nullptr, nullptr, nullptr} : state());
     StateView fin = state();
     const int Tm = p.max_steps;
     int* sigma_store = (int*)take(sizeof(int) * EN * Tm);
@@ -304,7 +307,7 @@ StateView state_at(mpm_ctx* h, int t) {
     const int k = h->prm.k_ckpt;
     if (t > 0 && t == h->t_final) return h->final_state;
     if (t % k == 0) return h->ckpt[t / k];
-    return h->window[t % k];
+    return h->window[((t / k) & 1) * k + t % k];
 }
 
 SlotView slot_at(mpm_ctx* h, int t) {
@@ -424,9 +427,9 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
 
 // re-forward of step t inside a segment: the grid of step t is in the grid
 // store, so only g2p runs (plus F_{t+1} = (I + dt C) F and the particle ids)
-void step_reforward(mpm_ctx* h, const KParams& k, int t) {
+void step_reforward(mpm_ctx* h, const KParams& k, int t, cudaStream_t st) {
     KScope sc(h, KC_G2P);
-    launch_g2p(k, slot_at(h, t), state_at(h, t), state_at(h, t + 1), nullptr, h->bcount, h->flags, true, h->stream);
+    launch_g2p(k, slot_at(h, t), state_at(h, t), state_at(h, t + 1), nullptr, h->bcount, h->flags, true, st);
 }
 
 // advance_grad() for step t, using the grid tiles stored for step t
@@ -563,6 +566,9 @@ mpm_status mpm_destroy(mpm_handle h) {
     if (h->side) cudaStreamDestroy(h->side);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
+    if (h->side2) cudaStreamDestroy(h->side2);
+    if (h->ev_seg) cudaEventDestroy(h->ev_seg);
+    if (h->ev_refwd) cudaEventDestroy(h->ev_refwd);
     delete h;
     return MPM_OK;
 }
@@ -605,6 +611,9 @@ mpm_status mpm_set_stream(mpm_handle h, void* s) {
         CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+        CU(cudaStreamCreateWithFlags(&h->side2, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&h->ev_seg, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&h->ev_refwd, cudaEventDisableTiming));
     }
     return MPM_OK;
 }
@@ -752,11 +761,30 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     mpm_status gs = run_graphed(h, std::make_tuple(1, T, (int)h->has_aid, h->window_seg * 2 + h->sbar_cur), [&]() {
         if (k.n_act > 0) cudaMemsetAsync(h->alpha_bar, 0, sizeof(float) * (size_t)T * A, h->stream);
         const int nseg = (T + kk - 1) / kk;
+        // Segment-wise recomputation of the states.  With the side streams the
+        // re-forward of segment s-1 (into window half (s-1) & 1) is enqueued on side2 as
+        // soon as the reverse of segment s+1 (the last reader of that half) is done, so it
+        // runs concurrently with the reverse of segment s; main waits for it before s-1.
+        const bool ahead = !h->prof.on && h->side2 != nullptr;
+        const int fwd_seg = h->window_seg;  // the forward left this segment in its window half
+        int prefetched = -1;
+        auto refwd = [&](int s, cudaStream_t st) {
+            const int t0 = s * kk, t1 = (t0 + kk < T) ? t0 + kk : T;
+            for (int t = t0; t < t1 - 1; ++t) step_reforward(h, k, t, st);
+        };
         for (int s = nseg - 1; s >= 0; --s) {
             const int t0 = s * kk, t1 = (t0 + kk < T) ? t0 + kk : T;
-            if (h->window_seg != s) {  // segment-wise recomputation of the states
-                for (int t = t0; t < t1 - 1; ++t) step_reforward(h, k, t);
-                h->window_seg = s;
+            if (s != fwd_seg) {
+                if (prefetched == s) cudaStreamWaitEvent(h->stream, h->ev_refwd, 0);
+                else refwd(s, h->stream);
+            }
+            h->window_seg = s;
+            if (ahead && s >= 1 && s - 1 != fwd_seg && kk > 1) {
+                cudaEventRecord(h->ev_seg, h->stream);
+                cudaStreamWaitEvent(h->side2, h->ev_seg, 0);
+                refwd(s - 1, h->side2);
+                cudaEventRecord(h->ev_refwd, h->side2);
+                prefetched = s - 1;
             }
             for (int t = t1 - 1; t >= t0; --t) {
                 step_backward(h, k, t, h->sbar[h->sbar_cur], h->sbar[h->sbar_cur ^ 1]);
