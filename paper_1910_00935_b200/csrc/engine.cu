@@ -411,6 +411,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     const StateView S = state_at(h, t);
     const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr, nullptr, nullptr};
     const int32_t* aid = h->has_aid ? h->aid : nullptr;
+    { KScope sc(h, KC_BIN); launch_canon(k, sl, Sn.pid, h->flags, h->stream); }
     { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
     { KScope sc(h, KC_GRID_OP); launch_grid_op(k, sl, h->stream); }
     if (!write_next) return;

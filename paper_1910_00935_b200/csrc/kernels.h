@@ -52,6 +52,10 @@ void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView&
 void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
                         cudaStream_t s);
 
+// canonical (cell, particle id) order of every active block's list; cell starts; the
+// particle ids of S_{t+1} (pid_next, nullable) in that order.  Runs before each p2g.
+void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* flags, cudaStream_t s);
+
 // ---- one forward step (advance())
 // p2g writes F_{t+1} and particle ids of S_{t+1} when Sn.rec / Sn.pid are non-null
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,

@@ -467,11 +467,11 @@ template <int D> struct RowL {  // particle row in shared memory (floats); strid
     static constexpr int STRIDE = D == 3 ? 28 : 12;
 };
 template <int D> constexpr int p2g_union_bytes() {
-    constexpr int a = Geo<D>::MAXP * 15, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
+    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 template <int D> constexpr int p2g_smem_bytes() {
-    return p2g_union_bytes<D>() + Geo<D>::MAXP * 4 + 2 * (Geo<D>::CELLS + 2) * 4;
+    return p2g_union_bytes<D>() + Geo<D>::MAXP * 4 + (Geo<D>::CELLS + 2) * 4;
 }
 
 // Thread (cell, o_x): sums over the cell's rows W_o (c + A o) (and W_o) for the
@@ -580,57 +580,48 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
     return ok;
 }
 
-// ---------------------------------------------------------------- P2G
-// p2g (P:578): canonicalise the block list, then per particle
-// Ft = (I + dt C) F; tau = tau(Ft) [+ actuation]; A = -dt V 4/dx^2 tau + m C;
-// node b+o receives W_o (m v + A (o - f) dx) and W_o m.  F_{t+1} = Ft.
-// CTA = 192 threads: phase 1 thread per particle (rows in smem), phase 2 thread per (cell, o_x).
-template <int D>
-__global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
-                                               const int32_t* __restrict__ aid,
-                                               const float* __restrict__ alpha, int* flags) {
-    using G = Geo<D>;
-    using L = Lay<D>;
-    constexpr int RS = RowL<D>::STRIDE;
+// ------------------------------------------------------------ canonical order
+// Per active block: put the scattered list in canonical (cell, particle id) order, so every
+// sum downstream has a fixed order (bitwise reproducible, independent of the scatter's
+// atomics).  Bucket by cell (warp-aggregated smem counters), then rank by particle id
+// inside the cell.  Writes sigma (canonical), the cell starts and -- when the step writes
+// S_{t+1} -- the particle ids of S_{t+1} (p2g's output order).  Its own high-occupancy
+// pass (256 threads, 26 KB smem) ahead of p2g.
+constexpr int canon_smem_bytes() { return 1728 * 15 + 2 * 66 * 4; }
+__global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __restrict__ pid_next, int* flags) {
+    constexpr int MAXP = 1728, CELLS = 64;
+    using G = Geo<3>;  // CELLS = 64 in 2D and 3D
     extern __shared__ __align__(16) unsigned char smem[];
-    int* s_idx = reinterpret_cast<int*>(smem);                       // phase 0 ...
-    int* s_pid = s_idx + G::MAXP;
-    int* s_bpid = s_pid + G::MAXP;                                   // pid in bucketed order
-    short* s_tmp = reinterpret_cast<short*>(s_bpid + G::MAXP);
-    unsigned char* s_cell = reinterpret_cast<unsigned char*>(s_tmp + G::MAXP);
-    float* s_row = reinterpret_cast<float*>(smem);                   // ... phase 1/2 rows ...
-    float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... node partials
-    int* s_ci = reinterpret_cast<int*>(smem + p2g_union_bytes<D>());  // canonical state index
-    int* s_cnt = s_ci + G::MAXP;
-    int* s_cst = s_cnt + G::CELLS + 2;
+    int* s_idx = reinterpret_cast<int*>(smem);
+    int* s_pid = s_idx + MAXP;
+    int* s_bpid = s_pid + MAXP;
+    int* s_cnt = s_bpid + MAXP;
+    int* s_cst = s_cnt + CELLS + 2;
+    short* s_tmp = reinterpret_cast<short*>(s_cst + CELLS + 2);
+    unsigned char* s_cell = reinterpret_cast<unsigned char*>(s_tmp + MAXP);
     const int tid = threadIdx.x, lane = tid & 31;
-    const int my_cell = tid / 3, my_ox = tid - 3 * (tid / 3);
     const int nact = *sl.nactive;
-    const int b0 = *sl.base;  // this step's offset in the grid-store pool
-    const int* blist = sl.blist + b0;
+    const int b0 = *sl.base;
     const int* bstart = sl.bstart + b0 + sl.step;
-    unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
-    float4* tiles_l = sl.part;  // partial tiles of this step (local block index)
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (CELLS + 1);
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
-        const int bid = blist[bi];
         const int start = bstart[bi], n = bstart[bi + 1] - start;
-        int e, c0[3];
-        block_origin<D>(p, bid, e, c0);
-        if (n > G::MAXP) {
+        if (n > MAXP) {  // reported; the block is dropped (no valid entries downstream)
             if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
+            for (int c = tid; c <= CELLS; c += kT) cstart[(int64_t)bi * (CELLS + 1) + c] = 0;
             continue;
         }
         // ---- phase 0: canonical (cell, particle id) order of the block's list.  The
         // scatter wrote each entry's cell and particle id next to it: coalesced loads only.
-        for (int q = tid; q < G::CELLS + 2; q += kTQ) s_cnt[q] = 0;
+        for (int q = tid; q < G::CELLS + 2; q += kT) s_cnt[q] = 0;
 #pragma unroll 4
-        for (int q = tid; q < n; q += kTQ) {
+        for (int q = tid; q < n; q += kT) {
             s_idx[q] = sl.sigma[start + q];
             s_pid[q] = sl.spid[start + q];
             s_cell[q] = sl.scell[start + q];
         }
         __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kTQ) {
+        for (int q0 = 0; q0 < n; q0 += kT) {
             const int q = q0 + tid;
             const bool in = q < n;
             const int cell = in ? (int)s_cell[q] : -1;
@@ -654,7 +645,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
             if (lane == 0) s_cst[G::CELLS + 1] = carry;
         }
         __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kTQ) {  // bucket by cell (order inside a cell arbitrary)
+        for (int q0 = 0; q0 < n; q0 += kT) {  // bucket by cell (order inside a cell arbitrary)
             const int q = q0 + tid;
             const bool in = q < n;
             const int cell = in ? (int)s_cell[q] : -1;
@@ -670,19 +661,60 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
             }
         }
         __syncthreads();
-        for (int r = tid; r < n; r += kTQ) {  // rank by particle id inside the cell
+        for (int r = tid; r < n; r += kT) {  // rank by particle id inside the cell
             const int q = s_tmp[r];
             const int cell = s_cell[q], pq = s_bpid[r];
             int rank = 0;
             const int m1 = s_cst[cell + 1];
             for (int m = s_cst[cell]; m < m1; ++m) rank += s_bpid[m] < pq;
             const int fl = s_cst[cell] + rank;
-            s_ci[fl] = s_idx[q];
             sl.sigma[start + fl] = s_idx[q];
-            if (Sn.pid) Sn.pid[start + fl] = pq;
+            if (pid_next) pid_next[start + fl] = pq;
         }
-        for (int c = tid; c <= G::CELLS; c += kTQ) cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
+        for (int c = tid; c <= G::CELLS; c += kT) cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
         if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
+        __syncthreads();
+    }
+    (void)p;
+}
+
+// ---------------------------------------------------------------- P2G
+// p2g (P:578): canonicalise the block list, then per particle
+// Ft = (I + dt C) F; tau = tau(Ft) [+ actuation]; A = -dt V 4/dx^2 tau + m C;
+// node b+o receives W_o (m v + A (o - f) dx) and W_o m.  F_{t+1} = Ft.
+// CTA = 192 threads: phase 1 thread per particle (rows in smem), phase 2 thread per (cell, o_x).
+template <int D>
+__global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
+                                               const int32_t* __restrict__ aid,
+                                               const float* __restrict__ alpha, int* flags) {
+    using G = Geo<D>;
+    using L = Lay<D>;
+    constexpr int RS = RowL<D>::STRIDE;
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* s_row = reinterpret_cast<float*>(smem);                   // phase 1/2 rows ...
+    float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... node partials
+    int* s_ci = reinterpret_cast<int*>(smem + p2g_union_bytes<D>());  // canonical state index
+    int* s_cst = s_ci + G::MAXP;  // [CELLS + 1] cell starts
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int my_cell = tid / 3, my_ox = tid - 3 * (tid / 3);
+    const int nact = *sl.nactive;
+    const int b0 = *sl.base;  // this step's offset in the grid-store pool
+    const int* blist = sl.blist + b0;
+    const int* bstart = sl.bstart + b0 + sl.step;
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
+    float4* tiles_l = sl.part;  // partial tiles of this step (local block index)
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
+        const int bid = blist[bi];
+        const int start = bstart[bi], n = bstart[bi + 1] - start;
+        int e, c0[3];
+        block_origin<D>(p, bid, e, c0);
+        if (n > G::MAXP) {
+            if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
+            continue;
+        }
+        // ---- the block's list in canonical (cell, particle id) order (k_canon)
+        for (int q = tid; q < n; q += kTQ) s_ci[q] = sl.sigma[start + q];
+        for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
         __syncthreads();
         const int nvalid = s_cst[G::CELLS];
         // ---- phases 1 + 2 over chunks of kTQ particles in canonical order; the particle
@@ -1440,6 +1472,7 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + kT - 1) / kT); }
 
 int g_grid[5][2];  // persistent grid size per kernel kind and dimension (set by tile_init)
 int g_sms = 148;
+int g_canon_grid = 148 * 8;
 
 }  // namespace
 
@@ -1469,6 +1502,9 @@ cudaError_t tile_init() {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     }
+    e = cudaFuncSetAttribute(k_canon, cudaFuncAttributeMaxDynamicSharedMemorySize, canon_smem_bytes());
+    if (e) return e;
+    g_canon_grid = occupancy_grid((const void*)k_canon, canon_smem_bytes(), kT);
     DISPATCH(2, {
         e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>());
         if (e) return e;
@@ -1529,6 +1565,10 @@ void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView&
 void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
                         cudaStream_t s) {
     k_bin_scatter<<<(unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s>>>(p, keys, pid, cursor, sl);
+}
+void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* flags, cudaStream_t s) {
+    k_canon<<<g_canon_grid < p.step_blocks ? g_canon_grid : (p.step_blocks > 0 ? p.step_blocks : 1), kT,
+              canon_smem_bytes(), s>>>(p, sl, pid_next, flags);
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
