@@ -130,7 +130,9 @@ def algorithmic_bytes(dim: int, N: int, A: float) -> dict:
         "p2g": N * (s + 4 + dd) + A * node,                      # S_t, aid -> F_{t+1}; grid flush
         "grid_op": A * 2 * node,                                  # (P, M) -> (U, z)
         "g2p": N * (d + d + d + dd) + A * node,                   # x_t -> x, v, C; read U
-        "g2p_grad": N * (d + 2 * d + dd + d) + A * 2 * node,      # x_t, (xb, vb, Cb)' -> xb; U, Ub
+        "g2p_grad": N * (d + 2 * d + dd) + A * node,              # x_t, (xb, vb, Cb)' -> U_bar tiles
+        "g2p_grad_gather": N * (d + 2 * d + dd + d) + A * node,   # x_t, (xb, vb, Cb)', U -> xb_t partial
+        "canon": N * 17,                                          # sigma, pid, cell -> sigma, pid
         "grid_op_grad": A * 4 * node,                             # P,M, U, Ub -> (Pb, Mb)
         "p2g_grad": N * (s + 4 + dd + d + s) + A * node,          # S_t, aid, Fb', xb -> S_bar_t
     }

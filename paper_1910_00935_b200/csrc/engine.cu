@@ -31,9 +31,10 @@ enum Phase { kCreated = 0, kBound, kHasState, kForward, kSeeded, kBackward };
 
 // kernel classes for the per-kernel device-time accounting (mpm_kernel_stats)
 enum KClass { KC_P2G = 0, KC_G2P, KC_BIN, KC_G2P_GRAD, KC_P2G_GRAD, KC_REDUCE_ABAR, KC_CTRL,
-              KC_LOSS, KC_LAYOUT, KC_GRID_OP, KC_GRID_OP_GRAD, KC_N };
+              KC_LOSS, KC_LAYOUT, KC_GRID_OP, KC_GRID_OP_GRAD, KC_G2P_GRAD_GATHER, KC_CANON, KC_N };
 const char* const kClassNames[KC_N] = {"p2g", "g2p", "bin", "g2p_grad", "p2g_grad", "reduce_abar",
-                                        "controller", "loss", "layout", "grid_op", "grid_op_grad"};
+                                        "controller", "loss", "layout", "grid_op", "grid_op_grad",
+                                        "g2p_grad_gather", "canon"};
 
 struct Profiler {
     bool on = false;
@@ -411,7 +412,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     const StateView S = state_at(h, t);
     const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr, nullptr, nullptr};
     const int32_t* aid = h->has_aid ? h->aid : nullptr;
-    { KScope sc(h, KC_BIN); launch_canon(k, sl, Sn.pid, h->flags, h->stream); }
+    { KScope sc(h, KC_CANON); launch_canon(k, sl, Sn.pid, h->flags, h->stream); }
     { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
     { KScope sc(h, KC_GRID_OP); launch_grid_op(k, sl, h->stream); }
     if (!write_next) return;
@@ -450,7 +451,7 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
         cudaEventRecord(h->ev_join, h->side);
         h->launches += 1;
     } else {
-        KScope sc(h, KC_G2P_GRAD);
+        KScope sc(h, KC_G2P_GRAD_GATHER);
         launch_g2p_grad_gather(k, sl, S, Sbn, h->xbar_part, h->stream);
     }
     { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, sl, S, Sbn, h->ubar, h->stream); }

@@ -460,7 +460,12 @@ constexpr int kTC = 64;  // thread-per-cell kernels: one thread per cell of a bl
 #ifndef MPM_G2P_THREADS
 #define MPM_G2P_THREADS 128
 #endif
-constexpr int kTQ = 192;  // p2g CTA: 3 threads per cell (64 cells) in the accumulation phase
+#ifndef MPM_SCATTER_THREADS
+#define MPM_SCATTER_THREADS 192
+#endif
+constexpr int kACC = 192;  // accumulation phase: 3 threads (o_x) per cell (64 cells)
+constexpr int kTQ = MPM_SCATTER_THREADS;  // p2g / g2p_grad CTA (>= kACC; the extra threads help in phases 1, 3)
+static_assert(kTQ >= kACC, "scatter CTA smaller than the accumulation phase");
 constexpr int kCH = MPM_P2G_CHUNK;  // rows per chunk: most blocks fit one chunk -> all 64 cells busy in phase 2
 
 template <int D> struct RowL {  // particle row in shared memory (floats); stride avoids STS.128 conflicts
@@ -746,14 +751,14 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
                 if (r + kTQ < nvalid) MPM_P2G_LOAD(r + kTQ);  // this thread's next particle
             }
             __syncthreads();
-            {
+            if (tid < kACC) {
                 const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], cend);
                 for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
             }
             __syncthreads();
         }
 #undef MPM_P2G_LOAD
-        acc.store(s_cb, my_cell, my_ox);  // the rows are dead after the last barrier
+        if (tid < kACC) acc.store(s_cb, my_cell, my_ox);  // the rows are dead after the last barrier
         __syncthreads();
         // ---- phase 3: node tile (plain stores)
         float4* tile = tiles_l + (int64_t)bi * G::TN;
@@ -1149,14 +1154,14 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
                 if (r + kTQ < nvalid) MPM_G2PG_LOAD(r + kTQ);  // this thread's next particle
             }
             __syncthreads();
-            {
+            if (tid < kACC) {
                 const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], cend);
                 for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
             }
             __syncthreads();
         }
 #undef MPM_G2PG_LOAD
-        acc.store(s_cb, my_cell, my_ox);
+        if (tid < kACC) acc.store(s_cb, my_cell, my_ox);
         __syncthreads();
         float4* tile = ubar + (int64_t)bi * G::TN;
         for (int q = tid; q < G::TN; q += kTQ) tile[q] = node_gather<D>(s_cb, q);
