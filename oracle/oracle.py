@@ -50,7 +50,8 @@ class _Cfg(ct.Structure):
                 ("n_sin", ct.c_int32), ("hidden", ct.c_int32),
                 ("dt", ct.c_double), ("E", ct.c_double), ("nu", ct.c_double),
                 ("p_mass", ct.c_double), ("p_vol", ct.c_double), ("gravity", ct.c_double),
-                ("eps_mass", ct.c_double), ("kappa", ct.c_double), ("omega", ct.c_double)]
+                ("eps_mass", ct.c_double), ("kappa", ct.c_double), ("omega", ct.c_double),
+                ("closed_loop", ct.c_int32), ("obs_sx", ct.c_double), ("obs_sv", ct.c_double)]
 
 
 MODELS = {"neohookean": 0, "nh": 0, "fixed_corotated": 1, "fcr": 1}
@@ -68,6 +69,8 @@ def make_cfg(p: dict) -> _Cfg:
     c.p_mass = float(p.get("p_mass", 1.0)); c.p_vol = float(p.get("p_vol", 1.0))
     c.gravity = float(p.get("gravity", 0.0)); c.eps_mass = float(p.get("eps_mass", 1e-10))
     c.kappa = float(p.get("kappa", 0.0)); c.omega = float(p.get("omega", 20.0))
+    c.closed_loop = int(bool(p.get("closed_loop", False)))
+    c.obs_sx = float(p.get("obs_sx", 10.0)); c.obs_sv = float(p.get("obs_sv", 1.0))
     return c
 
 
@@ -99,6 +102,11 @@ class Oracle:
             "oracle_n_theta": (ct.c_int64, [cfgp]),
             "oracle_controller": (None, [cfgp, P, ct.c_int32, P]),
             "oracle_controller_adj": (None, [cfgp, P, ct.c_int32, P, P]),
+            "oracle_n_obs": (ct.c_int, [cfgp]),
+            "oracle_controller_obs": (None, [cfgp, P, ct.c_int32, P, P]),
+            "oracle_controller_obs_adj": (None, [cfgp, P, ct.c_int32, P, P, P, P]),
+            "oracle_observe": (None, [cfgp, ct.c_int64, P, P, P, P]),
+            "oracle_observe_adj": (None, [cfgp, ct.c_int64, P, P, P, P]),
             "oracle_p2g": (ct.c_int, [cfgp, ct.c_int64, P, P, P, P, P, P, P, P]),
             "oracle_grid_op": (None, [cfgp, P, P]),
             "oracle_g2p": (ct.c_int, [cfgp, ct.c_int64, P, P, P, P, P]),
@@ -180,6 +188,35 @@ class Oracle:
         self.lib.oracle_controller_adj(ct.byref(self.cfg), self._p(th), int(t), self._p(ab),
                                        self._p(thb))
         return thb
+
+    def n_obs(self):
+        return int(self.lib.oracle_n_obs(ct.byref(self.cfg)))
+
+    def controller_obs(self, theta, t, obs):
+        th = self._a(theta); o = self._a(obs); a = np.zeros(self.cfg.n_act, self.dtype)
+        self.lib.oracle_controller_obs(ct.byref(self.cfg), self._p(th), int(t), self._p(o), self._p(a))
+        return a
+
+    def controller_obs_adj(self, theta, t, obs, alpha_bar):
+        th = self._a(theta); o = self._a(obs); ab = self._a(alpha_bar)
+        thb = np.zeros_like(th); ob = np.zeros(self.n_obs(), self.dtype)
+        self.lib.oracle_controller_obs_adj(ct.byref(self.cfg), self._p(th), int(t), self._p(o),
+                                           self._p(ab), self._p(thb), self._p(ob))
+        return thb, ob
+
+    def observe(self, x, v, aid):
+        x = self._a(x); v = self._a(v); N = x.size // self.d
+        o = np.zeros(max(self.n_obs(), 1), self.dtype)
+        self.lib.oracle_observe(ct.byref(self.cfg), N, self._p(x), self._p(v), self._p(self._aid(aid, N)),
+                                self._p(o))
+        return o[:self.n_obs()]
+
+    def observe_adj(self, N, aid, obs_bar):
+        ob = self._a(obs_bar)
+        xb = np.zeros((N, self.d), self.dtype); vb = np.zeros((N, self.d), self.dtype)
+        self.lib.oracle_observe_adj(ct.byref(self.cfg), N, self._p(self._aid(aid, N)), self._p(ob),
+                                    self._p(xb), self._p(vb))
+        return xb, vb
 
     def _state(self, x, v, C, F):
         d = self.d

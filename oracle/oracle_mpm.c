@@ -277,29 +277,36 @@ int oracle_stress_adj(const oracle_cfg* c, const real* F, const real* tb, real* 
 
 /* ------------------------------------------------------------ controller */
 
-/* R9: open-loop controller on sinusoid features
-   phi_j(t) = sin(omega t dt + 2 pi j / n_sin);
-   H > 0: alpha = tanh(W2 tanh(W1 phi + b1) + b2); H = 0: alpha = tanh(W phi + b).
-   theta = [W1 (H x n_sin), b1 (H), W2 (n_act x H), b2 (n_act)] (or [W, b]). */
+/* R9: controller on sinusoid features phi_j(t) = sin(omega t dt + 2 pi j / n_sin), plus,
+   closed loop (R22), the observation o_t of S_t:  input u = [phi(t), o_t] (n_in values);
+   H > 0: alpha = tanh(W2 tanh(W1 u + b1) + b2); H = 0: alpha = tanh(W u + b).
+   theta = [W1 (H x n_in), b1 (H), W2 (n_act x H), b2 (n_act)] (or [W (n_act x n_in), b]). */
+int oracle_n_obs(const oracle_cfg* c) { return c->closed_loop ? 2 * c->dim * c->n_act : 0; }
+
+static int n_in(const oracle_cfg* c) { return c->n_sin + oracle_n_obs(c); }
+
 int64_t oracle_n_theta(const oracle_cfg* c) {
-    int64_t H = c->hidden, S = c->n_sin, A = c->n_act;
+    int64_t H = c->hidden, S = n_in(c), A = c->n_act;
     return H > 0 ? H * S + H + A * H + A : A * S + A;
 }
 
-static void features(const oracle_cfg* c, int32_t t, real* phi) {
+/* u = [phi(t), o_t]; o = NULL -> zeros */
+static void inputs(const oracle_cfg* c, int32_t t, const real* obs, real* u) {
     for (int j = 0; j < c->n_sin; ++j)
-        phi[j] = sin((real)(c->omega * t * c->dt) + (real)(2.0 * M_PI * j / c->n_sin));
+        u[j] = sin((real)(c->omega * t * c->dt) + (real)(2.0 * M_PI * j / c->n_sin));
+    for (int j = 0; j < oracle_n_obs(c); ++j) u[c->n_sin + j] = obs ? obs[j] : 0;
 }
 
-void oracle_controller(const oracle_cfg* c, const real* theta, int32_t t, real* alpha) {
-    const int S = c->n_sin, H = c->hidden, A = c->n_act;
-    real phi[64], h[1024];
-    features(c, t, phi);
+void oracle_controller_obs(const oracle_cfg* c, const real* theta, int32_t t, const real* obs,
+                           real* alpha) {
+    const int S = n_in(c), H = c->hidden, A = c->n_act;
+    real u[1024], h[1024];
+    inputs(c, t, obs, u);
     if (H > 0) {
         const real *W1 = theta, *b1 = W1 + H * S, *W2 = b1 + H, *b2 = W2 + A * H;
         for (int i = 0; i < H; ++i) {
             real z = b1[i];
-            for (int j = 0; j < S; ++j) z += W1[i * S + j] * phi[j];
+            for (int j = 0; j < S; ++j) z += W1[i * S + j] * u[j];
             h[i] = tanh(z);
         }
         for (int a = 0; a < A; ++a) {
@@ -311,25 +318,31 @@ void oracle_controller(const oracle_cfg* c, const real* theta, int32_t t, real* 
         const real *W = theta, *b = W + A * S;
         for (int a = 0; a < A; ++a) {
             real z = b[a];
-            for (int j = 0; j < S; ++j) z += W[a * S + j] * phi[j];
+            for (int j = 0; j < S; ++j) z += W[a * S + j] * u[j];
             alpha[a] = tanh(z);
         }
     }
 }
 
-/* SURVEY.md A.3 "Controller": theta_bar += (d alpha_t / d theta)^T alpha_bar_t */
-void oracle_controller_adj(const oracle_cfg* c, const real* theta, int32_t t,
-                           const real* ab, real* thb) {
-    const int S = c->n_sin, H = c->hidden, A = c->n_act;
-    real phi[64], h[1024], alpha[256], z2b[256], hb[1024];
-    features(c, t, phi);
-    oracle_controller(c, theta, t, alpha);
+void oracle_controller(const oracle_cfg* c, const real* theta, int32_t t, real* alpha) {
+    oracle_controller_obs(c, theta, t, NULL, alpha);
+}
+
+/* SURVEY.md A.3 "Controller": theta_bar += (d alpha_t / d theta)^T alpha_bar_t;
+   closed loop: obs_bar = (d alpha_t / d o_t)^T alpha_bar_t */
+void oracle_controller_obs_adj(const oracle_cfg* c, const real* theta, int32_t t, const real* obs,
+                               const real* ab, real* thb, real* obs_bar) {
+    const int S = n_in(c), H = c->hidden, A = c->n_act, ns = c->n_sin;
+    real u[1024], h[1024], alpha[256], z2b[256], hb[1024], ub[1024];
+    inputs(c, t, obs, u);
+    oracle_controller_obs(c, theta, t, obs, alpha);
+    for (int j = 0; j < S; ++j) ub[j] = 0;
     if (H > 0) {
         const real *W1 = theta, *b1 = W1 + H * S, *W2 = b1 + H;
         real *W1b = thb, *b1b = W1b + H * S, *W2b = b1b + H, *b2b = W2b + A * H;
         for (int i = 0; i < H; ++i) {
             real z = b1[i];
-            for (int j = 0; j < S; ++j) z += W1[i * S + j] * phi[j];
+            for (int j = 0; j < S; ++j) z += W1[i * S + j] * u[j];
             h[i] = tanh(z);
         }
         for (int a = 0; a < A; ++a) {
@@ -342,14 +355,66 @@ void oracle_controller_adj(const oracle_cfg* c, const real* theta, int32_t t,
             for (int a = 0; a < A; ++a) s += W2[a * H + i] * z2b[a];
             hb[i] = s * (1 - h[i] * h[i]);
             b1b[i] += hb[i];
-            for (int j = 0; j < S; ++j) W1b[i * S + j] += hb[i] * phi[j];
+            for (int j = 0; j < S; ++j) W1b[i * S + j] += hb[i] * u[j];
+            for (int j = 0; j < S; ++j) ub[j] += W1[i * S + j] * hb[i];
         }
     } else {
+        const real* W = theta;
         real *Wb = thb, *bb = Wb + A * S;
         for (int a = 0; a < A; ++a) {
             real zb = ab[a] * (1 - alpha[a] * alpha[a]);
             bb[a] += zb;
-            for (int j = 0; j < S; ++j) Wb[a * S + j] += zb * phi[j];
+            for (int j = 0; j < S; ++j) Wb[a * S + j] += zb * u[j];
+            for (int j = 0; j < S; ++j) ub[j] += W[a * S + j] * zb;
+        }
+    }
+    if (obs_bar)
+        for (int j = 0; j < oracle_n_obs(c); ++j) obs_bar[j] = ub[ns + j];
+}
+
+void oracle_controller_adj(const oracle_cfg* c, const real* theta, int32_t t,
+                           const real* ab, real* thb) {
+    oracle_controller_obs_adj(c, theta, t, NULL, ab, thb, NULL);
+}
+
+/* R22: o[a] = (s_x (mean_a x - mean x), s_v mean_a v), a = 0..n_act-1 (equal particle
+   masses, R4: the means are plain averages over particles) */
+void oracle_observe(const oracle_cfg* c, int64_t N, const real* x, const real* v,
+                    const int32_t* aid, real* obs) {
+    const int d = c->dim, A = c->n_act;
+    real xm[MAXD] = {0};
+    for (int64_t p = 0; p < N; ++p)
+        for (int k = 0; k < d; ++k) xm[k] += x[p * d + k];
+    for (int k = 0; k < d; ++k) xm[k] /= (real)N;
+    for (int a = 0; a < A; ++a) {
+        real sx[MAXD] = {0}, sv[MAXD] = {0};
+        int64_t n = 0;
+        for (int64_t p = 0; p < N; ++p) {
+            if (!aid || aid[p] != a) continue;
+            ++n;
+            for (int k = 0; k < d; ++k) { sx[k] += x[p * d + k]; sv[k] += v[p * d + k]; }
+        }
+        for (int k = 0; k < d; ++k) {
+            obs[a * 2 * d + k] = n ? (real)c->obs_sx * (sx[k] / (real)n - xm[k]) : 0;
+            obs[a * 2 * d + d + k] = n ? (real)c->obs_sv * (sv[k] / (real)n) : 0;
+        }
+    }
+}
+
+void oracle_observe_adj(const oracle_cfg* c, int64_t N, const int32_t* aid, const real* ob,
+                        real* xb, real* vb) {
+    const int d = c->dim, A = c->n_act;
+    for (int a = 0; a < A; ++a) {
+        int64_t n = 0;
+        for (int64_t p = 0; p < N; ++p) n += (aid && aid[p] == a);
+        if (!n) continue;  /* o[a] = 0 for an empty group: no gradient */
+        for (int64_t p = 0; p < N; ++p) {
+            for (int k = 0; k < d; ++k) xb[p * d + k] -= (real)c->obs_sx * ob[a * 2 * d + k] / (real)N;
+            if (aid[p] != a) continue;
+            for (int k = 0; k < d; ++k) {
+                xb[p * d + k] += (real)c->obs_sx * ob[a * 2 * d + k] / (real)n;
+                vb[p * d + k] += (real)c->obs_sv * ob[a * 2 * d + d + k] / (real)n;
+            }
         }
     }
 }
@@ -760,7 +825,12 @@ int oracle_run(const oracle_cfg* c, int64_t N, int32_t T, int32_t k, const real*
     int st = ORACLE_OK;
     real* alpha = (real*)calloc((size_t)(T > 0 ? T : 1) * A, sizeof(real));
     real* alpha_bar = (real*)calloc((size_t)(T > 0 ? T : 1) * A, sizeof(real));
-    if (c->n_act > 0)
+    const int closed = c->closed_loop && c->n_act > 0;
+    const int NO = oracle_n_obs(c) > 0 ? oracle_n_obs(c) : 1;
+    real* obs = (real*)calloc((size_t)(T > 0 ? T : 1) * NO, sizeof(real));
+    real* obs_bar = (real*)calloc((size_t)NO, sizeof(real));
+    real* thb = (real*)calloc((size_t)(oracle_n_theta(c) > 0 ? oracle_n_theta(c) : 1), sizeof(real));
+    if (c->n_act > 0 && !closed)
         for (int t = 0; t < T; ++t) oracle_controller(c, theta, t, alpha + (int64_t)t * A);
 
     state_t* ckpt = (state_t*)malloc(sizeof(state_t) * (nseg > 0 ? nseg : 1));
@@ -771,6 +841,10 @@ int oracle_run(const oracle_cfg* c, int64_t N, int32_t T, int32_t k, const real*
     /* forward (the tape records t and the checkpoint slot) */
     for (int t = 0; t < T && !st; ++t) {
         if (t % k == 0) state_copy(d, N, &ckpt[t / k], cur.x, cur.v, cur.C, cur.F);
+        if (closed) {  /* R22: alpha_t from the observation of S_t */
+            oracle_observe(c, N, cur.x, cur.v, aid, obs + (int64_t)t * NO);
+            oracle_controller_obs(c, theta, t, obs + (int64_t)t * NO, alpha + (int64_t)t * A);
+        }
         st = oracle_step(c, N, cur.x, cur.v, cur.C, cur.F, aid, alpha + (int64_t)t * A, nxt.x,
                          nxt.v, nxt.C, nxt.F);
         if (!st && !state_finite(d, N, &nxt)) st = ORACLE_NONFINITE;
@@ -810,6 +884,11 @@ int oracle_run(const oracle_cfg* c, int64_t N, int32_t T, int32_t k, const real*
                                  bar.v, bar.C, bar.F, barn.x, barn.v, barn.C, barn.F,
                                  alpha_bar + (int64_t)t * A);
             state_t tmp = bar; bar = barn; barn = tmp;
+            if (closed && !st) {  /* controller and observation adjoints into S_bar_t */
+                oracle_controller_obs_adj(c, theta, t, obs + (int64_t)t * NO, alpha_bar + (int64_t)t * A,
+                                          thb, obs_bar);
+                oracle_observe_adj(c, N, aid, obs_bar, bar.x, bar.v);
+            }
         }
     }
     if (!st) {
@@ -817,7 +896,8 @@ int oracle_run(const oracle_cfg* c, int64_t N, int32_t T, int32_t k, const real*
         if (dv0) memcpy(dv0, bar.v, sizeof(real) * N * d);
         if (dC0) memcpy(dC0, bar.C, sizeof(real) * N * dd);
         if (dF0) memcpy(dF0, bar.F, sizeof(real) * N * dd);
-        if (dtheta) {
+        if (dtheta && closed) memcpy(dtheta, thb, sizeof(real) * oracle_n_theta(c));
+        if (dtheta && !closed) {
             int64_t nt = oracle_n_theta(c);
             memset(dtheta, 0, sizeof(real) * nt);
             if (c->n_act > 0)
@@ -831,6 +911,6 @@ int oracle_run(const oracle_cfg* c, int64_t N, int32_t T, int32_t k, const real*
     for (int s = 0; s < nseg; ++s) state_free(&ckpt[s]);
     free(ckpt);
     state_free(&cur); state_free(&nxt); state_free(&bar); state_free(&barn);
-    free(alpha); free(alpha_bar);
+    free(alpha); free(alpha_bar); free(obs); free(obs_bar); free(thb);
     return st;
 }

@@ -53,6 +53,8 @@ typedef struct {
     int32_t n_sin;     /* sinusoid time features */
     int32_t hidden;    /* H; 0 = one tanh layer */
     double dt, E, nu, p_mass, p_vol, gravity, eps_mass, kappa, omega;
+    int32_t closed_loop;  /* 1: the controller also sees the per-muscle observations (R22) */
+    double obs_sx, obs_sv;  /* observation scales s_x, s_v (R22) */
 } oracle_cfg;
 
 enum { ORACLE_OK = 0, ORACLE_OUT_OF_DOMAIN = 4, ORACLE_NONFINITE = 5, ORACLE_INVALID = 1 };
@@ -68,11 +70,25 @@ int oracle_stress_adj(const oracle_cfg* c, const real* F, const real* tau_bar, r
 /* strain energy density psi(F) (used only by tests to pin tau = dpsi/dF F^T) */
 int oracle_energy(const oracle_cfg* c, const real* F, real* psi);
 
-/* open-loop controller, all steps: alpha[T][n_act] */
+/* controller (R9; closed loop R22): alpha_t = MLP([phi(t), o_t]); o_t = NULL (or
+   closed_loop = 0) is the open-loop controller on the sinusoid features only */
 int64_t oracle_n_theta(const oracle_cfg* c);
+int oracle_n_obs(const oracle_cfg* c);
 void oracle_controller(const oracle_cfg* c, const real* theta, int32_t t, real* alpha);
 void oracle_controller_adj(const oracle_cfg* c, const real* theta, int32_t t,
                            const real* alpha_bar, real* theta_bar);
+void oracle_controller_obs(const oracle_cfg* c, const real* theta, int32_t t, const real* obs,
+                           real* alpha);
+/* theta_bar += (d alpha/d theta)^T alpha_bar; obs_bar (may be NULL) = (d alpha/d o)^T alpha_bar */
+void oracle_controller_obs_adj(const oracle_cfg* c, const real* theta, int32_t t, const real* obs,
+                               const real* alpha_bar, real* theta_bar, real* obs_bar);
+/* R22 observation of S_t: per actuator group a (particles with aid = a, n_a of them):
+   o[a][0:d] = s_x (mean_a x - mean x), o[a][d:2d] = s_v mean_a v  (0 for an empty group) */
+void oracle_observe(const oracle_cfg* c, int64_t N, const real* x, const real* v,
+                    const int32_t* aid, real* obs);
+/* its reverse: xb, vb += (d o / d (x, v))^T obs_bar */
+void oracle_observe_adj(const oracle_cfg* c, int64_t N, const int32_t* aid, const real* obs_bar,
+                        real* xb, real* vb);
 
 /* stages of one forward step (advance()) */
 int oracle_p2g(const oracle_cfg* c, int64_t N, const real* x, const real* v, const real* C,

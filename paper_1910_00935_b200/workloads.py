@@ -19,7 +19,7 @@ import numpy as np
 # shared defaults (SURVEY.md 8(d) "Small shared defaults"; R3-R9)
 _BASE = dict(E=25.0, nu=0.25, p_mass=1.0, p_vol=1.0, eps_mass=1e-10, bound=3,
              n_sin=4, omega=20.0, dt=1e-3, kappa=4.0, act_axis=1, hidden=32,
-             theta_std=0.01, k_ckpt=1)
+             theta_std=0.01, k_ckpt=1, closed_loop=False, obs_sx=10.0, obs_sv=1.0)
 
 CONFIGS: dict[str, dict] = {
     # C1a: 2D elastic block in free flight (no wall contact), COM loss, d/dv0
@@ -45,6 +45,14 @@ CONFIGS: dict[str, dict] = {
                loss="move_forward", target=[0.0, 0.0, 0.0], n_act=16,
                shape="robot3d", origin=(0.1, 0.0625, 0.359), h=1.0 / 128, seed=4000,
                episodes=64, origin_jitter=0.03),
+    # closed-loop variants of C2 / C3 -- the controller also sees, per muscle,
+    # its mean position relative to the body's centre of mass and its mean velocity (R22)
+    "c2cl": dict(_BASE, dim=2, n_grid=128, model="fixed_corotated", gravity=3.8, steps=1024,
+                 loss="move_forward", target=[0.0, 0.0, 0.0], n_act=4, closed_loop=True,
+                 shape="robot2d", origin=(0.1, 0.03), h=1.0 / 256, seed=2),
+    "c3cl": dict(_BASE, dim=3, n_grid=64, model="neohookean", gravity=10.0, steps=512, k_ckpt=32,
+                 loss="move_forward", target=[0.0, 0.0, 0.0], n_act=16, closed_loop=True,
+                 shape="robot3d", origin=(0.1, 0.0625, 0.359), h=1.0 / 128, seed=3),
     # C5: 3D cube, 102^3 = 1,061,208 particles, 128^3 grid, 2,048 steps, k = 32
     "c5": dict(_BASE, dim=3, n_grid=128, model="neohookean", gravity=10.0, steps=2048, k_ckpt=32,
                loss="com_target", target=[0.6, 0.3, 0.5], n_act=0, hidden=0,
@@ -64,6 +72,8 @@ def n_theta(p: dict) -> int:
     H, S, A = int(p.get("hidden", 0)), int(p.get("n_sin", 4)), int(p.get("n_act", 0))
     if A == 0:
         return 0
+    if p.get("closed_loop"):  # R22: + per-muscle observations (2d per actuator group)
+        S += 2 * int(p["dim"]) * A
     return H * S + H + A * H + A if H > 0 else A * S + A
 
 
