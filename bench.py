@@ -65,7 +65,8 @@ def _describe(p, n_particles, episodes, world, k):
              "robot2d": "2D robot (4 muscles)", "block2d": "2D elastic block"}[p["shape"]]
     return {"workload": f"{p['name']}: {shape}, {n_particles:,} particles x {episodes} episode(s)/GPU, "
                         f"{p['n_grid']}^{p['dim']} grid, {p['steps']} steps, checkpoint every {k}",
-            "config_index": {"c1a": 0, "c1b": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}[p["name"]],
+            "config_index": {"c1a": 0, "c1b": 0, "c2": 1, "c2cl": 1, "c3": 2, "c3cl": 2, "c4": 3, "c5": 4}[p["name"]],
+            "controller": ("closed loop (R22)" if p.get("closed_loop") else "open loop") if p.get("n_act") else "none",
             "dim": p["dim"], "particles_per_episode": n_particles, "episodes_per_gpu": episodes,
             "episodes_total": episodes * world, "n_grid": p["n_grid"], "time_steps": p["steps"],
             "k_ckpt": k, "model": p["model"], "parallelism": f"episodes x{world} (dp{world})",
@@ -412,7 +413,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c5", choices=["c1a", "c1b", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1a", "c1b", "c2", "c2cl", "c3", "c3cl", "c4", "c5"])
     ap.add_argument("--k-ckpt", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

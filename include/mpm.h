@@ -93,6 +93,13 @@ typedef struct {
     int64_t grid_store_blocks; /* capacity of the grid store that keeps every step's node tiles
                                   for the reverse pass (blocks summed over all steps);
                                   0 = automatic (about 3x a dense body).  MPM_ERR_OOM if exceeded. */
+    int32_t closed_loop;  /* 0 = open-loop controller on the sinusoid features (R9);
+                             1 = closed loop (R22): the controller input
+                             is [phi(t), o_t] with, per actuator group a of each episode,
+                             o_t[a] = (s_x (mean_a x_t - mean x_t), s_v mean_a v_t); n_theta grows
+                             accordingly and alpha_t differs per episode.  Default 0. */
+    float obs_scale_x;    /* s_x, default 10 */
+    float obs_scale_v;    /* s_v, default 1 */
 } mpm_params;
 
 /* Create a handle for n_particles per episode on an n_grid^dim grid over the

@@ -97,8 +97,12 @@ struct mpm_ctx {
     float4* ubar = nullptr;        // [max_active][TN]  U_bar partial tiles of the current step
     float4* part = nullptr;        // [max_active][TN]  p2g partial tiles / (Pb, Mb) tiles
     float* abar_part = nullptr;    // [max_active][n_act]
-    float* alpha = nullptr;        // [max_steps][n_act]
+    float* alpha = nullptr;        // [max_steps][n_act] ([max_steps][E][n_act] closed loop)
     float* alpha_bar = nullptr;
+    float* obs = nullptr;          // closed loop: [max_steps][E][2 d n_act] observations o_t
+    float* obs_cnt = nullptr;      // [E][n_act] particles per actuator group
+    float* obs_part = nullptr;     // [E][chunks][values] per-CTA observation sums
+    float* obs_inc = nullptr;      // [E][2 d n_act + d] adjoint increments of the current step
     float* theta = nullptr;
     float* theta_bar = nullptr;
     float* theta_part = nullptr;   // [max_steps][n_theta]
@@ -140,11 +144,17 @@ mpm_status fail(mpm_handle h, mpm_status st, const std::string& msg) {
             return fail(h, MPM_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
     } while (0)
 
-int64_t n_theta_of(const mpm_params& p) {
-    int64_t H = p.ctrl_hidden, S = p.n_sin, A = p.n_actuators;
+// controller inputs: n_sin sinusoid features (+ 2d per actuator group, closed loop R22)
+int64_t ctrl_inputs(const mpm_params& p, int dim) {
+    return (int64_t)p.n_sin + (p.closed_loop ? 2 * dim * (int64_t)p.n_actuators : 0);
+}
+int64_t n_theta_of(const mpm_params& p, int dim) {
+    int64_t H = p.ctrl_hidden, S = ctrl_inputs(p, dim), A = p.n_actuators;
     if (A <= 0) return 0;
     return H > 0 ? H * S + H + A * H + A : A * S + A;
 }
+
+bool closed_loop(const mpm_ctx* h) { return h->prm.closed_loop && h->prm.n_actuators > 0; }
 
 int block_edge(int dim) { return dim == 3 ? 4 : 8; }
 int tile_nodes(int dim) { return dim == 3 ? 216 : 100; }
@@ -161,6 +171,11 @@ KParams kparams(const mpm_ctx* h) {
     k.act_axis = p.act_axis;
     k.n_sin = p.n_sin;
     k.hidden = p.ctrl_hidden;
+    k.closed_loop = p.closed_loop && p.n_actuators > 0;
+    k.n_in = (int32_t)ctrl_inputs(p, h->dim);
+    k.a_estride = k.closed_loop ? p.n_actuators : 0;
+    k.obs_sx = p.obs_scale_x;
+    k.obs_sv = p.obs_scale_v;
     k.dt = h->dt;
     k.dx = 1.0f / (float)h->n_grid;
     k.inv_dx = (float)h->n_grid;
@@ -217,16 +232,19 @@ size_t carve(mpm_ctx* h, char* base) {
     const int kk = p.k_ckpt;
     const int n_ckpt = p.max_steps / kk + 1;
     const int A = p.n_actuators > 0 ? p.n_actuators : 1;
-    const int64_t nth = n_theta_of(p) > 0 ? n_theta_of(p) : 1;
+    const int64_t nth = n_theta_of(p, h->dim) > 0 ? n_theta_of(p, h->dim) : 1;
+    const bool closed = p.closed_loop && p.n_actuators > 0;
+    const size_t AE = (size_t)A * (closed ? E : 1);  // alpha_t entries: per episode when closed
+    const size_t n_obs = closed ? 2 * h->dim * A : 1;
     const int lblk = loss_blocks_per_episode(k);
     const size_t TN = tile_nodes(h->dim);
+    const size_t d = h->dim;
     size_t off = 0;
     auto take = [&](size_t bytes) -> char* {
         char* ptr = base ? base + off : nullptr;
         off += align_up(bytes);
         return ptr;
     };
-    const size_t d = h->dim;
     auto state = [&]() {
         StateView s;
         s.x = (float*)take(sizeof(float) * EN * d);
@@ -271,8 +289,14 @@ size_t carve(mpm_ctx* h, char* base) {
     float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
     float4* part = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
     float* abar_part = (float*)take(sizeof(float) * (size_t)max_active * A);  // per-step buffers
-    float* alpha = (float*)take(sizeof(float) * (size_t)p.max_steps * A);
-    float* alpha_bar = (float*)take(sizeof(float) * (size_t)p.max_steps * A);
+    float* alpha = (float*)take(sizeof(float) * (size_t)p.max_steps * AE);
+    float* alpha_bar = (float*)take(sizeof(float) * (size_t)p.max_steps * AE);
+    // closed loop (R22): observations of every step, group sizes, reduction partials, and the
+    // per-group adjoint increments of the current reverse step
+    float* obs = (float*)take(sizeof(float) * (closed ? (size_t)p.max_steps * E * n_obs : 1));
+    float* obs_cnt = (float*)take(sizeof(float) * (closed ? E * A : 1));
+    float* obs_part = (float*)take(sizeof(float) * (closed ? (size_t)obs_parts(k) * obs_values(k) : 1));
+    float* obs_inc = (float*)take(sizeof(float) * (closed ? E * (n_obs + d) : 1));
     float* theta = (float*)take(sizeof(float) * nth);
     float* theta_bar = (float*)take(sizeof(float) * nth);
     float* theta_part = (float*)take(sizeof(float) * (size_t)p.max_steps * nth);
@@ -297,6 +321,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->xbar_part = xbar_part;
         h->staging = staging; h->aid = aid; h->bcount = bcount; h->cursor = cursor; h->scan_part = scan_part; h->keys = keys;
         h->ubar = ubar; h->part = part; h->abar_part = abar_part;
+        h->obs = obs; h->obs_cnt = obs_cnt; h->obs_part = obs_part; h->obs_inc = obs_inc;
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
         h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
         h->flags = flags;
@@ -393,7 +418,8 @@ mpm_status sync_flags(mpm_handle h, const char* where) {
 }
 
 const float* alpha_at(mpm_ctx* h, int t) {
-    return h->alpha + (size_t)t * (h->prm.n_actuators > 0 ? h->prm.n_actuators : 1);
+    const size_t A = h->prm.n_actuators > 0 ? h->prm.n_actuators : 1;
+    return h->alpha + (size_t)t * A * (closed_loop(h) ? h->prm.n_episodes : 1);
 }
 
 // fresh binning of S_t into slot(t) (start of a forward or of a segment re-forward)
@@ -412,6 +438,14 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     const StateView S = state_at(h, t);
     const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr, nullptr, nullptr};
     const int32_t* aid = h->has_aid ? h->aid : nullptr;
+    if (k.closed_loop) {  // R22: alpha_t from the observation of S_t
+        KScope sc(h, KC_CTRL);
+        h->launches += 1;
+        launch_observe(k, S.x, S.vc, S.pid, h->aid, h->obs_part, h->stream);
+        const size_t no = (size_t)2 * k.dim * k.n_act;
+        launch_ctrl_obs_fwd(k, h->theta, t, h->obs_part, h->obs + (size_t)t * k.E * no, h->obs_cnt,
+                            const_cast<float*>(alpha_at(h, t)), h->stream);
+    }
     { KScope sc(h, KC_CANON); launch_canon(k, sl, Sn.pid, h->flags, h->stream); }
     { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
     { KScope sc(h, KC_GRID_OP); launch_grid_op(k, sl, h->stream); }
@@ -462,7 +496,17 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
                       Sb, h->abar_part, h->flags, h->stream); }
     if (k.n_act > 0) {
         KScope sc(h, KC_REDUCE_ABAR);
-        launch_reduce_abar(k, sl.nactive, h->abar_part, h->alpha_bar + (size_t)t * A, h->stream);
+        launch_reduce_abar(k, sl, h->abar_part, h->alpha_bar + (size_t)t * A * (k.closed_loop ? k.E : 1),
+                           h->stream);
+    }
+    if (k.closed_loop) {  // controller adjoint of step t; observation adjoint into S_bar_t
+        KScope sc(h, KC_CTRL);
+        h->launches += 1;
+        const size_t no = (size_t)2 * k.dim * k.n_act;
+        launch_ctrl_obs_bwd(k, h->theta, t, h->obs + (size_t)t * k.E * no, alpha_at(h, t),
+                            h->alpha_bar + (size_t)t * A * k.E, h->obs_cnt, h->theta_bar, h->obs_inc,
+                            h->stream);
+        launch_observe_adj(k, Sb, S.pid, h->aid, h->obs_inc, h->stream);
     }
 }
 
@@ -528,6 +572,9 @@ mpm_status mpm_default_params(int32_t dim, mpm_params* p) {
     p->deterministic = 1;
     p->loss_kind = MPM_LOSS_COM_TARGET;
     p->max_active_blocks = 0;
+    p->closed_loop = 0;
+    p->obs_scale_x = 10.0f;
+    p->obs_scale_v = 1.0f;
     return MPM_OK;
 }
 
@@ -590,7 +637,8 @@ mpm_status mpm_set_params(mpm_handle h, const mpm_params* p) {
         p->n_actuators < 0 || p->n_actuators > 32 || p->ctrl_hidden < 0 || p->ctrl_hidden > 1024 ||
         p->n_sin < 1 || p->n_sin > 64 || p->act_axis < 0 || p->act_axis >= h->dim ||
         !(p->p_mass > 0) || !(p->p_vol > 0) || p->eps_mass < 0 || p->max_active_blocks < 0 ||
-        (p->loss_kind != MPM_LOSS_COM_TARGET && p->loss_kind != MPM_LOSS_MOVE_FORWARD))
+        (p->loss_kind != MPM_LOSS_COM_TARGET && p->loss_kind != MPM_LOSS_MOVE_FORWARD) ||
+        (p->closed_loop != 0 && p->closed_loop != 1) || ctrl_inputs(*p, h->dim) > 1024)
         return fail(h, MPM_ERR_INVALID_ARG, "invalid mpm_params");
     if (p->model != MPM_MODEL_NEOHOOKEAN && p->model != MPM_MODEL_FIXED_COROTATED)
         return fail(h, MPM_ERR_INVALID_ARG, "unknown model");
@@ -638,7 +686,7 @@ mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     const KParams k = kparams(h);
     CU(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
     CU(cudaMemsetAsync(h->bcount, 0, sizeof(int) * k.TB, h->stream));
-    CU(cudaMemsetAsync(h->theta, 0, sizeof(float) * (n_theta_of(h->prm) > 0 ? n_theta_of(h->prm) : 1), h->stream));
+    CU(cudaMemsetAsync(h->theta, 0, sizeof(float) * (n_theta_of(h->prm, h->dim) > 0 ? n_theta_of(h->prm, h->dim) : 1), h->stream));
     h->phase = kBound;
     return MPM_OK;
 }
@@ -674,15 +722,15 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
 
 mpm_status mpm_n_theta(mpm_handle h, int64_t* n) {
     if (!h || !n) return MPM_ERR_INVALID_ARG;
-    *n = n_theta_of(h->prm);
+    *n = n_theta_of(h->prm, h->dim);
     return MPM_OK;
 }
 
 mpm_status mpm_set_controller(mpm_handle h, const float* theta, int64_t n) {
     if (!h) return MPM_ERR_INVALID_ARG;
     if (h->phase < kBound) return fail(h, MPM_ERR_BAD_SEQUENCE, "set_controller before bind_workspace");
-    if (n != n_theta_of(h->prm) || (n > 0 && !theta))
-        return fail(h, MPM_ERR_INVALID_ARG, "n_theta mismatch: expected " + std::to_string(n_theta_of(h->prm)));
+    if (n != n_theta_of(h->prm, h->dim) || (n > 0 && !theta))
+        return fail(h, MPM_ERR_INVALID_ARG, "n_theta mismatch: expected " + std::to_string(n_theta_of(h->prm, h->dim)));
     if (n > 0) return copy_in(h, h->theta, theta, sizeof(float) * n);
     return MPM_OK;
 }
@@ -695,7 +743,10 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
     const KParams k = kparams(h);
     h->t_final = steps;
     mpm_status gs = run_graphed(h, std::make_tuple(0, steps, (int)h->has_aid, -1), [&]() {
-        if (k.n_act > 0) { KScope sc(h, KC_CTRL); launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream); }
+        if (k.n_act > 0 && !k.closed_loop) {
+            KScope sc(h, KC_CTRL);
+            launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream);
+        }
         bin_fresh(h, k, 0);
         for (int t = 0; t < steps; ++t) step_forward(h, k, t, true, t + 1 < steps);
     });
@@ -761,7 +812,10 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     const int kk = h->prm.k_ckpt, T = steps;
     const int A = k.n_act > 0 ? k.n_act : 1;
     mpm_status gs = run_graphed(h, std::make_tuple(1, T, (int)h->has_aid, h->window_seg * 2 + h->sbar_cur), [&]() {
-        if (k.n_act > 0) cudaMemsetAsync(h->alpha_bar, 0, sizeof(float) * (size_t)T * A, h->stream);
+        if (k.n_act > 0)
+            cudaMemsetAsync(h->alpha_bar, 0, sizeof(float) * (size_t)T * A * (k.closed_loop ? k.E : 1), h->stream);
+        if (k.closed_loop)  // accumulated step by step (t descending) by ctrl_obs_bwd
+            cudaMemsetAsync(h->theta_bar, 0, sizeof(float) * n_theta_of(h->prm, h->dim), h->stream);
         const int nseg = (T + kk - 1) / kk;
         // Segment-wise recomputation of the states.  With the side streams the
         // re-forward of segment s-1 (into window half (s-1) & 1) is enqueued on side2 as
@@ -793,8 +847,8 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
                 h->sbar_cur ^= 1;
             }
         }
-        const int64_t nth = n_theta_of(h->prm);
-        if (nth > 0) {
+        const int64_t nth = n_theta_of(h->prm, h->dim);
+        if (nth > 0 && !k.closed_loop) {
             KScope sc(h, KC_CTRL);
             h->launches += 1;
             launch_ctrl_bwd(k, h->theta, T, h->alpha, h->alpha_bar, h->theta_part, h->theta_bar, nth, h->stream);
@@ -828,7 +882,7 @@ mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF
     if (dv0) CU(cudaMemcpyAsync(dv0, sv, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
     if (dC0) CU(cudaMemcpyAsync(dC0, sC, sizeof(float) * EN * d * d, cudaMemcpyDefault, h->stream));
     if (dF0) CU(cudaMemcpyAsync(dF0, sF, sizeof(float) * EN * d * d, cudaMemcpyDefault, h->stream));
-    const int64_t nth = n_theta_of(h->prm);
+    const int64_t nth = n_theta_of(h->prm, h->dim);
     if (dtheta && nth > 0)
         CU(cudaMemcpyAsync(dtheta, h->theta_bar, sizeof(float) * nth, cudaMemcpyDefault, h->stream));
     CU(cudaStreamSynchronize(h->stream));

@@ -79,11 +79,32 @@ void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* uba
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
                      const float* alpha_t, const AdjView& Sbn, const float* xbar_part,
                      const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s);
-void launch_reduce_abar(const KParams& p, const int* nactive, const float* abar_part, float* alpha_bar_t,
+// alpha_bar_t[a] (open loop) or alpha_bar_t[e][a] (closed loop) = fixed-order sum of the
+// per-block partials of the step
+void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s);
 
 // ---- measurement: distinct grid nodes with M > 0 in a slot's tiles -> *count (device)
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s);
+
+// ---- closed-loop controller (R22)
+int obs_parts(const KParams& p);   // per-CTA partials of one observation: [E][chunks]
+int obs_values(const KParams& p);  // values per partial: n_act (2d + 1) + d
+// per-CTA sums over S_t (x, v in its split arrays; particle id -> actuator id) -> part
+void launch_observe(const KParams& p, const float* x, const float* vc, const int* pid, const int32_t* aid,
+                    float* part, cudaStream_t s);
+// o_t per episode from the partials (fixed order), alpha_t[e] = MLP([phi(t), o_t[e]]);
+// stores o_t [E][2 d n_act] and the group sizes [E][n_act]
+void launch_ctrl_obs_fwd(const KParams& p, const float* theta, int32_t t, const float* part, float* obs_t,
+                         float* counts, float* alpha_t, cudaStream_t s);
+// theta_bar += sum_e (d alpha_t[e]/d theta)^T alpha_bar_t[e] (episodes in order, one CTA);
+// inc[e] = per-group adjoint increments of x_bar / v_bar from (d alpha_t/d o_t)^T alpha_bar_t
+void launch_ctrl_obs_bwd(const KParams& p, const float* theta, int32_t t, const float* obs_t,
+                         const float* alpha_t, const float* alpha_bar_t, const float* counts,
+                         float* theta_bar, float* inc, cudaStream_t s);
+// S_bar_t.x, .v += the observation adjoint (particle i of episode i / N, group aid[pid[i]])
+void launch_observe_adj(const KParams& p, const AdjView& Sb, const int* pid, const int32_t* aid,
+                        const float* inc, cudaStream_t s);
 
 // ---- controller (compute_actuation, P:577 / .grad P:591)
 void launch_ctrl_fwd(const KParams& p, const float* theta, int32_t T, float* alpha, cudaStream_t s);

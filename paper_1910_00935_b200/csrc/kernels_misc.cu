@@ -94,6 +94,214 @@ __global__ void k_ctrl_reduce(const float* __restrict__ part, int T, int64_t n_t
     thb[q] = s;
 }
 
+// ---------------------------------------------------- closed-loop controller
+// SURVEY 8(f) f1, R22.  o_t[e][a] = (s_x (mean_a x - mean x), s_v mean_a v) over the
+// particles of episode e with actuator id a; input u = [phi(t), o_t[e]]; alpha_t[e] = MLP(u).
+constexpr int kObsThreads = 256;
+constexpr int kMaxIn = 1024;
+
+__host__ __device__ inline int obs_nvals(int n_act, int dim) { return n_act * (2 * dim + 1) + dim; }
+
+// CTA (c, e): particles [c * 256, (c + 1) * 256) of episode e (S_t keeps each episode's
+// particles in one contiguous index range).  Per group a: sums of x, v and the count; plus
+// the sum of x over all particles.  Masked warp butterflies + warp order: fixed summation order.
+template <int D>
+__global__ void __launch_bounds__(kObsThreads) k_observe(KParams p, const float* __restrict__ X,
+                                                         const float* __restrict__ VC,
+                                                         const int* __restrict__ pid,
+                                                         const int32_t* __restrict__ aid,
+                                                         float* __restrict__ part) {
+    constexpr int W = kObsThreads / 32;
+    extern __shared__ float s_w[];  // [W][NV]
+    const int A = p.n_act, NV = obs_nvals(A, D);
+    const int c = blockIdx.x, e = blockIdx.y, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t r = (int64_t)c * kObsThreads + threadIdx.x;
+    const bool in = r < p.N;
+    const int64_t i = (int64_t)e * p.N + r;
+    float x[D], v[D];
+    int a_id = -1;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        x[k] = in ? X[soa(p.EN, k, i)] : 0.0f;
+        v[k] = in ? VC[soa(p.EN, k, i)] : 0.0f;
+    }
+    if (in && aid) a_id = aid[pid[i]];
+    float* w = s_w + warp * NV;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        float t = x[k];
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+        if (lane == 0) w[A * (2 * D + 1) + k] = t;
+    }
+    for (int a = 0; a < A; ++a) {
+        const bool mine = a_id == a;
+        float* wa = w + a * (2 * D + 1);
+        if (__ballot_sync(0xffffffffu, mine) == 0u) {
+            if (lane < 2 * D + 1) wa[lane] = 0.0f;
+            continue;
+        }
+        float q[2 * D + 1];
+#pragma unroll
+        for (int k = 0; k < D; ++k) { q[k] = mine ? x[k] : 0.0f; q[D + k] = mine ? v[k] : 0.0f; }
+        q[2 * D] = mine ? 1.0f : 0.0f;
+#pragma unroll
+        for (int k = 0; k < 2 * D + 1; ++k) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) q[k] += __shfl_xor_sync(0xffffffffu, q[k], off);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < 2 * D + 1; ++k) wa[k] = q[k];
+        }
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < NV; q += kObsThreads) {
+        float t = 0.0f;
+        for (int ww = 0; ww < W; ++ww) t += s_w[ww * NV + q];
+        part[((int64_t)e * gridDim.x + c) * NV + q] = t;
+    }
+}
+
+// one CTA per episode: reduce the partials (chunk order), form o_t[e], run the MLP
+template <int D>
+__global__ void k_ctrl_obs_fwd(KParams p, const float* __restrict__ th, int t, const float* __restrict__ part,
+                               int nch, float* __restrict__ obs_t, float* __restrict__ counts,
+                               float* __restrict__ alpha_t) {
+    __shared__ float tot[kMaxIn], u[kMaxIn], h[kMaxHidden];
+    const int e = blockIdx.x, A = p.n_act, NV = obs_nvals(A, D), S = p.n_in, ns = p.n_sin, H = p.hidden;
+    const int no = 2 * D * A;
+    for (int q = threadIdx.x; q < NV; q += blockDim.x) {
+        float s = 0.0f;
+        for (int c = 0; c < nch; ++c) s += part[((int64_t)e * nch + c) * NV + q];
+        tot[q] = s;
+    }
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) u[j] = feature(p, t, j);
+    __syncthreads();
+    for (int q = threadIdx.x; q < no; q += blockDim.x) {
+        const int a = q / (2 * D), k = q % (2 * D);
+        const float n = tot[a * (2 * D + 1) + 2 * D];
+        float o = 0.0f;
+        if (n > 0.0f) {
+            if (k < D) o = p.obs_sx * (tot[a * (2 * D + 1) + k] / n - tot[A * (2 * D + 1) + k] / (float)p.N);
+            else o = p.obs_sv * (tot[a * (2 * D + 1) + k] / n);
+        }
+        u[ns + q] = o;
+        obs_t[(int64_t)e * no + q] = o;
+    }
+    for (int a = threadIdx.x; a < A; a += blockDim.x) counts[e * A + a] = tot[a * (2 * D + 1) + 2 * D];
+    __syncthreads();
+    if (H > 0) {
+        const float *W1 = th, *b1 = W1 + H * S, *W2 = b1 + H, *b2 = W2 + A * H;
+        for (int i = threadIdx.x; i < H; i += blockDim.x) {
+            float z = b1[i];
+            for (int j = 0; j < S; ++j) z = fmaf(W1[i * S + j], u[j], z);
+            h[i] = tanhf(z);
+        }
+        __syncthreads();
+        for (int a = threadIdx.x; a < A; a += blockDim.x) {
+            float z = b2[a];
+            for (int i = 0; i < H; ++i) z = fmaf(W2[a * H + i], h[i], z);
+            alpha_t[e * A + a] = tanhf(z);
+        }
+    } else {
+        const float *Wm = th, *b = Wm + A * S;
+        for (int a = threadIdx.x; a < A; a += blockDim.x) {
+            float z = b[a];
+            for (int j = 0; j < S; ++j) z = fmaf(Wm[a * S + j], u[j], z);
+            alpha_t[e * A + a] = tanhf(z);
+        }
+    }
+}
+
+// one CTA, episodes in order (fixed accumulation order of theta_bar, no atomics):
+// z2b = ab (1 - alpha^2); theta_bar += outer products; u_bar = W^T (.); the observation part
+// of u_bar -> per-group increments inc[e] = [s_x ob_x[a] / n_a, s_v ob_v[a] / n_a]_a,
+// [-s_x sum_a ob_x[a] / N]  (groups with n_a = 0 observe 0 and get no gradient)
+template <int D>
+__global__ void k_ctrl_obs_bwd(KParams p, const float* __restrict__ th, int t, const float* __restrict__ obs_t,
+                               const float* __restrict__ alpha_t, const float* __restrict__ abar_t,
+                               const float* __restrict__ counts, float* __restrict__ thb,
+                               float* __restrict__ inc) {
+    __shared__ float u[kMaxIn], h[kMaxHidden], z2b[kMaxAct], hb[kMaxHidden], ub[kMaxIn];
+    const int A = p.n_act, S = p.n_in, ns = p.n_sin, H = p.hidden, no = 2 * D * A;
+    for (int e = 0; e < p.E; ++e) {
+        for (int j = threadIdx.x; j < S; j += blockDim.x)
+            u[j] = j < ns ? feature(p, t, j) : obs_t[(int64_t)e * no + (j - ns)];
+        for (int a = threadIdx.x; a < A; a += blockDim.x) {
+            const float al = alpha_t[e * A + a];
+            z2b[a] = abar_t[e * A + a] * (1.0f - al * al);
+        }
+        __syncthreads();
+        if (H > 0) {
+            const float *W1 = th, *b1 = W1 + H * S, *W2 = b1 + H;
+            float *W1b = thb, *b1b = W1b + H * S, *W2b = b1b + H, *b2b = W2b + A * H;
+            for (int i = threadIdx.x; i < H; i += blockDim.x) {
+                float z = b1[i];
+                for (int j = 0; j < S; ++j) z = fmaf(W1[i * S + j], u[j], z);
+                h[i] = tanhf(z);
+            }
+            __syncthreads();
+            for (int q = threadIdx.x; q < A * H; q += blockDim.x) W2b[q] = fmaf(z2b[q / H], h[q % H], W2b[q]);
+            for (int a = threadIdx.x; a < A; a += blockDim.x) b2b[a] += z2b[a];
+            for (int i = threadIdx.x; i < H; i += blockDim.x) {
+                float s = 0.0f;
+                for (int a = 0; a < A; ++a) s = fmaf(W2[a * H + i], z2b[a], s);
+                hb[i] = s * (1.0f - h[i] * h[i]);
+                b1b[i] += hb[i];
+            }
+            __syncthreads();
+            for (int q = threadIdx.x; q < H * S; q += blockDim.x) W1b[q] = fmaf(hb[q / S], u[q % S], W1b[q]);
+            for (int j = ns + (int)threadIdx.x; j < S; j += blockDim.x) {
+                float s = 0.0f;
+                for (int i = 0; i < H; ++i) s = fmaf(W1[i * S + j], hb[i], s);
+                ub[j] = s;
+            }
+        } else {
+            const float* Wm = th;
+            float *Wb = thb, *bb = Wb + A * S;
+            for (int q = threadIdx.x; q < A * S; q += blockDim.x) Wb[q] = fmaf(z2b[q / S], u[q % S], Wb[q]);
+            for (int a = threadIdx.x; a < A; a += blockDim.x) bb[a] += z2b[a];
+            for (int j = ns + (int)threadIdx.x; j < S; j += blockDim.x) {
+                float s = 0.0f;
+                for (int a = 0; a < A; ++a) s = fmaf(Wm[a * S + j], z2b[a], s);
+                ub[j] = s;
+            }
+        }
+        __syncthreads();
+        float* ie = inc + (int64_t)e * (no + D);
+        for (int q = threadIdx.x; q < no; q += blockDim.x) {
+            const int a = q / (2 * D), k = q % (2 * D);
+            const float n = counts[e * A + a];
+            ie[q] = n > 0.0f ? (k < D ? p.obs_sx : p.obs_sv) * ub[ns + q] / n : 0.0f;
+        }
+        for (int k = threadIdx.x; k < D; k += blockDim.x) {
+            float s = 0.0f;
+            for (int a = 0; a < A; ++a)
+                if (counts[e * A + a] > 0.0f) s += ub[ns + a * 2 * D + k];
+            ie[no + k] = -p.obs_sx * s / (float)p.N;
+        }
+        __syncthreads();
+    }
+}
+
+// x_bar_i += inc_x[a(i)] + inc_all, v_bar_i += inc_v[a(i)]  (particle i of episode i / N)
+template <int D>
+__global__ void k_observe_adj(KParams p, AdjView Sb, const int* __restrict__ pid, const int32_t* __restrict__ aid,
+                              const float* __restrict__ inc) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= p.EN) return;
+    const int e = (int)(i / p.N), no = 2 * D * p.n_act;
+    const float* ie = inc + (int64_t)e * (no + D);
+    const int a = aid ? aid[pid[i]] : -1;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const float gx = ie[no + k] + (a >= 0 ? ie[a * 2 * D + k] : 0.0f);
+        Sb.x[soa(p.EN, k, i)] += gx;
+        if (a >= 0) Sb.vc[soa(p.EN, k, i)] += ie[a * 2 * D + D + k];
+    }
+}
+
 // ---------------------------------------------------------------- loss
 constexpr int kLossThreads = 256;
 
@@ -252,6 +460,32 @@ void launch_ctrl_bwd(const KParams& p, const float* theta, int32_t T, const floa
     if (p.n_act <= 0 || T <= 0) return;
     k_ctrl_bwd<<<T, 128, 0, s>>>(p, theta, alpha, alpha_bar, theta_part, n_theta);
     k_ctrl_reduce<<<nblk(n_theta, 128), 128, 0, s>>>(theta_part, T, n_theta, theta_bar);
+}
+
+
+int obs_parts(const KParams& p) { return p.E * (int)((p.N + kObsThreads - 1) / kObsThreads); }
+int obs_values(const KParams& p) { return obs_nvals(p.n_act, p.dim); }
+
+void launch_observe(const KParams& p, const float* x, const float* vc, const int* pid, const int32_t* aid,
+                    float* part, cudaStream_t s) {
+    const int nch = (int)((p.N + kObsThreads - 1) / kObsThreads);
+    const size_t smem = sizeof(float) * (kObsThreads / 32) * obs_nvals(p.n_act, p.dim);
+    DISPATCH(p.dim, k_observe<DIM><<<dim3(nch, p.E), kObsThreads, smem, s>>>(p, x, vc, pid, aid, part));
+}
+void launch_ctrl_obs_fwd(const KParams& p, const float* theta, int32_t t, const float* part, float* obs_t,
+                         float* counts, float* alpha_t, cudaStream_t s) {
+    const int nch = (int)((p.N + kObsThreads - 1) / kObsThreads);
+    DISPATCH(p.dim, k_ctrl_obs_fwd<DIM><<<p.E, 128, 0, s>>>(p, theta, t, part, nch, obs_t, counts, alpha_t));
+}
+void launch_ctrl_obs_bwd(const KParams& p, const float* theta, int32_t t, const float* obs_t,
+                         const float* alpha_t, const float* alpha_bar_t, const float* counts,
+                         float* theta_bar, float* inc, cudaStream_t s) {
+    DISPATCH(p.dim, k_ctrl_obs_bwd<DIM><<<1, 256, 0, s>>>(p, theta, t, obs_t, alpha_t, alpha_bar_t, counts,
+                                                         theta_bar, inc));
+}
+void launch_observe_adj(const KParams& p, const AdjView& Sb, const int* pid, const int32_t* aid,
+                        const float* inc, cudaStream_t s) {
+    DISPATCH(p.dim, k_observe_adj<DIM><<<nblk(p.EN, 256), 256, 0, s>>>(p, Sb, pid, aid, inc));
 }
 
 int loss_blocks_per_episode(const KParams& p) {

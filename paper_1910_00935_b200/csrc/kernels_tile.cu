@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         for (int ch = 0; ch < nvalid; ch += kCH) {
             const int cend = min(nvalid, ch + kCH);
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
-                const float act = (aid && a_id >= 0) ? alpha[a_id] : 0.0f;
+                const float act = (aid && a_id >= 0) ? alpha[e * p.a_estride + a_id] : 0.0f;
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
                 if (!p2g_particle<D>(p, x, vc, F, act, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
                 write_row<D>(s_row + (r - ch) * RS, w, c, Adx);
@@ -1415,7 +1415,7 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
             float abar = 0.0f;
             if (in) {
                 const bool has_act = aid && a_id >= 0;
-                abar = p2g_grad_particle<D>(p, sG, x, vc, F, Fbn, xb, has_act, has_act ? alpha[a_id] : 0.0f, c0,
+                abar = p2g_grad_particle<D>(p, sG, x, vc, F, Fbn, xb, has_act, has_act ? alpha[e * p.a_estride + a_id] : 0.0f, c0,
                                             i, Sb, flags);
                 if (!has_act) a_id = -1;
             }
@@ -1442,15 +1442,17 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
 }
 
 // alpha_bar_t[a] = sum over active blocks (list order) of abar_part[b][a]
-__global__ void k_reduce_abar(const int* __restrict__ nactive, const float* __restrict__ part, int n_act,
-                              float* __restrict__ out) {
-    const int a = blockIdx.x;
-    const int n = *nactive;
+// (closed loop: per episode e = blockIdx.y, over the blocks of that episode)
+__global__ void k_reduce_abar(KParams p, SlotView sl, const float* __restrict__ part, float* __restrict__ out) {
+    const int a = blockIdx.x, e = blockIdx.y, n_act = p.n_act;
+    const int n = *sl.nactive;
+    const int* blist = sl.blist + *sl.base;
     float s = 0.0f;
-    for (int b = threadIdx.x; b < n; b += 32) s += part[(int64_t)b * n_act + a];
+    for (int b = threadIdx.x; b < n; b += 32)
+        if (!p.closed_loop || blist[b] / p.nbe == e) s += part[(int64_t)b * n_act + a];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (threadIdx.x == 0) out[a] = s;
+    if (threadIdx.x == 0) out[e * n_act + a] = s;
 }
 
 // measurement: number of distinct grid nodes with M > 0 in a step's resolved tiles.
@@ -1611,9 +1613,10 @@ void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, c
     cudaMemsetAsync(count, 0, sizeof(int64_t), s);
     DISPATCH(p.dim, k_count_active<DIM><<<node_grid(p), kT, 0, s>>>(p, sl, (unsigned long long*)count));
 }
-void launch_reduce_abar(const KParams& p, const int* nactive, const float* abar_part, float* alpha_bar_t,
+void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s) {
-    if (p.n_act > 0) k_reduce_abar<<<p.n_act, 32, 0, s>>>(nactive, abar_part, p.n_act, alpha_bar_t);
+    if (p.n_act > 0)
+        k_reduce_abar<<<dim3(p.n_act, p.closed_loop ? p.E : 1), 32, 0, s>>>(p, sl, abar_part, alpha_bar_t);
 }
 
 }  // namespace mpm

@@ -23,6 +23,10 @@ struct KParams {
     int32_t max_active;  // capacity (blocks) of the grid-store pool shared by all steps
     int32_t step_blocks; // capacity of one step's block-local buffers (U_bar tiles, partials)
     int64_t EN;          // particles, all episodes (N * E): component stride of the state arrays
+    int32_t closed_loop; // closed-loop controller (R22): alpha_t per episode from the observation
+    int32_t n_in;        // controller inputs: n_sin (+ 2 d n_act closed loop)
+    int32_t a_estride;   // episode stride of alpha_t / alpha_bar_t (n_act closed loop, else 0)
+    float obs_sx, obs_sv;  // observation scales (R22)
 };
 
 enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8 };

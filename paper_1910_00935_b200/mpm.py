@@ -43,7 +43,8 @@ class mpm_params(ct.Structure):
                 ("omega", ct.c_float), ("ctrl_hidden", ct.c_int32), ("n_episodes", ct.c_int32),
                 ("deterministic", ct.c_int32), ("loss_kind", ct.c_int32),
                 ("loss_target", ct.c_float * 3), ("max_active_blocks", ct.c_int32),
-                ("grid_store_blocks", ct.c_int64)]
+                ("grid_store_blocks", ct.c_int64), ("closed_loop", ct.c_int32),
+                ("obs_scale_x", ct.c_float), ("obs_scale_v", ct.c_float)]
 
 
 _lib = None
@@ -261,6 +262,8 @@ def sim_from_config(p: dict, n_particles: int, episodes: int | None = None,
                   n_actuators=int(p.get("n_act", 0)), act_strength=float(p.get("kappa", 0.0)),
                   act_axis=int(p.get("act_axis", 1)), n_sin=int(p.get("n_sin", 4)),
                   omega=float(p.get("omega", 20.0)), ctrl_hidden=int(p.get("hidden", 0)),
+                  closed_loop=int(bool(p.get("closed_loop", False))),
+                  obs_scale_x=float(p.get("obs_sx", 10.0)), obs_scale_v=float(p.get("obs_sv", 1.0)),
                   n_episodes=E_, deterministic=int(p.get("deterministic", 0)),
                   loss_kind={"com_target": 0, "move_forward": 1}[p.get("loss", "com_target")],
                   loss_target=list(p.get("target", [0, 0, 0])))

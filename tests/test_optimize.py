@@ -115,3 +115,13 @@ def test_c2_robot_learns_to_move_forward():
     assert all(np.isfinite(L))
     assert min(L) < L[0] - 0.05, L  # the centre of mass ends >= 0.05 further along +x
     assert L[-1] < L[0], L
+
+
+@pytest.mark.gpu
+def test_c2cl_closed_loop_robot_learns_to_move_forward():
+    """The closed-loop controller optimised end to end (f2) on C2."""
+    r = O.optimize("c2cl", iters=16, lr=0.05, method="adam", clip=1.0, log=print)
+    L = r["loss"]
+    assert all(np.isfinite(L))
+    assert min(L) < L[0] - 0.05, L
+    assert L[-1] < L[0], L
