@@ -51,6 +51,13 @@ def build(force: bool = False, verbose: bool = False, extra=(), out: str = LIB) 
         raise RuntimeError(f"nvcc failed (see {log})")
     if verbose:
         sys.stdout.write(res.stderr)
+    # every library symbol must resolve inside the library (a shared object links with
+    # undefined symbols silently; one would only fail at dlopen on the GPU box)
+    und = subprocess.run(["nm", "-uC", tmp], capture_output=True, text=True).stdout
+    bad = [l for l in und.splitlines() if "mpm::" in l]
+    if bad:
+        os.remove(tmp)
+        raise RuntimeError("undefined library symbols: " + "; ".join(bad))
     os.replace(tmp, out)
     return out
 

@@ -742,6 +742,7 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
         return fail(h, MPM_ERR_INVALID_ARG, "steps must be in [1, max_steps]");
     const KParams k = kparams(h);
     h->t_final = steps;
+    set_pdl(k.EN);
     mpm_status gs = run_graphed(h, std::make_tuple(0, steps, (int)h->has_aid, -1), [&]() {
         if (k.n_act > 0 && !k.closed_loop) {
             KScope sc(h, KC_CTRL);
@@ -811,6 +812,7 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     const KParams k = kparams(h);
     const int kk = h->prm.k_ckpt, T = steps;
     const int A = k.n_act > 0 ? k.n_act : 1;
+    set_pdl(k.EN);
     mpm_status gs = run_graphed(h, std::make_tuple(1, T, (int)h->has_aid, h->window_seg * 2 + h->sbar_cur), [&]() {
         if (k.n_act > 0)
             cudaMemsetAsync(h->alpha_bar, 0, sizeof(float) * (size_t)T * A * (k.closed_loop ? k.E : 1), h->stream);

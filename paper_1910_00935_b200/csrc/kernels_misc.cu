@@ -19,6 +19,7 @@ __device__ __forceinline__ float feature(const KParams& p, int t, int j) {
 // one block per time step: alpha_t = tanh(W2 tanh(W1 phi + b1) + b2)  (H > 0)
 //                          alpha_t = tanh(W phi + b)                  (H = 0)
 __global__ void k_ctrl_fwd(KParams p, const float* __restrict__ th, float* __restrict__ alpha) {
+    pdl_begin();
     __shared__ float phi[kMaxSin], h[kMaxHidden];
     const int t = blockIdx.x, S = p.n_sin, H = p.hidden, A = p.n_act;
     for (int j = threadIdx.x; j < S; j += blockDim.x) phi[j] = feature(p, t, j);
@@ -49,6 +50,7 @@ __global__ void k_ctrl_fwd(KParams p, const float* __restrict__ th, float* __res
 // one block per time step: the step's contribution (d alpha_t/d theta)^T alpha_bar_t
 __global__ void k_ctrl_bwd(KParams p, const float* __restrict__ th, const float* __restrict__ alpha,
                            const float* __restrict__ abar, float* __restrict__ part, int64_t n_theta) {
+    pdl_begin();
     __shared__ float phi[kMaxSin], h[kMaxHidden], z2b[kMaxAct], hb[kMaxHidden];
     const int t = blockIdx.x, S = p.n_sin, H = p.hidden, A = p.n_act;
     float* out = part + (int64_t)t * n_theta;
@@ -87,6 +89,7 @@ __global__ void k_ctrl_bwd(KParams p, const float* __restrict__ th, const float*
 // theta_bar[q] = sum over t (ascending, fixed order) of part[t][q]
 __global__ void k_ctrl_reduce(const float* __restrict__ part, int T, int64_t n_theta,
                               float* __restrict__ thb) {
+    pdl_begin();
     const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (q >= n_theta) return;
     float s = 0.0f;
@@ -111,6 +114,7 @@ __global__ void __launch_bounds__(kObsThreads) k_observe(KParams p, const float*
                                                          const int* __restrict__ pid,
                                                          const int32_t* __restrict__ aid,
                                                          float* __restrict__ part) {
+    pdl_begin();
     constexpr int W = kObsThreads / 32;
     extern __shared__ float s_w[];  // [W][NV]
     const int A = p.n_act, NV = obs_nvals(A, D);
@@ -168,6 +172,7 @@ template <int D>
 __global__ void k_ctrl_obs_fwd(KParams p, const float* __restrict__ th, int t, const float* __restrict__ part,
                                int nch, float* __restrict__ obs_t, float* __restrict__ counts,
                                float* __restrict__ alpha_t) {
+    pdl_begin();
     __shared__ float tot[kMaxIn], u[kMaxIn], h[kMaxHidden];
     const int e = blockIdx.x, A = p.n_act, NV = obs_nvals(A, D), S = p.n_in, ns = p.n_sin, H = p.hidden;
     const int no = 2 * D * A;
@@ -223,6 +228,7 @@ __global__ void k_ctrl_obs_bwd(KParams p, const float* __restrict__ th, int t, c
                                const float* __restrict__ alpha_t, const float* __restrict__ abar_t,
                                const float* __restrict__ counts, float* __restrict__ thb,
                                float* __restrict__ inc) {
+    pdl_begin();
     __shared__ float u[kMaxIn], h[kMaxHidden], z2b[kMaxAct], hb[kMaxHidden], ub[kMaxIn];
     const int A = p.n_act, S = p.n_in, ns = p.n_sin, H = p.hidden, no = 2 * D * A;
     for (int e = 0; e < p.E; ++e) {
@@ -289,6 +295,7 @@ __global__ void k_ctrl_obs_bwd(KParams p, const float* __restrict__ th, int t, c
 template <int D>
 __global__ void k_observe_adj(KParams p, AdjView Sb, const int* __restrict__ pid, const int32_t* __restrict__ aid,
                               const float* __restrict__ inc) {
+    pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= p.EN) return;
     const int e = (int)(i / p.N), no = 2 * D * p.n_act;
@@ -309,6 +316,7 @@ constexpr int kLossThreads = 256;
 // component k of particle i = base[k * EN + i] (the first d components of a state array)
 template <int D>
 __global__ void k_sum_partial(KParams p, const float* __restrict__ base, float* __restrict__ part) {
+    pdl_begin();
     __shared__ float red[D][kLossThreads];
     const int e = blockIdx.y, nb = gridDim.x;
     const int64_t chunk = (p.N + nb - 1) / nb;
@@ -336,6 +344,7 @@ __global__ void k_sum_partial(KParams p, const float* __restrict__ base, float* 
 
 template <int D>
 __global__ void k_sum_parts(const float* __restrict__ part, int nb, float* __restrict__ out) {
+    pdl_begin();
     const int e = blockIdx.x;
     if (threadIdx.x != 0) return;
 #pragma unroll
@@ -351,6 +360,7 @@ template <int D>
 __global__ void k_loss_final(KParams p, const float* __restrict__ part, int nb, int kind,
                              float3 target, float* __restrict__ loss, float* __restrict__ seed,
                              int* flags) {
+    pdl_begin();
     const int e = blockIdx.x;
     if (threadIdx.x != 0) return;
     float com[D];
@@ -383,6 +393,7 @@ __global__ void k_loss_final(KParams p, const float* __restrict__ part, int nb, 
 
 template <int D>
 __global__ void k_seed(KParams p, const float* __restrict__ seed, AdjView Sb) {
+    pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= p.N * p.E) return;
     const int64_t e = i / p.N;
@@ -400,6 +411,7 @@ __global__ void k_pack(KParams p, const float* __restrict__ x, const float* __re
                        const float* __restrict__ C, const float* __restrict__ F,
                        const int* __restrict__ src, float* __restrict__ dx, float* __restrict__ dvc,
                        float* __restrict__ df, int* __restrict__ ident_pid, bool zero_f) {
+    pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= p.N * p.E) return;
     if (ident_pid) ident_pid[i] = (int)i;
@@ -421,6 +433,7 @@ __global__ void k_unpack(KParams p, const float* __restrict__ sx, const float* _
                          const float* __restrict__ sf, const int* __restrict__ dst,
                          float* __restrict__ x, float* __restrict__ v, float* __restrict__ C,
                          float* __restrict__ F) {
+    pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= p.N * p.E) return;
     const int64_t o = dst ? (int64_t)dst[i] : i;
@@ -451,15 +464,15 @@ inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 void launch_ctrl_fwd(const KParams& p, const float* theta, int32_t T, float* alpha, cudaStream_t s) {
     if (p.n_act <= 0 || T <= 0) return;
-    k_ctrl_fwd<<<T, 128, 0, s>>>(p, theta, alpha);
+    launch_k(k_ctrl_fwd, T, 128, 0, s, p, theta, alpha);
 }
 
 void launch_ctrl_bwd(const KParams& p, const float* theta, int32_t T, const float* alpha,
                      const float* alpha_bar, float* theta_part, float* theta_bar, int64_t n_theta,
                      cudaStream_t s) {
     if (p.n_act <= 0 || T <= 0) return;
-    k_ctrl_bwd<<<T, 128, 0, s>>>(p, theta, alpha, alpha_bar, theta_part, n_theta);
-    k_ctrl_reduce<<<nblk(n_theta, 128), 128, 0, s>>>(theta_part, T, n_theta, theta_bar);
+    launch_k(k_ctrl_bwd, T, 128, 0, s, p, theta, alpha, alpha_bar, theta_part, n_theta);
+    launch_k(k_ctrl_reduce, nblk(n_theta, 128), 128, 0, s, theta_part, T, n_theta, theta_bar);
 }
 
 
@@ -470,22 +483,22 @@ void launch_observe(const KParams& p, const float* x, const float* vc, const int
                     float* part, cudaStream_t s) {
     const int nch = (int)((p.N + kObsThreads - 1) / kObsThreads);
     const size_t smem = sizeof(float) * (kObsThreads / 32) * obs_nvals(p.n_act, p.dim);
-    DISPATCH(p.dim, k_observe<DIM><<<dim3(nch, p.E), kObsThreads, smem, s>>>(p, x, vc, pid, aid, part));
+    DISPATCH(p.dim, launch_k(k_observe<DIM>, dim3(nch, p.E), kObsThreads, smem, s, p, x, vc, pid, aid, part));
 }
 void launch_ctrl_obs_fwd(const KParams& p, const float* theta, int32_t t, const float* part, float* obs_t,
                          float* counts, float* alpha_t, cudaStream_t s) {
     const int nch = (int)((p.N + kObsThreads - 1) / kObsThreads);
-    DISPATCH(p.dim, k_ctrl_obs_fwd<DIM><<<p.E, 128, 0, s>>>(p, theta, t, part, nch, obs_t, counts, alpha_t));
+    DISPATCH(p.dim, launch_k(k_ctrl_obs_fwd<DIM>, p.E, 128, 0, s, p, theta, t, part, nch, obs_t, counts, alpha_t));
 }
 void launch_ctrl_obs_bwd(const KParams& p, const float* theta, int32_t t, const float* obs_t,
                          const float* alpha_t, const float* alpha_bar_t, const float* counts,
                          float* theta_bar, float* inc, cudaStream_t s) {
-    DISPATCH(p.dim, k_ctrl_obs_bwd<DIM><<<1, 256, 0, s>>>(p, theta, t, obs_t, alpha_t, alpha_bar_t, counts,
+    DISPATCH(p.dim, launch_k(k_ctrl_obs_bwd<DIM>, 1, 256, 0, s, p, theta, t, obs_t, alpha_t, alpha_bar_t, counts,
                                                          theta_bar, inc));
 }
 void launch_observe_adj(const KParams& p, const AdjView& Sb, const int* pid, const int32_t* aid,
                         const float* inc, cudaStream_t s) {
-    DISPATCH(p.dim, k_observe_adj<DIM><<<nblk(p.EN, 256), 256, 0, s>>>(p, Sb, pid, aid, inc));
+    DISPATCH(p.dim, launch_k(k_observe_adj<DIM>, nblk(p.EN, 256), 256, 0, s, p, Sb, pid, aid, inc));
 }
 
 int loss_blocks_per_episode(const KParams& p) {
@@ -498,30 +511,30 @@ void launch_loss(const KParams& p, const float* x, int loss_kind, float3 target,
     const int nb = loss_blocks_per_episode(p);
     float* seed = com_part + (int64_t)p.E * nb * p.dim;
     DISPATCH(p.dim, {
-        k_sum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, x, com_part);
-        k_loss_final<DIM><<<p.E, 32, 0, s>>>(p, com_part, nb, loss_kind, target, loss, seed, flags);
-        k_seed<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, seed, Sb);
+        launch_k(k_sum_partial<DIM>, dim3(nb, p.E), kLossThreads, 0, s, p, x, com_part);
+        launch_k(k_loss_final<DIM>, p.E, 32, 0, s, p, com_part, nb, loss_kind, target, loss, seed, flags);
+        launch_k(k_seed<DIM>, nblk(p.N * p.E, 256), 256, 0, s, p, seed, Sb);
     });
 }
 
 void launch_v_sum(const KParams& p, const float* vc_bar, float* part, float* out, cudaStream_t s) {
     const int nb = loss_blocks_per_episode(p);
     DISPATCH(p.dim, {
-        k_sum_partial<DIM><<<dim3(nb, p.E), kLossThreads, 0, s>>>(p, vc_bar, part);
-        k_sum_parts<DIM><<<p.E, 32, 0, s>>>(part, nb, out);
+        launch_k(k_sum_partial<DIM>, dim3(nb, p.E), kLossThreads, 0, s, p, vc_bar, part);
+        launch_k(k_sum_parts<DIM>, p.E, 32, 0, s, part, nb, out);
     });
 }
 
 void launch_pack(const KParams& p, const float* x, const float* v, const float* C, const float* F,
                  const int* src, float* dx, float* dvc, float* df, int* ident_pid, bool zero_f,
                  cudaStream_t s) {
-    DISPATCH(p.dim, k_pack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, x, v, C, F, src, dx, dvc, df,
+    DISPATCH(p.dim, launch_k(k_pack<DIM>, nblk(p.N * p.E, 256), 256, 0, s, p, x, v, C, F, src, dx, dvc, df,
                                                                      ident_pid, zero_f));
 }
 
 void launch_unpack(const KParams& p, const float* sx, const float* svc, const float* sf, const int* dst,
                    float* x, float* v, float* C, float* F, cudaStream_t s) {
-    DISPATCH(p.dim, k_unpack<DIM><<<nblk(p.N * p.E, 256), 256, 0, s>>>(p, sx, svc, sf, dst, x, v, C, F));
+    DISPATCH(p.dim, launch_k(k_unpack<DIM>, nblk(p.N * p.E, 256), 256, 0, s, p, sx, svc, sf, dst, x, v, C, F));
 }
 
 }  // namespace mpm

@@ -20,6 +20,8 @@
 //    g2p_grad scatters U_bar with p2g's (cell, o_x) scheme.
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace mpm {
 
 namespace {
@@ -218,6 +220,7 @@ template <int D>
 __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restrict__ X,
                                                  int* __restrict__ keys, int* __restrict__ bcount,
                                                  int* flags) {
+    pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool in = i < p.N * p.E;
     int key = 0;
@@ -250,6 +253,7 @@ constexpr int kScanChunk = kT * kScanPer;
 template <int MODE>
 __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bcount, int* __restrict__ cursor,
                                                 SlotView sl, int2* __restrict__ part, int* flags) {
+    pdl_begin();
     __shared__ int s_wt[kW], s_wa[kW];
     __shared__ int s_base[2];
     const int TB = p.TB, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -337,6 +341,7 @@ constexpr int kScatterPer = 4;
 __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __restrict__ keys,
                                                     const int* __restrict__ pid, int* __restrict__ cursor,
                                                     SlotView sl) {
+    pdl_begin();
     const int64_t n = p.N * p.E;
     const int lane = threadIdx.x & 31;
     int64_t j[kScatterPer];
@@ -594,6 +599,7 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
 // pass (256 threads, 26 KB smem) ahead of p2g.
 constexpr int canon_smem_bytes() { return 1728 * 15 + 2 * 66 * 4; }
 __global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __restrict__ pid_next, int* flags) {
+    pdl_begin();
     constexpr int MAXP = 1728, CELLS = 64;
     using G = Geo<3>;  // CELLS = 64 in 2D and 3D
     extern __shared__ __align__(16) unsigned char smem[];
@@ -692,6 +698,7 @@ template <int D>
 __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
                                                const int32_t* __restrict__ aid,
                                                const float* __restrict__ alpha, int* flags) {
+    pdl_begin();
     using G = Geo<D>;
     using L = Lay<D>;
     constexpr int RS = RowL<D>::STRIDE;
@@ -778,6 +785,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
 // (sign bit set, also for M = 0: -0.0f; nodes outside the grid: (0, 0, 0, -0)).  Stored per step: g2p / g2p_grad / grid_op_grad read it.
 template <int D>
 __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
+    pdl_begin();
     using G = Geo<D>;
     const int nact = *sl.nactive;
     const int b0 = *sl.base;
@@ -809,6 +817,7 @@ __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
 // Mb = -(ub . u0)/(M + eps).  Output tile (Pb, Mb) -> sl.part (local block index).
 template <int D>
 __global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, const float4* __restrict__ ubar) {
+    pdl_begin();
     using G = Geo<D>;
     const int nact = *sl.nactive;
     const int b0 = *sl.base;
@@ -946,6 +955,7 @@ template <int D>
 __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
                                             int* __restrict__ keys, int* __restrict__ bcount, int* flags,
                                             bool refwd) {
+    pdl_begin();
     using G = Geo<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
     __shared__ __align__(8) uint64_t s_bar[2];
@@ -1111,6 +1121,7 @@ __device__ __forceinline__ void g2pg_gather(const KParams& p, const float4* __re
 template <int D>
 __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, SlotView sl, StateView S, AdjView Sbn,
                                                             float4* __restrict__ ubar) {
+    pdl_begin();
     using G = Geo<D>;
     constexpr int RS = RowL<D>::STRIDE;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -1175,6 +1186,7 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
 template <int D>
 __global__ void __launch_bounds__(kTG) k_g2p_grad_gather(KParams p, SlotView sl, StateView S, AdjView Sbn,
                                                         float* __restrict__ xbp) {
+    pdl_begin();
     using G = Geo<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
     __shared__ __align__(8) uint64_t s_bar[2];
@@ -1361,6 +1373,7 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
                                                  const float* __restrict__ alpha, AdjView Sbn,
                                                  const float* __restrict__ xbp, AdjView Sb,
                                                  float* __restrict__ abar_part, int* flags) {
+    pdl_begin();
     using G = Geo<D>;
     using L = Lay<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
@@ -1444,6 +1457,7 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
 // alpha_bar_t[a] = sum over active blocks (list order) of abar_part[b][a]
 // (closed loop: per episode e = blockIdx.y, over the blocks of that episode)
 __global__ void k_reduce_abar(KParams p, SlotView sl, const float* __restrict__ part, float* __restrict__ out) {
+    pdl_begin();
     const int a = blockIdx.x, e = blockIdx.y, n_act = p.n_act;
     const int n = *sl.nactive;
     const int* blist = sl.blist + *sl.base;
@@ -1459,6 +1473,7 @@ __global__ void k_reduce_abar(KParams p, SlotView sl, const float* __restrict__ 
 // Each node is counted once, in the tile of the block that owns it (local n < B).
 template <int D>
 __global__ void __launch_bounds__(kT) k_count_active(KParams p, SlotView sl, unsigned long long* count) {
+    pdl_begin();
     using G = Geo<D>;
     const int nact = *sl.nactive;
     const int b0 = *sl.base;
@@ -1498,6 +1513,21 @@ static int occupancy_grid(const void* fn, int smem, int threads = kT) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, threads, smem);
     return sms * (per > 0 ? per : 1);
+}
+
+// Programmatic dependent launch pays where a step is a chain of short, launch-bound kernels
+// (C1-C3: +4% measured on C2) and costs where big persistent kernels share the SMs with the
+// backward's side streams (waiting dependent CTAs hold SM slots: -12% on C5).  The engine
+// enables it per call for small problems (set_pdl); MPM_B200_PDL=0/1 forces it.
+bool g_pdl = false;
+static int g_pdl_force = -1;
+
+void set_pdl(int64_t particles) {
+    if (g_pdl_force < 0) {
+        const char* v = getenv("MPM_B200_PDL");
+        g_pdl_force = v ? (v[0] != '0') : 2;
+    }
+    g_pdl = g_pdl_force == 2 ? particles <= 262144 : g_pdl_force == 1;
 }
 
 cudaError_t tile_init() {
@@ -1560,26 +1590,25 @@ static unsigned pgrid(const KParams& p, int kind) {
 }
 
 void launch_bin_keys(const KParams& p, const float* x, int* keys, int* bcount, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_bin_keys<DIM><<<nblk(p.N * p.E), kT, 0, s>>>(p, x, keys, bcount, flags));
+    DISPATCH(p.dim, launch_k(k_bin_keys<DIM>, nblk(p.N * p.E), kT, 0, s, p, x, keys, bcount, flags));
 }
 int scan_chunks(const KParams& p) { return (p.TB + kScanChunk - 1) / kScanChunk; }
 void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
                      cudaStream_t s) {
     const int nc = scan_chunks(p);
-    k_bin_scan<0><<<nc, kT, 0, s>>>(p, bcount, cursor, sl, (int2*)part, flags);
-    k_bin_scan<1><<<nc, kT, 0, s>>>(p, bcount, cursor, sl, (int2*)part, flags);
+    launch_k(k_bin_scan<0>, nc, kT, 0, s, p, bcount, cursor, sl, (int2*)part, flags);
+    launch_k(k_bin_scan<1>, nc, kT, 0, s, p, bcount, cursor, sl, (int2*)part, flags);
 }
 void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
                         cudaStream_t s) {
-    k_bin_scatter<<<(unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s>>>(p, keys, pid, cursor, sl);
+    launch_k(k_bin_scatter, (unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s, p, keys, pid, cursor, sl);
 }
 void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* flags, cudaStream_t s) {
-    k_canon<<<g_canon_grid < p.step_blocks ? g_canon_grid : (p.step_blocks > 0 ? p.step_blocks : 1), kT,
-              canon_smem_bytes(), s>>>(p, sl, pid_next, flags);
+    launch_k(k_canon, g_canon_grid < p.step_blocks ? g_canon_grid : (p.step_blocks > 0 ? p.step_blocks : 1), kT, canon_smem_bytes(), s, p, sl, pid_next, flags);
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_p2g<DIM><<<pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s>>>(p, sl, S, Sn, aid, alpha_t, flags));
+    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t, flags));
 }
 static unsigned node_grid(const KParams& p) {
     const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? Geo<3>::TN : Geo<2>::TN) + kT - 1) / kT;
@@ -1587,36 +1616,36 @@ static unsigned node_grid(const KParams& p) {
     return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
 }
 void launch_grid_op(const KParams& p, const SlotView& sl, cudaStream_t s) {
-    DISPATCH(p.dim, k_grid_op<DIM><<<node_grid(p), kT, 0, s>>>(p, sl));
+    DISPATCH(p.dim, launch_k(k_grid_op<DIM>, node_grid(p), kT, 0, s, p, sl));
 }
 void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* ubar, cudaStream_t s) {
-    DISPATCH(p.dim, k_grid_op_grad<DIM><<<node_grid(p), kT, 0, s>>>(p, sl, ubar));
+    DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM>, node_grid(p), kT, 0, s, p, sl, ubar));
 }
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
                 int* bcount, int* flags, bool refwd, cudaStream_t s) {
-    DISPATCH(p.dim, k_g2p<DIM><<<pgrid(p, 1), kTG, 0, s>>>(p, sl, S, Sn, keys, bcount, flags, refwd));
+    DISPATCH(p.dim, launch_k(k_g2p<DIM>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bcount, flags, refwd));
 }
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, cudaStream_t s) {
-    DISPATCH(p.dim, k_g2p_grad<DIM><<<pgrid(p, 2), kTQ, g2pg_smem_bytes<DIM>(), s>>>(p, sl, S, Sbn, ubar));
+    DISPATCH(p.dim, launch_k(k_g2p_grad<DIM>, pgrid(p, 2), kTQ, g2pg_smem_bytes<DIM>(), s, p, sl, S, Sbn, ubar));
 }
 void launch_g2p_grad_gather(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                             float* xbp, cudaStream_t s) {
-    DISPATCH(p.dim, k_g2p_grad_gather<DIM><<<pgrid(p, 4), kTG, 0, s>>>(p, sl, S, Sbn, xbp));
+    DISPATCH(p.dim, launch_k(k_g2p_grad_gather<DIM>, pgrid(p, 4), kTG, 0, s, p, sl, S, Sbn, xbp));
 }
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
                      const float* alpha_t, const AdjView& Sbn, const float* xbp,
                      const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, k_p2g_grad<DIM><<<pgrid(p, 3), kTP, 0, s>>>(p, sl, S, aid, alpha_t, Sbn, xbp, Sb, abar_part, flags));
+    DISPATCH(p.dim, launch_k(k_p2g_grad<DIM>, pgrid(p, 3), kTP, 0, s, p, sl, S, aid, alpha_t, Sbn, xbp, Sb, abar_part, flags));
 }
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s) {
     cudaMemsetAsync(count, 0, sizeof(int64_t), s);
-    DISPATCH(p.dim, k_count_active<DIM><<<node_grid(p), kT, 0, s>>>(p, sl, (unsigned long long*)count));
+    DISPATCH(p.dim, launch_k(k_count_active<DIM>, node_grid(p), kT, 0, s, p, sl, (unsigned long long*)count));
 }
 void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s) {
     if (p.n_act > 0)
-        k_reduce_abar<<<dim3(p.n_act, p.closed_loop ? p.E : 1), 32, 0, s>>>(p, sl, abar_part, alpha_bar_t);
+        launch_k(k_reduce_abar, dim3(p.n_act, p.closed_loop ? p.E : 1), 32, 0, s, p, sl, abar_part, alpha_bar_t);
 }
 
 }  // namespace mpm

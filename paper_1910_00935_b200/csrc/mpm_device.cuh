@@ -60,6 +60,15 @@ template <int D> struct Lay {
 // element (component k, particle i) of a component-major array with n particles
 __device__ __forceinline__ int64_t soa(int64_t n, int k, int64_t i) { return (int64_t)k * n + i; }
 
+// Programmatic dependent launch (sm_90+): every kernel is launched with programmatic stream
+// serialization allowed (launch_k in kernels.h), waits for its predecessor grid's results as
+// its first action and immediately lets its own dependent grid be scheduled, so the next
+// kernel's launch and CTA rasterisation overlap this kernel's tail instead of following it.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // quadratic B-spline N_0..N_2 at f in [1/2, 3/2) and derivatives (R1)
 __device__ __forceinline__ void bspline(float f, float w[3], float dw[3]) {
     float a = 1.5f - f, b = f - 1.0f, c = f - 0.5f;
