@@ -51,7 +51,8 @@ class _Cfg(ct.Structure):
                 ("dt", ct.c_double), ("E", ct.c_double), ("nu", ct.c_double),
                 ("p_mass", ct.c_double), ("p_vol", ct.c_double), ("gravity", ct.c_double),
                 ("eps_mass", ct.c_double), ("kappa", ct.c_double), ("omega", ct.c_double),
-                ("closed_loop", ct.c_int32), ("obs_sx", ct.c_double), ("obs_sv", ct.c_double)]
+                ("closed_loop", ct.c_int32), ("obs_sx", ct.c_double), ("obs_sv", ct.c_double),
+                ("mat", ct.c_void_p)]
 
 
 MODELS = {"neohookean": 0, "nh": 0, "fixed_corotated": 1, "fcr": 1}
@@ -83,6 +84,7 @@ class Oracle:
         self.dtype = np.float64 if precision == "f64" else np.float32
         self.p = dict(params)
         self.cfg = make_cfg(params)
+        self._mat = None  # per-particle materials (R23), kept alive for cfg.mat
         self.d = self.cfg.dim
         self.n = self.cfg.n_grid
         self.nn = self.n ** self.d
@@ -188,6 +190,12 @@ class Oracle:
         self.lib.oracle_controller_adj(ct.byref(self.cfg), self._p(th), int(t), self._p(ab),
                                        self._p(thb))
         return thb
+
+    def set_materials(self, mat):
+        """per-particle material ids (0 solid, 1 fluid; R23), caller order; None = all solid."""
+        self._mat = None if mat is None else np.ascontiguousarray(np.asarray(mat, np.int32).ravel())
+        self.cfg.mat = None if self._mat is None else self._mat.ctypes.data
+        return self
 
     def n_obs(self):
         return int(self.lib.oracle_n_obs(ct.byref(self.cfg)))

@@ -173,10 +173,15 @@ static int polar2(const real* F, real* R, real* a, real* b, real* r2) {
 
 /* R2: Neo-Hookean tau = mu (F F^T - I) + lambda ln J I;
        fixed-corotated (2D) tau = 2 mu (F - R) F^T + lambda (J - 1) J I */
-int oracle_stress(const oracle_cfg* c, const real* F, real* tau) {
+/* R23: a fluid particle keeps only the volumetric term of the model (mu = 0) */
+static int stress_m(const oracle_cfg* c, const real* F, int fluid, real* tau);
+int oracle_stress(const oracle_cfg* c, const real* F, real* tau) { return stress_m(c, F, 0, tau); }
+
+static int stress_m(const oracle_cfg* c, const real* F, int fluid, real* tau) {
     const int d = c->dim;
     real mu, lam;
     oracle_lame(c, &mu, &lam);
+    if (fluid) mu = 0;
     real J = det(d, F);
     if (c->model == 0) {
         if (!(J > 0)) return ORACLE_NONFINITE;
@@ -235,10 +240,16 @@ int oracle_energy(const oracle_cfg* c, const real* F, real* psi) {
    NH : Fbar += mu (tb + tb^T) F + lambda tr(tb) F^{-T}
    FCR: Fbar += 2mu (tb + tb^T) F - 2mu tb^T R + lambda (2J - 1) tr(tb) cof(F)
         plus the rotation path Rbar = -2mu tb F through psi = atan2(b, a). */
+static int stress_adj_m(const oracle_cfg* c, const real* F, const real* tb, int fluid, real* Fb);
 int oracle_stress_adj(const oracle_cfg* c, const real* F, const real* tb, real* Fb) {
+    return stress_adj_m(c, F, tb, 0, Fb);
+}
+
+static int stress_adj_m(const oracle_cfg* c, const real* F, const real* tb, int fluid, real* Fb) {
     const int d = c->dim;
     real mu, lam;
     oracle_lame(c, &mu, &lam);
+    if (fluid) mu = 0;
     real J = det(d, F);
     real S[9], SF[9], K[9];
     for (int i = 0; i < d; ++i)
@@ -423,9 +434,9 @@ void oracle_observe_adj(const oracle_cfg* c, int64_t N, const int32_t* aid, cons
 
 /* Kirchhoff stress including actuation (R8): tau += kappa a (F e)(F e)^T */
 static int total_stress(const oracle_cfg* c, const real* Ft, int32_t aid, const real* alpha,
-                        real* tau) {
+                        int fluid, real* tau) {
     const int d = c->dim;
-    int st = oracle_stress(c, Ft, tau);
+    int st = stress_m(c, Ft, fluid, tau);
     if (st) return st;
     if (aid >= 0) {
         real q[MAXD];
@@ -457,7 +468,8 @@ int oracle_p2g(const oracle_cfg* c, int64_t N, const real* x, const real* v, con
         for (int i = 0; i < dd; ++i) G[i] = dt * Cp[i];
         for (int i = 0; i < d; ++i) G[i * d + i] += 1;
         matmul(d, G, Fp, Ft);
-        st = total_stress(c, Ft, aid ? aid[p] : -1, alpha, tau);
+        const int fluid = c->mat && c->mat[p] == 1;
+        st = total_stress(c, Ft, aid ? aid[p] : -1, alpha, fluid, tau);
         if (st) return st;
         for (int i = 0; i < dd; ++i) A[i] = -dt * V * 4 * inv_dx * inv_dx * tau[i] + m * Cp[i];
         for (int s = 0; s < nst; ++s) {
@@ -476,7 +488,14 @@ int oracle_p2g(const oracle_cfg* c, int64_t N, const real* x, const real* v, con
             }
             g[d] += W * m;
         }
-        if (F_next) memcpy(F_next + p * dd, Ft, sizeof(real) * dd);
+        if (F_next) {
+            if (fluid) {  /* R23: F_{t+1} = J^(1/d) I (the fluid forgets its shear) */
+                const real s = pow(det(d, Ft), (real)1 / d);
+                for (int i = 0; i < dd; ++i) F_next[p * dd + i] = (i % (d + 1) == 0) ? s : 0;
+            } else {
+                memcpy(F_next + p * dd, Ft, sizeof(real) * dd);
+            }
+        }
     }
     return ORACLE_OK;
 }
@@ -651,7 +670,8 @@ int oracle_p2g_adj(const oracle_cfg* c, int64_t N, const real* x, const real* v,
         for (int i = 0; i < dd; ++i) G[i] = dt * Cp[i];
         for (int i = 0; i < d; ++i) G[i * d + i] += 1;
         matmul(d, G, Fp, Ft);
-        st = total_stress(c, Ft, a_id, alpha, tau);
+        const int fluid = c->mat && c->mat[p] == 1;
+        st = total_stress(c, Ft, a_id, alpha, fluid, tau);
         if (st) return st;
         for (int i = 0; i < dd; ++i) A[i] = -dt * V * 4 * inv_dx * inv_dx * tau[i] + m * Cp[i];
 
@@ -688,7 +708,15 @@ int oracle_p2g_adj(const oracle_cfg* c, int64_t N, const real* x, const real* v,
             taub[i] = -dt * V * 4 * inv_dx * inv_dx * Ab[i];
             Ftb[i] = Fbn ? Fbn[p * dd + i] : 0;
         }
-        st = oracle_stress_adj(c, Ft, taub, Ftb);
+        if (fluid) {  /* reverse of F_{t+1} = J^(1/d) I: Ftb = (1/d) J^(1/d - 1) tr(Fb') cof(Ft) */
+            const real J = det(d, Ft);
+            real K[9], tr = 0;
+            cofactor(d, Ft, K);
+            for (int i = 0; i < d; ++i) tr += Ftb[i * d + i];
+            const real s = pow(J, (real)1 / d - 1) * tr / d;
+            for (int i = 0; i < dd; ++i) Ftb[i] = s * K[i];
+        }
+        st = stress_adj_m(c, Ft, taub, fluid, Ftb);
         if (st) return st;
         if (a_id >= 0) {
             real q[MAXD], sq[MAXD];

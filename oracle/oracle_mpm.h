@@ -55,6 +55,8 @@ typedef struct {
     double dt, E, nu, p_mass, p_vol, gravity, eps_mass, kappa, omega;
     int32_t closed_loop;  /* 1: the controller also sees the per-muscle observations (R22) */
     double obs_sx, obs_sv;  /* observation scales s_x, s_v (R22) */
+    const int32_t* mat;     /* per-particle material (R23): 0 elastic solid, 1 weakly compressible
+                               fluid (mu = 0, F reset to J^(1/d) I); NULL = all solid */
 } oracle_cfg;
 
 enum { ORACLE_OK = 0, ORACLE_OUT_OF_DOMAIN = 4, ORACLE_NONFINITE = 5, ORACLE_INVALID = 1 };

@@ -53,6 +53,12 @@ CONFIGS: dict[str, dict] = {
     "c3cl": dict(_BASE, dim=3, n_grid=64, model="neohookean", gravity=10.0, steps=512, k_ckpt=32,
                  loss="move_forward", target=[0.0, 0.0, 0.0], n_act=16, closed_loop=True,
                  shape="robot3d", origin=(0.1, 0.0625, 0.359), h=1.0 / 128, seed=3),
+    # the 3D robot coupled with a block of weakly compressible liquid
+    # ("a robot (30K) coupled with liquid (13K)"; R23) that falls on its body
+    "c3liquid": dict(_BASE, dim=3, n_grid=64, model="neohookean", gravity=10.0, steps=512, k_ckpt=32,
+                     loss="move_forward", target=[0.0, 0.0, 0.0], n_act=16,
+                     shape="robot3d_liquid", origin=(0.1, 0.0625, 0.359), h=1.0 / 128, seed=6,
+                     liquid_lower=(0.15, 0.34, 0.375), liquid_counts=(24, 24, 24)),
     # C5: 3D cube, 102^3 = 1,061,208 particles, 128^3 grid, 2,048 steps, k = 32
     "c5": dict(_BASE, dim=3, n_grid=128, model="neohookean", gravity=10.0, steps=2048, k_ckpt=32,
                loss="com_target", target=[0.6, 0.3, 0.5], n_act=0, hidden=0,
@@ -133,6 +139,12 @@ def make_inputs(p: dict | str, episode: int = 0, rank: int = 0) -> dict:
             aid = (np.arange(len(x)) % int(p["n_act"])).astype(np.int32)
     elif shape == "robot2d":
         x, aid = _robot2d(rng, p["origin"], p["h"])
+    elif shape == "robot3d_liquid":  # robot (30K) + liquid (13K)
+        x, aid = _robot3d(rng, np.array(p["origin"], np.float64), p["h"])
+        xl = _lattice(rng, p["liquid_lower"], p["liquid_counts"], p["h"])
+        mat = np.concatenate([np.zeros(len(x), np.int32), np.ones(len(xl), np.int32)])
+        x = np.concatenate([x, xl])
+        aid = np.concatenate([aid, np.full(len(xl), -1, np.int32)])
     elif shape == "robot3d":
         origin = np.array(p["origin"], np.float64)
         if p.get("origin_jitter"):
@@ -142,6 +154,11 @@ def make_inputs(p: dict | str, episode: int = 0, rank: int = 0) -> dict:
     else:
         raise ValueError(shape)
     N = len(x)
+    if shape != "robot3d_liquid":
+        mat = np.zeros(N, np.int32)
+        if p.get("fluid_every"):  # tiny mixed blocks: every k-th particle is fluid (and passive)
+            mat[:: int(p["fluid_every"])] = 1
+            aid = np.where(mat == 1, -1, aid).astype(np.int32)
     v = np.zeros((N, d))
     if "v_base" in p:
         vb = np.array(p["v_base"][:d], np.float64)
@@ -164,6 +181,7 @@ def make_inputs(p: dict | str, episode: int = 0, rank: int = 0) -> dict:
     theta = th_rng.normal(0.0, p.get("theta_std", 0.01), size=n_theta(p))
     f32 = lambda a: np.ascontiguousarray(a, dtype=np.float32)  # noqa: E731
     return dict(x=f32(x), v=f32(v), C=f32(C), F=f32(F), aid=np.ascontiguousarray(aid, np.int32),
+                mat=np.ascontiguousarray(mat, np.int32),
                 theta=f32(theta))
 
 

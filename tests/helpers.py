@@ -43,6 +43,8 @@ def gpu_run(p, inputs, steps=None, k_ckpt=None, episodes=1, seed=None, **over):
 def oracle_run(p, inp, steps=None, precision="f64"):
     from oracle import Oracle
     o = Oracle(p, precision)
+    if inp.get("mat") is not None and np.any(inp["mat"]):
+        o.set_materials(inp["mat"])
     return o.run(inp["x"], inp["v"], inp["C"], inp["F"], inp["aid"], inp["theta"],
                  steps=steps or p["steps"], k_ckpt=1 if (steps or p["steps"]) <= 256 else 16)
 
@@ -51,6 +53,8 @@ def oracle_tape(p, inp, T, lam):
     """oracle forward T steps + reverse with the linear loss <lam, S_T>."""
     from oracle import Oracle
     o = Oracle(p)
+    if inp.get("mat") is not None and np.any(inp["mat"]):
+        o.set_materials(inp["mat"])
     x, v, C, F = (inp[k].astype(np.float64) for k in "xvCF")
     th = inp["theta"].astype(np.float64)
     hist = []
