@@ -62,10 +62,11 @@ def _workload(name: str, world: int, rank: int = 0):
 
 def _describe(p, n_particles, episodes, world, k):
     shape = {"cube3d": "3D elastic cube", "robot3d": "3D robot (16 muscles)",
+             "robot3d_liquid": "3D robot (16 muscles) + liquid block",
              "robot2d": "2D robot (4 muscles)", "block2d": "2D elastic block"}[p["shape"]]
     return {"workload": f"{p['name']}: {shape}, {n_particles:,} particles x {episodes} episode(s)/GPU, "
                         f"{p['n_grid']}^{p['dim']} grid, {p['steps']} steps, checkpoint every {k}",
-            "config_index": {"c1a": 0, "c1b": 0, "c2": 1, "c2cl": 1, "c3": 2, "c3cl": 2, "c4": 3, "c5": 4}[p["name"]],
+            "config_index": {"c1a": 0, "c1b": 0, "c2": 1, "c2cl": 1, "c3": 2, "c3cl": 2, "c3liquid": 2, "c4": 3, "c5": 4}[p["name"]],
             "controller": ("closed loop (R22)" if p.get("closed_loop") else "open loop") if p.get("n_act") else "none",
             "dim": p["dim"], "particles_per_episode": n_particles, "episodes_per_gpu": episodes,
             "episodes_total": episodes * world, "n_grid": p["n_grid"], "time_steps": p["steps"],
@@ -168,6 +169,8 @@ def oracle_sample(p, inp, steps=1):
     episode, `steps` time steps of forward + loss + backward, fp64, one thread."""
     from oracle import Oracle
     o = Oracle(p)
+    if inp.get("mat") is not None and np.any(inp["mat"]):
+        o.set_materials(inp["mat"])
     t0 = time.perf_counter()
     o.run(inp["x"], inp["v"], inp["C"], inp["F"], inp["aid"], inp["theta"], steps=steps,
           k_ckpt=steps)
@@ -258,6 +261,8 @@ def run_ours(args):
 
     k = int(args.k_ckpt) if args.k_ckpt else _pick_k(p, N, per, T, dev)
     sim = mpm.sim_from_config(p, N, episodes=per, max_steps=T, k_ckpt=k)
+    if any(np.any(i["mat"]) for i in inps):  # fluid particles (R23): a property of the workload
+        sim.set_materials(cat("mat"))
     nth = sim.n_theta
     shared_len = nth if nth > 0 else per * p["dim"]
     loss_d = torch.zeros(per, device=dev)
@@ -413,7 +418,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c5", choices=["c1a", "c1b", "c2", "c2cl", "c3", "c3cl", "c4", "c5"])
+    ap.add_argument("--config", default="c5", choices=["c1a", "c1b", "c2", "c2cl", "c3", "c3cl", "c3liquid", "c4", "c5"])
     ap.add_argument("--k-ckpt", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

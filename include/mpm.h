@@ -131,6 +131,13 @@ mpm_status mpm_bind_workspace(mpm_handle h, void* device_ptr, size_t bytes);
 mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const float* C,
                          const float* F, const int32_t* actuator_id);
 
+/* Per-particle material (R23), host or device pointer, [E][N] caller
+ * order: 0 = the elastic solid of mpm_params.model; nonzero = weakly compressible fluid (mu = 0,
+ * volumetric stress only, F reset to J^(1/d) I after every step).  NULL (the default after
+ * bind) = all solid.  Persists across mpm_set_state; clears a recorded tape.  Fluid particles
+ * should be passive (actuator_id -1). */
+mpm_status mpm_set_materials(mpm_handle h, const int32_t* material);
+
 /* Number of controller parameters for the current params, and set them
  * (host or device pointer, n_theta floats). */
 mpm_status mpm_n_theta(mpm_handle h, int64_t* n_theta);

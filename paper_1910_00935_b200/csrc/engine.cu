@@ -114,6 +114,8 @@ struct mpm_ctx {
     // tape
     Phase phase = kCreated;
     bool has_aid = false;
+    bool has_mat = false;          // any fluid particle (R23) set by mpm_set_materials
+    int32_t* mat = nullptr;        // [EN] material by particle id (0 solid, nonzero fluid)
     int32_t recorded = 0;
     int32_t t_final = 0;
     int window_seg = -1;
@@ -176,6 +178,7 @@ KParams kparams(const mpm_ctx* h) {
     k.a_estride = k.closed_loop ? p.n_actuators : 0;
     k.obs_sx = p.obs_scale_x;
     k.obs_sv = p.obs_scale_v;
+    k.mat = h->has_mat ? h->mat : nullptr;
     k.dt = h->dt;
     k.dx = 1.0f / (float)h->n_grid;
     k.inv_dx = (float)h->n_grid;
@@ -281,6 +284,7 @@ size_t carve(mpm_ctx* h, char* base) {
     AdjView sb1 = adj();
     float* staging = (float*)take(sizeof(float) * sf);
     int32_t* aid = (int32_t*)take(sizeof(int32_t) * EN);
+    int32_t* mat = (int32_t*)take(sizeof(int32_t) * EN);
     float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
     int* bcount = (int*)take(sizeof(int) * k.TB);
     int* cursor = (int*)take(sizeof(int) * k.TB);
@@ -319,7 +323,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->final_state = fin;
         h->sbar[0] = sb0; h->sbar[1] = sb1;
         h->xbar_part = xbar_part;
-        h->staging = staging; h->aid = aid; h->bcount = bcount; h->cursor = cursor; h->scan_part = scan_part; h->keys = keys;
+        h->staging = staging; h->aid = aid; h->mat = mat; h->bcount = bcount; h->cursor = cursor; h->scan_part = scan_part; h->keys = keys;
         h->ubar = ubar; h->part = part; h->abar_part = abar_part;
         h->obs = obs; h->obs_cnt = obs_cnt; h->obs_part = obs_part; h->obs_inc = obs_inc;
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
@@ -720,6 +724,22 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
     return MPM_OK;
 }
 
+mpm_status mpm_set_materials(mpm_handle h, const int32_t* material) {
+    if (!h) return MPM_ERR_INVALID_ARG;
+    if (h->phase < kBound) return fail(h, MPM_ERR_BAD_SEQUENCE, "set_materials before bind_workspace");
+    const KParams k = kparams(h);
+    const size_t EN = (size_t)k.E * k.N;
+    h->has_mat = material != nullptr;
+    if (h->has_mat) {
+        mpm_status st = copy_in(h, h->mat, material, sizeof(int32_t) * EN);
+        if (st) return st;
+    }
+    // a new material layout invalidates a recorded tape
+    if (h->phase > kHasState) h->phase = kHasState;
+    h->recorded = 0;
+    return MPM_OK;
+}
+
 mpm_status mpm_n_theta(mpm_handle h, int64_t* n) {
     if (!h || !n) return MPM_ERR_INVALID_ARG;
     *n = n_theta_of(h->prm, h->dim);
@@ -743,7 +763,7 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
     const KParams k = kparams(h);
     h->t_final = steps;
     set_pdl(k.EN);
-    mpm_status gs = run_graphed(h, std::make_tuple(0, steps, (int)h->has_aid, -1), [&]() {
+    mpm_status gs = run_graphed(h, std::make_tuple(0, steps, (int)h->has_aid + 2 * (int)h->has_mat, -1), [&]() {
         if (k.n_act > 0 && !k.closed_loop) {
             KScope sc(h, KC_CTRL);
             launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream);
@@ -813,7 +833,7 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     const int kk = h->prm.k_ckpt, T = steps;
     const int A = k.n_act > 0 ? k.n_act : 1;
     set_pdl(k.EN);
-    mpm_status gs = run_graphed(h, std::make_tuple(1, T, (int)h->has_aid, h->window_seg * 2 + h->sbar_cur), [&]() {
+    mpm_status gs = run_graphed(h, std::make_tuple(1, T, (int)h->has_aid + 2 * (int)h->has_mat, h->window_seg * 2 + h->sbar_cur), [&]() {
         if (k.n_act > 0)
             cudaMemsetAsync(h->alpha_bar, 0, sizeof(float) * (size_t)T * A * (k.closed_loop ? k.E : 1), h->stream);
         if (k.closed_loop)  // accumulated step by step (t descending) by ctrl_obs_bwd

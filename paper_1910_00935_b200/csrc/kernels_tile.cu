@@ -568,8 +568,8 @@ __device__ __forceinline__ void write_row(float* row, const float w[3][3], const
 // per-particle p2g math: returns c = m v - A dx f and A dx (for NodeAcc) and Ft
 template <int D>
 __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, const float* vc, const float* F,
-                                             float act, const int c0[3], float w[3][3], float* c, float* Adx,
-                                             float* Ft) {
+                                             float act, bool fluid, const int c0[3], float w[3][3], float* c,
+                                             float* Adx, float* Ft) {
     const float* v = vc;
     const float* C = vc + D;
     int lb[3];
@@ -577,7 +577,7 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
     particle_weights<D>(p, x, c0, lb, fx, w, dw);
     deform_update<D>(p.dt, C, F, Ft);
     float tau[D * D];
-    const bool ok = kirchhoff<D>(p, Ft, act, tau);
+    const bool ok = kirchhoff<D>(p, Ft, act, tau, fluid);
 #pragma unroll
     for (int q = 0; q < D * D; ++q) Adx[q] = p.dx * fmaf(p.stress_scale, tau[q], p.p_mass * C[q]);
 #pragma unroll
@@ -735,13 +735,18 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         acc.zero();
         float x[3], vc[L::VC], F[L::FF];
         int a_id = -1;
+        bool fluid = false;
 #define MPM_P2G_LOAD(R)                                                                          \
     do {                                                                                         \
         const int i_ = s_ci[(R)];                                                                 \
         _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i_));      \
         _Pragma("unroll") for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + soa(p.EN, q, i_)); \
         _Pragma("unroll") for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + soa(p.EN, q, i_));  \
-        if (aid) a_id = __ldg(aid + __ldg(S.pid + i_));                                           \
+        if (aid || p.mat) {                                                                       \
+            const int pd_ = __ldg(S.pid + i_);                                                    \
+            if (aid) a_id = __ldg(aid + pd_);                                                     \
+            if (p.mat) fluid = __ldg(p.mat + pd_) != 0;                                           \
+        }                                                                                         \
     } while (0)
         if (tid < nvalid) MPM_P2G_LOAD(tid);
         for (int ch = 0; ch < nvalid; ch += kCH) {
@@ -749,9 +754,10 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
                 const float act = (aid && a_id >= 0) ? alpha[e * p.a_estride + a_id] : 0.0f;
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
-                if (!p2g_particle<D>(p, x, vc, F, act, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
+                if (!p2g_particle<D>(p, x, vc, F, act, fluid, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
                 write_row<D>(s_row + (r - ch) * RS, w, c, Adx);
                 if (Sn.f) {
+                    if (fluid) fluid_reset<D>(Ft, Ft);  // R23 (Ft is dead after the row)
 #pragma unroll
                     for (int q = 0; q < D * D; ++q) Sn.f[soa(p.EN, q, start + r)] = Ft[q];
                 }
@@ -929,9 +935,11 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
             F[q] = __ldg(S.f + soa(p.EN, q, i));
         }
         deform_update<D>(p.dt, C, F, Ft);
+        const int pd = __ldg(S.pid + i);
+        if (p.mat && __ldg(p.mat + pd) != 0) fluid_reset<D>(Ft, Ft);  // R23
 #pragma unroll
         for (int q = 0; q < D * D; ++q) Sn.f[soa(p.EN, q, j)] = Ft[q];
-        Sn.pid[j] = __ldg(S.pid + i);
+        Sn.pid[j] = pd;
     }
     int key = -1;
     if (keys) {
@@ -1251,8 +1259,8 @@ template <int D>
 __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float4* __restrict__ sG,
                                                    const float* x, const float* vc, const float* F,
                                                    const float* Fbn, const float* xbp, bool has_act,
-                                                   float act, const int c0[3], int64_t i, const AdjView& Sb,
-                                                   int* flags) {
+                                                   float act, bool fluid, const int c0[3], int64_t i,
+                                                   const AdjView& Sb, int* flags) {
     using L = Lay<D>;
     const float* v = vc;
     const float* C = vc + D;
@@ -1270,7 +1278,7 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
             Ft[a * D + b] = fmaf(p.dt, s, F[a * D + b]);
         }
     float tau[D * D], Adx[D * D], c[3];
-    kirchhoff<D>(p, Ft, act, tau);
+    kirchhoff<D>(p, Ft, act, tau, fluid);
 #pragma unroll
     for (int q = 0; q < D * D; ++q) Adx[q] = p.dx * fmaf(p.stress_scale, tau[q], p.p_mass * C[q]);
 #pragma unroll
@@ -1340,7 +1348,8 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
         taub[q] = p.stress_scale * Ab[q];
         Ftb[q] = Fbn[q];
     }
-    const float abar = kirchhoff_adj<D>(p, Ft, has_act, act, taub, Ftb);
+    if (fluid) fluid_reset_adj<D>(Ft, Fbn, Ftb);  // R23: F_{t+1} = J^(1/d) I
+    const float abar = kirchhoff_adj<D>(p, Ft, has_act, act, taub, Ftb, fluid);
     bool fin = true;
 #pragma unroll
     for (int a = 0; a < D; ++a)
@@ -1409,6 +1418,7 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
             float x[3], vc[L::VC], F[L::FF], Fbn[L::FF], xb[3];
             int64_t i = 0;
             int a_id = -1;
+            bool fluid = false;
             if (in) {
                 const int j = start + r;
                 i = sl.sigma[j];
@@ -1422,14 +1432,18 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
                 for (int q = 0; q < L::FF; ++q) Fbn[q] = __ldg(Sbn.f + soa(p.EN, q, j));
 #pragma unroll
                 for (int k = 0; k < D; ++k) xb[k] = __ldg(xbp + soa(p.EN, k, j));
-                if (aid) a_id = __ldg(aid + __ldg(S.pid + i));
+                if (aid || p.mat) {
+                    const int pd = __ldg(S.pid + i);
+                    if (aid) a_id = __ldg(aid + pd);
+                    if (p.mat) fluid = __ldg(p.mat + pd) != 0;
+                }
             }
             if (r0 == 0) sG = pipe.wait(it);
             float abar = 0.0f;
             if (in) {
                 const bool has_act = aid && a_id >= 0;
-                abar = p2g_grad_particle<D>(p, sG, x, vc, F, Fbn, xb, has_act, has_act ? alpha[e * p.a_estride + a_id] : 0.0f, c0,
-                                            i, Sb, flags);
+                abar = p2g_grad_particle<D>(p, sG, x, vc, F, Fbn, xb, has_act,
+                                            has_act ? alpha[e * p.a_estride + a_id] : 0.0f, fluid, c0, i, Sb, flags);
                 if (!has_act) a_id = -1;
             }
             if (p.n_act > 0) {  // per-actuator warp sums (fixed butterfly) into the warp's slot

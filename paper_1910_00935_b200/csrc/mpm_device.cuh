@@ -27,6 +27,7 @@ struct KParams {
     int32_t n_in;        // controller inputs: n_sin (+ 2 d n_act closed loop)
     int32_t a_estride;   // episode stride of alpha_t / alpha_bar_t (n_act closed loop, else 0)
     float obs_sx, obs_sv;  // observation scales (R22)
+    const int32_t* mat;  // per-particle material by particle id (R23: nonzero = fluid), or null
 };
 
 enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8 };
@@ -152,13 +153,16 @@ template <int D> __device__ __forceinline__ void deform_update(float dt, const f
 // NH : tau = mu (F F^T - I) + lambda ln J I
 // FCR: tau = 2 mu (F - R) F^T + lambda (J - 1) J I   (2D closed-form polar R)
 // returns false on a degenerate deformation (R14).
+// fluid (R23): the volumetric term only (mu = 0)
 template <int D>
-__device__ __forceinline__ bool kirchhoff(const KParams& p, const float* Fm, float act, float* tau) {
+__device__ __forceinline__ bool kirchhoff(const KParams& p, const float* Fm, float act, float* tau,
+                                          bool fluid = false) {
+    const float mu = fluid ? 0.0f : p.mu;
     float J = det<D>(Fm);
     bool ok = true;
     if (D == 3 || p.model == 0) {
         ok = J > 0.0f;
-        float iso = p.lam * logf(fmaxf(J, 1e-30f)) - p.mu;
+        float iso = p.lam * logf(fmaxf(J, 1e-30f)) - mu;
 #pragma unroll
         for (int i = 0; i < D; ++i)
 #pragma unroll
@@ -166,7 +170,7 @@ __device__ __forceinline__ bool kirchhoff(const KParams& p, const float* Fm, flo
                 float s = 0.0f;
 #pragma unroll
                 for (int k = 0; k < D; ++k) s = fmaf(Fm[i * D + k], Fm[j * D + k], s);
-                tau[i * D + j] = p.mu * s + (i == j ? iso : 0.0f);
+                tau[i * D + j] = mu * s + (i == j ? iso : 0.0f);
             }
     } else {
         float a = Fm[0] + Fm[3], b = Fm[2] - Fm[1];
@@ -176,10 +180,10 @@ __device__ __forceinline__ bool kirchhoff(const KParams& p, const float* Fm, flo
         float cs = a * ir, sn = b * ir;
         float M0 = Fm[0] - cs, M1 = Fm[1] + sn, M2 = Fm[2] - sn, M3 = Fm[3] - cs;  // F - R
         float iso = p.lam * (J - 1.0f) * J;
-        tau[0] = 2.0f * p.mu * (M0 * Fm[0] + M1 * Fm[1]) + iso;
-        tau[1] = 2.0f * p.mu * (M0 * Fm[2] + M1 * Fm[3]);
-        tau[2] = 2.0f * p.mu * (M2 * Fm[0] + M3 * Fm[1]);
-        tau[3] = 2.0f * p.mu * (M2 * Fm[2] + M3 * Fm[3]) + iso;
+        tau[0] = 2.0f * mu * (M0 * Fm[0] + M1 * Fm[1]) + iso;
+        tau[1] = 2.0f * mu * (M0 * Fm[2] + M1 * Fm[3]);
+        tau[2] = 2.0f * mu * (M2 * Fm[0] + M3 * Fm[1]);
+        tau[3] = 2.0f * mu * (M2 * Fm[2] + M3 * Fm[3]) + iso;
     }
     if (act != 0.0f) {
         // q = F e (column act_axis); selects keep F in registers (no dynamic indexing)
@@ -199,7 +203,8 @@ __device__ __forceinline__ bool kirchhoff(const KParams& p, const float* Fm, flo
 // (returns kappa q^T tb q, the contribution to alpha_bar).
 template <int D>
 __device__ __forceinline__ float kirchhoff_adj(const KParams& p, const float* Fm, bool has_act,
-                                               float act, const float* tb, float* Fb) {
+                                               float act, const float* tb, float* Fb, bool fluid = false) {
+    const float mu = fluid ? 0.0f : p.mu;
     float S[D * D], K[D * D];
 #pragma unroll
     for (int i = 0; i < D; ++i)
@@ -211,7 +216,7 @@ __device__ __forceinline__ float kirchhoff_adj(const KParams& p, const float* Fm
 #pragma unroll
     for (int i = 0; i < D; ++i) tr += tb[i * D + i];
     const bool nh = (D == 3 || p.model == 0);
-    float musym = nh ? p.mu : 2.0f * p.mu;
+    float musym = nh ? mu : 2.0f * mu;
     float kiso = nh ? p.lam * tr / J : p.lam * (2.0f * J - 1.0f) * tr;
     // (tb + tb^T) F term and the isotropic term
 #pragma unroll
@@ -231,13 +236,13 @@ __device__ __forceinline__ float kirchhoff_adj(const KParams& p, const float* Fm
         // -2 mu tb^T R
         float tR0 = tb[0] * cs + tb[2] * sn, tR1 = -tb[0] * sn + tb[2] * cs;
         float tR2 = tb[1] * cs + tb[3] * sn, tR3 = -tb[1] * sn + tb[3] * cs;
-        Fb[0] -= 2.0f * p.mu * tR0; Fb[1] -= 2.0f * p.mu * tR1;
-        Fb[2] -= 2.0f * p.mu * tR2; Fb[3] -= 2.0f * p.mu * tR3;
+        Fb[0] -= 2.0f * mu * tR0; Fb[1] -= 2.0f * mu * tR1;
+        Fb[2] -= 2.0f * mu * tR2; Fb[3] -= 2.0f * mu * tR3;
         // rotation path: Rb = -2 mu tb F; psi_b = <Rb, dR/dpsi>
-        float Rb0 = -2.0f * p.mu * (tb[0] * Fm[0] + tb[1] * Fm[2]);
-        float Rb1 = -2.0f * p.mu * (tb[0] * Fm[1] + tb[1] * Fm[3]);
-        float Rb2 = -2.0f * p.mu * (tb[2] * Fm[0] + tb[3] * Fm[2]);
-        float Rb3 = -2.0f * p.mu * (tb[2] * Fm[1] + tb[3] * Fm[3]);
+        float Rb0 = -2.0f * mu * (tb[0] * Fm[0] + tb[1] * Fm[2]);
+        float Rb1 = -2.0f * mu * (tb[0] * Fm[1] + tb[1] * Fm[3]);
+        float Rb2 = -2.0f * mu * (tb[2] * Fm[0] + tb[3] * Fm[2]);
+        float Rb3 = -2.0f * mu * (tb[2] * Fm[1] + tb[3] * Fm[3]);
         float psib = -sn * Rb0 - cs * Rb1 + cs * Rb2 - sn * Rb3;
         float ga = -psib * b / r2, gb = psib * a / r2;  // d psi/da = -b/r^2, d psi/db = a/r^2
         Fb[0] += ga; Fb[3] += ga; Fb[2] += gb; Fb[1] -= gb;
@@ -265,6 +270,27 @@ __device__ __forceinline__ float kirchhoff_adj(const KParams& p, const float* Fm
                 if (k == e) Fb[i * D + k] = fmaf(s, sq[i], Fb[i * D + k]);
     }
     return abar;
+}
+
+// R23 fluid: F_{t+1} = J^(1/d) I with J = det(Ft) (shear forgotten)
+template <int D> __device__ __forceinline__ void fluid_reset(const float* Ft, float* Fn) {
+    const float J = det<D>(Ft);
+    const float s = D == 3 ? cbrtf(J) : sqrtf(J);
+#pragma unroll
+    for (int q = 0; q < D * D; ++q) Fn[q] = (q % (D + 1) == 0) ? s : 0.0f;
+}
+// its reverse: Ftb = d/dFt <Fb', J^(1/d) I> = (1/d) J^(1/d - 1) tr(Fb') cof(Ft)
+template <int D> __device__ __forceinline__ void fluid_reset_adj(const float* Ft, const float* Fbn, float* Ftb) {
+    const float J = det<D>(Ft);
+    const float s = D == 3 ? cbrtf(J) : sqrtf(J);
+    float tr = 0.0f;
+#pragma unroll
+    for (int i = 0; i < D; ++i) tr += Fbn[i * D + i];
+    float K[D * D];
+    cof<D>(Ft, K);
+    const float g = s / J * tr / (float)D;
+#pragma unroll
+    for (int q = 0; q < D * D; ++q) Ftb[q] = g * K[q];
 }
 
 }  // namespace mpm

@@ -26,7 +26,8 @@ EXPORTS = ["mpm_create", "mpm_destroy", "mpm_last_error", "mpm_default_params", 
            "mpm_set_params", "mpm_set_stream", "mpm_workspace_bytes", "mpm_bind_workspace",
            "mpm_set_state", "mpm_n_theta", "mpm_set_controller", "mpm_forward", "mpm_loss",
            "mpm_seed_adjoint", "mpm_backward", "mpm_grads", "mpm_get_state", "mpm_launch_count",
-           "mpm_grad_v0_sum", "mpm_set_profiling", "mpm_reset_kernel_stats", "mpm_kernel_stats", "mpm_active_nodes"]
+           "mpm_grad_v0_sum", "mpm_set_profiling", "mpm_reset_kernel_stats", "mpm_kernel_stats", "mpm_active_nodes",
+           "mpm_set_materials"]
 
 
 class MpmError(RuntimeError):
@@ -74,7 +75,7 @@ def load() -> ct.CDLL:
             "mpm_grad_v0_sum": [H, P], "mpm_set_profiling": [H, ct.c_int32], "mpm_reset_kernel_stats": [H],
             "mpm_kernel_stats": [H, ct.c_int32, ct.POINTER(ct.c_char_p), ct.POINTER(ct.c_double),
                                  ct.POINTER(ct.c_int64)],
-            "mpm_active_nodes": [H, ct.POINTER(ct.c_int64)],
+            "mpm_active_nodes": [H, ct.POINTER(ct.c_int64)], "mpm_set_materials": [H, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -150,6 +151,14 @@ class Sim:
     def set_state(self, x, v=None, C=None, F=None, aid=None):
         keep = [_ptr(a) for a in (x, v, C, F)] + [_ptr(aid, np.int32)]
         self._check("mpm_set_state", self.L.mpm_set_state(self.h, *[k[0] for k in keep]))
+
+    def set_materials(self, mat):
+        """per-particle material [E][N] (0 solid, 1 fluid; R23), or None = all solid."""
+        if mat is None:
+            self._check("mpm_set_materials", self.L.mpm_set_materials(self.h, None))
+            return
+        ptr, keep = _ptr(mat, np.int32)
+        self._check("mpm_set_materials", self.L.mpm_set_materials(self.h, ptr))
 
     def set_controller(self, theta):
         if self.n_theta == 0:

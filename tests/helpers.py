@@ -24,6 +24,8 @@ def gpu_run(p, inputs, steps=None, k_ckpt=None, episodes=1, seed=None, **over):
     sim = mpm.sim_from_config(p, N, episodes=E, max_steps=T, k_ckpt=k_ckpt, **over)
     cat = lambda k: np.ascontiguousarray(np.stack([i[k] for i in inputs]))  # noqa: E731
     sim.set_state(cat("x"), cat("v"), cat("C"), cat("F"), cat("aid"))
+    if all("mat" in i for i in inputs) and any(np.any(i["mat"]) for i in inputs):
+        sim.set_materials(cat("mat"))
     sim.set_controller(inputs[0]["theta"])
     sim.forward(T)
     st = sim.get_state()

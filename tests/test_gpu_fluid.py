@@ -1,0 +1,65 @@
+"""Weakly compressible fluid particles (R23) on the CUDA path vs
+the fp64 CPU oracle, through the C-ABI (mpm_set_materials), on the same seeded inputs."""
+import numpy as np
+import pytest
+
+from helpers import gpu_run, inputs, oracle_tape, rel
+from paper_1910_00935_b200 import workloads as W
+from test_gpu_parity import _assert, _compare_episode
+
+pytestmark = pytest.mark.gpu
+
+STATE_TOL = 1e-4
+GRAD_TOL = 1e-3
+
+TINY = {
+    "2d_fcr_mixed_floor": lambda: W.tiny(2, steps=10, hidden=3, seed=12, fluid_every=2, bound=3, floor=True,
+                                         v_base=(0.3, -1.5)),
+    "3d_nh_mixed": lambda: W.tiny(3, steps=6, hidden=0, seed=13, fluid_every=3),
+    "2d_nh_all_fluid": lambda: W.tiny(2, steps=8, model="neohookean", seed=14, fluid_every=1, n_act=0),
+}
+
+
+@pytest.mark.parametrize("case", list(TINY))
+def test_tiny_fluid_every_adjoint_path(case):
+    p = TINY[case]()
+    inp = W.make_inputs(p)
+    assert inp["mat"].any()
+    N, d = inp["x"].shape
+    rng = np.random.default_rng(17)
+    lam = [rng.standard_normal((N, d)), rng.standard_normal((N, d)),
+           rng.standard_normal((N, d, d)), rng.standard_normal((N, d, d))]
+    lam = [l.astype(np.float32) for l in lam]
+    ref = oracle_tape(p, inp, p["steps"], lam)
+    got = gpu_run(p, inp, seed=lam)
+    for k in "xvCF":
+        assert rel(got[k][0], ref[k]) < STATE_TOL, (k, rel(got[k][0], ref[k]))
+    for k in ("dx0", "dv0", "dC0", "dF0", "dtheta"):
+        if k == "dtheta" and ref[k].size == 0:
+            continue
+        assert rel(got[k].reshape(ref[k].shape), ref[k]) < GRAD_TOL, (k, rel(got[k].reshape(ref[k].shape), ref[k]))
+    # the fluid particles' F is isotropic after every step (R23)
+    F = got["F"][0][inp["mat"] == 1]
+    off = F - np.einsum("nii->n", F)[:, None, None] / d * np.eye(d)
+    assert np.abs(off).max() < 1e-6 * np.abs(F).max()
+
+
+def test_fluid_checkpoint_invariant_and_reproducible():
+    """the segment re-forward applies the same F reset bit for bit (k = 1 vs k = 4)."""
+    p = W.tiny(3, steps=12, hidden=3, seed=15, fluid_every=2, bound=3, floor=True, v_base=(0.2, -1.5, 0.1))
+    inp = W.make_inputs(p)
+    a = gpu_run(p, inp, k_ckpt=1)
+    b = gpu_run(p, inp, k_ckpt=4)
+    c = gpu_run(p, inp, k_ckpt=4)
+    for k in ("x", "v", "C", "F", "dx0", "dv0", "dC0", "dF0", "dtheta"):
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+        np.testing.assert_array_equal(b[k], c[k], err_msg=k)
+
+
+def test_robot3d_with_liquid_c3liquid():
+    """P:612's robot (30K) coupled with liquid (13.8K), 64 steps, k = 32: states and gradients
+    vs the oracle."""
+    p, inp = inputs("c3liquid", steps=64)
+    got = gpu_run(p, inp, k_ckpt=32)
+    errs, _ = _compare_episode(p, inp, got, grads=("dx0", "dv0", "dtheta"))
+    _assert(errs, "c3liquid")
