@@ -135,7 +135,7 @@ def make_inputs(p: dict | str, episode: int = 0, rank: int = 0) -> dict:
     if shape in ("block2d", "cube3d", "block"):
         x = _lattice(rng, p["lower"], p["counts"], p["h"])
         aid = np.full(len(x), -1, np.int32)
-        if "act_ids" in p:  # tiny test blocks: alternate actuator ids
+        if "act_ids" in p and int(p.get("n_act", 0)) > 0:  # tiny test blocks: alternate actuator ids
             aid = (np.arange(len(x)) % int(p["n_act"])).astype(np.int32)
     elif shape == "robot2d":
         x, aid = _robot2d(rng, p["origin"], p["h"])
