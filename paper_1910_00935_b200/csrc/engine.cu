@@ -92,7 +92,7 @@ struct mpm_ctx {
     int32_t* aid = nullptr;        // caller order
     int* bcount = nullptr;         // [TB] block histogram (kept zero between uses)
     int* cursor = nullptr;         // [TB]
-    int* scan_part = nullptr;      // [scan chunks] int2
+    int* scan_part = nullptr;      // [scan chunks + 2] int64: epoch-tagged chunk totals, epoch, ticket
     int* keys = nullptr;           // [EN]
     float4* ubar = nullptr;        // [max_active][TN]  U_bar partial tiles of the current step
     float4* part = nullptr;        // [max_active][TN]  p2g partial tiles / (Pb, Mb) tiles
@@ -288,7 +288,7 @@ size_t carve(mpm_ctx* h, char* base) {
     float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
     int* bcount = (int*)take(sizeof(int) * k.TB);
     int* cursor = (int*)take(sizeof(int) * k.TB);
-    int* scan_part = (int*)take(sizeof(int) * 2 * (scan_chunks(k) + 1));
+    int* scan_part = (int*)take(sizeof(int64_t) * (scan_chunks(k) + 2));  // chunk totals, epoch, ticket
     int* keys = (int*)take(sizeof(int) * EN);
     float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
     float4* part = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
@@ -430,7 +430,7 @@ const float* alpha_at(mpm_ctx* h, int t) {
 void bin_fresh(mpm_ctx* h, const KParams& k, int t) {
     const SlotView sl = slot_at(h, t);
     KScope sc(h, KC_BIN);
-    h->launches += 3;
+    h->launches += 2;
     launch_bin_keys(k, state_at(h, t).x, h->keys, h->bcount, h->flags, h->stream);
     launch_bin_scan(k, h->bcount, h->cursor, sl, h->scan_part, h->flags, h->stream);
     launch_bin_scatter(k, h->keys, state_at(h, t).pid, h->cursor, sl, h->stream);
@@ -459,7 +459,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     if (bin_next) {
         const SlotView nx = slot_at(h, t + 1);
         KScope sc(h, KC_BIN);
-        h->launches += 2;
+        h->launches += 1;
         launch_bin_scan(k, h->bcount, h->cursor, nx, h->scan_part, h->flags, h->stream);
         launch_bin_scatter(k, h->keys, Sn.pid, h->cursor, nx, h->stream);
     }
@@ -689,6 +689,7 @@ mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     carve(h, h->ws);
     const KParams k = kparams(h);
     CU(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
+    CU(cudaMemsetAsync(h->scan_part, 0, sizeof(int64_t) * (scan_chunks(kparams(h)) + 2), h->stream));
     CU(cudaMemsetAsync(h->bcount, 0, sizeof(int) * k.TB, h->stream));
     CU(cudaMemsetAsync(h->theta, 0, sizeof(float) * (n_theta_of(h->prm, h->dim) > 0 ? n_theta_of(h->prm, h->dim) : 1), h->stream));
     h->phase = kBound;

@@ -242,9 +242,12 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
 }
 
 // Exclusive scan of the dense block histogram -> active block list (block-id order),
-// starts, block map, scatter cursors; clears the histogram.  Two launches over chunks of
-// 256 x 16 entries: k_bin_scan<0> writes per-chunk totals, k_bin_scan<1> adds the totals
-// of the earlier chunks (fixed order) and writes the outputs.
+// starts, block map, scatter cursors; clears the histogram.  One launch over chunks of
+// 256 x 4 entries (MODE 2): every CTA publishes its chunk totals tagged with the launch's
+// epoch, then sums the totals of all earlier chunks (look-back; integer sums, so the order
+// does not matter) -- all chunk CTAs are co-resident (<= 32 at 128^3, 256 for 64 episodes
+// at 64^3).  The last CTA (ticket) advances the epoch.  (MODE 0 + MODE 1: the two-launch
+// variant, kept for reference.)
 #ifndef MPM_SCAN_PER
 #define MPM_SCAN_PER 4
 #endif
@@ -256,7 +259,10 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
     pdl_begin();
     __shared__ int s_wt[kW], s_wa[kW];
     __shared__ int s_base[2];
+    __shared__ unsigned s_epoch;
+    unsigned long long* part64 = reinterpret_cast<unsigned long long*>(part);
     const int TB = p.TB, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (MODE == 2 && tid == 0) s_epoch = ((unsigned)part64[gridDim.x] + 1u) & 0xFFFFu;
     const int i0 = blockIdx.x * kScanChunk + tid * kScanPer;
     int c[kScanPer];
     if (i0 + kScanPer <= TB) {
@@ -279,6 +285,33 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
         if (lane >= off) { it += a; ia += b; }
     }
     if (lane == 31) { s_wt[warp] = it; s_wa[warp] = ia; }
+    if (MODE == 2) {
+        __syncthreads();
+        const unsigned long long ep = s_epoch;
+        if (tid == 0) {  // publish this chunk's totals, tagged with the epoch
+            unsigned bt = 0, ba = 0;
+            for (int w = 0; w < kW; ++w) { bt += (unsigned)s_wt[w]; ba += (unsigned)s_wa[w]; }
+            const unsigned long long v = (ep << 48) | ((unsigned long long)(ba & 0xFFFFu) << 32) | bt;
+            atomicExch(part64 + blockIdx.x, v);
+        }
+        if (warp == kW - 1) {  // look back over all earlier chunks
+            int bt = 0, ba = 0;
+            for (int k = lane; k < (int)blockIdx.x; k += 32) {
+                unsigned long long v;
+                do {
+                    v = atomicAdd(part64 + k, 0ull);
+                } while ((v >> 48) != ep);
+                bt += (int)(unsigned)(v & 0xFFFFFFFFull);
+                ba += (int)((v >> 32) & 0xFFFFull);
+            }
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                bt += __shfl_xor_sync(0xffffffffu, bt, off);
+                ba += __shfl_xor_sync(0xffffffffu, ba, off);
+            }
+            if (lane == 0) { s_base[0] = bt; s_base[1] = ba; }
+        }
+    }
     if (MODE == 1 && warp == kW - 1) {  // sum of the earlier chunks' totals (fixed order)
         int bt = 0, ba = 0;
         for (int k = lane; k < (int)blockIdx.x; k += 32) { bt += part[k].x; ba += part[k].y; }
@@ -331,6 +364,16 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
         *sl.nactive = n;
         *sl.base = b0;
         if (li <= cap) sl.bstart[b0 + sl.step + n] = pos;
+    }
+    if (MODE == 2) {  // the last CTA to finish advances the epoch for the next launch
+        __syncthreads();
+        if (tid == 0) {
+            unsigned* ticket = reinterpret_cast<unsigned*>(part64 + gridDim.x + 1);
+            if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+                part64[gridDim.x] = s_epoch;
+                *ticket = 0u;
+            }
+        }
     }
 }
 
@@ -1610,8 +1653,7 @@ int scan_chunks(const KParams& p) { return (p.TB + kScanChunk - 1) / kScanChunk;
 void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
                      cudaStream_t s) {
     const int nc = scan_chunks(p);
-    launch_k(k_bin_scan<0>, nc, kT, 0, s, p, bcount, cursor, sl, (int2*)part, flags);
-    launch_k(k_bin_scan<1>, nc, kT, 0, s, p, bcount, cursor, sl, (int2*)part, flags);
+    launch_k(k_bin_scan<2>, nc, kT, 0, s, p, bcount, cursor, sl, (int2*)part, flags);
 }
 void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
                         cudaStream_t s) {
