@@ -493,6 +493,9 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
 constexpr int kTC = 64;  // thread-per-cell kernels: one thread per cell of a block (CELLS = 64)
 
 // Tuning knobs (overridable with -D for A/B builds, tools/build_variant.py)
+#ifndef MPM_P2GG_NESTED
+#define MPM_P2GG_NESTED 1
+#endif
 #ifndef MPM_P2G_CHUNK
 #define MPM_P2G_CHUNK 576
 #endif
@@ -1334,6 +1337,68 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
     float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f}, Sm[3][3];
 #pragma unroll
     for (int q = 0; q < 9; ++q) (&Sm[0][0])[q] = 0.f;
+    if (D == 3 && MPM_P2GG_NESTED) {
+        // Nested separable form of the 27-node gather below (same sums, re-associated): the
+        // weights factor per axis, W_o = w0 w1 w2 and dW/df = (dw0 w1 w2, w0 dw1 w2, w0 w1 dw2),
+        // so the z sums are formed per (o0, o1), the y sums per o0, then the x sums:
+        //   S0 = sum w0 sum w1 sum w2 g,  Sm[b] = the same with o_b w_b on axis b,
+        //   fb = (sum dw0 sum w1 sum w2 Wb, sum w0 sum dw1 sum w2 Wb, sum w0 sum w1 sum dw2 Wb)
+        // with Wb_o = g_o . (c + Adx o) + m Mb_o per node.  ~30% fewer FP operations.
+        float fx0 = 0.f, fx1 = 0.f, fx2 = 0.f;
+#pragma unroll
+        for (int o0 = 0; o0 < 3; ++o0) {
+            float Gy[3] = {0.f, 0.f, 0.f}, Hy[3] = {0.f, 0.f, 0.f}, Ky[3] = {0.f, 0.f, 0.f};
+            float Ay = 0.f, By = 0.f, Cy = 0.f;
+            float mx[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) mx[a] = fmaf((float)o0, Adx[a * D], c[a]);
+#pragma unroll
+            for (int o1 = 0; o1 < 3; ++o1) {
+                float Gz[3] = {0.f, 0.f, 0.f}, Hz[3] = {0.f, 0.f, 0.f}, Az = 0.f, Bz = 0.f;
+                float my[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) my[a] = fmaf((float)o1, Adx[a * D + 1], mx[a]);
+#pragma unroll
+                for (int o2 = 0; o2 < 3; ++o2) {
+                    const float4 g4 = sG[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
+                    const float g[3] = {g4.x, g4.y, g4.z};
+                    float Wb = g4.w * p.p_mass;
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) Wb = fmaf(g[a], fmaf((float)o2, Adx[a * D + 2], my[a]), Wb);
+                    const float w2 = w[2][o2];
+#pragma unroll
+                    for (int a = 0; a < 3; ++a) {
+                        Gz[a] = fmaf(w2, g[a], Gz[a]);
+                        if (o2) Hz[a] = fmaf((float)o2 * w2, g[a], Hz[a]);
+                    }
+                    Az = fmaf(w2, Wb, Az);
+                    Bz = fmaf(dw[2][o2], Wb, Bz);
+                }
+                const float w1 = w[1][o1];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    Gy[a] = fmaf(w1, Gz[a], Gy[a]);
+                    Hy[a] = fmaf(w1, Hz[a], Hy[a]);
+                    if (o1) Ky[a] = fmaf((float)o1 * w1, Gz[a], Ky[a]);
+                }
+                Ay = fmaf(w1, Az, Ay);
+                By = fmaf(dw[1][o1], Az, By);
+                Cy = fmaf(w1, Bz, Cy);
+            }
+            const float w0 = w[0][o0];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                S0[a] = fmaf(w0, Gy[a], S0[a]);
+                Sm[2][a] = fmaf(w0, Hy[a], Sm[2][a]);
+                Sm[1][a] = fmaf(w0, Ky[a], Sm[1][a]);
+                if (o0) Sm[0][a] = fmaf((float)o0 * w0, Gy[a], Sm[0][a]);
+            }
+            fx0 = fmaf(dw[0][o0], Ay, fx0);
+            fx1 = fmaf(w0, By, fx1);
+            fx2 = fmaf(w0, Cy, fx2);
+        }
+        fb[0] = fx0; fb[1] = fx1; fb[2] = fx2;
+    } else
 #pragma unroll
     for (int o0 = 0; o0 < 3; ++o0) {
         float mx[3];
