@@ -243,17 +243,15 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
 
 // Exclusive scan of the dense block histogram -> active block list (block-id order),
 // starts, block map, scatter cursors; clears the histogram.  One launch over chunks of
-// 256 x 4 entries (MODE 2): every CTA publishes its chunk totals tagged with the launch's
+// 256 x 4 entries: every CTA publishes its chunk totals tagged with the launch's
 // epoch, then sums the totals of all earlier chunks (look-back; integer sums, so the order
 // does not matter) -- all chunk CTAs are co-resident (<= 32 at 128^3, 256 for 64 episodes
-// at 64^3).  The last CTA (ticket) advances the epoch.  (MODE 0 + MODE 1: the two-launch
-// variant, kept for reference.)
+// at 64^3).  The last CTA (ticket) advances the epoch.
 #ifndef MPM_SCAN_PER
 #define MPM_SCAN_PER 4
 #endif
 constexpr int kScanPer = MPM_SCAN_PER;
 constexpr int kScanChunk = kT * kScanPer;
-template <int MODE>
 __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bcount, int* __restrict__ cursor,
                                                 SlotView sl, int2* __restrict__ part, int* flags) {
     pdl_begin();
@@ -262,7 +260,7 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
     __shared__ unsigned s_epoch;
     unsigned long long* part64 = reinterpret_cast<unsigned long long*>(part);
     const int TB = p.TB, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (MODE == 2 && tid == 0) s_epoch = ((unsigned)part64[gridDim.x] + 1u) & 0xFFFFu;
+    if (tid == 0) s_epoch = ((unsigned)part64[gridDim.x] + 1u) & 0xFFFFu;
     const int i0 = blockIdx.x * kScanChunk + tid * kScanPer;
     int c[kScanPer];
     if (i0 + kScanPer <= TB) {
@@ -285,7 +283,7 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
         if (lane >= off) { it += a; ia += b; }
     }
     if (lane == 31) { s_wt[warp] = it; s_wa[warp] = ia; }
-    if (MODE == 2) {
+    {
         __syncthreads();
         const unsigned long long ep = s_epoch;
         if (tid == 0) {  // publish this chunk's totals, tagged with the epoch
@@ -312,25 +310,7 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
             if (lane == 0) { s_base[0] = bt; s_base[1] = ba; }
         }
     }
-    if (MODE == 1 && warp == kW - 1) {  // sum of the earlier chunks' totals (fixed order)
-        int bt = 0, ba = 0;
-        for (int k = lane; k < (int)blockIdx.x; k += 32) { bt += part[k].x; ba += part[k].y; }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            bt += __shfl_xor_sync(0xffffffffu, bt, off);
-            ba += __shfl_xor_sync(0xffffffffu, ba, off);
-        }
-        if (lane == 0) { s_base[0] = bt; s_base[1] = ba; }
-    }
     __syncthreads();
-    if (MODE == 0) {
-        if (tid == 0) {
-            int bt = 0, ba = 0;
-            for (int w = 0; w < kW; ++w) { bt += s_wt[w]; ba += s_wa[w]; }
-            part[blockIdx.x] = make_int2(bt, ba);
-        }
-        return;
-    }
     // pool offset of this step: right after the previous step's blocks
     const int b0 = sl.step > 0 ? sl.base[-1] + sl.nactive[-1] : 0;
     int pos = s_base[0] + it - tot, li = s_base[1] + ia - act;
@@ -365,7 +345,7 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
         *sl.base = b0;
         if (li <= cap) sl.bstart[b0 + sl.step + n] = pos;
     }
-    if (MODE == 2) {  // the last CTA to finish advances the epoch for the next launch
+    {  // the last CTA to finish advances the epoch for the next launch
         __syncthreads();
         if (tid == 0) {
             unsigned* ticket = reinterpret_cast<unsigned*>(part64 + gridDim.x + 1);
@@ -418,53 +398,6 @@ __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __rest
 }
 
 // ----------------------------------------------------- cell accumulation
-// A thread owns one cell and sums, over the cell's particles (canonical order), the
-// contributions W_o (c + A o) (and W_o when MASS) to the 3^d nodes cell + o, in
-// registers: separable weights W_o = wx[ox] wy[oy] wz[oz] and an incremental
-// m = c + A o.  (p2g: c = m v - A dx f, A = A dx;  g2p_grad: c = vh - B f, A = B.)
-template <int D, bool MASS> struct NodeAcc {
-    static constexpr int NN = Geo<D>::NST;
-    float4 a[NN];  // o = (ox*3 + oy)*3 + oz (3D) / ox*3 + oy (2D)
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int k = 0; k < NN; ++k) a[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    __device__ __forceinline__ void add(const float w[3][3], const float* c, const float* A) {
-#pragma unroll
-        for (int ox = 0; ox < 3; ++ox) {
-            float mx[3];
-#pragma unroll
-            for (int q = 0; q < D; ++q) mx[q] = fmaf((float)ox, A[q * D], c[q]);
-#pragma unroll
-            for (int oy = 0; oy < 3; ++oy) {
-                const float Wxy = w[0][ox] * w[1][oy];
-                float my[3];
-#pragma unroll
-                for (int q = 0; q < D; ++q) my[q] = fmaf((float)oy, A[q * D + 1], mx[q]);
-#pragma unroll
-                for (int oz = 0; oz < (D == 3 ? 3 : 1); ++oz) {
-                    const float W = D == 3 ? Wxy * w[2][oz] : Wxy;
-                    float4& acc = a[D == 3 ? (ox * 3 + oy) * 3 + oz : ox * 3 + oy];
-                    if (D == 3) {
-                        acc.x = fmaf(W, fmaf((float)oz, A[2], my[0]), acc.x);
-                        acc.y = fmaf(W, fmaf((float)oz, A[5], my[1]), acc.y);
-                        acc.z = fmaf(W, fmaf((float)oz, A[8], my[2]), acc.z);
-                    } else {
-                        acc.x = fmaf(W, my[0], acc.x);
-                        acc.y = fmaf(W, my[1], acc.y);
-                    }
-                    if (MASS) acc.w += W;
-                }
-            }
-        }
-    }
-    __device__ __forceinline__ void store(float4* cellbuf, int cell) const {
-        float4* dst = cellbuf + cell * NN;
-#pragma unroll
-        for (int k = 0; k < NN; ++k) dst[k] = a[k];
-    }
-};
-
 // thread per tile node: sum the (cell, o) partials with cell + o = node (fixed order)
 template <int D>
 __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, int q) {
@@ -489,8 +422,6 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
             }
     return s;
 }
-
-constexpr int kTC = 64;  // thread-per-cell kernels: one thread per cell of a block (CELLS = 64)
 
 // Tuning knobs (overridable with -D for A/B builds, tools/build_variant.py)
 #ifndef MPM_P2GG_NESTED
@@ -1718,7 +1649,7 @@ int scan_chunks(const KParams& p) { return (p.TB + kScanChunk - 1) / kScanChunk;
 void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
                      cudaStream_t s) {
     const int nc = scan_chunks(p);
-    launch_k(k_bin_scan<2>, nc, kT, 0, s, p, bcount, cursor, sl, (int2*)part, flags);
+    launch_k(k_bin_scan, nc, kT, 0, s, p, bcount, cursor, sl, (int2*)part, flags);
 }
 void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
                         cudaStream_t s) {

@@ -42,10 +42,6 @@ template <int D> struct Geo {
     static constexpr int TE = B + 2;                 // tile edge in nodes
     static constexpr int TN = D == 3 ? 216 : 100;    // tile nodes
     static constexpr int NST = D == 3 ? 27 : 9;      // stencil offsets
-    static constexpr int NSUB = D == 3 ? 1 : 3;      // particle sub-streams per cell warp
-    static constexpr int ROW = D == 3 ? 24 : 12;     // floats per particle row (cell phase):
-                                                     // 3D [wy*wz (9), c (3), A dx (9), wx (3)]
-                                                     // 2D [wy (3), c (2), A dx (4), wx (3)]
     static constexpr int MAXP = 1728;                // particles per block (27 per cell)
 };
 
