@@ -63,3 +63,29 @@ def test_robot3d_with_liquid_c3liquid():
     got = gpu_run(p, inp, k_ckpt=32)
     errs, _ = _compare_episode(p, inp, got, grads=("dx0", "dv0", "dtheta"))
     _assert(errs, "c3liquid")
+
+
+def test_clearing_materials_restores_the_solid_run():
+    """mpm_set_materials(NULL) after a fluid run gives the all-solid results bit for bit."""
+    from paper_1910_00935_b200 import mpm
+    p = W.tiny(2, steps=6, hidden=3, seed=21, fluid_every=2)
+    inp = W.make_inputs(p)
+    N = len(inp["x"])
+
+    def run(mat):
+        sim = mpm.sim_from_config(p, N, max_steps=6)
+        sim.set_state(inp["x"][None], inp["v"][None], inp["C"][None], inp["F"][None], inp["aid"][None])
+        sim.set_controller(inp["theta"])
+        if mat is not None:
+            sim.set_materials(mat)
+            sim.set_materials(None)
+        sim.forward(6)
+        sim.loss()
+        sim.backward(6)
+        out = {**sim.get_state(), **sim.grads()}
+        sim.close()
+        return out
+
+    a, b = run(None), run(inp["mat"][None])
+    for k in ("x", "v", "C", "F", "dx0", "dv0", "dC0", "dF0", "dtheta"):
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)

@@ -288,3 +288,22 @@ def test_native_library_is_what_runs():
     p, inp = inputs("c1a", steps=8)
     got = gpu_run(p, inp, steps=8)
     assert got["launches"] >= 8 * 4 + 8 * 2
+
+
+def test_block_particle_overflow_is_an_error():
+    """more than 1728 particles (27 per cell on average) in one 4^3 block: MPM_ERR_UNSUPPORTED,
+    never a silent drop (mpm.h)."""
+    from paper_1910_00935_b200 import mpm
+    p = W.tiny(3, steps=2, n_act=0, hidden=0, bound=1)
+    rng = np.random.default_rng(3)
+    N = 1800
+    x = (0.3125 + 0.25 * rng.random((N, 3))).astype(np.float32)  # base cells 2..3: all in block 0
+    v = np.zeros((N, 3), np.float32)
+    C = np.zeros((N, 3, 3), np.float32)
+    F = np.broadcast_to(np.eye(3, dtype=np.float32), (N, 3, 3)).copy()
+    sim = mpm.sim_from_config(p, N, max_steps=2)
+    sim.set_state(x, v, C, F, None)
+    with pytest.raises(mpm.MpmError) as e:
+        sim.forward(2)
+    assert e.value.status == 7
+    sim.close()
