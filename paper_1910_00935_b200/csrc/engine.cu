@@ -2,12 +2,13 @@
 // segment checkpointing (Appendix D), error reporting and the
 // per-kernel timing hooks.
 //
-// Tape layout: S_t (records + particle ids) lives in the
-// final-state buffer (t = T), a checkpoint slot (t % k == 0) or the k-slot
-// window; each window slot j also holds the binning and the node tiles of the
-// step t with t % k == j, so the backward reuses the grid of every step of the
-// segment in the window without re-running p2g.  Adjoint states are kept in
-// caller (particle-id) order.
+// Tape layout: S_t (split arrays + particle ids) lives in the
+// final-state buffer (t = T), a checkpoint slot (t % k == 0) or the double-buffered
+// k-slot window (half (t / k) & 1); the binning and the resolved node tiles of every
+// step live in the grid store, so the reverse never re-runs p2g and a segment's
+// re-forward is g2p only.  Adjoint states are indexed like the state they belong to.
+// Streams: main; side (g2p_grad's gather part); side2 (segment re-forward), all
+// captured into the forward / backward CUDA graphs.
 #include <algorithm>
 #include <cstdlib>
 #include <functional>

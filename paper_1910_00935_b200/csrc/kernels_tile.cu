@@ -1,11 +1,11 @@
 // kernels_tile.cu -- the MLS-MPM step and its adjoint on sm_100a, sorted-tile scheme.
 //
-// Equations: DESIGN.md R1-R14; kernel order: PAPER.md
+// Equations: DESIGN.md R1-R14, R22-R23; kernel order: PAPER.md
 // Appendix D.1 (advance / advance_grad).
 //
 // Layout:
 //  * particles are binned every step by the B^d block of cells that holds their
-//    base cell (bin_* kernels); p2g puts each block's list sigma in canonical
+//    base cell (bin_* kernels); k_canon puts each block's list sigma in canonical
 //    (cell, particle id) order, so every sum below has a fixed order -> results are
 //    bitwise reproducible run to run, and there are no atomics in the hot loops;
 //  * p2g: one CTA per active block (persistent loop).  Thread per particle: the
@@ -14,9 +14,10 @@
 //    accumulates its 3^(d-1) nodes in registers (separable weights, incremental
 //    m = c + A dx o); a thread per tile node sums the <= 3^d (cell, o) partials and
 //    stores the block's (B+2)^d node tile with plain stores;
-//  * g2p / g2p_grad / p2g_grad stage their node tile in shared memory by summing the
-//    <= 2^d overlapping block tiles (grid_op / grid_op_grad fused into the staging);
-//    g2p uses nested separable sums for v and the first moments that give C;
+//  * grid_op / grid_op_grad resolve every active block's tile once per step (sum of the
+//    <= 2^d overlapping partial tiles, fixed order); g2p, g2p_grad's gather part and
+//    p2g_grad stage their resolved node tile with cp.async.bulk (TMA engine) + mbarrier,
+//    double buffered across blocks; g2p and p2g_grad use nested separable sums;
 //    g2p_grad scatters U_bar with p2g's (cell, o_x) scheme.
 #include "kernels.h"
 
