@@ -937,6 +937,10 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
     return key;
 }
 
+// NOTE: the forward and the segment re-forward MUST run this same compiled kernel (refwd is a
+// runtime flag, not a template parameter): two instantiations may contract the FMAs of the
+// shared math differently, and the re-forwarded S_{t+1} would then differ in the last bit
+// from the forward's (checkpoint invariance is tested bitwise).
 template <int D>
 __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
                                             int* __restrict__ keys, int* __restrict__ bcount, int* flags,
