@@ -268,9 +268,19 @@ __device__ __forceinline__ float kirchhoff_adj(const KParams& p, const float* Fm
     return abar;
 }
 
+// det with every rounding explicit (no FMA contraction left to the compiler): p2g and the
+// re-forward g2p both evaluate the fluid reset, and their F_{t+1} must agree bit for bit
+template <int D> __device__ __forceinline__ float det_rn(const float* F) {
+    if (D == 2) return __fsub_rn(__fmul_rn(F[0], F[3]), __fmul_rn(F[1], F[2]));
+    const float a = __fsub_rn(__fmul_rn(F[4], F[8]), __fmul_rn(F[5], F[7]));
+    const float b = __fsub_rn(__fmul_rn(F[3], F[8]), __fmul_rn(F[5], F[6]));
+    const float c = __fsub_rn(__fmul_rn(F[3], F[7]), __fmul_rn(F[4], F[6]));
+    return __fadd_rn(__fsub_rn(__fmul_rn(F[0], a), __fmul_rn(F[1], b)), __fmul_rn(F[2], c));
+}
+
 // R23 fluid: F_{t+1} = J^(1/d) I with J = det(Ft) (shear forgotten)
 template <int D> __device__ __forceinline__ void fluid_reset(const float* Ft, float* Fn) {
-    const float J = det<D>(Ft);
+    const float J = det_rn<D>(Ft);
     const float s = D == 3 ? cbrtf(J) : sqrtf(J);
 #pragma unroll
     for (int q = 0; q < D * D; ++q) Fn[q] = (q % (D + 1) == 0) ? s : 0.0f;
