@@ -682,6 +682,10 @@ mpm_status mpm_workspace_bytes(mpm_handle h, size_t* bytes) {
 mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     if (!h || !dptr) return MPM_ERR_INVALID_ARG;
     if (((uintptr_t)dptr & 255) != 0) return fail(h, MPM_ERR_INVALID_ARG, "workspace not 256-B aligned");
+    // the one-launch binning scan looks back over co-resident CTAs (kernels_tile.cu): keep its
+    // grid well inside one wave (8 CTAs of 256 threads per SM)
+    if (scan_chunks(kparams(h)) > 1024)
+        return fail(h, MPM_ERR_UNSUPPORTED, "more than 1M grid blocks (episodes x blocks per episode) per handle");
     const size_t need = carve(h, nullptr);
     if (bytes < need)
         return fail(h, MPM_ERR_OOM, "workspace too small: need " + std::to_string(need) + " bytes");
