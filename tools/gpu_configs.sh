@@ -2,7 +2,7 @@
 cd "$(dirname "$0")/.."; mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3 > gpurun_out/opt_gpu.txt
 cat gpurun_out/opt_gpu.txt
-for c in c2 c2cl c3 c3cl c4 c1a; do
+for c in c2 c2cl c3 c3cl c3liquid c4 c1a; do
   timeout 600 python bench.py --config $c --steps 5 --warmup 3 > gpurun_out/bench_$c.json 2> gpurun_out/bench_$c.err
   python -c "
 import json,sys; d=json.load(open('gpurun_out/bench_$c.json')); r=d['roofline']
