@@ -55,6 +55,8 @@ def _workload(name: str, world: int, rank: int = 0):
     from paper_1910_00935_b200 import workloads as W
     from paper_1910_00935_b200.dist import episode_shard
     p = W.config(name)
+    if os.environ.get("BENCH_HORIZON"):  # experiments only (e.g. k = 1 vs 2 at a horizon where k = 1 fits)
+        p["steps"] = int(os.environ["BENCH_HORIZON"])
     if name == "c4":
         return p, episode_shard(int(p["episodes"]), rank, world), "strong"
     return p, range(rank, rank + 1), "weak"
