@@ -80,3 +80,19 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 bad = re.findall(r"(?:^|\n)\s*(?:import oracle|from oracle|#include[^\n]*oracle)|oracle_mpm|liboracle", txt)
                 assert not bad, (f, bad)
+
+
+def test_invalid_create_arguments_fail_before_any_device_call(lib):
+    """mpm_create validates its arguments on the host (no GPU needed): no particles, a grid
+    too small for the 3^d stencil, an unsupported dimension, a non-positive dt or E, or a
+    Poisson ratio outside (-1, 1/2) (lambda would be infinite or negative) -> MPM_ERR_INVALID_ARG."""
+    h = ct.c_void_p()
+    cases = [(0, 64, 3, 1e-3, 25.0, 0.25), (100, 2, 3, 1e-3, 25.0, 0.25), (100, 64, 4, 1e-3, 25.0, 0.25),
+             (100, 64, 3, 0.0, 25.0, 0.25), (100, 64, 3, 1e-3, -1.0, 0.25), (100, 64, 3, 1e-3, 25.0, 0.5),
+             (100, 64, 2, 1e-3, 25.0, -1.0), (1 << 31, 64, 3, 1e-3, 25.0, 0.25)]
+    for args in cases:
+        st = lib.mpm_create(*args, ct.byref(h))
+        assert st == 1, (args, st)
+        assert not h.value
+    assert lib.mpm_create(100, 64, 3, 1e-3, 25.0, 0.25, None) == 1
+    assert lib.mpm_destroy(None) == 1
