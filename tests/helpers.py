@@ -48,7 +48,8 @@ def oracle_run(p, inp, steps=None, precision="f64"):
     if inp.get("mat") is not None and np.any(inp["mat"]):
         o.set_materials(inp["mat"])
     return o.run(inp["x"], inp["v"], inp["C"], inp["F"], inp["aid"], inp["theta"],
-                 steps=steps or p["steps"], k_ckpt=1 if (steps or p["steps"]) <= 256 else 16)
+                 steps=steps or p["steps"],
+                 k_ckpt=1 if (steps or p["steps"]) * len(inp["x"]) <= 5_000_000 else 16)
 
 
 def oracle_tape(p, inp, T, lam):
