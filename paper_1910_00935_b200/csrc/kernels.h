@@ -11,7 +11,7 @@ namespace mpm {
 
 // every kernel launch of the library: programmatic stream serialization (PDL) allowed, so the
 // kernel may be scheduled while its predecessor drains (each kernel starts with pdl_begin()).
-extern bool g_pdl;
+bool pdl_enabled();  // programmatic dependent launch for this host thread's launches
 void set_pdl(int64_t particles);  // choose PDL for the next launches (see kernels_tile.cu)
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
@@ -23,7 +23,7 @@ inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);

@@ -22,6 +22,7 @@
 #include "kernels.h"
 
 #include <cstdlib>
+#include <mutex>
 
 namespace mpm {
 
@@ -1577,7 +1578,8 @@ static int occupancy_grid(const void* fn, int smem, int threads = kT) {
 // (C1-C3: +4% measured on C2) and costs where big persistent kernels share the SMs with the
 // backward's side streams (waiting dependent CTAs hold SM slots: -12% on C5).  The engine
 // enables it per call for small problems (set_pdl); MPM_B200_PDL=0/1 forces it.
-bool g_pdl = false;
+static thread_local bool g_pdl = false;  // per host thread: handles on different threads stay independent
+bool pdl_enabled() { return g_pdl; }
 static int g_pdl_force = -1;
 
 void set_pdl(int64_t particles) {
@@ -1588,15 +1590,17 @@ void set_pdl(int64_t particles) {
     g_pdl = g_pdl_force == 2 ? particles <= 262144 : g_pdl_force == 1;
 }
 
+// Kernel attributes are per device: initialise once for every device a handle is created
+// on (one process may drive several GPUs).  The launch grids assume identical GPUs.
 cudaError_t tile_init() {
-    static bool done = false;
-    if (done) return cudaSuccess;
-    cudaError_t e = cudaSuccess;
-    {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    static std::mutex mu;
+    static unsigned long long done_mask = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e) return e;
+    if (dev < 64 && (done_mask >> dev) & 1ull) return cudaSuccess;
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaFuncSetAttribute(k_canon, cudaFuncAttributeMaxDynamicSharedMemorySize, canon_smem_bytes());
     if (e) return e;
     g_canon_grid = occupancy_grid((const void*)k_canon, canon_smem_bytes(), kT);
@@ -1630,7 +1634,7 @@ cudaError_t tile_init() {
         g_grid[3][1] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
         g_grid[4][1] = occupancy_grid((const void*)k_g2p_grad_gather<DIM>, 0, kTG);
     });
-    done = true;
+    if (dev < 64) done_mask |= 1ull << dev;
     return cudaGetLastError();
 }
 
