@@ -211,12 +211,19 @@ def run_reference(args):
     return 0
 
 
-def _pick_k(p, N, per, T, dev):
+def _pick_k(p, N, per, T, dev, world=1):
     """Smallest checkpoint interval whose tape fits in 90% of free HBM (Appendix D.2:
-    k trades re-forward work for memory; on a 180 GB B200 the 1M-particle cube fits k = 2)."""
+    k trades re-forward work for memory; on a 180 GB B200 the 1M-particle cube fits k = 2).
+    Under torchrun every rank must run the same k (the same re-forward work): the ranks agree
+    on the MIN of their free memory, and the largest shard sizes the workspace."""
     import torch
     from paper_1910_00935_b200 import mpm
     free, _ = torch.cuda.mem_get_info(dev)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([float(free), -float(per)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        free, per = int(t[0].item()), int(-t[1].item())
     for k in (1, 2, 4, 8, 16, 32, 64, 128):
         if k > T:
             break
@@ -261,7 +268,7 @@ def run_ours(args):
     host["theta"] = torch.from_numpy(inps[0]["theta"]).pin_memory()
     devin = {key: t.to(dev) for key, t in host.items()}
 
-    k = int(args.k_ckpt) if args.k_ckpt else _pick_k(p, N, per, T, dev)
+    k = int(args.k_ckpt) if args.k_ckpt else _pick_k(p, N, per, T, dev, world)
     sim = mpm.sim_from_config(p, N, episodes=per, max_steps=T, k_ckpt=k)
     if any(np.any(i["mat"]) for i in inps):  # fluid particles (R23): a property of the workload
         sim.set_materials(cat("mat"))
@@ -317,16 +324,13 @@ def run_ours(args):
 
     for _ in range(args.warmup):
         dev_step()
-    # active grid nodes (A) for the algorithmic byte count: after a forward, the
-    # grid holds step T-1's; after the backward, step 0's -- use their mean
+    # active grid nodes (A) for the algorithmic byte count: the grid store keeps every recorded
+    # step's node tiles, so A is averaged over 9 steps spread over the horizon
     sim.set_state(devin["x"], devin["v"], devin["C"], devin["F"], devin["aid"])
     sim.set_controller(devin["theta"])
     sim.forward(T)
-    A_end = sim.active_nodes()
-    sim.loss(loss_d)
-    sim.backward(T)
-    A_start = sim.active_nodes()
-    A = 0.5 * (A_end + A_start) / per
+    a_steps = sorted({min(T - 1, (T - 1) * j // 8) for j in range(9)})
+    A = float(np.mean([sim.active_nodes(t) for t in a_steps])) / per
 
     # timed region (CUDA graphs replayed; no per-kernel events so nothing perturbs it)
     l0 = sim.launch_count()

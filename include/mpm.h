@@ -19,7 +19,8 @@
  *     mpm_last_error(h) holds a one-line message.  Out-of-bounds is a hard
  *     error, never a silent wrap or clamp; non-finite results are errors.
  *   - Opaque handle; calls on one handle are NOT thread-safe; separate handles
- *     are independent.
+ *     are independent.  A handle belongs to the device current at mpm_create;
+ *     every entry point makes that device current and restores the caller's.
  *   - Memory: the library never allocates device memory.  The caller (PyTorch)
  *     allocates one workspace of mpm_workspace_bytes() and binds it; every
  *     library buffer (states, checkpoints, grids, adjoints) lives inside it.
@@ -126,8 +127,11 @@ mpm_status mpm_workspace_bytes(mpm_handle h, size_t* bytes);
 mpm_status mpm_bind_workspace(mpm_handle h, void* device_ptr, size_t bytes);
 
 /* Copy in the initial state S_0 (host or device pointers, layouts above).
- * actuator_id may be NULL (all passive).  Values are validated on the next
- * mpm_forward (out-of-domain -> MPM_ERR_OUT_OF_DOMAIN). Clears any tape. */
+ * actuator_id may be NULL (all passive); ids must be -1 (passive) or in [0, n_actuators).
+ * Values are validated on the device and reported by the next mpm_forward
+ * (out-of-domain -> MPM_ERR_OUT_OF_DOMAIN, an actuator id out of range ->
+ * MPM_ERR_INVALID_ARG; the kernels treat such ids as passive, never index with them).
+ * Clears any tape. */
 mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const float* C,
                          const float* F, const int32_t* actuator_id);
 
@@ -188,8 +192,11 @@ mpm_status mpm_set_profiling(mpm_handle h, int32_t enable);
 mpm_status mpm_reset_kernel_stats(mpm_handle h);
 mpm_status mpm_kernel_stats(mpm_handle h, int32_t idx, const char** name, double* total_ms,
                             int64_t* count);
-/* Grid nodes with M > 0 in the grid of the last executed step, summed over episodes
- * (the "active nodes" A of the algorithmic byte count). Synchronises. */
+/* Grid nodes with M > 0 in the grid of step `step` of the recorded forward (0 <= step <
+ * recorded, else MPM_ERR_INVALID_ARG), summed over episodes: the "active nodes" A of the
+ * algorithmic byte count.  mpm_active_nodes = the last recorded step.
+ * Synchronises. */
+mpm_status mpm_active_nodes_at(mpm_handle h, int32_t step, int64_t* count);
 mpm_status mpm_active_nodes(mpm_handle h, int64_t* count);
 
 #ifdef __cplusplus

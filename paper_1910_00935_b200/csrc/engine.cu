@@ -135,6 +135,20 @@ struct mpm_ctx {
 
 namespace {
 
+// Makes the handle's device current for the duration of an entry point (one process may
+// drive several GPUs, each through its own handles) and restores the caller's device.
+struct DevGuard {
+    int prev = -1;
+    bool changed = false;
+    explicit DevGuard(const mpm_ctx* h) {
+        if (!h || cudaGetDevice(&prev) != cudaSuccess) return;
+        if (prev != h->device) changed = cudaSetDevice(h->device) == cudaSuccess;
+    }
+    ~DevGuard() {
+        if (changed) cudaSetDevice(prev);
+    }
+};
+
 mpm_status fail(mpm_handle h, mpm_status st, const std::string& msg) {
     if (h) h->err = msg;
     return st;
@@ -409,6 +423,8 @@ mpm_status sync_flags(mpm_handle h, const char* where) {
     if (f) {
         CU(cudaMemsetAsync(h->flags, 0, sizeof(int), h->stream));
         CU(cudaStreamSynchronize(h->stream));
+        if (f & FLAG_BAD_ACTUATOR)
+            return fail(h, MPM_ERR_INVALID_ARG, std::string(where) + ": actuator id outside [-1, n_actuators)");
         if (f & FLAG_ACTIVE_OVERFLOW)
             return fail(h, MPM_ERR_OOM, std::string(where) + ": active blocks exceed max_active_blocks (" +
                                             std::to_string(h->max_active) + ")");
@@ -446,7 +462,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     if (k.closed_loop) {  // R22: alpha_t from the observation of S_t
         KScope sc(h, KC_CTRL);
         h->launches += 1;
-        launch_observe(k, S.x, S.vc, S.pid, h->aid, h->obs_part, h->stream);
+        launch_observe(k, S.x, S.vc, S.pid, aid, h->obs_part, h->stream);
         const size_t no = (size_t)2 * k.dim * k.n_act;
         launch_ctrl_obs_fwd(k, h->theta, t, h->obs_part, h->obs + (size_t)t * k.E * no, h->obs_cnt,
                             const_cast<float*>(alpha_at(h, t)), h->stream);
@@ -511,7 +527,7 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
         launch_ctrl_obs_bwd(k, h->theta, t, h->obs + (size_t)t * k.E * no, alpha_at(h, t),
                             h->alpha_bar + (size_t)t * A * k.E, h->obs_cnt, h->theta_bar, h->obs_inc,
                             h->stream);
-        launch_observe_adj(k, Sb, S.pid, h->aid, h->obs_inc, h->stream);
+        launch_observe_adj(k, Sb, S.pid, h->has_aid ? h->aid : nullptr, h->obs_inc, h->stream);
     }
 }
 
@@ -614,6 +630,7 @@ mpm_status mpm_create(int64_t n_particles, int32_t n_grid, int32_t dim, float dt
 
 mpm_status mpm_destroy(mpm_handle h) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->h_flags) cudaFreeHost(h->h_flags);
     for (auto ev : h->prof.pool) cudaEventDestroy(ev);
     for (auto& g : h->graphs) cudaGraphExecDestroy(g.second.exec);
@@ -661,6 +678,7 @@ mpm_status mpm_set_params(mpm_handle h, const mpm_params* p) {
 
 mpm_status mpm_set_stream(mpm_handle h, void* s) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     h->stream = (cudaStream_t)s;
     if (!h->side) {  // the side stream of the backward's parallel branch (see step_backward)
         CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
@@ -675,17 +693,15 @@ mpm_status mpm_set_stream(mpm_handle h, void* s) {
 
 mpm_status mpm_workspace_bytes(mpm_handle h, size_t* bytes) {
     if (!h || !bytes) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     *bytes = carve(h, nullptr);
     return MPM_OK;
 }
 
 mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     if (!h || !dptr) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (((uintptr_t)dptr & 255) != 0) return fail(h, MPM_ERR_INVALID_ARG, "workspace not 256-B aligned");
-    // the one-launch binning scan looks back over co-resident CTAs (kernels_tile.cu): keep its
-    // grid well inside one wave (8 CTAs of 256 threads per SM)
-    if (scan_chunks(kparams(h)) > 1024)
-        return fail(h, MPM_ERR_UNSUPPORTED, "more than 1M grid blocks (episodes x blocks per episode) per handle");
     const size_t need = carve(h, nullptr);
     if (bytes < need)
         return fail(h, MPM_ERR_OOM, "workspace too small: need " + std::to_string(need) + " bytes");
@@ -704,6 +720,7 @@ mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
 mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const float* C,
                          const float* F, const int32_t* actuator_id) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase < kBound) return fail(h, MPM_ERR_BAD_SEQUENCE, "set_state before bind_workspace");
     if (!x) return fail(h, MPM_ERR_INVALID_ARG, "x is required");
     const KParams k = kparams(h);
@@ -722,6 +739,10 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
                   h->ckpt[0].vc, h->ckpt[0].f, h->ckpt[0].pid, false, h->stream); }
     h->has_aid = actuator_id != nullptr && h->prm.n_actuators > 0;  // ids are meaningless without actuators
     if (h->has_aid && (st = copy_in(h, h->aid, actuator_id, sizeof(int32_t) * EN))) return st;
+    if (h->has_aid) {  // ids outside [-1, n_actuators): MPM_ERR_INVALID_ARG at the next mpm_forward
+        KScope sc(h, KC_LAYOUT);
+        launch_check_aid(k, h->aid, h->flags, h->stream);
+    }
     CU(cudaGetLastError());
     h->phase = kHasState;
     h->recorded = 0;
@@ -732,6 +753,7 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
 
 mpm_status mpm_set_materials(mpm_handle h, const int32_t* material) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase < kBound) return fail(h, MPM_ERR_BAD_SEQUENCE, "set_materials before bind_workspace");
     const KParams k = kparams(h);
     const size_t EN = (size_t)k.E * k.N;
@@ -754,6 +776,7 @@ mpm_status mpm_n_theta(mpm_handle h, int64_t* n) {
 
 mpm_status mpm_set_controller(mpm_handle h, const float* theta, int64_t n) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase < kBound) return fail(h, MPM_ERR_BAD_SEQUENCE, "set_controller before bind_workspace");
     if (n != n_theta_of(h->prm, h->dim) || (n > 0 && !theta))
         return fail(h, MPM_ERR_INVALID_ARG, "n_theta mismatch: expected " + std::to_string(n_theta_of(h->prm, h->dim)));
@@ -763,6 +786,7 @@ mpm_status mpm_set_controller(mpm_handle h, const float* theta, int64_t n) {
 
 mpm_status mpm_forward(mpm_handle h, int32_t steps) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase < kHasState) return fail(h, MPM_ERR_BAD_SEQUENCE, "forward before set_state");
     if (steps < 1 || steps > h->prm.max_steps)
         return fail(h, MPM_ERR_INVALID_ARG, "steps must be in [1, max_steps]");
@@ -789,6 +813,7 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
 
 mpm_status mpm_loss(mpm_handle h, float* loss_out) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase < kForward) return fail(h, MPM_ERR_BAD_SEQUENCE, "loss before forward");
     const KParams k = kparams(h);
     const float3 tgt = make_float3(h->prm.loss_target[0], h->prm.loss_target[1], h->prm.loss_target[2]);
@@ -807,6 +832,7 @@ mpm_status mpm_loss(mpm_handle h, float* loss_out) {
 mpm_status mpm_seed_adjoint(mpm_handle h, const float* dx, const float* dv, const float* dC,
                             const float* dF) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase < kForward) return fail(h, MPM_ERR_BAD_SEQUENCE, "seed_adjoint before forward");
     const KParams k = kparams(h);
     const size_t EN = (size_t)k.E * k.N, d = (size_t)h->dim;
@@ -832,6 +858,7 @@ mpm_status mpm_seed_adjoint(mpm_handle h, const float* dx, const float* dv, cons
 
 mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase != kSeeded) return fail(h, MPM_ERR_BAD_SEQUENCE, "backward needs forward + loss/seed_adjoint");
     if (steps != h->recorded)
         return fail(h, MPM_ERR_BAD_SEQUENCE, "backward steps != recorded forward steps");
@@ -892,6 +919,7 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
 
 mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF0, float* dtheta) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase != kBackward) return fail(h, MPM_ERR_BAD_SEQUENCE, "grads before backward");
     const KParams k = kparams(h);
     const size_t EN = (size_t)k.E * k.N, d = (size_t)h->dim;
@@ -920,6 +948,7 @@ mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF
 
 mpm_status mpm_grad_v0_sum(mpm_handle h, float* out) {
     if (!h || !out) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase != kBackward) return fail(h, MPM_ERR_BAD_SEQUENCE, "grad_v0_sum before backward");
     const KParams k = kparams(h);
     float* res = h->com_part + (size_t)k.E * (loss_blocks_per_episode(k) + 1) * 3;
@@ -934,6 +963,7 @@ mpm_status mpm_grad_v0_sum(mpm_handle h, float* out) {
 
 mpm_status mpm_get_state(mpm_handle h, float* x, float* v, float* C, float* F) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (h->phase < kHasState) return fail(h, MPM_ERR_BAD_SEQUENCE, "get_state before set_state");
     const KParams k = kparams(h);
     const size_t EN = (size_t)k.E * k.N, d = (size_t)h->dim;
@@ -954,6 +984,7 @@ mpm_status mpm_get_state(mpm_handle h, float* x, float* v, float* C, float* F) {
 
 mpm_status mpm_set_profiling(mpm_handle h, int32_t enable) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     if (enable && h->prof.pool.empty()) {
         h->prof.pool.resize(2 * 65536);
         for (auto& ev : h->prof.pool) CU(cudaEventCreate(&ev));
@@ -968,6 +999,7 @@ mpm_status mpm_set_profiling(mpm_handle h, int32_t enable) {
 
 mpm_status mpm_reset_kernel_stats(mpm_handle h) {
     if (!h) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     CU(cudaStreamSynchronize(h->stream));
     prof_harvest(h);
     for (int c = 0; c < KC_N; ++c) { h->prof.ms[c] = 0; h->prof.n[c] = 0; }
@@ -977,6 +1009,7 @@ mpm_status mpm_reset_kernel_stats(mpm_handle h) {
 mpm_status mpm_kernel_stats(mpm_handle h, int32_t idx, const char** name, double* total_ms,
                             int64_t* count) {
     if (!h || idx < 0 || idx >= KC_N) return MPM_ERR_INVALID_ARG;
+    DevGuard dg(h);
     CU(cudaStreamSynchronize(h->stream));
     prof_harvest(h);
     if (name) *name = kClassNames[idx];
@@ -985,18 +1018,25 @@ mpm_status mpm_kernel_stats(mpm_handle h, int32_t idx, const char** name, double
     return MPM_OK;
 }
 
-mpm_status mpm_active_nodes(mpm_handle h, int64_t* count) {
+mpm_status mpm_active_nodes_at(mpm_handle h, int32_t step, int64_t* count) {
     if (!h || !count) return MPM_ERR_INVALID_ARG;
-    if (h->phase < kForward || h->window_seg < 0)
-        return fail(h, MPM_ERR_BAD_SEQUENCE, "active_nodes before forward");
+    DevGuard dg(h);
+    if (h->phase < kForward) return fail(h, MPM_ERR_BAD_SEQUENCE, "active_nodes before forward");
+    if (step < 0 || step >= h->recorded) return fail(h, MPM_ERR_INVALID_ARG, "step outside the recorded forward");
     const KParams k = kparams(h);
-    // a step whose grid tiles are in the window: the last step of the window segment
-    { KScope sc(h, KC_LAYOUT); launch_count_active(k, slot_at(h, h->recorded - 1), h->counter, h->stream); }
+    // the grid store keeps the binning and resolved node tiles of every recorded step
+    { KScope sc(h, KC_LAYOUT); launch_count_active(k, slot_at(h, step), h->counter, h->stream); }
     int64_t c = 0;
     CU(cudaMemcpyAsync(&c, h->counter, sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream));
     CU(cudaStreamSynchronize(h->stream));
     *count = c;
     return MPM_OK;
+}
+
+mpm_status mpm_active_nodes(mpm_handle h, int64_t* count) {
+    if (!h || !count) return MPM_ERR_INVALID_ARG;
+    if (h->phase < kForward) return fail(h, MPM_ERR_BAD_SEQUENCE, "active_nodes before forward");
+    return mpm_active_nodes_at(h, h->recorded - 1, count);
 }
 
 mpm_status mpm_launch_count(mpm_handle h, int64_t* count) {

@@ -109,6 +109,9 @@ void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_
 // ---- measurement: distinct grid nodes with M > 0 in a slot's tiles -> *count (device)
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s);
 
+// actuator ids outside [-1, n_act) -> FLAG_BAD_ACTUATOR
+void launch_check_aid(const KParams& p, const int32_t* aid, int* flags, cudaStream_t s);
+
 // ---- closed-loop controller (R22)
 int obs_parts(const KParams& p);   // per-CTA partials of one observation: [E][chunks]
 int obs_values(const KParams& p);  // values per partial: n_act (2d + 1) + d

@@ -300,7 +300,8 @@ __global__ void k_observe_adj(KParams p, AdjView Sb, const int* __restrict__ pid
     if (i >= p.EN) return;
     const int e = (int)(i / p.N), no = 2 * D * p.n_act;
     const float* ie = inc + (int64_t)e * (no + D);
-    const int a = aid ? aid[pid[i]] : -1;
+    int a = aid ? aid[pid[i]] : -1;
+    if (a >= p.n_act) a = -1;  // out-of-range ids: flagged by mpm_set_state, no gradient here
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         const float gx = ie[no + k] + (a >= 0 ? ie[a * 2 * D + k] : 0.0f);
@@ -449,6 +450,16 @@ __global__ void k_unpack(KParams p, const float* __restrict__ sx, const float* _
     }
 }
 
+// actuator ids must be -1 (passive) or in [0, n_act): anything else raises FLAG_BAD_ACTUATOR,
+// reported as MPM_ERR_INVALID_ARG by the next synchronising call
+__global__ void k_check_aid(int64_t n, int n_act, const int32_t* __restrict__ aid, int* flags) {
+    pdl_begin();
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int a = aid[i];
+    if (a < -1 || a >= n_act) atomicOr(flags, FLAG_BAD_ACTUATOR);
+}
+
 inline unsigned nblk(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -475,6 +486,10 @@ void launch_ctrl_bwd(const KParams& p, const float* theta, int32_t T, const floa
     launch_k(k_ctrl_reduce, nblk(n_theta, 128), 128, 0, s, theta_part, T, n_theta, theta_bar);
 }
 
+
+void launch_check_aid(const KParams& p, const int32_t* aid, int* flags, cudaStream_t s) {
+    launch_k(k_check_aid, nblk(p.EN, 256), 256, 0, s, p.EN, p.n_act, aid, flags);
+}
 
 int obs_parts(const KParams& p) { return p.E * (int)((p.N + kObsThreads - 1) / kObsThreads); }
 int obs_values(const KParams& p) { return obs_nvals(p.n_act, p.dim); }

@@ -245,10 +245,13 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
 
 // Exclusive scan of the dense block histogram -> active block list (block-id order),
 // starts, block map, scatter cursors; clears the histogram.  One launch over chunks of
-// 256 x 4 entries: every CTA publishes its chunk totals tagged with the launch's
-// epoch, then sums the totals of all earlier chunks (look-back; integer sums, so the order
-// does not matter) -- all chunk CTAs are co-resident (<= 32 at 128^3, 256 for 64 episodes
-// at 64^3).  The last CTA (ticket) advances the epoch.
+// 256 x 4 entries (single-pass scan with decoupled look-back): a CTA takes its chunk index
+// from an atomic ticket when it starts, publishes its chunk totals tagged with the launch's
+// epoch, then sums the totals of all earlier chunks (integer sums, so the order does not
+// matter).  Earlier chunks belong to CTAs that started earlier and never wait on later
+// ones, so the look-back makes progress whatever the CTA dispatch order or co-residency
+// (MPS, concurrent kernels).  The last CTA to finish (second ticket) resets the chunk ticket
+// and advances the epoch for the next launch.
 #ifndef MPM_SCAN_PER
 #define MPM_SCAN_PER 4
 #endif
@@ -260,10 +263,18 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
     __shared__ int s_wt[kW], s_wa[kW];
     __shared__ int s_base[2];
     __shared__ unsigned s_epoch;
+    __shared__ int s_chunk;
     unsigned long long* part64 = reinterpret_cast<unsigned long long*>(part);
+    // tickets: [0] CTAs finished, [1] chunk indices handed out
+    unsigned* ticket = reinterpret_cast<unsigned*>(part64 + gridDim.x + 1);
     const int TB = p.TB, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_epoch = ((unsigned)part64[gridDim.x] + 1u) & 0xFFFFu;
-    const int i0 = blockIdx.x * kScanChunk + tid * kScanPer;
+    if (tid == 0) {
+        s_epoch = ((unsigned)part64[gridDim.x] + 1u) & 0xFFFFu;
+        s_chunk = (int)atomicAdd(ticket + 1, 1u);
+    }
+    __syncthreads();
+    const int chunk = s_chunk;
+    const int i0 = chunk * kScanChunk + tid * kScanPer;
     int c[kScanPer];
     if (i0 + kScanPer <= TB) {
 #pragma unroll
@@ -292,11 +303,11 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
             unsigned bt = 0, ba = 0;
             for (int w = 0; w < kW; ++w) { bt += (unsigned)s_wt[w]; ba += (unsigned)s_wa[w]; }
             const unsigned long long v = (ep << 48) | ((unsigned long long)(ba & 0xFFFFu) << 32) | bt;
-            atomicExch(part64 + blockIdx.x, v);
+            atomicExch(part64 + chunk, v);
         }
         if (warp == kW - 1) {  // look back over all earlier chunks
             int bt = 0, ba = 0;
-            for (int k = lane; k < (int)blockIdx.x; k += 32) {
+            for (int k = lane; k < chunk; k += 32) {
                 unsigned long long v;
                 do {
                     v = atomicAdd(part64 + k, 0ull);
@@ -341,7 +352,7 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
             sl.bmap[b] = -1;
         }
     }
-    if (blockIdx.x == gridDim.x - 1 && tid == kT - 1) {  // grand totals
+    if (chunk == (int)gridDim.x - 1 && tid == kT - 1) {  // grand totals
         const int n = max(0, min(li, cap));
         *sl.nactive = n;
         *sl.base = b0;
@@ -350,10 +361,11 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
     {  // the last CTA to finish advances the epoch for the next launch
         __syncthreads();
         if (tid == 0) {
-            unsigned* ticket = reinterpret_cast<unsigned*>(part64 + gridDim.x + 1);
-            if (atomicAdd(ticket, 1u) == gridDim.x - 1) {
+            __threadfence();
+            if (atomicAdd(ticket, 1u) == gridDim.x - 1) {  // every CTA has its chunk by now
                 part64[gridDim.x] = s_epoch;
-                *ticket = 0u;
+                ticket[1] = 0u;
+                ticket[0] = 0u;
             }
         }
     }
@@ -731,7 +743,8 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         for (int ch = 0; ch < nvalid; ch += kCH) {
             const int cend = min(nvalid, ch + kCH);
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
-                const float act = (aid && a_id >= 0) ? alpha[e * p.a_estride + a_id] : 0.0f;
+                // ids outside [0, n_act) are passive here (mpm_set_state flags them as an error)
+                const float act = (aid && a_id >= 0 && a_id < p.n_act) ? alpha[e * p.a_estride + a_id] : 0.0f;
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
                 if (!p2g_particle<D>(p, x, vc, F, act, fluid, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
                 write_row<D>(s_row + (r - ch) * RS, w, c, Adx);
@@ -1486,7 +1499,7 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
             if (r0 == 0) sG = pipe.wait(it);
             float abar = 0.0f;
             if (in) {
-                const bool has_act = aid && a_id >= 0;
+                const bool has_act = aid && a_id >= 0 && a_id < p.n_act;
                 abar = p2g_grad_particle<D>(p, sG, x, vc, F, Fbn, xb, has_act,
                                             has_act ? alpha[e * p.a_estride + a_id] : 0.0f, fluid, c0, i, Sb, flags);
                 if (!has_act) a_id = -1;
@@ -1551,9 +1564,21 @@ __global__ void __launch_bounds__(kT) k_count_active(KParams p, SlotView sl, uns
 
 inline unsigned nblk(int64_t n) { return (unsigned)((n + kT - 1) / kT); }
 
-int g_grid[5][2];  // persistent grid size per kernel kind and dimension (set by tile_init)
-int g_sms = 148;
-int g_canon_grid = 148 * 8;
+// launch-grid table per device (tile_init fills the entry of every device a handle is created
+// on; launches read the entry of the current device -- the engine makes the handle's device
+// current in every entry point)
+struct DevTab {
+    int grid[5][2];  // persistent grid size per kernel kind and dimension
+    int sms = 148;
+    int canon_grid = 148 * 8;
+};
+constexpr int kMaxDev = 64;
+DevTab g_tab[kMaxDev];
+const DevTab& tab() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return g_tab[dev >= 0 && dev < kMaxDev ? dev : 0];
+}
 
 }  // namespace
 
@@ -1599,42 +1624,36 @@ cudaError_t tile_init() {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e) return e;
-    if (dev < 64 && (done_mask >> dev) & 1ull) return cudaSuccess;
-    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (dev < 0 || dev >= kMaxDev) return cudaErrorInvalidDevice;
+    if ((done_mask >> dev) & 1ull) return cudaSuccess;
+    DevTab& T = g_tab[dev];
+    cudaDeviceGetAttribute(&T.sms, cudaDevAttrMultiProcessorCount, dev);
     e = cudaFuncSetAttribute(k_canon, cudaFuncAttributeMaxDynamicSharedMemorySize, canon_smem_bytes());
     if (e) return e;
-    g_canon_grid = occupancy_grid((const void*)k_canon, canon_smem_bytes(), kT);
-    DISPATCH(2, {
-        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>());
-        if (e) return e;
-        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e) return e;
-        e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e) return e;
-        e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
-        if (e) return e;
-        g_grid[0][0] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);
-        g_grid[1][0] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
-        g_grid[2][0] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTQ);
-        g_grid[3][0] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
-        g_grid[4][0] = occupancy_grid((const void*)k_g2p_grad_gather<DIM>, 0, kTG);
-    });
-    DISPATCH(3, {
-        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>());
-        if (e) return e;
-        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e) return e;
-        e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-        if (e) return e;
-        e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, g2pg_smem_bytes<DIM>());
-        if (e) return e;
-        g_grid[0][1] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);
-        g_grid[1][1] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);
-        g_grid[2][1] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTQ);
-        g_grid[3][1] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);
-        g_grid[4][1] = occupancy_grid((const void*)k_g2p_grad_gather<DIM>, 0, kTG);
-    });
-    if (dev < 64) done_mask |= 1ull << dev;
+    T.canon_grid = occupancy_grid((const void*)k_canon, canon_smem_bytes(), kT);
+#define MPM_INIT_DIM(DI)                                                                                          \
+    do {                                                                                                          \
+        constexpr int DIM = (DI) == 2 ? 2 : 3;                                                                    \
+        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>()); \
+        if (e) return e;                                                                                          \
+        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                \
+        if (e) return e;                                                                                          \
+        e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);           \
+        if (e) return e;                                                                                          \
+        e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                                 g2pg_smem_bytes<DIM>());                                                         \
+        if (e) return e;                                                                                          \
+        const int di = DIM == 3 ? 1 : 0;                                                                          \
+        T.grid[0][di] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);                      \
+        T.grid[1][di] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);                                          \
+        T.grid[2][di] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTQ);                \
+        T.grid[3][di] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);                                     \
+        T.grid[4][di] = occupancy_grid((const void*)k_g2p_grad_gather<DIM>, 0, kTG);                              \
+    } while (0)
+    MPM_INIT_DIM(2);
+    MPM_INIT_DIM(3);
+#undef MPM_INIT_DIM
+    done_mask |= 1ull << dev;
     return cudaGetLastError();
 }
 
@@ -1645,9 +1664,10 @@ cudaError_t tile_init() {
 #define MPM_CAP_GATHER 0  // CTAs per SM of g2p_grad's gather part (0: occupancy limit)
 #endif
 static unsigned pgrid(const KParams& p, int kind) {
-    int g = g_grid[kind][p.dim == 3 ? 1 : 0];
-    if (kind == 2 && MPM_CAP_G2PG > 0) g = min(g, g_sms * MPM_CAP_G2PG);
-    if (kind == 4 && MPM_CAP_GATHER > 0) g = min(g, g_sms * MPM_CAP_GATHER);
+    const DevTab& T = tab();
+    int g = T.grid[kind][p.dim == 3 ? 1 : 0];
+    if (kind == 2 && MPM_CAP_G2PG > 0) g = min(g, T.sms * MPM_CAP_G2PG);
+    if (kind == 4 && MPM_CAP_GATHER > 0) g = min(g, T.sms * MPM_CAP_GATHER);
     return (unsigned)(p.step_blocks < g ? p.step_blocks : g);
 }
 
@@ -1665,7 +1685,9 @@ void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* 
     launch_k(k_bin_scatter, (unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s, p, keys, pid, cursor, sl);
 }
 void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* flags, cudaStream_t s) {
-    launch_k(k_canon, g_canon_grid < p.step_blocks ? g_canon_grid : (p.step_blocks > 0 ? p.step_blocks : 1), kT, canon_smem_bytes(), s, p, sl, pid_next, flags);
+    const int cg = tab().canon_grid;
+    launch_k(k_canon, cg < p.step_blocks ? cg : (p.step_blocks > 0 ? p.step_blocks : 1), kT, canon_smem_bytes(), s, p, sl,
+             pid_next, flags);
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
@@ -1673,7 +1695,7 @@ void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const 
 }
 static unsigned node_grid(const KParams& p) {
     const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? Geo<3>::TN : Geo<2>::TN) + kT - 1) / kT;
-    const int64_t cap = (int64_t)g_sms * 8;
+    const int64_t cap = (int64_t)tab().sms * 8;
     return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
 }
 void launch_grid_op(const KParams& p, const SlotView& sl, cudaStream_t s) {

@@ -30,7 +30,8 @@ struct KParams {
     const int32_t* mat;  // per-particle material by particle id (R23: nonzero = fluid), or null
 };
 
-enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8 };
+enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8,
+             FLAG_BAD_ACTUATOR = 16 };
 
 // Block geometry of the sorted-tile scheme: particles
 // are binned by the B^d block of cells containing their base cell; a block's

@@ -27,7 +27,7 @@ EXPORTS = ["mpm_create", "mpm_destroy", "mpm_last_error", "mpm_default_params", 
            "mpm_set_state", "mpm_n_theta", "mpm_set_controller", "mpm_forward", "mpm_loss",
            "mpm_seed_adjoint", "mpm_backward", "mpm_grads", "mpm_get_state", "mpm_launch_count",
            "mpm_grad_v0_sum", "mpm_set_profiling", "mpm_reset_kernel_stats", "mpm_kernel_stats", "mpm_active_nodes",
-           "mpm_set_materials"]
+           "mpm_active_nodes_at", "mpm_set_materials"]
 
 
 class MpmError(RuntimeError):
@@ -76,6 +76,7 @@ def load() -> ct.CDLL:
             "mpm_kernel_stats": [H, ct.c_int32, ct.POINTER(ct.c_char_p), ct.POINTER(ct.c_double),
                                  ct.POINTER(ct.c_int64)],
             "mpm_active_nodes": [H, ct.POINTER(ct.c_int64)], "mpm_set_materials": [H, P],
+            "mpm_active_nodes_at": [H, ct.c_int32, ct.POINTER(ct.c_int64)],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -238,9 +239,13 @@ class Sim:
             i += 1
         return out
 
-    def active_nodes(self) -> int:
+    def active_nodes(self, step: int | None = None) -> int:
+        """grid nodes with M > 0 at `step` of the recorded forward (default: the last step)"""
         c = ct.c_int64()
-        self._check("mpm_active_nodes", self.L.mpm_active_nodes(self.h, ct.byref(c)))
+        if step is None:
+            self._check("mpm_active_nodes", self.L.mpm_active_nodes(self.h, ct.byref(c)))
+        else:
+            self._check("mpm_active_nodes_at", self.L.mpm_active_nodes_at(self.h, int(step), ct.byref(c)))
         return int(c.value)
 
     def close(self):

@@ -12,6 +12,8 @@ o_t[a] = (s_x (mean_a x_t - mean x_t), s_v mean_a v_t).  Pinned here by
 * whole-trajectory central differences of the closed-loop episode (x0, v0, C0, F0, theta) with
   floor contact, so the loss depends on theta (rel <= 1e-6).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -163,3 +165,65 @@ def test_closed_loop_trajectory_fd(case):
         # C0 enters the COM loss only through the (small) contact response: its central
         # differences carry ~1e-6 relative cancellation noise at h = 1e-6
         assert err < (1e-5 if key == "C" else 1e-6), (case, key, err)
+
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "controller_observe.txt")
+
+
+def _golden():
+    out = {}
+    with open(GOLDEN) as f:
+        for line in f:
+            line = line.split("#")[0].strip()
+            if line:
+                k, *v = line.split()
+                out[k] = np.array([float(x) for x in v])
+    return out
+
+
+def test_observation_worked_example():
+    """R22 on the hand-evaluated five-particle example of tests/golden/controller_observe.txt
+    (s_x = 10, s_v = 2; a passive particle shifts the centre of mass but no group velocity):
+    pins both o_x and o_v, their layout and the scales."""
+    g = _golden()
+    o = Oracle(_cl(2, n_act=2, obs_sv=2.0))
+    x = g["obs_x"].reshape(5, 2)
+    v = g["obs_v"].reshape(5, 2)
+    aid = g["obs_aid"].astype(np.int32)
+    np.testing.assert_allclose(o.observe(x, v, aid), g["obs_expected"], rtol=0, atol=1e-14)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_observed_velocity_identities(dim):
+    """o_v (R22) is pinned by (i) sum_a n_a o_v[a] = s_v * (sum of v over grouped particles),
+    (ii) a Galilean shift v -> v + c moves o_v[a] by s_v c for every non-empty group and leaves
+    o_x unchanged, (iii) o_v does not depend on x, (iv) an empty group observes zero."""
+    A, sv = 3, 2.5
+    o = Oracle(_cl(dim, n_act=A, obs_sv=sv))
+    rng = np.random.default_rng(4)
+    N = 17
+    x, v = _state(o, N, rng)
+    aid = rng.integers(-1, A - 1, size=N).astype(np.int32)  # group A-1 stays empty
+    aid[:2] = [0, 1]
+    ob = o.observe(x, v, aid).reshape(A, 2, dim)
+    n = np.bincount(aid[aid >= 0], minlength=A)
+    np.testing.assert_allclose((n[:, None] * ob[:, 1, :]).sum(0), sv * v[aid >= 0].sum(0), rtol=1e-13, atol=1e-13)
+    c_ = rng.standard_normal(dim)
+    ob2 = o.observe(x, v + c_, aid).reshape(A, 2, dim)
+    for a in range(A):
+        if n[a]:
+            np.testing.assert_allclose(ob2[a, 1], ob[a, 1] + sv * c_, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(ob2[:, 0], ob[:, 0], rtol=0, atol=1e-15)
+    ob3 = o.observe(x + 0.01 * rng.standard_normal(x.shape), v, aid).reshape(A, 2, dim)
+    np.testing.assert_array_equal(ob3[:, 1], ob[:, 1])
+    assert np.all(ob[A - 1] == 0)
+
+
+def test_closed_loop_controller_worked_example():
+    """Closed-loop MLP input order u = [phi(t), o_t] (R22): the hand-built example of
+    tests/golden/controller_observe.txt (h = (0.5, -0.25), alpha = 0.5)."""
+    g = _golden()
+    o = Oracle(_cl(2, n_act=1, hidden=2))
+    assert o.n_theta() == len(g["closed_theta"]) == 21
+    np.testing.assert_allclose(o.controller_obs(g["closed_theta"], 0, g["closed_obs"]), g["closed_alpha"],
+                               rtol=0, atol=1e-14)

@@ -172,6 +172,57 @@ def test_controller_closed_form_one_layer():
                                np.tanh(W_ @ phi + b), rtol=1e-14)
 
 
+def _golden_map(name):
+    return {r[0]: np.array([float(x) for x in r[1:]]) for r in _golden_rows(name)}
+
+
+def test_controller_two_layer_worked_example():
+    """H > 0 (R9): the hand-built worked example of tests/golden/controller_observe.txt --
+    theta laid out [W1, b1, W2, b2], hidden tanh, W2 of shape n_act x H, exact intermediates
+    h = (0.5, -0.25) and alpha = (0.5, -0.75, 0.125)."""
+    g = _golden_map("controller_observe.txt")
+    o = Oracle(_cfg2(hidden=2, n_act=3))
+    assert o.n_theta() == len(g["open_theta"]) == 19
+    np.testing.assert_allclose(o.controller(g["open_theta"], 0), g["open_alpha"], rtol=0, atol=1e-14)
+
+
+def test_controller_two_layer_saturated_hidden_layer():
+    """H > 0 limit: with a hidden pre-activation of magnitude >= 40, tanh(z) = sign(z) exactly in
+    fp64, so alpha = tanh(W2 sign(W1 phi + b1) + b2) -- a closed form that no longer contains the
+    hidden tanh; checked at several t and for H != n_act (a transposed W2 or a dropped hidden
+    nonlinearity fails it)."""
+    H, A, S = 5, 3, 4
+    cfg = _cfg2(hidden=H, n_act=A)
+    o = Oracle(cfg)
+    rng = np.random.default_rng(5)
+    W1 = rng.choice([-1.0, 1.0], size=(H, S)) * 100.0
+    b1 = rng.standard_normal(H) * 10.0
+    W2 = rng.standard_normal((A, H)) * 0.3
+    b2 = rng.standard_normal(A) * 0.1
+    th = np.concatenate([W1.ravel(), b1, W2.ravel(), b2])
+    checked, signs = 0, set()
+    for t in range(0, 200, 7):
+        phi = np.sin(cfg["omega"] * t * cfg["dt"] + 2 * np.pi * np.arange(S) / S)
+        z = W1 @ phi + b1
+        if np.min(np.abs(z)) < 40:
+            continue
+        np.testing.assert_allclose(o.controller(th, t), np.tanh(W2 @ np.sign(z) + b2), rtol=0, atol=1e-15)
+        checked += 1
+        signs.add(tuple(np.sign(z)))
+    assert checked >= 5 and len(signs) >= 2  # several t, with different hidden sign patterns
+
+
+def test_controller_zero_output_layer_gives_tanh_of_bias():
+    """H > 0: W2 = 0 makes alpha = tanh(b2) whatever W1, b1 and t (the output layer alone)."""
+    H, A = 4, 3
+    o = Oracle(_cfg2(hidden=H, n_act=A))
+    rng = np.random.default_rng(8)
+    b2 = np.array([0.3, -1.2, 0.0])
+    th = np.concatenate([rng.standard_normal(H * 4), rng.standard_normal(H), np.zeros(A * H), b2])
+    for t in (0, 9):
+        np.testing.assert_allclose(o.controller(th, t), np.tanh(b2), rtol=0, atol=1e-16)
+
+
 # ------------------------------------------------------------ P2G / grid / G2P
 def _random_state(o, N, rng, center=0.5, spread=0.08):
     d = o.d
