@@ -5,9 +5,8 @@ on the long robot horizons)."""
 import numpy as np
 import pytest
 
-from helpers import gpu_run, inputs, oracle_run, rel
+from helpers import check, compare_episode, gpu_run, inputs, oracle_run, rel
 from paper_1910_00935_b200 import workloads as W
-from test_gpu_parity import _assert, _compare_episode
 
 pytestmark = pytest.mark.gpu
 
@@ -35,13 +34,8 @@ def test_tiny_closed_loop_matches_oracle(case):
     inp = W.make_inputs(p)
     inp["theta"] = (inp["theta"] * 0.5).astype(np.float32)
     got = gpu_run(p, inp)
-    ref = oracle_run(p, inp)
-    for k in "xvCF":
-        assert rel(got[k][0], ref[k]) < STATE_TOL, (k, rel(got[k][0], ref[k]))
-    assert abs(got["loss"][0] - ref["loss"]) < STATE_TOL * max(abs(ref["loss"]), 1e-6)
-    for k in ("dx0", "dv0", "dC0", "dF0", "dtheta"):
-        g = got[k].reshape(ref[k].shape) if k == "dtheta" else got[k][0]
-        assert rel(g, ref[k]) < GRAD_TOL, (k, rel(g, ref[k]))
+    rows, ref = compare_episode(f"tiny_closed_loop/{case}", p, inp, got, with_f32=False)
+    check(rows, case)
     assert np.linalg.norm(ref["dtheta"]) > 0
 
 
@@ -79,13 +73,13 @@ def test_robot2d_closed_loop_c2cl():
     """C2 robot with the closed-loop controller (4 muscles x 2d observations), 256 steps."""
     p, inp = inputs("c2cl", steps=256)
     got = gpu_run(p, inp)
-    errs, _ = _compare_episode(p, inp, got, grads=("dx0", "dv0", "dtheta"))
-    _assert(errs, "c2cl")
+    rows, _ = compare_episode("c2cl@256", p, inp, got, grads=("dx0", "dv0", "dtheta"))
+    check(rows, "c2cl")
 
 
 def test_robot3d_closed_loop_c3cl_checkpointed():
     """C3 geometry, 16 muscles x 6 observations (input 100, H = 32), k = 32, 96 steps."""
     p, inp = inputs("c3cl", steps=96)
     got = gpu_run(p, inp, k_ckpt=32)
-    errs, _ = _compare_episode(p, inp, got, grads=("dx0", "dv0", "dtheta"))
-    _assert(errs, "c3cl")
+    rows, _ = compare_episode("c3cl@96", p, inp, got, grads=("dx0", "dv0", "dtheta"))
+    check(rows, "c3cl")

@@ -8,6 +8,7 @@ import socket
 import subprocess
 import sys
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -38,3 +39,47 @@ def test_two_ranks_on_one_gpu(config, scaling, episodes_total):
     assert d["n_gpus"] == 2 and d["scaling"] == scaling
     assert d["config"]["episodes_total"] == episodes_total
     assert d["value"] > 0 and d["e2e"]["value"] > 0
+
+
+def _t6_worker(rank, world, port, T, out):
+    """one C4 episode per rank on the same GPU, theta_bar all-reduced over gloo"""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from helpers import gpu_run
+        from paper_1910_00935_b200 import workloads as W
+        from paper_1910_00935_b200.dist import allreduce_shared_grad, episode_shard
+        torch.cuda.set_device(0)
+        p = W.config("c4", steps=T)
+        shard = episode_shard(world, rank, world)
+        got = gpu_run(p, [W.make_inputs(p, episode=e) for e in shard], k_ckpt=32)
+        g = torch.from_numpy(np.ascontiguousarray(got["dtheta"])).cuda()
+        allreduce_shared_grad(g)
+        out[rank] = g.cpu().numpy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_allreduced_theta_bar_equals_single_process_sum():
+    """SURVEY 4.2 T6 / 8(e) on the CUDA path: two ranks (gloo, both on this GPU), one C4 episode
+    each at a post-contact horizon, all-reduce(SUM) of theta_bar == one process holding both
+    episodes (rel <= 1e-6; the two differ only in the fp32 summation order of the per-block
+    actuator-gradient partials)."""
+    import torch.multiprocessing as mp
+    from helpers import gpu_run
+    from paper_1910_00935_b200 import workloads as W
+    T = 128
+    p = W.config("c4", steps=T)
+    single = gpu_run(p, [W.make_inputs(p, episode=e) for e in range(2)], k_ckpt=32)["dtheta"]
+    out = mp.Manager().dict()
+    mp.spawn(_t6_worker, args=(2, _port(), T, out), nprocs=2, join=True)
+    np.testing.assert_array_equal(out[0], out[1])  # every rank holds the same sum
+    r = np.linalg.norm(out[0] - single) / np.linalg.norm(single)
+    print(f"[T6] |theta_bar| {np.linalg.norm(single):.3e}, all-reduced vs single process rel {r:.2e}")
+    assert np.linalg.norm(single) > 1e-4
+    assert r < 1e-6

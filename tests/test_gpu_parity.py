@@ -1,18 +1,18 @@
 """CUDA path (through the C-ABI) vs the fp64 CPU oracle, element by element on
 the same seeded inputs.  Gates (BASELINE.json north_star): final particle
-states rel <= 1e-4 (per array, ||d||/||ref||), gradients rel-L2 <= 1e-3."""
-import os
+states rel <= 1e-4 (per array, ||d||/||ref||), gradients rel-L2 <= 1e-3, plus an
+element-wise bound max|d|/max|ref| <= 10x those; every comparison is recorded
+(tests/helpers.py: record)."""
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import pytest
 
-from helpers import gpu_run, inputs, oracle_run, oracle_tape, rel
+from helpers import (GRAD_TOL, check, compare_arrays, compare_episode, gpu_run, inputs, oracle_pair,
+                     oracle_run, oracle_tape, rel)
 from paper_1910_00935_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
-
-STATE_TOL = 1e-4
-GRAD_TOL = 1e-3
 
 TINY = {
     "2d_fcr_act_hidden": lambda: W.tiny(2, steps=12, hidden=4, seed=1),
@@ -37,59 +37,17 @@ def test_tiny_every_adjoint_path(case):
     lam = [l.astype(np.float32) for l in lam]
     ref = oracle_tape(p, inp, p["steps"], lam)
     got = gpu_run(p, inp, seed=lam)
-    for k in "xvCF":
-        assert rel(got[k][0], ref[k]) < STATE_TOL, (k, rel(got[k][0], ref[k]))
-    for k in ("dx0", "dv0", "dC0", "dF0", "dtheta"):
-        assert rel(got[k].reshape(ref[k].shape), ref[k]) < GRAD_TOL, (k, rel(got[k].reshape(ref[k].shape), ref[k]))
-
-
-def _errors(p, got, ref, e, grads):
-    errs = {k: rel(got[k][e], ref[k]) for k in "xvCF"}
-    for k in grads:
-        if k == "dtheta":
-            if ref[k].size:
-                errs[k] = rel(got[k], ref[k])
-        elif np.linalg.norm(ref[k]) > 1e-12:
-            errs[k] = rel(got[k][e], ref[k])
-    if got.get("loss") is not None:
-        errs["loss"] = abs(float(got["loss"][e]) - ref["loss"]) / max(abs(ref["loss"]), 1e-12)
-    return errs
-
-
-def _compare_episode(p, inp, got, steps=None, e=0, grads=("dx0", "dv0", "dC0", "dF0", "dtheta")):
-    """errors of the GPU run vs the fp64 oracle, and the gate per array:
-    the north_star tolerance, or -- where the oracle's own fp32 build already
-    deviates from fp64 by more than that (cancellation-heavy C and dtheta on
-    resting robots) -- 2x that fp32-vs-fp64 deviation (SURVEY.md 8(c) fallback,
-    DESIGN.md "Parity gates")."""
-    ref = oracle_run(p, inp, steps=steps)
-    ref32 = oracle_run(p, inp, steps=steps, precision="f32")
-    errs = _errors(p, got, ref, e, grads)
-    as_got = {k: ref32[k][None] for k in ("x", "v", "C", "F", "dx0", "dv0", "dC0", "dF0")}
-    as_got["dtheta"] = ref32["dtheta"]
-    as_got["loss"] = np.array([ref32["loss"]])
-    dev32 = _errors(p, as_got, ref, 0, grads)
-    tols = {}
-    for k in errs:
-        base = STATE_TOL if k in ("x", "v", "C", "F", "loss") else GRAD_TOL
-        tols[k] = max(base, 2.0 * dev32.get(k, 0.0))
-    print(f"[parity] {p.get('name')} e={e}: " + ", ".join(
-        f"{k} {errs[k]:.2e} (gate {tols[k]:.1e}, oracle-f32 {dev32.get(k, 0):.1e})" for k in errs))
-    return (errs, tols), ref
-
-
-def _assert(errs, tag):
-    errs, tols = errs
-    for k, v in errs.items():
-        assert v < tols[k], (tag, k, v, tols[k], errs)
+    pairs = {k: (got[k][0], ref[k]) for k in "xvCF"}
+    pairs.update({k: (got[k].reshape(ref[k].shape), ref[k]) for k in ("dx0", "dv0", "dC0", "dF0", "dtheta")})
+    check(compare_arrays(f"tiny/{case}", pairs), case)
 
 
 @pytest.mark.parametrize("name", ["c1a", "c1b"])
 def test_block_full_horizon(name):
     p, inp = inputs(name)
     got = gpu_run(p, inp)
-    errs, ref = _compare_episode(p, inp, got, grads=("dx0", "dv0"))
-    _assert(errs, name)
+    rows, ref = compare_episode(name, p, inp, got, grads=("dx0", "dv0"))
+    check(rows, name)
     if name == "c1a":  # no wall contact: closed form dL/dC0 = dL/dF0 = 0 (SURVEY 8(c))
         scale = np.abs(got["dv0"]).max()
         assert np.abs(got["dC0"]).max() < 1e-3 * scale and np.abs(got["dF0"]).max() < 1e-3 * scale
@@ -98,35 +56,44 @@ def test_block_full_horizon(name):
 def test_robot2d_c2_full_horizon():
     p, inp = inputs("c2")
     got = gpu_run(p, inp)
-    errs, _ = _compare_episode(p, inp, got, grads=("dx0", "dv0", "dtheta"))
-    _assert(errs, "c2")
+    rows, _ = compare_episode("c2@1024", p, inp, got, grads=("dx0", "dv0", "dtheta"))
+    check(rows, "c2")
 
 
-def test_robot3d_c3_checkpointed():
-    """C3 geometry, 16 muscles, H = 32, k = 32, first 128 steps (4 segments)."""
-    p, inp = inputs("c3", steps=128)
+def test_robot3d_c3_full_horizon_checkpointed():
+    """C3 at its full horizon (SURVEY 8(c) "Parity gates"; "512~2048 time steps"): 3D robot,
+    16 muscles, H = 32, 512 steps with k = 32 (16 segments)."""
+    p, inp = inputs("c3")
+    assert p["steps"] == 512
     got = gpu_run(p, inp, k_ckpt=32)
-    errs, _ = _compare_episode(p, inp, got, grads=("dx0", "dv0", "dtheta"))
-    _assert(errs, "c3")
+    rows, ref = compare_episode("c3@512", p, inp, got, grads=("dx0", "dv0", "dtheta"))
+    check(rows, "c3")
+    assert np.linalg.norm(ref["dtheta"]) > 1e-4  # the robot walks: theta_bar is not rounding noise
 
 
-def test_batched_episodes_c4():
-    """4 independent C4 episodes in one launch: per-episode states and the
-    summed controller gradient equal the per-episode oracle runs."""
-    p = W.config("c4", steps=48)
+def test_batched_episodes_c4_post_contact():
+    """4 independent C4 episodes in one launch, 128 steps (k = 32): past the landing, so each
+    episode's theta_bar is ~1e-3 (not the ~1e-9 rounding noise of a body still in free fall).
+    Per-episode states / initial-state gradients and the summed controller gradient equal the
+    per-episode oracle runs."""
+    T = 128
+    p = W.config("c4", steps=T)
     inps = [W.make_inputs(p, episode=e) for e in range(4)]
-    got = gpu_run(p, inps, k_ckpt=16)
+    got = gpu_run(p, inps, k_ckpt=32)
+    with ThreadPoolExecutor(8) as ex:
+        futs = [ex.submit(oracle_run, p, inp, T, prec) for inp in inps for prec in ("f64", "f32")]
+        res = [f.result() for f in futs]
     dth = dth32 = 0
-    for e, inp in enumerate(inps):
-        errs, ref = _compare_episode(p, inp, got, e=e, grads=("dx0", "dv0"))
-        errs[0].pop("loss", None)
-        assert abs(got["loss"][e] - ref["loss"]) < 1e-4 * abs(ref["loss"])
-        _assert(errs, f"c4[{e}]")
+    for e in range(4):
+        ref, ref32 = res[2 * e], res[2 * e + 1]
+        assert np.linalg.norm(ref["dtheta"]) > 1e-4, e
+        rows, _ = compare_episode("c4@128", p, inps[e], got, e=e, grads=("dx0", "dv0"), refs=(ref, ref32))
+        check(rows, f"c4[{e}]")
         dth = dth + ref["dtheta"]
-        dth32 = dth32 + oracle_run(p, inp, precision="f32")["dtheta"]
-    gate = max(GRAD_TOL, 2 * rel(dth32, dth))
-    print(f"[parity] c4 sum dtheta {rel(got['dtheta'], dth):.2e} (gate {gate:.1e})")
-    assert rel(got["dtheta"], dth) < gate
+        dth32 = dth32 + ref32["dtheta"]
+    rows = compare_arrays("c4@128/sum_dtheta", {"dtheta": (got["dtheta"], dth)},
+                          {"dtheta": (rel(dth32, dth), 0.0)})
+    check(rows, "c4 sum dtheta")
 
 
 @pytest.mark.parametrize("k", [1, 7, 64])
@@ -311,14 +278,14 @@ def test_block_particle_overflow_is_an_error():
     sim.close()
 
 
-@pytest.mark.skipif(os.environ.get("MPM_SLOW_TESTS") != "1", reason="~10 min of CPU oracle; MPM_SLOW_TESTS=1")
 def test_c5_full_size_64_steps_through_landing():
     """SURVEY 8(c) horizons: C5 at full size (1,061,208 particles, 128^3) for 64 steps with the
     checkpoint interval the bench uses (k = 2) -- the cube lands on the sticky floor near step
     50, so contact, the select rule and the re-forward are all exercised -- vs the fp64 oracle
-    on every particle (states, L, dL/dx0, dL/dv0), with the oracle-fp32 fallback gate."""
+    on every particle (states, L, dL/dx0, dL/dv0).  ~6 min of CPU oracle (fp64 and fp32 builds
+    in two threads)."""
     p, inp = inputs("c5", steps=64)
     got = gpu_run(p, inp, steps=64, k_ckpt=2)
-    errs, ref = _compare_episode(p, inp, got, steps=64, grads=("dx0", "dv0"))
-    _assert(errs, "c5@64")
+    rows, ref = compare_episode("c5@64", p, inp, got, steps=64, grads=("dx0", "dv0"))
+    check(rows, "c5@64")
     assert ref["x"][:, 1].min() < 3.5 / 128  # it did reach the floor

@@ -125,3 +125,25 @@ def test_c2cl_closed_loop_robot_learns_to_move_forward():
     assert all(np.isfinite(L))
     assert min(L) < L[0] - 0.05, L
     assert L[-1] < L[0], L
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["tiny3d", "c2@256"])
+def test_adam_loop_through_the_cuda_path_matches_the_oracle_loop(case):
+    """f2 parity: 3 Adam iterations of optimize() driven by the CUDA path (mpm.Sim through the
+    C-ABI) and by the fp64 oracle (OracleSim) from the same theta_0 give the same losses and
+    the same theta_3 (rel <= 1e-3): the loop, not just a descending loss, is checked."""
+    if case == "tiny3d":
+        p, kw = _cfg(), dict(lr=1e-2)
+    else:
+        p, kw = W.config("c2", steps=256), dict(lr=0.05, clip=1.0)
+    gpu = O.optimize(p, iters=3, method="adam", **kw)
+    ref = O.optimize(p, iters=3, method="adam", sim=OracleSim(p), device="cpu", **kw)
+    th, th_ref = gpu["theta"].cpu().double().numpy(), ref["theta"].numpy()
+    th0 = W.make_inputs(p)["theta"].astype(np.float64)
+    step_rel = np.linalg.norm(th - th_ref) / np.linalg.norm(th_ref - th0)  # vs the distance moved
+    print(f"[f2] {case}: losses gpu {gpu['loss']} oracle {ref['loss']}; theta_3 rel {np.linalg.norm(th - th_ref) / np.linalg.norm(th_ref):.2e}, "
+          f"rel to the update {step_rel:.2e}")
+    np.testing.assert_allclose(gpu["loss"], ref["loss"], rtol=1e-4, atol=1e-7)
+    assert np.linalg.norm(th - th_ref) / np.linalg.norm(th_ref) < 1e-3
+    assert step_rel < 1e-2
