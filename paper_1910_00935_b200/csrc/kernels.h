@@ -75,8 +75,10 @@ void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* 
                         cudaStream_t s);
 
 // canonical (cell, particle id) order of every active block's list; cell starts; the
-// particle ids of S_{t+1} (pid_next, nullable) in that order.  Runs before each p2g.
-void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* flags, cudaStream_t s);
+// particle ids of S_{t+1} (pid_next, nullable) in that order.  Runs before each p2g.  A block
+// with more than MAXP particles is dropped (FLAG_BLOCK_OVERFLOW) and its rows' next bin keys
+// (keys_next, nullable) are set to -1.
+void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* keys_next, int* flags, cudaStream_t s);
 
 // ---- one forward step (advance())
 // p2g writes F_{t+1} and particle ids of S_{t+1} when Sn.rec / Sn.pid are non-null

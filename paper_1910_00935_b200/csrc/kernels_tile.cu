@@ -589,7 +589,8 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
 // S_{t+1} -- the particle ids of S_{t+1} (p2g's output order).  Its own high-occupancy
 // pass (256 threads, 26 KB smem) ahead of p2g.
 constexpr int canon_smem_bytes() { return 1728 * 15 + 2 * 66 * 4; }
-__global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __restrict__ pid_next, int* flags) {
+__global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __restrict__ pid_next,
+                                              int* __restrict__ keys_next, int* flags) {
     pdl_begin();
     constexpr int MAXP = 1728, CELLS = 64;
     using G = Geo<3>;  // CELLS = 64 in 2D and 3D
@@ -611,6 +612,10 @@ __global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __res
         if (n > MAXP) {  // reported; the block is dropped (no valid entries downstream)
             if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
             for (int c = tid; c <= CELLS; c += kT) cstart[(int64_t)bi * (CELLS + 1) + c] = 0;
+            // g2p writes no bin key for the dropped rows of S_{t+1}: mark them so the next
+            // binning skips them instead of scattering stale keys
+            if (keys_next)
+                for (int q = tid; q < n; q += kT) keys_next[start + q] = -1;
             continue;
         }
         // ---- phase 0: canonical (cell, particle id) order of the block's list.  The
@@ -1684,10 +1689,10 @@ void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* 
                         cudaStream_t s) {
     launch_k(k_bin_scatter, (unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s, p, keys, pid, cursor, sl);
 }
-void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* flags, cudaStream_t s) {
+void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* keys_next, int* flags, cudaStream_t s) {
     const int cg = tab().canon_grid;
     launch_k(k_canon, cg < p.step_blocks ? cg : (p.step_blocks > 0 ? p.step_blocks : 1), kT, canon_smem_bytes(), s, p, sl,
-             pid_next, flags);
+             pid_next, keys_next, flags);
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {

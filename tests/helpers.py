@@ -67,11 +67,13 @@ def compare_arrays(case, pairs, dev32=None, e=0):
         rows.append(dict(episode=e, array=k, l2_err=l2, l2_gate=l2_gate, max_err=mx, max_gate=mx_gate,
                          oracle_f32_l2=d32[0] if dev32 else None, oracle_f32_max=d32[1] if dev32 else None,
                          fallback=bool(l2_gate > base or mx_gate > ELEM_FACTOR * base),
+                         # passed only thanks to the widened gate
+                         fallback_used=bool(l2 >= base or mx >= ELEM_FACTOR * base),
                          passed=bool(l2 < l2_gate and mx < mx_gate)))
     record(case, rows)
     print(f"[parity] {case} e={e}: " + ", ".join(
         f"{r['array']} {r['l2_err']:.1e}/{r['max_err']:.1e} (gates {r['l2_gate']:.0e}/{r['max_gate']:.0e}"
-        f"{', fallback' if r['fallback'] else ''})" for r in rows))
+        f"{', fallback gate USED' if r['fallback_used'] else ''})" for r in rows))
     return rows
 
 

@@ -42,6 +42,9 @@ def main():
             sim.backward(T)
             g = sim.grads()
         sim.close()
+    del sim
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()  # leak-check: return torch's cached blocks before exit
     print(f"{name}: N={N} T={T} k={k} loss={L[0]:.6e} |dv0|={np.linalg.norm(g['dv0']):.6e}")
 
 
