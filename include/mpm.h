@@ -199,6 +199,41 @@ mpm_status mpm_kernel_stats(mpm_handle h, int32_t idx, const char** name, double
 mpm_status mpm_active_nodes_at(mpm_handle h, int32_t step, int64_t* count);
 mpm_status mpm_active_nodes(mpm_handle h, int64_t* count);
 
+/* ---- one body over several slab subdomains -----
+ * The grid is split along x into contiguous slabs of blocks (block edge 4 cells in 3D, 8 in 2D);
+ * one handle per slab, on one device or several (NVLink peer access).  Subdomain g owns the
+ * blocks with block x-index in [x_lo, x_hi) and, at every step, the particles whose base cell
+ * lies in them: particles migrate between neighbours each step, and the grid-node sums at a slab
+ * face read the neighbour's partial tiles from its memory.  The result (states, loss, gradients)
+ * is bitwise equal to the single-domain run of the same body.
+ * Scope: one episode, a passive body (n_actuators = 0, solid and/or fluid), k_ckpt = 1, particles
+ * moving less than one slab per step (else MPM_ERR_UNSUPPORTED / MPM_ERR_OOM).
+ * Sequence per handle: mpm_create(capacity, ...) -> [set_params] -> mpm_set_subdomain -> bind ->
+ * mpm_dd_link(all) -> mpm_set_state_ids -> [mpm_set_materials([n_body], by id)] ->
+ * mpm_dd_forward(all) -> mpm_dd_loss(all) -> mpm_dd_backward(all) -> mpm_grads (the rows given to
+ * set_state_ids, in that order) / mpm_get_state_ids. */
+
+/* Before bind: this handle is the subdomain [x_lo, x_hi) (block x-indices) of a body of n_body
+ * particles (ids 0..n_body-1); mpm_create's n_particles is the subdomain's particle capacity.
+ * migrate_cap: emigrants per direction and step (0 = capacity / 8 + 1024). */
+mpm_status mpm_set_subdomain(mpm_handle h, int32_t x_lo, int32_t x_hi, int64_t n_body, int32_t migrate_cap);
+/* After bind: hs[0..n-1] are the subdomains in slab order (1 <= n <= 4), slabs contiguous and
+ * covering the grid, parameters identical.  Enables peer access between their devices. */
+mpm_status mpm_dd_link(mpm_handle* hs, int32_t n);
+/* The subdomain's particles at t = 0 (n <= capacity; host or device pointers, layouts as
+ * mpm_set_state with N = n) and their body-wide ids (int32 [n]).  Particles outside the slab
+ * are reported by mpm_dd_forward (MPM_ERR_OOM). */
+mpm_status mpm_set_state_ids(mpm_handle h, int64_t n, const float* x, const float* v, const float* C,
+                             const float* F, const int32_t* ids);
+/* forward(T) / loss / backward(T) of the whole body over the linked subdomains (every handle's
+ * work on its own stream; synchronises all).  loss_out: host or device, 1 float (may be NULL). */
+mpm_status mpm_dd_forward(mpm_handle* hs, int32_t n, int32_t steps);
+mpm_status mpm_dd_loss(mpm_handle* hs, int32_t n, float* loss_out);
+mpm_status mpm_dd_backward(mpm_handle* hs, int32_t n, int32_t steps);
+/* Rows of S_T this subdomain holds (its particles of step T-1), and those rows with their ids. */
+mpm_status mpm_dd_rows(mpm_handle h, int64_t* rows);
+mpm_status mpm_get_state_ids(mpm_handle h, float* x, float* v, float* C, float* F, int32_t* ids);
+
 #ifdef __cplusplus
 }
 #endif

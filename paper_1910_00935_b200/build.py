@@ -12,7 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libmpm_b200.so")
-SOURCES = ["engine.cu", "kernels_tile.cu", "kernels_misc.cu"]
+SOURCES = ["engine.cu", "engine_dd.cu", "kernels_tile.cu", "kernels_misc.cu"]
 HEADERS = ["kernels.h", "mpm_device.cuh", "engine.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",

@@ -98,6 +98,9 @@ KParams kparams(const mpm_ctx* h) {
     k.TB = k.nbe * k.E;
     k.max_active = h->pool_blocks;
     k.step_blocks = h->step_blocks;
+    k.n_body = h->dd ? h->n_body : h->N;
+    k.x_lo = h->dd ? h->x_lo : 0;
+    k.x_hi = h->dd ? h->x_hi : k.nb;
     return k;
 }
 
@@ -179,7 +182,7 @@ size_t carve(mpm_ctx* h, char* base) {
     AdjView sb1 = adj();
     float* staging = (float*)take(sizeof(float) * sf);
     int32_t* aid = (int32_t*)take(sizeof(int32_t) * EN);
-    int32_t* mat = (int32_t*)take(sizeof(int32_t) * EN);
+    int32_t* mat = (int32_t*)take(sizeof(int32_t) * std::max<size_t>(EN, (size_t)h->n_body));  // by particle id
     float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
     int* bcount = (int*)take(sizeof(int) * k.TB);
     int* cursor = (int*)take(sizeof(int) * k.TB);
@@ -199,6 +202,15 @@ size_t carve(mpm_ctx* h, char* base) {
     float* theta = (float*)take(sizeof(float) * nth);
     float* theta_bar = (float*)take(sizeof(float) * nth);
     float* theta_part = (float*)take(sizeof(float) * (size_t)p.max_steps * nth);
+    int* ntot_arr = (int*)take(sizeof(int) * (Tm + 1));
+    float* blk_part = (float*)take(sizeof(float) * (size_t)max_active * d);
+    // f3 (decomposed body): migration records of every step
+    const size_t dd_T = h->dd ? (size_t)Tm + 1 : 1;
+    const size_t mcap = h->dd ? (size_t)h->mig_cap : 1;
+    int* out_cnt = (int*)take(sizeof(int) * dd_T * 2);
+    int* out_rows = (int*)take(sizeof(int) * dd_T * 2 * mcap);
+    int* imm_base = (int*)take(sizeof(int) * dd_T * 2);
+    int* nrows_arr = (int*)take(sizeof(int) * dd_T);
     float* loss = (float*)take(sizeof(float) * E);
     float* com_part = (float*)take(sizeof(float) * E * (lblk + 2) * 3);
     int64_t* counter = (int64_t*)take(sizeof(int64_t) * 2);
@@ -224,6 +236,8 @@ size_t carve(mpm_ctx* h, char* base) {
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
         h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
         h->flags = flags;
+        h->ntot_arr = ntot_arr; h->blk_part = blk_part;
+        h->out_cnt = out_cnt; h->out_rows = out_rows; h->imm_base = imm_base; h->nrows_arr = nrows_arr;
     }
     return off;
 }
@@ -250,7 +264,13 @@ SlotView slot_at(mpm_ctx* h, int t) {
     s.cstart = h->cstart_pool;
     s.tiles = h->tiles_pool;
     s.part = h->part;
+    s.ntot = h->ntot_arr + t;
     s.step = t;
+    s.halo = Halo{0, k.nb, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+    if (h->dd) {
+        s.halo.x_lo = h->x_lo;
+        s.halo.x_hi = h->x_hi;
+    }
     return s;
 }
 
@@ -278,6 +298,10 @@ mpm_status sync_flags(mpm_handle h, const char* where) {
     if (f) {
         CU(cudaMemsetAsync(h->flags, 0, sizeof(int), h->stream));
         CU(cudaStreamSynchronize(h->stream));
+        if (f & FLAG_MIGRATION)
+            return fail(h, MPM_ERR_OOM, std::string(where) +
+                                            ": subdomain (f3): capacity or migration buffer exceeded, or a particle "
+                                            "outside its slab / moving past a whole slab in one step");
         if (f & FLAG_BAD_ACTUATOR)
             return fail(h, MPM_ERR_INVALID_ARG, std::string(where) + ": actuator id outside [-1, n_actuators)");
         if (f & FLAG_ACTIVE_OVERFLOW)
@@ -303,7 +327,7 @@ void bin_fresh(mpm_ctx* h, const KParams& k, int t) {
     const SlotView sl = slot_at(h, t);
     KScope sc(h, KC_BIN);
     h->launches += 2;
-    launch_bin_keys(k, state_at(h, t).x, h->keys, h->bcount, h->flags, h->stream);
+    launch_bin_keys(k, state_at(h, t).x, h->dd ? h->n0 : k.N * k.E, h->keys, h->bcount, h->flags, h->stream);
     launch_bin_scan(k, h->bcount, h->cursor, sl, h->scan_part, h->flags, h->stream);
     launch_bin_scatter(k, h->keys, state_at(h, t).pid, h->cursor, sl, h->stream);
 }
@@ -327,7 +351,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     { KScope sc(h, KC_GRID_OP); launch_grid_op(k, sl, h->stream); }
     if (!write_next) return;
     { KScope sc(h, KC_G2P);
-      launch_g2p(k, sl, S, Sn, bin_next ? h->keys : nullptr, h->bcount, h->flags, false, h->stream); }
+      launch_g2p(k, sl, S, Sn, bin_next ? h->keys : nullptr, h->bcount, h->flags, false, Migr{}, h->stream); }
     if (bin_next) {
         const SlotView nx = slot_at(h, t + 1);
         KScope sc(h, KC_BIN);
@@ -341,7 +365,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
 // store, so only g2p runs (plus F_{t+1} = (I + dt C) F and the particle ids)
 void step_reforward(mpm_ctx* h, const KParams& k, int t, cudaStream_t st) {
     KScope sc(h, KC_G2P);
-    launch_g2p(k, slot_at(h, t), state_at(h, t), state_at(h, t + 1), nullptr, h->bcount, h->flags, true, st);
+    launch_g2p(k, slot_at(h, t), state_at(h, t), state_at(h, t + 1), nullptr, h->bcount, h->flags, true, Migr{}, st);
 }
 
 // advance_grad() for step t, using the grid tiles stored for step t
@@ -416,6 +440,17 @@ mpm_status run_graphed(mpm_handle h, std::tuple<int, int, int, int> key, const s
     h->window_seg = it->second.window_seg;
     h->sbar_cur = it->second.sbar_cur;
     return MPM_OK;
+}
+
+// COM loss of S_T in fixed block order (step T-1's blocks, partition independent: a decomposed
+// body gives the same bits, f3) + the adjoint seed S_bar_T
+void launch_loss_blocks(mpm_ctx* h, const KParams& k) {
+    const SlotView last = slot_at(h, h->recorded - 1);
+    launch_block_com(k, last, state_at(h, h->recorded).x, h->blk_part, h->stream);
+    const ListSrc src{h->blk_part, h->blist_pool, last.base, last.nactive};
+    const float3 tgt = make_float3(h->prm.loss_target[0], h->prm.loss_target[1], h->prm.loss_target[2]);
+    float* seed = h->com_part;
+    launch_loss_blocks(k, &src, 1, h->prm.loss_kind, tgt, h->loss, seed, h->sbar[0], h->flags, h->stream);
 }
 
 mpm_status copy_in(mpm_handle h, void* dst, const void* src, size_t bytes) {
@@ -578,6 +613,7 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
                          const float* F, const int32_t* actuator_id) {
     if (!h) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
+    if (h->dd) return fail(h, MPM_ERR_BAD_SEQUENCE, "a subdomain handle takes mpm_set_state_ids");
     if (h->phase < kBound) return fail(h, MPM_ERR_BAD_SEQUENCE, "set_state before bind_workspace");
     if (!x) return fail(h, MPM_ERR_INVALID_ARG, "x is required");
     const KParams k = kparams(h);
@@ -615,8 +651,8 @@ mpm_status mpm_set_materials(mpm_handle h, const int32_t* material) {
     const KParams k = kparams(h);
     const size_t EN = (size_t)k.E * k.N;
     h->has_mat = material != nullptr;
-    if (h->has_mat) {
-        mpm_status st = copy_in(h, h->mat, material, sizeof(int32_t) * EN);
+    if (h->has_mat) {  // indexed by particle id: [E][N], or [n_body] for a subdomain (f3)
+        mpm_status st = copy_in(h, h->mat, material, sizeof(int32_t) * (h->dd ? (size_t)h->n_body : EN));
         if (st) return st;
     }
     // a new material layout invalidates a recorded tape
@@ -644,6 +680,7 @@ mpm_status mpm_set_controller(mpm_handle h, const float* theta, int64_t n) {
 mpm_status mpm_forward(mpm_handle h, int32_t steps) {
     if (!h) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
+    if (h->dd) return fail(h, MPM_ERR_BAD_SEQUENCE, "a subdomain handle runs through mpm_dd_forward");
     if (h->phase < kHasState) return fail(h, MPM_ERR_BAD_SEQUENCE, "forward before set_state");
     if (steps < 1 || steps > h->prm.max_steps)
         return fail(h, MPM_ERR_INVALID_ARG, "steps must be in [1, max_steps]");
@@ -671,14 +708,13 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
 mpm_status mpm_loss(mpm_handle h, float* loss_out) {
     if (!h) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
+    if (h->dd) return fail(h, MPM_ERR_BAD_SEQUENCE, "a subdomain handle runs through mpm_dd_loss");
     if (h->phase < kForward) return fail(h, MPM_ERR_BAD_SEQUENCE, "loss before forward");
     const KParams k = kparams(h);
-    const float3 tgt = make_float3(h->prm.loss_target[0], h->prm.loss_target[1], h->prm.loss_target[2]);
     h->sbar_cur = 0;
     { KScope sc(h, KC_LOSS);
       h->launches += 2;
-      launch_loss(k, state_at(h, h->recorded).x, h->prm.loss_kind, tgt, h->com_part, h->loss, h->sbar[0],
-                  h->flags, h->stream); }
+      launch_loss_blocks(h, k); }
     if (loss_out) CU(cudaMemcpyAsync(loss_out, h->loss, sizeof(float) * k.E, cudaMemcpyDefault, h->stream));
     mpm_status st = sync_flags(h, "mpm_loss");
     if (st) return st;
@@ -716,6 +752,7 @@ mpm_status mpm_seed_adjoint(mpm_handle h, const float* dx, const float* dv, cons
 mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     if (!h) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
+    if (h->dd) return fail(h, MPM_ERR_BAD_SEQUENCE, "a subdomain handle runs through mpm_dd_backward");
     if (h->phase != kSeeded) return fail(h, MPM_ERR_BAD_SEQUENCE, "backward needs forward + loss/seed_adjoint");
     if (steps != h->recorded)
         return fail(h, MPM_ERR_BAD_SEQUENCE, "backward steps != recorded forward steps");
@@ -780,6 +817,7 @@ mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF
     if (h->phase != kBackward) return fail(h, MPM_ERR_BAD_SEQUENCE, "grads before backward");
     const KParams k = kparams(h);
     const size_t EN = (size_t)k.E * k.N, d = (size_t)h->dim;
+    const size_t rows = h->dd ? (size_t)h->n0 : EN;  // a subdomain returns its t = 0 particles (f3)
     float* sx = h->staging;
     float* sv = sx + EN * d;
     float* sC = sv + EN * d;
@@ -789,12 +827,12 @@ mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF
         // S_bar_0 is indexed like S_0, i.e. in caller order
         const AdjView& B0 = h->sbar[h->sbar_cur];
         launch_unpack(k, B0.x, B0.vc, B0.f, nullptr, dx0 ? sx : nullptr, dv0 ? sv : nullptr,
-                      dC0 ? sC : nullptr, dF0 ? sF : nullptr, h->stream);
+                      dC0 ? sC : nullptr, dF0 ? sF : nullptr, h->stream, (int64_t)rows);
     }
-    if (dx0) CU(cudaMemcpyAsync(dx0, sx, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
-    if (dv0) CU(cudaMemcpyAsync(dv0, sv, sizeof(float) * EN * d, cudaMemcpyDefault, h->stream));
-    if (dC0) CU(cudaMemcpyAsync(dC0, sC, sizeof(float) * EN * d * d, cudaMemcpyDefault, h->stream));
-    if (dF0) CU(cudaMemcpyAsync(dF0, sF, sizeof(float) * EN * d * d, cudaMemcpyDefault, h->stream));
+    if (dx0) CU(cudaMemcpyAsync(dx0, sx, sizeof(float) * rows * d, cudaMemcpyDefault, h->stream));
+    if (dv0) CU(cudaMemcpyAsync(dv0, sv, sizeof(float) * rows * d, cudaMemcpyDefault, h->stream));
+    if (dC0) CU(cudaMemcpyAsync(dC0, sC, sizeof(float) * rows * d * d, cudaMemcpyDefault, h->stream));
+    if (dF0) CU(cudaMemcpyAsync(dF0, sF, sizeof(float) * rows * d * d, cudaMemcpyDefault, h->stream));
     const int64_t nth = n_theta_of(h->prm, h->dim);
     if (dtheta && nth > 0)
         CU(cudaMemcpyAsync(dtheta, h->theta_bar, sizeof(float) * nth, cudaMemcpyDefault, h->stream));

@@ -117,6 +117,20 @@ struct mpm_ctx {
     };
     std::map<std::tuple<int, int, int, int>, GraphRec> graphs;
     bool use_graphs = true;
+    int* ntot_arr = nullptr;       // [T_max + 1] sorted particles per step (set by the scan)
+    float* blk_part = nullptr;     // [max_active][d] per-block COM partials of the loss
+    // ---- slab subdomain of a decomposed body (engine_dd.cu)
+    bool dd = false;               // set by mpm_set_subdomain
+    int x_lo = 0, x_hi = 0;        // owned block x-index range
+    int64_t n_body = 0;            // particles of the whole body (ids 0..n_body-1)
+    int64_t n0 = 0;                // particles of this subdomain at t = 0 (mpm_set_state_ids)
+    int mig_cap = 0;               // emigrants per direction and step
+    mpm_ctx* nbr[2] = {nullptr, nullptr};  // left / right neighbour (mpm_dd_link)
+    int* out_cnt = nullptr;        // [T_max][2]        emigrants of step t by direction
+    int* out_rows = nullptr;       // [T_max][2][cap]   their rows of S_{t+1}
+    int* imm_base = nullptr;       // [T_max + 1][2]    first row of S_t's immigrants from each side
+    int* nrows_arr = nullptr;      // [T_max + 1]       rows of S_t (sorted of t-1 + immigrants)
+    cudaEvent_t dd_ev[4] = {};     // per-phase events of the decomposed step
 };
 
 namespace eng {

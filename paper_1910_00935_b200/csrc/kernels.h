@@ -43,6 +43,28 @@ struct AdjView {
     float* f;
 };
 
+// SURVEY 8(f) f3 (one body over slab subdomains, engine_dd.cu): this subdomain owns the grid
+// blocks with block x-index in [x_lo, x_hi); the neighbours (0 = left, 1 = right) own the
+// adjacent columns.  A node tile near a slab face is covered by partial tiles of the neighbour's
+// face column: covered_sum reads them from the neighbour's memory (same device or NVLink peer)
+// in the same fixed order as a single-domain run.  Single domain: x_lo = 0, x_hi = nb, no
+// neighbours.
+struct Halo {
+    int x_lo, x_hi;
+    const int* bmap[2];      // neighbour's block map of this step (null: no neighbour)
+    const float4* tiles[2];  // neighbour's per-step partial tiles (local block index)
+    const int* base[2];      // neighbour's pool base of this step (device scalar)
+};
+
+// particles leaving the slab in g2p (f3): per direction (0 = left, 1 = right) a count and the
+// rows of S_{t+1} that emigrate; cnt == null in a single-domain run
+struct Migr {
+    int x_lo, x_hi;
+    int* cnt;   // [2]
+    int* rows;  // [2][cap]
+    int cap;
+};
+
 // one time step's binning + grid.  The block lists, cell
 // starts and node tiles of all steps live in one pool; step t's entries start at pool
 // index *base (set on the device by the step's scan), so only the active blocks of
@@ -60,13 +82,17 @@ struct SlotView {
     float4* tiles;           // pool [P][TN]      resolved node tiles (u1, M or -1 = sticky)
     float4* part;            // [max_active][TN]  per-step scratch: p2g partial (P, M) tiles,
                              //                   backward: grid_op_grad output (Pb, Mb)
+    int* ntot;               // [1]    sorted particles of this step (set by the scan)
     int step;                // t
+    Halo halo;               // f3 neighbours (covered sums of grid_op / grid_op_grad)
 };
 
 cudaError_t tile_init();
 
 // ---- binning (bin_keys only for a fresh sort; g2p emits keys for the next step)
-void launch_bin_keys(const KParams& p, const float* x, int* keys, int* bcount, int* flags, cudaStream_t s);
+// rows >= n_live get key -1 (not binned); n_live = N * E in a single-domain run
+void launch_bin_keys(const KParams& p, const float* x, int64_t n_live, int* keys, int* bcount, int* flags,
+                     cudaStream_t s);
 int scan_chunks(const KParams& p);  // entries of `part` (int2) the scan needs
 void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
                      cudaStream_t s);
@@ -88,8 +114,39 @@ void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const 
 void launch_grid_op(const KParams& p, const SlotView& sl, cudaStream_t s);
 // g2p writes x, v, C of S_{t+1}; keys != null -> next bin keys;
 // refwd: segment re-forward from stored tiles -- also writes F_{t+1} = (I + dt C) F and the ids
+// mg.cnt != null (f3): particles whose next block leaves [mg.x_lo, mg.x_hi) get key -1 and are listed
+// in the outbox mg.rows by direction
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
-                int* bcount, int* flags, bool refwd, cudaStream_t s);
+                int* bcount, int* flags, bool refwd, const Migr& mg, cudaStream_t s);
+
+// ---- f3 migration (engine_dd.cu)
+// append the neighbours' emigrants of step t to S_{t+1} (rows nsorted_t + ...), bin keys + histogram;
+// imm_base[side] = first row of the immigrants from that side, *nrows = rows of S_{t+1}
+struct MigSrc {
+    StateView S;     // the neighbour's S_{t+1} (peer pointers)
+    const int* cnt;  // the neighbour's outbox count toward this subdomain (null: no neighbour)
+    const int* rows;
+};
+void launch_immigrate(const KParams& p, const StateView& S, const int* nsorted, MigSrc left, MigSrc right,
+                      int x_lo, int x_hi, int cap, int* keys, int* bcount, int* imm_base, int* nrows, int* flags,
+                      cudaStream_t s);
+// backward: S_bar_{t+1} rows of this subdomain's emigrants of step t <- the neighbour's immigrant rows
+void launch_adj_pull(const KParams& p, const AdjView& Sb, const int* cnt, const int* rows, int cap,
+                     const AdjView& nb_left, const int* nb_left_base, const AdjView& nb_right,
+                     const int* nb_right_base, cudaStream_t s);
+
+// ---- COM loss in fixed block order (partition independent, f3): per-block sums of x over the
+// rows S_T holds in step T-1's sorted order, then per episode a fixed-order sum over the
+// concatenation of up to 4 block lists (the subdomains of a decomposed body, in slab order)
+void launch_block_com(const KParams& p, const SlotView& sl_last, const float* x, float* part, cudaStream_t s);
+struct ListSrc {
+    const float* part;  // [n][d] per-block partial sums (list order)
+    const int* blist;   // block-list pool; this step's list starts at pool index *base
+    const int* base;    // device scalar: pool offset of the step
+    const int* n;       // device scalar: entries
+};
+void launch_loss_blocks(const KParams& p, const ListSrc* src, int nsrc, int loss_kind, float3 target, float* loss,
+                        float* seed, const AdjView& Sb, int* flags, cudaStream_t s);
 
 // ---- one reverse step (advance_grad()); Sbn is indexed like S_{t+1}, Sb like S_t
 // g2p_grad in two independent passes over step t's blocks: the U_bar scatter and
@@ -154,6 +211,6 @@ void launch_pack(const KParams& p, const float* x, const float* v, const float* 
                  cudaStream_t s);
 // unpack: caller row dst[i] (dst == null: i) <- row i
 void launch_unpack(const KParams& p, const float* sx, const float* svc, const float* sf, const int* dst,
-                   float* x, float* v, float* C, float* F, cudaStream_t s);
+                   float* x, float* v, float* C, float* F, cudaStream_t s, int64_t n_rows = -1);
 
 }  // namespace mpm

@@ -433,10 +433,10 @@ template <int D>
 __global__ void k_unpack(KParams p, const float* __restrict__ sx, const float* __restrict__ svc,
                          const float* __restrict__ sf, const int* __restrict__ dst,
                          float* __restrict__ x, float* __restrict__ v, float* __restrict__ C,
-                         float* __restrict__ F) {
+                         float* __restrict__ F, int64_t n_rows) {
     pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i >= p.N * p.E) return;
+    if (i >= n_rows) return;
     const int64_t o = dst ? (int64_t)dst[i] : i;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -448,6 +448,60 @@ __global__ void k_unpack(KParams p, const float* __restrict__ sx, const float* _
         if (C) C[o * D * D + q] = svc[soa(p.EN, D + q, i)];
         if (F) F[o * D * D + q] = sf[soa(p.EN, q, i)];
     }
+}
+
+// COM loss in fixed block order (kernels.h launch_loss_blocks): episode e = blockIdx.x, one warp.
+// Global index g runs over the concatenated block lists (subdomains in slab order); lane g mod 32
+// accumulates its entries in order, then a fixed butterfly -> xbar = sum / n_body; L; seed.
+constexpr int kMaxListSrc = 4;
+struct ListSrcs {
+    ListSrc s[kMaxListSrc];
+    int n;
+};
+template <int D>
+__global__ void k_loss_blocks(KParams p, ListSrcs src, int kind, float3 target, float* __restrict__ loss,
+                              float* __restrict__ seed, int* flags) {
+    pdl_begin();
+    const int e = blockIdx.x, lane = threadIdx.x;
+    float acc[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc[k] = 0.0f;
+    int off = 0;
+    for (int q = 0; q < src.n; ++q) {
+        const ListSrc& L = src.s[q];
+        const int n = *L.n;
+        const int* bl = L.blist + *L.base;
+        for (int idx = ((lane - off) % 32 + 32) % 32; idx < n; idx += 32) {
+            if (bl[idx] / p.nbe != e) continue;
+#pragma unroll
+            for (int k = 0; k < D; ++k) acc[k] += L.part[(int64_t)idx * D + k];
+        }
+        off += n;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    if (lane != 0) return;
+    const float tg[3] = {target.x, target.y, target.z};
+    float L = 0.0f, g[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        const float com = acc[k] / (float)p.n_body;  // equal masses: sum m x / sum m = mean x
+        g[k] = 0.0f;
+        if (kind == 0) {
+            const float dlt = com - tg[k];
+            L = fmaf(dlt, dlt, L);
+            g[k] = 2.0f * dlt;
+        } else if (k == 0) {
+            L = -com;
+            g[0] = -1.0f;
+        }
+    }
+    loss[e] = L;
+    if (!isfinite(L)) atomicOr(flags, FLAG_NONFINITE);
+#pragma unroll
+    for (int k = 0; k < D; ++k) seed[e * D + k] = g[k] / (float)p.n_body;  // dL/dxbar * m / (n_body m)
 }
 
 // actuator ids must be -1 (passive) or in [0, n_act): anything else raises FLAG_BAD_ACTUATOR,
@@ -532,6 +586,17 @@ void launch_loss(const KParams& p, const float* x, int loss_kind, float3 target,
     });
 }
 
+void launch_loss_blocks(const KParams& p, const ListSrc* src, int nsrc, int loss_kind, float3 target, float* loss,
+                        float* seed, const AdjView& Sb, int* flags, cudaStream_t s) {
+    ListSrcs ls{};
+    ls.n = nsrc < kMaxListSrc ? nsrc : kMaxListSrc;
+    for (int q = 0; q < ls.n; ++q) ls.s[q] = src[q];
+    DISPATCH(p.dim, {
+        launch_k(k_loss_blocks<DIM>, p.E, 32, 0, s, p, ls, loss_kind, target, loss, seed, flags);
+        launch_k(k_seed<DIM>, nblk(p.N * p.E, 256), 256, 0, s, p, seed, Sb);
+    });
+}
+
 void launch_v_sum(const KParams& p, const float* vc_bar, float* part, float* out, cudaStream_t s) {
     const int nb = loss_blocks_per_episode(p);
     DISPATCH(p.dim, {
@@ -548,8 +613,10 @@ void launch_pack(const KParams& p, const float* x, const float* v, const float* 
 }
 
 void launch_unpack(const KParams& p, const float* sx, const float* svc, const float* sf, const int* dst,
-                   float* x, float* v, float* C, float* F, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_unpack<DIM>, nblk(p.N * p.E, 256), 256, 0, s, p, sx, svc, sf, dst, x, v, C, F));
+                   float* x, float* v, float* C, float* F, cudaStream_t s, int64_t n_rows) {
+    const int64_t n = n_rows >= 0 ? n_rows : p.N * p.E;
+    if (n <= 0) return;
+    DISPATCH(p.dim, launch_k(k_unpack<DIM>, nblk(n, 256), 256, 0, s, p, sx, svc, sf, dst, x, v, C, F, n));
 }
 
 }  // namespace mpm

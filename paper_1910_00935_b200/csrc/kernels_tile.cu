@@ -21,6 +21,7 @@
 //    g2p_grad scatters U_bar with p2g's (cell, o_x) scheme.
 #include "kernels.h"
 
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -80,10 +81,14 @@ template <int D> __device__ __forceinline__ int cell_of(const int lb[3]) {
 // Sum of the <= 2^d block tiles that cover global node g (episode e): every
 // block whose cells [c0, c0 + B) satisfy c0 <= g < c0 + B + 2 holds a partial
 // of that node.  Fixed enumeration order -> deterministic.
+// f3: a covering block outside this subdomain's slab [x_lo, x_hi) belongs to a neighbour, whose
+// block map and (pool-indexed) tiles nt[0] (left) / nt[1] (right) are read instead -- the same
+// blocks in the same order as a single-domain run.
 template <int D>
 __device__ __forceinline__ float4 covered_sum(const KParams& p, int e, const int g[3],
                                               const int* __restrict__ bmap,
-                                              const float4* __restrict__ tiles) {
+                                              const float4* __restrict__ tiles, const Halo& hl,
+                                              const float4* nt0, const float4* nt1) {
     using G = Geo<D>;
     // per axis: option 0 = the block holding g (local l0), option 1 = the previous
     // block (local l0 + B), valid when l0 < 2.  All 2^d combinations unrolled.
@@ -105,13 +110,23 @@ __device__ __forceinline__ float4 covered_sum(const KParams& p, int e, const int
                 if ((a && !ok1[0]) || (b && !ok1[1]) || (c && !ok1[2])) continue;
                 const int bb[3] = {b0[0] - a, b0[1] - b, b0[2] - c};
                 if (bb[0] >= p.nb || bb[1] >= p.nb || (D == 3 && bb[2] >= p.nb)) continue;
-                const int ti = __ldg(bmap + block_lin<D>(p, e, bb));
+                const int* bm = bmap;
+                const float4* tl = tiles;
+                if (bb[0] < hl.x_lo) { bm = hl.bmap[0]; tl = nt0; }
+                else if (bb[0] >= hl.x_hi) { bm = hl.bmap[1]; tl = nt1; }
+                if (bm == nullptr) continue;
+                const int ti = __ldg(bm + block_lin<D>(p, e, bb));
                 if (ti < 0) continue;
                 const int lq = tile_lin<D>(l0[0] + a * G::B, l0[1] + b * G::B, l0[2] + c * G::B);
-                const float4 v = __ldg(tiles + (int64_t)ti * G::TN + lq);
+                const float4 v = __ldg(tl + (int64_t)ti * G::TN + lq);
                 acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
             }
     return acc;
+}
+
+// neighbour tiles indexed by the neighbour's pool (tile) indices of this step (f3)
+template <int D> __device__ __forceinline__ const float4* halo_tiles(const Halo& hl, int s) {
+    return hl.tiles[s] ? hl.tiles[s] - (int64_t)(*hl.base[s]) * Geo<D>::TN : nullptr;
 }
 
 // grid_op (R5-R7): u0 = P/(M + eps); u1 = u0 - dt g e_y; z = sticky walls
@@ -219,12 +234,13 @@ __device__ __forceinline__ void particle_weights(const KParams& p, const float* 
 
 // ---------------------------------------------------------------- binning
 template <int D>
-__global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restrict__ X,
+__global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restrict__ X, int64_t n_live,
                                                  int* __restrict__ keys, int* __restrict__ bcount,
                                                  int* flags) {
     pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const bool in = i < p.N * p.E;
+    if (i >= n_live && i < p.N * p.E) keys[i] = -1;  // rows beyond the live ones (f3 capacity)
+    const bool in = i < n_live;
     int key = 0;
     if (in) {
         float x[3];
@@ -238,9 +254,13 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
         key = block_lin<D>(p, e, bb);
         int cell = cell_of<D>(lb);
         if (!ok) { atomicOr(flags, FLAG_OUT_OF_DOMAIN); key = e * p.nbe; cell = Geo<D>::CELLS; }
-        keys[i] = key * 128 + cell;
+        if (ok && (bb[0] < p.x_lo || bb[0] >= p.x_hi)) {  // f3: a particle outside the subdomain's slab
+            atomicOr(flags, FLAG_MIGRATION);
+            key = -1;
+        }
+        keys[i] = key < 0 ? -1 : key * 128 + cell;
     }
-    count_key(in, key, bcount);
+    count_key(in && key >= 0, key, bcount);
 }
 
 // Exclusive scan of the dense block histogram -> active block list (block-id order),
@@ -356,6 +376,7 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
         const int n = max(0, min(li, cap));
         *sl.nactive = n;
         *sl.base = b0;
+        *sl.ntot = pos;  // sorted entries of this step
         if (li <= cap) sl.bstart[b0 + sl.step + n] = pos;
     }
     {  // the last CTA to finish advances the epoch for the next launch
@@ -796,6 +817,8 @@ __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
     const float4* part_g = sl.part - (int64_t)b0 * G::TN;  // bmap holds pool indices
     float4* rt = sl.tiles + (int64_t)b0 * G::TN;
     const int64_t total = (int64_t)nact * G::TN;
+    const float4* nt0 = halo_tiles<D>(sl.halo, 0);
+    const float4* nt1 = halo_tiles<D>(sl.halo, 1);
     for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
         const int bi = (int)(idx / G::TN), q = (int)(idx - (int64_t)bi * G::TN);
         int e, c0[3], n[3];
@@ -805,7 +828,7 @@ __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
         const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
         float4 out = make_float4(0.f, 0.f, 0.f, -0.0f);
         if (inside) {
-            const float4 pm = covered_sum<D>(p, e, g, sl.bmap, part_g);
+            const float4 pm = covered_sum<D>(p, e, g, sl.bmap, part_g, sl.halo, nt0, nt1);
             float u0[3], u1[3];
             out = grid_velocity<D>(p, g, pm, u0, u1) ? make_float4(0.f, 0.f, 0.f, -pm.w)
                                                       : make_float4(u1[0], u1[1], u1[2], pm.w);
@@ -828,6 +851,8 @@ __global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, con
     const float4* ub_g = ubar - (int64_t)b0 * G::TN;
     const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
     const int64_t total = (int64_t)nact * G::TN;
+    const float4* nt0 = halo_tiles<D>(sl.halo, 0);
+    const float4* nt1 = halo_tiles<D>(sl.halo, 1);
     for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
         const float4 r = __ldg(rt + idx);
         float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -837,7 +862,7 @@ __global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, con
             block_origin<D>(p, __ldg(blist + bi), e, c0);
             local_node<D>(q, n);
             const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-            const float4 ub = covered_sum<D>(p, e, g, sl.bmap, ub_g);
+            const float4 ub = covered_sum<D>(p, e, g, sl.bmap, ub_g, sl.halo, nt0, nt1);
             const float u0[3] = {r.x, r.y + p.dt * p.gravity, r.z};
             const float denom = r.w + p.eps_mass;
             const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
@@ -903,7 +928,7 @@ template <int D>
 __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __restrict__ sU, const float* x,
                                             const int c0[3], int j, int e, int bid, const StateView& Sn,
                                             int* __restrict__ keys, int* flags, bool refwd,
-                                            const StateView& S, int64_t i) {
+                                            const StateView& S, int64_t i, const Migr& mg) {
     using G = Geo<D>;
     using L = Lay<D>;
     const float c4 = 4.0f * p.inv_dx;
@@ -947,6 +972,14 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
             int lc[3] = {b[0] & (G::B - 1), b[1] & (G::B - 1), b[2] & (G::B - 1)};
             key = block_lin<D>(p, e, bb);
             cell = cell_of<D>(lc);
+            if (mg.cnt && (bb[0] < mg.x_lo || bb[0] >= mg.x_hi)) {  // f3: leaves the slab
+                const int dir = bb[0] < mg.x_lo ? 0 : 1;
+                const int slot = atomicAdd(mg.cnt + dir, 1);
+                if (slot < mg.cap) mg.rows[dir * mg.cap + slot] = j;
+                else atomicOr(flags, FLAG_MIGRATION);
+                keys[j] = -1;
+                return -1;
+            }
         } else {
             atomicOr(flags, FLAG_OUT_OF_DOMAIN);
             key = bid;  // p2g of the next step drops it into the junk bucket
@@ -963,7 +996,7 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
 template <int D>
 __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
                                             int* __restrict__ keys, int* __restrict__ bcount, int* flags,
-                                            bool refwd) {
+                                            bool refwd, Migr mg) {
     pdl_begin();
     using G = Geo<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
@@ -1003,11 +1036,11 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
         }
         const float4* sU = pipe.wait(it);
         int key = -1;
-        if (va) key = g2p_particle<D>(p, sU, xa, c0, start + tid, e, bid, Sn, keys, flags, refwd, S, ia);
-        if (keys) count_key(va, key, bcount);
+        if (va) key = g2p_particle<D>(p, sU, xa, c0, start + tid, e, bid, Sn, keys, flags, refwd, S, ia, mg);
+        if (keys) count_key(va && key >= 0, key, bcount);
         key = -1;
-        if (vb) key = g2p_particle<D>(p, sU, xb, c0, start + tid + kTG, e, bid, Sn, keys, flags, refwd, S, ib);
-        if (keys) count_key(vb, key, bcount);
+        if (vb) key = g2p_particle<D>(p, sU, xb, c0, start + tid + kTG, e, bid, Sn, keys, flags, refwd, S, ib, mg);
+        if (keys) count_key(vb && key >= 0, key, bcount);
         for (int r0 = 2 * kTG; r0 < nvalid; r0 += kTG) {
             const int r = r0 + tid;
             const bool in = r < nvalid;
@@ -1017,9 +1050,9 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
                 float x[3];
 #pragma unroll
                 for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i));
-                key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags, refwd, S, i);
+                key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags, refwd, S, i, mg);
             }
-            if (keys) count_key(in, key, bcount);
+            if (keys) count_key(in && key >= 0, key, bcount);
         }
         __syncthreads();
     }
@@ -1567,6 +1600,122 @@ __global__ void __launch_bounds__(kT) k_count_active(KParams p, SlotView sl, uns
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, c);
 }
 
+// ------------------------------------------------------------ f3 migration
+// Rows of S_{t+1} that arrive from the neighbours (their g2p(t) outboxes): appended after this
+// subdomain's sorted rows of step t (left neighbour's first), state copied from the neighbour's
+// S_{t+1} (peer memory), bin key + histogram of step t+1.  blockIdx.y = side (0 left, 1 right).
+// The immigrants' storage order follows the outbox (atomic) order; no sum depends on it (every
+// block list is canonicalised by (cell, particle id)).
+template <int D>
+__global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const int* __restrict__ nsorted,
+                                                  MigSrc left, MigSrc right, int x_lo, int x_hi, int cap,
+                                                  int* __restrict__ keys, int* __restrict__ bcount,
+                                                  int* __restrict__ imm_base, int* __restrict__ nrows, int* flags) {
+    pdl_begin();
+    using L = Lay<D>;
+    const int side = blockIdx.y;
+    const MigSrc& src = side == 0 ? left : right;
+    const int n_left = left.cnt ? min(*left.cnt, cap) : 0;
+    const int n_right = right.cnt ? min(*right.cnt, cap) : 0;
+    const int base = *nsorted + (side == 0 ? 0 : n_left);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        imm_base[side] = base;
+        if (side == 0) *nrows = *nsorted + n_left + n_right;
+    }
+    const int n = side == 0 ? n_left : n_right;
+    const int m = blockIdx.x * kT + threadIdx.x;
+    const bool in = m < n;
+    int key = -1;
+    if (in) {
+        const int j = src.rows[(side == 0 ? 1 : 0) * cap + m];  // the neighbour's outbox toward us
+        const int64_t dst = (int64_t)base + m;
+        if (dst >= p.N) {
+            atomicOr(flags, FLAG_MIGRATION);  // capacity of this subdomain exceeded
+        } else {
+            float x[3];
+#pragma unroll
+            for (int k = 0; k < D; ++k) {
+                x[k] = src.S.x[soa(p.EN, k, j)];
+                S.x[soa(p.EN, k, dst)] = x[k];
+            }
+#pragma unroll
+            for (int q = 0; q < L::VC; ++q) S.vc[soa(p.EN, q, dst)] = src.S.vc[soa(p.EN, q, j)];
+#pragma unroll
+            for (int q = 0; q < L::FF; ++q) S.f[soa(p.EN, q, dst)] = src.S.f[soa(p.EN, q, j)];
+            S.pid[dst] = src.S.pid[j];
+            int b[3];
+            if (base_cell<D>(p, x, b)) {
+                const int bb[3] = {b[0] >> Geo<D>::LOGB, b[1] >> Geo<D>::LOGB, b[2] >> Geo<D>::LOGB};
+                const int lc[3] = {b[0] & (Geo<D>::B - 1), b[1] & (Geo<D>::B - 1), b[2] & (Geo<D>::B - 1)};
+                if (bb[0] >= x_lo && bb[0] < x_hi) {
+                    key = block_lin<D>(p, 0, bb);
+                    keys[dst] = key * 128 + cell_of<D>(lc);
+                } else {
+                    atomicOr(flags, FLAG_MIGRATION);  // moved past this slab in one step
+                    keys[dst] = -1;
+                }
+            } else {
+                atomicOr(flags, FLAG_OUT_OF_DOMAIN);
+                keys[dst] = -1;
+            }
+        }
+    }
+    count_key(in && key >= 0, key, bcount);
+}
+
+// backward of the migration: the adjoint of an emigrant's S_{t+1} row was computed by the
+// neighbour (at its immigrant row imm_base + m); copy it back to the emigrant's row j here.
+template <int D>
+__global__ void __launch_bounds__(kT) k_adj_pull(KParams p, AdjView Sb, const int* __restrict__ cnt,
+                                                 const int* __restrict__ rows, int cap, AdjView nbl,
+                                                 const int* __restrict__ nbl_base, AdjView nbr,
+                                                 const int* __restrict__ nbr_base) {
+    pdl_begin();
+    using L = Lay<D>;
+    const int dir = blockIdx.y;  // 0: emigrants to the left neighbour, 1: to the right
+    const AdjView& nb = dir == 0 ? nbl : nbr;
+    const int* nbase = dir == 0 ? nbl_base : nbr_base;
+    if (!nbase) return;
+    const int n = min(cnt[dir], cap);
+    const int m = blockIdx.x * kT + threadIdx.x;
+    if (m >= n) return;
+    const int j = rows[dir * cap + m];
+    const int64_t src = (int64_t)nbase[dir == 0 ? 1 : 0] + m;  // we are the neighbour's right / left side
+#pragma unroll
+    for (int k = 0; k < D; ++k) Sb.x[soa(p.EN, k, j)] = nb.x[soa(p.EN, k, src)];
+#pragma unroll
+    for (int q = 0; q < L::VC; ++q) Sb.vc[soa(p.EN, q, j)] = nb.vc[soa(p.EN, q, src)];
+#pragma unroll
+    for (int q = 0; q < L::FF; ++q) Sb.f[soa(p.EN, q, j)] = nb.f[soa(p.EN, q, src)];
+}
+
+// per-block sums of x over the rows S_T holds for the blocks of step T-1 (sorted order, fixed
+// lane-strided + butterfly order): part[bi][k]
+template <int D>
+__global__ void __launch_bounds__(kT) k_block_com(KParams p, SlotView sl, const float* __restrict__ X,
+                                                  float* __restrict__ part) {
+    pdl_begin();
+    const int nact = *sl.nactive;
+    const int b0 = *sl.base;
+    const int* bstart = sl.bstart + b0 + sl.step;
+    const unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
+    const int lane = threadIdx.x & 31;
+    for (int bi = blockIdx.x * kW + (threadIdx.x >> 5); bi < nact; bi += gridDim.x * kW) {
+        const int start = bstart[bi];
+        const int nvalid = cstart[(int64_t)bi * (Geo<D>::CELLS + 1) + Geo<D>::CELLS];
+        float acc[3] = {0.f, 0.f, 0.f};
+        for (int r = lane; r < nvalid; r += 32)
+#pragma unroll
+            for (int k = 0; k < D; ++k) acc[k] += X[soa(p.EN, k, start + r)];
+#pragma unroll
+        for (int k = 0; k < D; ++k) {
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+            if (lane == 0) part[(int64_t)bi * D + k] = acc[k];
+        }
+    }
+}
+
 inline unsigned nblk(int64_t n) { return (unsigned)((n + kT - 1) / kT); }
 
 // launch-grid table per device (tile_init fills the entry of every device a handle is created
@@ -1676,8 +1825,9 @@ static unsigned pgrid(const KParams& p, int kind) {
     return (unsigned)(p.step_blocks < g ? p.step_blocks : g);
 }
 
-void launch_bin_keys(const KParams& p, const float* x, int* keys, int* bcount, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_bin_keys<DIM>, nblk(p.N * p.E), kT, 0, s, p, x, keys, bcount, flags));
+void launch_bin_keys(const KParams& p, const float* x, int64_t n_live, int* keys, int* bcount, int* flags,
+                     cudaStream_t s) {
+    DISPATCH(p.dim, launch_k(k_bin_keys<DIM>, nblk(p.N * p.E), kT, 0, s, p, x, n_live, keys, bcount, flags));
 }
 int scan_chunks(const KParams& p) { return (p.TB + kScanChunk - 1) / kScanChunk; }
 void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
@@ -1710,8 +1860,8 @@ void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* uba
     DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM>, node_grid(p), kT, 0, s, p, sl, ubar));
 }
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
-                int* bcount, int* flags, bool refwd, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_g2p<DIM>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bcount, flags, refwd));
+                int* bcount, int* flags, bool refwd, const Migr& mg, cudaStream_t s) {
+    DISPATCH(p.dim, launch_k(k_g2p<DIM>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bcount, flags, refwd, mg));
 }
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, cudaStream_t s) {
@@ -1736,4 +1886,25 @@ void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_
         launch_k(k_reduce_abar, dim3(p.n_act, p.closed_loop ? p.E : 1), 32, 0, s, p, sl, abar_part, alpha_bar_t);
 }
 
+}  // namespace mpm
+
+namespace mpm {
+void launch_immigrate(const KParams& p, const StateView& S, const int* nsorted, MigSrc left, MigSrc right,
+                      int x_lo, int x_hi, int cap, int* keys, int* bcount, int* imm_base, int* nrows, int* flags,
+                      cudaStream_t s) {
+    const dim3 grid((unsigned)((cap + kT - 1) / kT), 2);
+    DISPATCH(p.dim, launch_k(k_immigrate<DIM>, grid, kT, 0, s, p, S, nsorted, left, right, x_lo, x_hi, cap, keys,
+                             bcount, imm_base, nrows, flags));
+}
+void launch_adj_pull(const KParams& p, const AdjView& Sb, const int* cnt, const int* rows, int cap,
+                     const AdjView& nb_left, const int* nb_left_base, const AdjView& nb_right,
+                     const int* nb_right_base, cudaStream_t s) {
+    const dim3 grid((unsigned)((cap + kT - 1) / kT), 2);
+    DISPATCH(p.dim, launch_k(k_adj_pull<DIM>, grid, kT, 0, s, p, Sb, cnt, rows, cap, nb_left, nb_left_base,
+                             nb_right, nb_right_base));
+}
+void launch_block_com(const KParams& p, const SlotView& sl_last, const float* x, float* part, cudaStream_t s) {
+    const int grid = (int)std::min<int64_t>(((int64_t)p.step_blocks + kW - 1) / kW, (int64_t)tab().sms * 8);
+    DISPATCH(p.dim, launch_k(k_block_com<DIM>, grid > 0 ? grid : 1, kT, 0, s, p, sl_last, x, part));
+}
 }  // namespace mpm

@@ -28,10 +28,14 @@ struct KParams {
     int32_t a_estride;   // episode stride of alpha_t / alpha_bar_t (n_act closed loop, else 0)
     float obs_sx, obs_sv;  // observation scales (R22)
     const int32_t* mat;  // per-particle material by particle id (R23: nonzero = fluid), or null
+    int64_t n_body;      // particles of one whole body (episode): N, or the total over the
+                         // subdomains of a decomposed body (f3; N is then a subdomain's capacity)
+    int32_t x_lo, x_hi;  // owned block x-index range (f3 subdomain); single domain: [0, nb)
 };
 
 enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8,
-             FLAG_BAD_ACTUATOR = 16 };
+             FLAG_BAD_ACTUATOR = 16,
+             FLAG_MIGRATION = 32 };  // f3: a particle jumped past a neighbour slab, or a capacity overflowed
 
 // Block geometry of the sorted-tile scheme: particles
 // are binned by the B^d block of cells containing their base cell; a block's

@@ -27,7 +27,9 @@ EXPORTS = ["mpm_create", "mpm_destroy", "mpm_last_error", "mpm_default_params", 
            "mpm_set_state", "mpm_n_theta", "mpm_set_controller", "mpm_forward", "mpm_loss",
            "mpm_seed_adjoint", "mpm_backward", "mpm_grads", "mpm_get_state", "mpm_launch_count",
            "mpm_grad_v0_sum", "mpm_set_profiling", "mpm_reset_kernel_stats", "mpm_kernel_stats", "mpm_active_nodes",
-           "mpm_active_nodes_at", "mpm_set_materials"]
+           "mpm_active_nodes_at", "mpm_set_materials", "mpm_set_subdomain", "mpm_dd_link",
+           "mpm_set_state_ids", "mpm_dd_forward", "mpm_dd_loss", "mpm_dd_backward", "mpm_dd_rows",
+           "mpm_get_state_ids"]
 
 
 class MpmError(RuntimeError):
@@ -77,6 +79,14 @@ def load() -> ct.CDLL:
                                  ct.POINTER(ct.c_int64)],
             "mpm_active_nodes": [H, ct.POINTER(ct.c_int64)], "mpm_set_materials": [H, P],
             "mpm_active_nodes_at": [H, ct.c_int32, ct.POINTER(ct.c_int64)],
+            "mpm_set_subdomain": [H, ct.c_int32, ct.c_int32, ct.c_int64, ct.c_int32],
+            "mpm_dd_link": [ct.POINTER(ct.c_void_p), ct.c_int32],
+            "mpm_set_state_ids": [H, ct.c_int64, P, P, P, P, P],
+            "mpm_dd_forward": [ct.POINTER(ct.c_void_p), ct.c_int32, ct.c_int32],
+            "mpm_dd_loss": [ct.POINTER(ct.c_void_p), ct.c_int32, P],
+            "mpm_dd_backward": [ct.POINTER(ct.c_void_p), ct.c_int32, ct.c_int32],
+            "mpm_dd_rows": [H, ct.POINTER(ct.c_int64)],
+            "mpm_get_state_ids": [H, P, P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -105,7 +115,9 @@ class Sim:
     """One mpm handle with a torch-owned workspace on the current CUDA device."""
 
     def __init__(self, n_particles: int, n_grid: int, dim: int, dt: float, E: float, nu: float,
-                 params: dict | None = None, stream=None, probe_only: bool = False):
+                 params: dict | None = None, stream=None, probe_only: bool = False, subdomain=None):
+        """subdomain = (x_lo, x_hi, n_body[, migrate_cap]): this handle is one slab of a decomposed
+        body (include/mpm.h); n_particles is then its particle capacity."""
         import torch
         self.L = load()
         self.h = ct.c_void_p()
@@ -123,6 +135,10 @@ class Sim:
                 setattr(p, k, v)
         self._check("mpm_set_params", self.L.mpm_set_params(self.h, ct.byref(p)))
         self.params = p
+        if subdomain is not None:
+            lo, hi, nbody, *cap = subdomain
+            self._check("mpm_set_subdomain", self.L.mpm_set_subdomain(self.h, int(lo), int(hi), int(nbody),
+                                                                      int(cap[0]) if cap else 0))
         self.E = int(p.n_episodes)
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         self._check("mpm_set_stream", self.L.mpm_set_stream(self.h, ct.c_void_p(self.stream.cuda_stream)))
@@ -216,6 +232,35 @@ class Sim:
         self._check("mpm_get_state", self.L.mpm_get_state(self.h, *[_ptr(bufs[k])[0] for k in shapes]))
         return bufs
 
+    # ---- slab subdomain of a decomposed body (f3)
+    def set_state_ids(self, x, v, C, F, ids):
+        n = int(len(ids))
+        keep = [_ptr(a) for a in (x, v, C, F)] + [_ptr(ids, np.int32)]
+        self._check("mpm_set_state_ids", self.L.mpm_set_state_ids(self.h, n, *[k[0] for k in keep]))
+
+    def dd_rows(self) -> int:
+        c = ct.c_int64()
+        self._check("mpm_dd_rows", self.L.mpm_dd_rows(self.h, ct.byref(c)))
+        return int(c.value)
+
+    def get_state_ids(self):
+        """S_T rows of this subdomain (its particles of step T-1) and their body-wide ids."""
+        n, d = self.dd_rows(), self.dim
+        out = {"x": np.zeros((n, d), np.float32), "v": np.zeros((n, d), np.float32),
+               "C": np.zeros((n, d, d), np.float32), "F": np.zeros((n, d, d), np.float32),
+               "ids": np.zeros(n, np.int32)}
+        self._check("mpm_get_state_ids", self.L.mpm_get_state_ids(
+            self.h, *[_ptr(out[k], np.int32 if k == "ids" else np.float32)[0] for k in ("x", "v", "C", "F", "ids")]))
+        return out
+
+    def grads_rows(self, n: int):
+        """gradients of the n rows given to set_state_ids (that order)"""
+        d = self.dim
+        out = {"dx0": np.zeros((n, d), np.float32), "dv0": np.zeros((n, d), np.float32),
+               "dC0": np.zeros((n, d, d), np.float32), "dF0": np.zeros((n, d, d), np.float32)}
+        self._check("mpm_grads", self.L.mpm_grads(self.h, *[_ptr(out[k])[0] for k in ("dx0", "dv0", "dC0", "dF0")], None))
+        return out
+
     def launch_count(self) -> int:
         c = ct.c_int64()
         self._check("mpm_launch_count", self.L.mpm_launch_count(self.h, ct.byref(c)))
@@ -260,9 +305,41 @@ class Sim:
             pass
 
 
+def _handles(sims):
+    arr = (ct.c_void_p * len(sims))(*[s.h.value for s in sims])
+    return arr, len(sims)
+
+
+def _dd_call(name, sims, *args):
+    arr, n = _handles(sims)
+    st = getattr(load(), name)(arr, n, *args)
+    if st != MPM_OK:
+        msgs = "; ".join((load().mpm_last_error(s.h) or b"").decode() for s in sims)
+        raise MpmError(name, st, msgs)
+
+
+def dd_link(sims):
+    """link the slab subdomains of one body (in slab order)"""
+    _dd_call("mpm_dd_link", sims)
+
+
+def dd_forward(sims, steps: int):
+    _dd_call("mpm_dd_forward", sims, int(steps))
+
+
+def dd_loss(sims) -> float:
+    out = np.zeros(1, np.float32)
+    _dd_call("mpm_dd_loss", sims, ct.c_void_p(out.ctypes.data))
+    return float(out[0])
+
+
+def dd_backward(sims, steps: int):
+    _dd_call("mpm_dd_backward", sims, int(steps))
+
+
 def sim_from_config(p: dict, n_particles: int, episodes: int | None = None,
                     max_steps: int | None = None, k_ckpt: int | None = None, probe_only: bool = False,
-                    **overrides) -> Sim:
+                    subdomain=None, **overrides) -> Sim:
     """Build a Sim from a workload config dict (paper_1910_00935_b200.workloads)."""
     dim = int(p["dim"])
     model = p.get("model", "neohookean")
@@ -283,4 +360,4 @@ def sim_from_config(p: dict, n_particles: int, episodes: int | None = None,
                   loss_target=list(p.get("target", [0, 0, 0])))
     params.update(overrides)
     return Sim(int(n_particles), int(p["n_grid"]), dim, float(p["dt"]), float(p["E"]),
-               float(p["nu"]), params, probe_only=probe_only)
+               float(p["nu"]), params, probe_only=probe_only, subdomain=subdomain)
