@@ -166,11 +166,26 @@ def _traffic(kernel: str):
 
 
 # -------------------------------------------------------------- CPU oracle
-def oracle_sample(p, inp, steps=1):
+def host_info():
+    """the host the CPU baseline ran on: logical cores and the lscpu model name"""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "model": model}
+
+
+def oracle_sample(p, inp, steps=1, precision="f64"):
     """time the CPU oracle (as it stands) on a bounded sample: all particles of the
-    episode, `steps` time steps of forward + loss + backward, fp64, one thread."""
+    episode, `steps` time steps of forward + loss + backward, one thread (fp64 build, or the
+    fp32 build of the same C source)."""
     from oracle import Oracle
-    o = Oracle(p)
+    o = Oracle(p, precision)
     if inp.get("mat") is not None and np.any(inp["mat"]):
         o.set_materials(inp["mat"])
     t0 = time.perf_counter()
@@ -205,7 +220,7 @@ def run_reference(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _describe(p, N, 1, 1, p["k_ckpt"]),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -387,9 +402,12 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         v_cpu, dt_cpu = oracle_sample(p, inps[0], steps=4)
+        v_f32, dt_f32 = oracle_sample(p, inps[0], steps=4, precision="f32")
         cpu = {"value": v_cpu, "unit": UNIT, "cores": 1, "kind": "oracle",
                "sample": f"{p['name']} episode 0, all {N:,} particles, 4 time steps of forward + "
-                         f"loss + backward, fp64, single thread ({dt_cpu:.1f} s)"}
+                         f"loss + backward, fp64, single thread ({dt_cpu:.1f} s)",
+               "f32_build": {"value": v_f32, "unit": UNIT, "seconds": dt_f32},
+               "host": host_info()}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -398,7 +416,12 @@ def run_ours(args):
                 "config": _describe(p, N, per, world, k), "roofline": roofline,
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                        "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps},
+                        "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.steps,
+                        "outputs": "per step: the initial state S_0 (x, v, C, F, actuator ids) + theta copied "
+                                   "in from pinned host memory; the loss and the shared-parameter gradient "
+                                   "(theta_bar, or sum_p dL/dv0_p for the cube) read back; the device-timed "
+                                   "`value` additionally writes the per-particle gradients dL/d(x0, v0, C0, F0) "
+                                   "into device buffers"},
                 "gpu_launches": int(launches), "clocks": clocks.summary(),
                 "loss": [float(x) for x in loss_d.cpu()]}
         print(json.dumps(line), flush=True)
