@@ -3,7 +3,7 @@
  *
  * What it computes (PAPER.md, "P:n" = line n):
  *   - diffmpm, the differentiable elastic-object simulator (section 4.1):
- *     MLS-MPM after ChainQueen; the equations used are DESIGN.md readings R1-R24.
+ *     MLS-MPM after ChainQueen; the equations used are DESIGN.md readings R1-R25.
  *   - One time step = advance() of Appendix D.1:
  *     clear_grid -> compute_actuation -> p2g -> grid_op -> g2p.
  *   - Its reverse = advance_grad(): recompute the grid, then

@@ -215,6 +215,12 @@ __device__ __forceinline__ void count_key(bool valid, int key, int* bcount) {
     const int leader = __ffs(peers) - 1;
     if (valid && (int)(threadIdx.x & 31) == leader) atomicAdd(&bcount[key], __popc(peers));
 }
+// block and (block, cell) histograms of a binned entry: bcount[block], ccount[block][cell]
+// (cell 64 = the junk bucket of an out-of-domain particle)
+__device__ __forceinline__ void count_bin(bool valid, int block, int cell, int* bcount, int* ccount) {
+    count_key(valid, block, bcount);
+    count_key(valid, block * kCellStride + cell, ccount);
+}
 
 // weights and base of a particle relative to the block origin
 template <int D>
@@ -236,12 +242,12 @@ __device__ __forceinline__ void particle_weights(const KParams& p, const float* 
 template <int D>
 __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restrict__ X, int64_t n_live,
                                                  int* __restrict__ keys, int* __restrict__ bcount,
-                                                 int* flags) {
+                                                 int* __restrict__ ccount, int* flags) {
     pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n_live && i < p.N * p.E) keys[i] = -1;  // rows beyond the live ones (f3 capacity)
     const bool in = i < n_live;
-    int key = 0;
+    int key = 0, cell = 0;
     if (in) {
         float x[3];
 #pragma unroll
@@ -252,7 +258,7 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
         int bb[3] = {b[0] >> Geo<D>::LOGB, b[1] >> Geo<D>::LOGB, b[2] >> Geo<D>::LOGB};
         int lb[3] = {b[0] & (Geo<D>::B - 1), b[1] & (Geo<D>::B - 1), b[2] & (Geo<D>::B - 1)};
         key = block_lin<D>(p, e, bb);
-        int cell = cell_of<D>(lb);
+        cell = cell_of<D>(lb);
         if (!ok) { atomicOr(flags, FLAG_OUT_OF_DOMAIN); key = e * p.nbe; cell = Geo<D>::CELLS; }
         if (ok && (bb[0] < p.x_lo || bb[0] >= p.x_hi)) {  // f3: a particle outside the subdomain's slab
             atomicOr(flags, FLAG_MIGRATION);
@@ -260,7 +266,7 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
         }
         keys[i] = key < 0 ? -1 : key * 128 + cell;
     }
-    count_key(in && key >= 0, key, bcount);
+    count_bin(in && key >= 0, key, cell, bcount, ccount);
 }
 
 // Exclusive scan of the dense block histogram -> active block list (block-id order),
@@ -277,8 +283,33 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
 #endif
 constexpr int kScanPer = MPM_SCAN_PER;
 constexpr int kScanChunk = kT * kScanPer;
-__global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bcount, int* __restrict__ cursor,
-                                                SlotView sl, int2* __restrict__ part, int* flags) {
+// Also, per active block, the exclusive scan of its 65 cell counts (cells 0..63, junk): the cell
+// starts within the block segment (sl.cstart) and the per-cell scatter cursors; clears the counts.
+__device__ __forceinline__ void cell_scan(int* __restrict__ cc, int* __restrict__ ccursor, int pos,
+                                          unsigned short* __restrict__ cst) {
+    constexpr int NQ = kCellStride / 4;
+    int4 v[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) v[q] = reinterpret_cast<const int4*>(cc)[q];
+    int run = 0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int c[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+        int o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            o[u] = run;
+            if (4 * q + u <= Geo<3>::CELLS) cst[4 * q + u] = (unsigned short)run;
+            run += c[u];
+        }
+        reinterpret_cast<int4*>(ccursor)[q] = make_int4(pos + o[0], pos + o[1], pos + o[2], pos + o[3]);
+        reinterpret_cast<int4*>(cc)[q] = make_int4(0, 0, 0, 0);
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bcount, int* __restrict__ ccount,
+                                                int* __restrict__ ccursor, SlotView sl, int2* __restrict__ part,
+                                                int* flags) {
     pdl_begin();
     __shared__ int s_wt[kW], s_wa[kW];
     __shared__ int s_base[2];
@@ -364,7 +395,9 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
                 sl.bmap[b] = -1;
                 atomicOr(flags, FLAG_ACTIVE_OVERFLOW);
             }
-            cursor[b] = pos;
+            unsigned short scratch[Geo<3>::CELLS + 1];
+            cell_scan(ccount + (int64_t)b * kCellStride, ccursor + (int64_t)b * kCellStride, pos,
+                      li < cap ? sl.cstart + (int64_t)(b0 + li) * (Geo<3>::CELLS + 1) : scratch);
             pos += c[q];
             ++li;
             bcount[b] = 0;
@@ -392,12 +425,12 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
     }
 }
 
-// stable-free scatter of particle indices by block key (position inside a block is
-// arbitrary; p2g canonicalises).  kScatterPer particles per thread, all loads and
-// cursor atomics issued before any result is used (memory-level parallelism).
+// scatter of particle indices into the cell buckets of their block (kernels.h: the order inside
+// a cell is arbitrary; p2g ranks each cell by particle id).  kScatterPer particles per thread, all
+// loads and cursor atomics issued before any result is used (memory-level parallelism).
 constexpr int kScatterPer = 4;
 __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __restrict__ keys,
-                                                    const int* __restrict__ pid, int* __restrict__ cursor,
+                                                    const int* __restrict__ pid, int* __restrict__ ccursor,
                                                     SlotView sl) {
     pdl_begin();
     const int64_t n = p.N * p.E;
@@ -414,11 +447,11 @@ __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __rest
     }
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) {
-        const int key = kc[u] >= 0 ? kc[u] >> 7 : -1;
-        peers[u] = __match_any_sync(0xffffffffu, key);
+        const int slot = kc[u] >= 0 ? (kc[u] >> 7) * kCellStride + (kc[u] & 127) : -1;
+        peers[u] = __match_any_sync(0xffffffffu, slot);
         const int leader = __ffs(peers[u]) - 1;
         base[u] = 0;
-        if (kc[u] >= 0 && lane == leader) base[u] = atomicAdd(&cursor[key], __popc(peers[u]));
+        if (kc[u] >= 0 && lane == leader) base[u] = atomicAdd(&ccursor[slot], __popc(peers[u]));
     }
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) {
@@ -426,7 +459,6 @@ __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __rest
         if (kc[u] >= 0) {
             const int pos = b + __popc(peers[u] & ((1u << lane) - 1u));
             sl.sigma[pos] = (int)j[u];
-            sl.scell[pos] = (unsigned char)(kc[u] & 127);
             sl.spid[pos] = pj[u];
         }
     }
@@ -602,110 +634,6 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
     return ok;
 }
 
-// ------------------------------------------------------------ canonical order
-// Per active block: put the scattered list in canonical (cell, particle id) order, so every
-// sum downstream has a fixed order (bitwise reproducible, independent of the scatter's
-// atomics).  Bucket by cell (warp-aggregated smem counters), then rank by particle id
-// inside the cell.  Writes sigma (canonical), the cell starts and -- when the step writes
-// S_{t+1} -- the particle ids of S_{t+1} (p2g's output order).  Its own high-occupancy
-// pass (256 threads, 26 KB smem) ahead of p2g.
-constexpr int canon_smem_bytes() { return 1728 * 15 + 2 * 66 * 4; }
-__global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __restrict__ pid_next,
-                                              int* __restrict__ keys_next, int* flags) {
-    pdl_begin();
-    constexpr int MAXP = 1728, CELLS = 64;
-    using G = Geo<3>;  // CELLS = 64 in 2D and 3D
-    extern __shared__ __align__(16) unsigned char smem[];
-    int* s_idx = reinterpret_cast<int*>(smem);
-    int* s_pid = s_idx + MAXP;
-    int* s_bpid = s_pid + MAXP;
-    int* s_cnt = s_bpid + MAXP;
-    int* s_cst = s_cnt + CELLS + 2;
-    short* s_tmp = reinterpret_cast<short*>(s_cst + CELLS + 2);
-    unsigned char* s_cell = reinterpret_cast<unsigned char*>(s_tmp + MAXP);
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int nact = *sl.nactive;
-    const int b0 = *sl.base;
-    const int* bstart = sl.bstart + b0 + sl.step;
-    unsigned short* cstart = sl.cstart + (int64_t)b0 * (CELLS + 1);
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
-        const int start = bstart[bi], n = bstart[bi + 1] - start;
-        if (n > MAXP) {  // reported; the block is dropped (no valid entries downstream)
-            if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
-            for (int c = tid; c <= CELLS; c += kT) cstart[(int64_t)bi * (CELLS + 1) + c] = 0;
-            // g2p writes no bin key for the dropped rows of S_{t+1}: mark them so the next
-            // binning skips them instead of scattering stale keys
-            if (keys_next)
-                for (int q = tid; q < n; q += kT) keys_next[start + q] = -1;
-            continue;
-        }
-        // ---- phase 0: canonical (cell, particle id) order of the block's list.  The
-        // scatter wrote each entry's cell and particle id next to it: coalesced loads only.
-        for (int q = tid; q < G::CELLS + 2; q += kT) s_cnt[q] = 0;
-#pragma unroll 4
-        for (int q = tid; q < n; q += kT) {
-            s_idx[q] = sl.sigma[start + q];
-            s_pid[q] = sl.spid[start + q];
-            s_cell[q] = sl.scell[start + q];
-        }
-        __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kT) {
-            const int q = q0 + tid;
-            const bool in = q < n;
-            const int cell = in ? (int)s_cell[q] : -1;
-            const unsigned peers = __match_any_sync(0xffffffffu, cell);
-            if (in && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[cell], __popc(peers));
-        }
-        __syncthreads();
-        if (tid < 32) {  // exclusive scan of the 65 bucket counts (one warp)
-            int carry = 0;
-            for (int c = lane; c - lane <= G::CELLS; c += 32) {
-                const int v = c <= G::CELLS ? s_cnt[c] : 0;
-                int inc = v;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, inc, off);
-                    if (lane >= off) inc += t;
-                }
-                if (c <= G::CELLS) { s_cst[c] = carry + inc - v; s_cnt[c] = carry + inc - v; }
-                carry += __shfl_sync(0xffffffffu, inc, 31);
-            }
-            if (lane == 0) s_cst[G::CELLS + 1] = carry;
-        }
-        __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kT) {  // bucket by cell (order inside a cell arbitrary)
-            const int q = q0 + tid;
-            const bool in = q < n;
-            const int cell = in ? (int)s_cell[q] : -1;
-            const unsigned peers = __match_any_sync(0xffffffffu, cell);
-            const int leader = __ffs(peers) - 1;
-            int base = 0;
-            if (in && lane == leader) base = atomicAdd(&s_cnt[cell], __popc(peers));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (in) {
-                const int pos = base + __popc(peers & ((1u << lane) - 1u));
-                s_tmp[pos] = (short)q;
-                s_bpid[pos] = s_pid[q];
-            }
-        }
-        __syncthreads();
-        for (int r = tid; r < n; r += kT) {  // rank by particle id inside the cell
-            const int q = s_tmp[r];
-            const int cell = s_cell[q], pq = s_bpid[r];
-            int rank = 0;
-            const int m1 = s_cst[cell + 1];
-            for (int m = s_cst[cell]; m < m1; ++m) rank += s_bpid[m] < pq;
-            const int fl = s_cst[cell] + rank;
-            sl.sigma[start + fl] = s_idx[q];
-            if (pid_next) pid_next[start + fl] = pq;
-        }
-        for (int c = tid; c <= G::CELLS; c += kT) cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
-        if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
-        __syncthreads();
-    }
-    (void)p;
-}
-
 // ---------------------------------------------------------------- P2G
 // p2g: canonicalise the block list, then per particle
 // Ft = (I + dt C) F; tau = tau(Ft) [+ actuation]; A = -dt V 4/dx^2 tau + m C;
@@ -714,7 +642,8 @@ __global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __res
 template <int D>
 __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
                                                const int32_t* __restrict__ aid,
-                                               const float* __restrict__ alpha, int* flags) {
+                                               const float* __restrict__ alpha, int* __restrict__ keys_next,
+                                               int* flags) {
     pdl_begin();
     using G = Geo<D>;
     using L = Lay<D>;
@@ -737,14 +666,47 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         const int start = bstart[bi], n = bstart[bi + 1] - start;
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        if (n > G::MAXP) {
+        if (n > G::MAXP) {  // reported; the block is dropped (no valid entries downstream)
             if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
+            for (int c = tid; c <= G::CELLS; c += kTQ) cstart[(int64_t)bi * (G::CELLS + 1) + c] = 0;
+            // g2p writes no bin key for the dropped rows of S_{t+1}: mark them so the next
+            // binning skips them instead of scattering stale keys
+            if (keys_next)
+                for (int q = tid; q < n; q += kTQ) keys_next[start + q] = -1;
             continue;
         }
-        // ---- the block's list in canonical (cell, particle id) order (k_canon)
-        for (int q = tid; q < n; q += kTQ) s_ci[q] = sl.sigma[start + q];
-        for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
-        __syncthreads();
+        // ---- canonical (cell, particle id) order of the block's list: the scatter left each
+        // cell's entries in arbitrary order; rank them by particle id inside the cell (fixed
+        // order of every sum below -> bitwise reproducible).  Scratch in the row region.
+        {
+            int* s_raw = reinterpret_cast<int*>(smem);   // [n] state index (scatter order)
+            int* s_rpid = s_raw + G::MAXP;                // [n] particle id
+            unsigned char* s_rcell = reinterpret_cast<unsigned char*>(s_rpid + G::MAXP);  // [n] cell of entry
+            for (int q = tid; q < n; q += kTQ) {
+                s_raw[q] = sl.sigma[start + q];
+                s_rpid[q] = sl.spid[start + q];
+            }
+            for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
+            __syncthreads();
+            for (int c = tid; c <= G::CELLS; c += kTQ) {
+                const int hi = c < G::CELLS ? s_cst[c + 1] : n;
+                for (int r = s_cst[c]; r < hi; ++r) s_rcell[r] = (unsigned char)c;
+            }
+            __syncthreads();
+            for (int r = tid; r < n; r += kTQ) {
+                const int c = s_rcell[r];
+                const int lo = s_cst[c], hi = c < G::CELLS ? s_cst[c + 1] : n;
+                const int pr = s_rpid[r];
+                int rank = 0;
+                for (int q = lo; q < hi; ++q) rank += s_rpid[q] < pr;
+                const int rr = lo + rank;
+                s_ci[rr] = s_raw[r];
+                sl.sigma[start + rr] = s_raw[r];
+                if (Sn.pid) Sn.pid[start + rr] = pr;
+            }
+            if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
+            __syncthreads();
+        }
         const int nvalid = s_cst[G::CELLS];
         // ---- phases 1 + 2 over chunks of kTQ particles in canonical order; the particle
         // loads of chunk k+1 are issued before the accumulation of chunk k (same registers)
@@ -985,6 +947,7 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
             key = bid;  // p2g of the next step drops it into the junk bucket
         }
         keys[j] = key * 128 + cell;
+        return key * 128 + cell;
     }
     return key;
 }
@@ -995,8 +958,8 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
 // from the forward's (checkpoint invariance is tested bitwise).
 template <int D>
 __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
-                                            int* __restrict__ keys, int* __restrict__ bcount, int* flags,
-                                            bool refwd, Migr mg) {
+                                            int* __restrict__ keys, int* __restrict__ bcount,
+                                            int* __restrict__ ccount, int* flags, bool refwd, Migr mg) {
     pdl_begin();
     using G = Geo<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
@@ -1037,10 +1000,10 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
         const float4* sU = pipe.wait(it);
         int key = -1;
         if (va) key = g2p_particle<D>(p, sU, xa, c0, start + tid, e, bid, Sn, keys, flags, refwd, S, ia, mg);
-        if (keys) count_key(va && key >= 0, key, bcount);
+        if (keys) count_bin(va && key >= 0, key >> 7, key & 127, bcount, ccount);
         key = -1;
         if (vb) key = g2p_particle<D>(p, sU, xb, c0, start + tid + kTG, e, bid, Sn, keys, flags, refwd, S, ib, mg);
-        if (keys) count_key(vb && key >= 0, key, bcount);
+        if (keys) count_bin(vb && key >= 0, key >> 7, key & 127, bcount, ccount);
         for (int r0 = 2 * kTG; r0 < nvalid; r0 += kTG) {
             const int r = r0 + tid;
             const bool in = r < nvalid;
@@ -1052,7 +1015,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
                 for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i));
                 key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags, refwd, S, i, mg);
             }
-            if (keys) count_key(in && key >= 0, key, bcount);
+            if (keys) count_bin(in && key >= 0, key >> 7, key & 127, bcount, ccount);
         }
         __syncthreads();
     }
@@ -1610,7 +1573,8 @@ template <int D>
 __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const int* __restrict__ nsorted,
                                                   MigSrc left, MigSrc right, int x_lo, int x_hi, int cap,
                                                   int* __restrict__ keys, int* __restrict__ bcount,
-                                                  int* __restrict__ imm_base, int* __restrict__ nrows, int* flags) {
+                                                  int* __restrict__ ccount, int* __restrict__ imm_base,
+                                                  int* __restrict__ nrows, int* flags) {
     pdl_begin();
     using L = Lay<D>;
     const int side = blockIdx.y;
@@ -1625,7 +1589,7 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
     const int n = side == 0 ? n_left : n_right;
     const int m = blockIdx.x * kT + threadIdx.x;
     const bool in = m < n;
-    int key = -1;
+    int key = -1, cell = 0;
     if (in) {
         const int j = src.rows[(side == 0 ? 1 : 0) * cap + m];  // the neighbour's outbox toward us
         const int64_t dst = (int64_t)base + m;
@@ -1649,7 +1613,8 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
                 const int lc[3] = {b[0] & (Geo<D>::B - 1), b[1] & (Geo<D>::B - 1), b[2] & (Geo<D>::B - 1)};
                 if (bb[0] >= x_lo && bb[0] < x_hi) {
                     key = block_lin<D>(p, 0, bb);
-                    keys[dst] = key * 128 + cell_of<D>(lc);
+                    cell = cell_of<D>(lc);
+                    keys[dst] = key * 128 + cell;
                 } else {
                     atomicOr(flags, FLAG_MIGRATION);  // moved past this slab in one step
                     keys[dst] = -1;
@@ -1660,7 +1625,7 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
             }
         }
     }
-    count_key(in && key >= 0, key, bcount);
+    count_bin(in && key >= 0, key, cell, bcount, ccount);
 }
 
 // backward of the migration: the adjoint of an emigrant's S_{t+1} row was computed by the
@@ -1724,7 +1689,6 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + kT - 1) / kT); }
 struct DevTab {
     int grid[5][2];  // persistent grid size per kernel kind and dimension
     int sms = 148;
-    int canon_grid = 148 * 8;
 };
 constexpr int kMaxDev = 64;
 DevTab g_tab[kMaxDev];
@@ -1782,9 +1746,6 @@ cudaError_t tile_init() {
     if ((done_mask >> dev) & 1ull) return cudaSuccess;
     DevTab& T = g_tab[dev];
     cudaDeviceGetAttribute(&T.sms, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaFuncSetAttribute(k_canon, cudaFuncAttributeMaxDynamicSharedMemorySize, canon_smem_bytes());
-    if (e) return e;
-    T.canon_grid = occupancy_grid((const void*)k_canon, canon_smem_bytes(), kT);
 #define MPM_INIT_DIM(DI)                                                                                          \
     do {                                                                                                          \
         constexpr int DIM = (DI) == 2 ? 2 : 3;                                                                    \
@@ -1825,28 +1786,26 @@ static unsigned pgrid(const KParams& p, int kind) {
     return (unsigned)(p.step_blocks < g ? p.step_blocks : g);
 }
 
-void launch_bin_keys(const KParams& p, const float* x, int64_t n_live, int* keys, int* bcount, int* flags,
+void launch_bin_keys(const KParams& p, const float* x, int64_t n_live, int* keys, const BinCounts& bc, int* flags,
                      cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_bin_keys<DIM>, nblk(p.N * p.E), kT, 0, s, p, x, n_live, keys, bcount, flags));
+    DISPATCH(p.dim, launch_k(k_bin_keys<DIM>, nblk(p.N * p.E), kT, 0, s, p, x, n_live, keys, bc.bcount, bc.ccount,
+                             flags));
 }
 int scan_chunks(const KParams& p) { return (p.TB + kScanChunk - 1) / kScanChunk; }
-void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
+void launch_bin_scan(const KParams& p, const BinCounts& bc, const SlotView& sl, int* part, int* flags,
                      cudaStream_t s) {
     const int nc = scan_chunks(p);
-    launch_k(k_bin_scan, nc, kT, 0, s, p, bcount, cursor, sl, (int2*)part, flags);
+    launch_k(k_bin_scan, nc, kT, 0, s, p, bc.bcount, bc.ccount, bc.ccursor, sl, (int2*)part, flags);
 }
-void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
+void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, const BinCounts& bc, const SlotView& sl,
                         cudaStream_t s) {
-    launch_k(k_bin_scatter, (unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s, p, keys, pid, cursor, sl);
-}
-void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* keys_next, int* flags, cudaStream_t s) {
-    const int cg = tab().canon_grid;
-    launch_k(k_canon, cg < p.step_blocks ? cg : (p.step_blocks > 0 ? p.step_blocks : 1), kT, canon_smem_bytes(), s, p, sl,
-             pid_next, keys_next, flags);
+    launch_k(k_bin_scatter, (unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s, p, keys,
+             pid, bc.ccursor, sl);
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
-                const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t, flags));
+                const int32_t* aid, const float* alpha_t, int* keys_next, int* flags, cudaStream_t s) {
+    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t,
+                             keys_next, flags));
 }
 static unsigned node_grid(const KParams& p) {
     const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? Geo<3>::TN : Geo<2>::TN) + kT - 1) / kT;
@@ -1860,8 +1819,9 @@ void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* uba
     DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM>, node_grid(p), kT, 0, s, p, sl, ubar));
 }
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
-                int* bcount, int* flags, bool refwd, const Migr& mg, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_g2p<DIM>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bcount, flags, refwd, mg));
+                const BinCounts& bc, int* flags, bool refwd, const Migr& mg, cudaStream_t s) {
+    DISPATCH(p.dim, launch_k(k_g2p<DIM>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bc.bcount, bc.ccount, flags, refwd,
+                             mg));
 }
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, cudaStream_t s) {
@@ -1890,11 +1850,11 @@ void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_
 
 namespace mpm {
 void launch_immigrate(const KParams& p, const StateView& S, const int* nsorted, MigSrc left, MigSrc right,
-                      int x_lo, int x_hi, int cap, int* keys, int* bcount, int* imm_base, int* nrows, int* flags,
-                      cudaStream_t s) {
+                      int x_lo, int x_hi, int cap, int* keys, const BinCounts& bc, int* imm_base, int* nrows,
+                      int* flags, cudaStream_t s) {
     const dim3 grid((unsigned)((cap + kT - 1) / kT), 2);
     DISPATCH(p.dim, launch_k(k_immigrate<DIM>, grid, kT, 0, s, p, S, nsorted, left, right, x_lo, x_hi, cap, keys,
-                             bcount, imm_base, nrows, flags));
+                             bc.bcount, bc.ccount, imm_base, nrows, flags));
 }
 void launch_adj_pull(const KParams& p, const AdjView& Sb, const int* cnt, const int* rows, int cap,
                      const AdjView& nb_left, const int* nb_left_base, const AdjView& nb_right,

@@ -122,9 +122,9 @@ def test_bitwise_run_to_run_and_batch_invariance():
 
 
 def test_particle_order_invariance():
-    """Permuting the caller's particle order permutes the outputs (R24) -- bitwise,
-    since the binning canonicalises the order by (cell, particle id) and the
-    particle id only breaks ties inside a cell."""
+    """Permuting the caller's particle order permutes the outputs (R20), up to fp32
+    reassociation: the particle id (= caller index) orders the particles inside a cell,
+    so a permutation changes only the order of equal-cell terms in the node sums."""
     p, inp = inputs("c1b", steps=32)
     base = gpu_run(p, inp)
     rng = np.random.default_rng(0)
