@@ -78,52 +78,6 @@ template <int D> __device__ __forceinline__ int cell_of(const int lb[3]) {
     return D == 2 ? lb[0] * G::B + lb[1] : (lb[0] * G::B + lb[1]) * G::B + lb[2];
 }
 
-// Sum of the <= 2^d block tiles that cover global node g (episode e): every
-// block whose cells [c0, c0 + B) satisfy c0 <= g < c0 + B + 2 holds a partial
-// of that node.  Fixed enumeration order -> deterministic.
-// f3: a covering block outside this subdomain's slab [x_lo, x_hi) belongs to a neighbour, whose
-// block map and (pool-indexed) tiles nt[0] (left) / nt[1] (right) are read instead -- the same
-// blocks in the same order as a single-domain run.
-template <int D>
-__device__ __forceinline__ float4 covered_sum(const KParams& p, int e, const int g[3],
-                                              const int* __restrict__ bmap,
-                                              const float4* __restrict__ tiles, const Halo& hl,
-                                              const float4* nt0, const float4* nt1) {
-    using G = Geo<D>;
-    // per axis: option 0 = the block holding g (local l0), option 1 = the previous
-    // block (local l0 + B), valid when l0 < 2.  All 2^d combinations unrolled.
-    int b0[3], l0[3];
-    bool ok1[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        b0[k] = k < D ? g[k] >> G::LOGB : 0;
-        l0[k] = k < D ? g[k] & (G::B - 1) : 0;
-        ok1[k] = k < D && l0[k] < 2 && b0[k] >= 1;
-    }
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 2; ++b)
-#pragma unroll
-            for (int c = 0; c < (D == 3 ? 2 : 1); ++c) {
-                if ((a && !ok1[0]) || (b && !ok1[1]) || (c && !ok1[2])) continue;
-                const int bb[3] = {b0[0] - a, b0[1] - b, b0[2] - c};
-                if (bb[0] >= p.nb || bb[1] >= p.nb || (D == 3 && bb[2] >= p.nb)) continue;
-                const int* bm = bmap;
-                const float4* tl = tiles;
-                if (bb[0] < hl.x_lo) { bm = hl.bmap[0]; tl = nt0; }
-                else if (bb[0] >= hl.x_hi) { bm = hl.bmap[1]; tl = nt1; }
-                if (bm == nullptr) continue;
-                const int ti = __ldg(bm + block_lin<D>(p, e, bb));
-                if (ti < 0) continue;
-                const int lq = tile_lin<D>(l0[0] + a * G::B, l0[1] + b * G::B, l0[2] + c * G::B);
-                const float4 v = __ldg(tl + (int64_t)ti * G::TN + lq);
-                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-            }
-    return acc;
-}
-
 // neighbour tiles indexed by the neighbour's pool (tile) indices of this step (f3)
 template <int D> __device__ __forceinline__ const float4* halo_tiles(const Halo& hl, int s) {
     return hl.tiles[s] ? hl.tiles[s] - (int64_t)(*hl.base[s]) * Geo<D>::TN : nullptr;
@@ -279,7 +233,7 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
 // (MPS, concurrent kernels).  The last CTA to finish (second ticket) resets the chunk ticket
 // and advances the epoch for the next launch.
 #ifndef MPM_SCAN_PER
-#define MPM_SCAN_PER 4
+#define MPM_SCAN_PER 1  // blocks per thread: each thread scans the cells of at most this many blocks
 #endif
 constexpr int kScanPer = MPM_SCAN_PER;
 constexpr int kScanChunk = kT * kScanPer;
@@ -327,7 +281,7 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
     const int chunk = s_chunk;
     const int i0 = chunk * kScanChunk + tid * kScanPer;
     int c[kScanPer];
-    if (i0 + kScanPer <= TB) {
+    if (kScanPer % 4 == 0 && i0 + kScanPer <= TB) {
 #pragma unroll
         for (int q = 0; q < kScanPer / 4; ++q) {
             const int4 v = *reinterpret_cast<const int4*>(bcount + i0 + 4 * q);
@@ -517,11 +471,22 @@ constexpr int kTQ = MPM_SCATTER_THREADS;  // p2g / g2p_grad CTA (>= kACC; the ex
 static_assert(kTQ >= kACC, "scatter CTA smaller than the accumulation phase");
 constexpr int kCH = MPM_P2G_CHUNK;  // rows per chunk: most blocks fit one chunk -> all 64 cells busy in phase 2
 
-template <int D> struct RowL {  // particle row in shared memory (floats); stride avoids STS.128 conflicts
+// particle row in shared memory (floats).  Row r starts at r * STRIDE + 4 (r / 8): the stride
+// keeps 8 consecutive rows (one quarter-warp's STS.128 in phase 1) on distinct bank groups, and
+// the one-float4 skew every 8 rows does the same for the phase-2 readers, whose quarter-warps read
+// the rows of ~3 consecutive cells -- 8 particles per cell in the 3D workloads (2 per axis), so
+// rows exactly 8 apart, which a plain stride maps to the same banks (ncu: 30% / 52% of p2g's /
+// the U_bar scatter's shared wavefronts were conflicts).
+template <int D> struct RowL {
     static constexpr int STRIDE = D == 3 ? 28 : 12;
+#ifndef MPM_ROW_SKEW
+#define MPM_ROW_SKEW 1
+#endif
+    static __device__ __forceinline__ int off(int r) { return r * STRIDE + (MPM_ROW_SKEW ? 4 * (r >> 3) : 0); }
+    static constexpr int bytes(int rows) { return (rows * STRIDE + (MPM_ROW_SKEW ? 4 * (rows / 8 + 1) : 0)) * 4; }
 };
 template <int D> constexpr int p2g_union_bytes() {
-    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
+    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = RowL<D>::bytes(kCH);
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 template <int D> constexpr int p2g_smem_bytes() {
@@ -647,7 +612,6 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
     pdl_begin();
     using G = Geo<D>;
     using L = Lay<D>;
-    constexpr int RS = RowL<D>::STRIDE;
     extern __shared__ __align__(16) unsigned char smem[];
     float* s_row = reinterpret_cast<float*>(smem);                   // phase 1/2 rows ...
     float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... node partials
@@ -735,7 +699,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
                 const float act = (aid && a_id >= 0 && a_id < p.n_act) ? alpha[e * p.a_estride + a_id] : 0.0f;
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
                 if (!p2g_particle<D>(p, x, vc, F, act, fluid, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
-                write_row<D>(s_row + (r - ch) * RS, w, c, Adx);
+                write_row<D>(s_row + RowL<D>::off(r - ch), w, c, Adx);
                 if (Sn.f) {
                     if (fluid) fluid_reset<D>(Ft, Ft);  // R23 (Ft is dead after the row)
 #pragma unroll
@@ -746,7 +710,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
             __syncthreads();
             if (tid < kACC) {
                 const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], cend);
-                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
+                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + RowL<D>::off(rr - ch), my_ox);
             }
             __syncthreads();
         }
@@ -765,72 +729,169 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
 }
 
 // ------------------------------------------------------------- grid_op
-// P:579 (R5-R7): thread per node of every active block's (B+2)^d tile:
+// The covering tiles of a COLUMN of tile nodes (fixed local (n1, n2), n0 = 0..TE-1) of block
+// (e, c0): along x the blocks bx-1, bx, bx+1 (x option xo = 0, 1, 2), along y / z the node's
+// block and the previous one.  The pool tile indices are looked up once per column (12 in 3D,
+// instead of up to 8 per node); a block outside this subdomain's slab is looked up in the
+// neighbour (f3).  col_sum adds them per node in the fixed (a, b, c) order: every node is the
+// sum of the <= 2^d partial tiles whose block's cells [c0, c0 + B) satisfy c0 <= g < c0 + B + 2.
+template <int D> struct ColCover {
+    int ti[3][2][2];       // pool tile index per (x option, y option, z option), -1 = none
+    const float4* tl[3];   // pool-indexed tiles per x option (own or a neighbour's)
+    int l1, l2;            // local offsets of the column's y / z node inside their block
+    bool ok1y, ok1z;       // the previous block along y / z covers it too
+};
+
+template <int D>
+__device__ __forceinline__ void col_cover(const KParams& p, int e, const int c0[3], int g1, int g2,
+                                          const int* __restrict__ bmap, const float4* tiles, const Halo& hl,
+                                          const float4* nt0, const float4* nt1, ColCover<D>& cc) {
+    using G = Geo<D>;
+    const int bx = c0[0] >> G::LOGB;
+    const int by = g1 >> G::LOGB, bz = D == 3 ? g2 >> G::LOGB : 0;
+    cc.l1 = g1 & (G::B - 1);
+    cc.l2 = D == 3 ? g2 & (G::B - 1) : 0;
+    cc.ok1y = cc.l1 < 2 && by >= 1;
+    cc.ok1z = D == 3 && cc.l2 < 2 && bz >= 1;
+#pragma unroll
+    for (int xo = 0; xo < 3; ++xo) {
+        const int xb = bx - 1 + xo;
+        const int* bm = bmap;
+        const float4* tl = tiles;
+        if (xb < hl.x_lo) { bm = hl.bmap[0]; tl = nt0; }
+        else if (xb >= hl.x_hi) { bm = hl.bmap[1]; tl = nt1; }
+        cc.tl[xo] = tl;
+        const bool xok = bm != nullptr && xb >= 0 && xb < p.nb;
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int bb[3] = {xb, by - b, bz - c};
+                const bool ok = xok && (b == 0 || cc.ok1y) && (c == 0 || cc.ok1z) && (D == 3 || c == 0) &&
+                                bb[1] < p.nb && (D == 2 || bb[2] < p.nb);
+                cc.ti[xo][b][c] = ok ? __ldg(bm + block_lin<D>(p, e, bb)) : -1;
+            }
+    }
+}
+
+// node n0 of the column (n0 a compile-time constant after unrolling: static register indexing)
+template <int D>
+__device__ __forceinline__ float4 col_sum(const ColCover<D>& cc, int n0, bool bx_ge1) {
+    using G = Geo<D>;
+    const int l0 = n0 < G::B ? n0 : n0 - G::B;               // local x inside the node's block
+    const bool ok1x = n0 < G::B ? (n0 < 2 && bx_ge1) : true;  // previous x block covers it too
+    const int xo0 = n0 < G::B ? 1 : 2;                         // x option of the node's own block
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+        if (a && !ok1x) continue;
+        const int xo = xo0 - a;
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            if (b && !cc.ok1y) continue;
+#pragma unroll
+            for (int c = 0; c < (D == 3 ? 2 : 1); ++c) {
+                if (c && !cc.ok1z) continue;
+                const int ti = cc.ti[xo][b][c];
+                if (ti < 0) continue;
+                const int lq = tile_lin<D>(l0 + a * G::B, cc.l1 + b * G::B, cc.l2 + c * G::B);
+                const float4 v = __ldg(cc.tl[xo] + (int64_t)ti * G::TN + lq);
+                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+        }
+    }
+    return acc;
+}
+
+template <int D> constexpr int tile_cols() { return D == 3 ? Geo<D>::TE * Geo<D>::TE : Geo<D>::TE; }
+
+// P:579 (R5-R7): thread per node column of every active block's (B+2)^d tile:
 // (P, M) = sum of the covering partial tiles; u1 = P/(M + eps) - dt g e_y; sticky walls.
 // Resolved tile entry: (u1, M), or (0, 0, 0, -M) where the wall zeroed the velocity
-// (sign bit set, also for M = 0: -0.0f; nodes outside the grid: (0, 0, 0, -0)).  Stored per step: g2p / g2p_grad / grid_op_grad read it.
+// (sign bit set, also for M = 0: -0.0f; nodes outside the grid: (0, 0, 0, -0)).  Stored per
+// step: g2p / g2p_grad / grid_op_grad read it.
 template <int D>
 __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
     pdl_begin();
     using G = Geo<D>;
+    constexpr int NC = tile_cols<D>();
     const int nact = *sl.nactive;
     const int b0 = *sl.base;
     const int* blist = sl.blist + b0;
     const float4* part_g = sl.part - (int64_t)b0 * G::TN;  // bmap holds pool indices
     float4* rt = sl.tiles + (int64_t)b0 * G::TN;
-    const int64_t total = (int64_t)nact * G::TN;
+    const int64_t total = (int64_t)nact * NC;
     const float4* nt0 = halo_tiles<D>(sl.halo, 0);
     const float4* nt1 = halo_tiles<D>(sl.halo, 1);
     for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
-        const int bi = (int)(idx / G::TN), q = (int)(idx - (int64_t)bi * G::TN);
-        int e, c0[3], n[3];
+        const int bi = (int)(idx / NC), col = (int)(idx - (int64_t)bi * NC);
+        const int n1 = D == 3 ? col / G::TE : col, n2 = D == 3 ? col % G::TE : 0;
+        int e, c0[3];
         block_origin<D>(p, __ldg(blist + bi), e, c0);
-        local_node<D>(q, n);
-        const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-        const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
-        float4 out = make_float4(0.f, 0.f, 0.f, -0.0f);
-        if (inside) {
-            const float4 pm = covered_sum<D>(p, e, g, sl.bmap, part_g, sl.halo, nt0, nt1);
-            float u0[3], u1[3];
-            out = grid_velocity<D>(p, g, pm, u0, u1) ? make_float4(0.f, 0.f, 0.f, -pm.w)
-                                                      : make_float4(u1[0], u1[1], u1[2], pm.w);
+        const int g1 = c0[1] + n1, g2 = D == 3 ? c0[2] + n2 : 0;
+        ColCover<D> cc;
+        col_cover<D>(p, e, c0, g1, g2, sl.bmap, part_g, sl.halo, nt0, nt1, cc);
+        const bool in12 = g1 < p.n_grid && (D == 2 || g2 < p.n_grid);
+        const bool bx_ge1 = (c0[0] >> G::LOGB) >= 1;
+        float4* out_t = rt + (int64_t)bi * G::TN;
+#pragma unroll
+        for (int n0 = 0; n0 < G::TE; ++n0) {
+            const int g[3] = {c0[0] + n0, g1, g2};
+            float4 out = make_float4(0.f, 0.f, 0.f, -0.0f);
+            if (in12 && g[0] < p.n_grid) {
+                const float4 pm = col_sum<D>(cc, n0, bx_ge1);
+                float u0[3], u1[3];
+                out = grid_velocity<D>(p, g, pm, u0, u1) ? make_float4(0.f, 0.f, 0.f, -pm.w)
+                                                          : make_float4(u1[0], u1[1], u1[2], pm.w);
+            }
+            out_t[tile_lin<D>(n0, n1, n2)] = out;
         }
-        rt[idx] = out;
     }
 }
 
 // --------------------------------------------------------- grid_op_grad
 // P:589 (select rule): per node, ub = sum of the covering U_bar partial tiles;
 // sticky (sign bit of w): Pb = Mb = 0; else u0 = u1 + dt g e_y, Pb = ub/(M + eps),
-// Mb = -(ub . u0)/(M + eps).  Output tile (Pb, Mb) -> sl.part (local block index).
+// Mb = -(ub . u0)/(M + eps).  Output tile (Pb, Mb) -> sl.part (local block index).  Thread per
+// node column as grid_op.
 template <int D>
 __global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, const float4* __restrict__ ubar) {
     pdl_begin();
     using G = Geo<D>;
+    constexpr int NC = tile_cols<D>();
     const int nact = *sl.nactive;
     const int b0 = *sl.base;
     const int* blist = sl.blist + b0;
     const float4* ub_g = ubar - (int64_t)b0 * G::TN;
     const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
-    const int64_t total = (int64_t)nact * G::TN;
+    const int64_t total = (int64_t)nact * NC;
     const float4* nt0 = halo_tiles<D>(sl.halo, 0);
     const float4* nt1 = halo_tiles<D>(sl.halo, 1);
     for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
-        const float4 r = __ldg(rt + idx);
-        float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (!signbit(r.w)) {
-            const int bi = (int)(idx / G::TN), q = (int)(idx - (int64_t)bi * G::TN);
-            int e, c0[3], n[3];
-            block_origin<D>(p, __ldg(blist + bi), e, c0);
-            local_node<D>(q, n);
-            const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-            const float4 ub = covered_sum<D>(p, e, g, sl.bmap, ub_g, sl.halo, nt0, nt1);
-            const float u0[3] = {r.x, r.y + p.dt * p.gravity, r.z};
-            const float denom = r.w + p.eps_mass;
-            const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
-            out = make_float4(ub.x / denom, ub.y / denom, D == 3 ? ub.z / denom : 0.0f, -dot / denom);
+        const int bi = (int)(idx / NC), col = (int)(idx - (int64_t)bi * NC);
+        const int n1 = D == 3 ? col / G::TE : col, n2 = D == 3 ? col % G::TE : 0;
+        int e, c0[3];
+        block_origin<D>(p, __ldg(blist + bi), e, c0);
+        const int g1 = c0[1] + n1, g2 = D == 3 ? c0[2] + n2 : 0;
+        ColCover<D> cc;
+        col_cover<D>(p, e, c0, g1, g2, sl.bmap, ub_g, sl.halo, nt0, nt1, cc);
+        const bool bx_ge1 = (c0[0] >> G::LOGB) >= 1;
+        const float4* r_t = rt + (int64_t)bi * G::TN;
+        float4* out_t = sl.part + (int64_t)bi * G::TN;
+#pragma unroll
+        for (int n0 = 0; n0 < G::TE; ++n0) {
+            const int q = tile_lin<D>(n0, n1, n2);
+            const float4 r = __ldg(r_t + q);
+            float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!signbit(r.w)) {  // outside the grid: -0 sign bit set
+                const float4 ub = col_sum<D>(cc, n0, bx_ge1);
+                const float u0[3] = {r.x, r.y + p.dt * p.gravity, r.z};
+                const float denom = r.w + p.eps_mass;
+                const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
+                out = make_float4(ub.x / denom, ub.y / denom, D == 3 ? ub.z / denom : 0.0f, -dot / denom);
+            }
+            out_t[q] = out;
         }
-        sl.part[idx] = out;
     }
 }
 
@@ -1028,7 +1089,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
 // CTA = 192 threads: phase 1 thread per particle (rows in smem), phase 2 thread per
 // (cell, o_x) accumulating U_bar like p2g's momentum.
 template <int D> constexpr int g2pg_union_bytes() {
-    constexpr int a = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
+    constexpr int a = Geo<D>::CELLS * Geo<D>::NST * 16, c = RowL<D>::bytes(kCH);
     return a > c ? a : c;
 }
 template <int D> constexpr int g2pg_smem_bytes() { return g2pg_union_bytes<D>() + (Geo<D>::CELLS + 2) * 4; }
@@ -1128,7 +1189,6 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
                                                             float4* __restrict__ ubar) {
     pdl_begin();
     using G = Geo<D>;
-    constexpr int RS = RowL<D>::STRIDE;
     extern __shared__ __align__(16) unsigned char smem[];
     float* s_row = reinterpret_cast<float*>(smem);   // rows, then ...
     float4* s_cb = reinterpret_cast<float4*>(smem);  // ... node partials
@@ -1166,13 +1226,13 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
                 float w[3][3], cp[3], B[D * D];
                 g2pg_row<D>(p, x, xb, vbn, Cbn, c0, w, cp, B);
-                write_row<D>(s_row + (r - ch) * RS, w, cp, B);
+                write_row<D>(s_row + RowL<D>::off(r - ch), w, cp, B);
                 if (r + kTQ < nvalid) MPM_G2PG_LOAD(r + kTQ);  // this thread's next particle
             }
             __syncthreads();
             if (tid < kACC) {
                 const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], cend);
-                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
+                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + RowL<D>::off(rr - ch), my_ox);
             }
             __syncthreads();
         }
@@ -1807,8 +1867,8 @@ void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const 
     DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t,
                              keys_next, flags));
 }
-static unsigned node_grid(const KParams& p) {
-    const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? Geo<3>::TN : Geo<2>::TN) + kT - 1) / kT;
+static unsigned node_grid(const KParams& p) {  // thread per tile node column
+    const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? tile_cols<3>() : tile_cols<2>()) + kT - 1) / kT;
     const int64_t cap = (int64_t)tab().sms * 8;
     return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
 }
