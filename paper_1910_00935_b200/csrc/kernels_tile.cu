@@ -22,6 +22,7 @@
 #include "kernels.h"
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -220,6 +221,9 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
         }
         keys[i] = key < 0 ? -1 : key * 128 + cell;
     }
+#ifdef MPM_DEBUG_CST
+    if (i < 6) printf("bin_keys i %d key %d cell %d ccount %p bcount %p\n", (int)i, key, cell, ccount, bcount);
+#endif
     count_bin(in && key >= 0, key, cell, bcount, ccount);
 }
 
@@ -239,6 +243,7 @@ constexpr int kScanPer = MPM_SCAN_PER;
 constexpr int kScanChunk = kT * kScanPer;
 // Also, per active block, the exclusive scan of its 65 cell counts (cells 0..63, junk): the cell
 // starts within the block segment (sl.cstart) and the per-cell scatter cursors; clears the counts.
+// cst == null: a block past the active-list capacity (its cell starts are not kept)
 __device__ __forceinline__ void cell_scan(int* __restrict__ cc, int* __restrict__ ccursor, int pos,
                                           unsigned short* __restrict__ cst) {
     constexpr int NQ = kCellStride / 4;
@@ -253,12 +258,15 @@ __device__ __forceinline__ void cell_scan(int* __restrict__ cc, int* __restrict_
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             o[u] = run;
-            if (4 * q + u <= Geo<3>::CELLS) cst[4 * q + u] = (unsigned short)run;
+            if (cst && 4 * q + u <= Geo<3>::CELLS) cst[4 * q + u] = (unsigned short)run;
             run += c[u];
         }
         reinterpret_cast<int4*>(ccursor)[q] = make_int4(pos + o[0], pos + o[1], pos + o[2], pos + o[3]);
         reinterpret_cast<int4*>(cc)[q] = make_int4(0, 0, 0, 0);
     }
+#ifdef MPM_DEBUG_CST
+    printf("cell_scan cc %p cst %p run %d v6 %d %d v8 %d %d cst64 %d\n", cc, cst, run, v[6].x, v[6].y, v[8].x, v[8].y, (int)cst[64]);
+#endif
 }
 
 __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bcount, int* __restrict__ ccount,
@@ -349,9 +357,13 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
                 sl.bmap[b] = -1;
                 atomicOr(flags, FLAG_ACTIVE_OVERFLOW);
             }
-            unsigned short scratch[Geo<3>::CELLS + 1];
+#ifdef MPM_DEBUG_CST
+            if (b < 4) printf("scan step %d b %d c %d li %d cap %d pos %d b0 %d ccount %p cc %d %d %d %d .. %d\n", sl.step, b, c[q], li, cap, pos, b0,
+                              ccount, ccount[b * kCellStride], ccount[b * kCellStride + 1], ccount[b * kCellStride + 8],
+                              ccount[b * kCellStride + 9], ccount[b * kCellStride + 64]);
+#endif
             cell_scan(ccount + (int64_t)b * kCellStride, ccursor + (int64_t)b * kCellStride, pos,
-                      li < cap ? sl.cstart + (int64_t)(b0 + li) * (Geo<3>::CELLS + 1) : scratch);
+                      li < cap ? sl.cstart + (int64_t)(b0 + li) * (Geo<3>::CELLS + 1) : nullptr);
             pos += c[q];
             ++li;
             bcount[b] = 0;
@@ -669,6 +681,11 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
                 if (Sn.pid) Sn.pid[start + rr] = pr;
             }
             if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
+#ifdef MPM_DEBUG_CST
+            if (tid == 0 && s_cst[G::CELLS] != n)
+                printf("p2g step %d bi %d bid %d b0 %d start %d n %d cst0 %d cst1 %d cst63 %d cst64 %d cstart %p\n", sl.step, bi, bid, b0,
+                       start, n, s_cst[0], s_cst[1], s_cst[63], s_cst[64], cstart);
+#endif
             __syncthreads();
         }
         const int nvalid = s_cst[G::CELLS];
