@@ -167,6 +167,8 @@ size_t carve(mpm_ctx* h, char* base) {
     StateView fin = state();
     const int Tm = p.max_steps;
     int* sigma_store = (int*)take(sizeof(int) * EN * Tm);
+    unsigned char* scell0 = (unsigned char*)take(EN);
+    unsigned char* scell1 = (unsigned char*)take(EN);
     int* spid0 = (int*)take(sizeof(int) * EN);
     int* spid1 = (int*)take(sizeof(int) * EN);
     int* bmap_store = (int*)take(sizeof(int) * (size_t)k.TB * Tm);
@@ -183,8 +185,7 @@ size_t carve(mpm_ctx* h, char* base) {
     int32_t* mat = (int32_t*)take(sizeof(int32_t) * std::max<size_t>(EN, (size_t)h->n_body));  // by particle id
     float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
     int* bcount = (int*)take(sizeof(int) * k.TB);
-    int* ccount = (int*)take(sizeof(int) * (size_t)k.TB * kCellStride);
-    int* ccursor = (int*)take(sizeof(int) * (size_t)k.TB * kCellStride);
+    int* cursor = (int*)take(sizeof(int) * k.TB);
     int* scan_part = (int*)take(sizeof(int64_t) * (scan_chunks(k) + 2));  // chunk totals, epoch, ticket
     int* keys = (int*)take(sizeof(int) * EN);
     float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
@@ -218,7 +219,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->max_active = max_active;
         h->step_blocks = max_active;
         h->pool_blocks = pool;
-        h->sigma_store = sigma_store;
+        h->sigma_store = sigma_store; h->scell_ring[0] = scell0; h->scell_ring[1] = scell1;
         h->spid_ring[0] = spid0; h->spid_ring[1] = spid1; h->bmap_store = bmap_store;
         h->nactive_arr = nactive_arr; h->base_arr = base_arr; h->blist_pool = blist_pool;
         h->bstart_pool = bstart_pool; h->cstart_pool = cstart_pool; h->tiles_pool = tiles_pool;
@@ -229,7 +230,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->final_state = fin;
         h->sbar[0] = sb0; h->sbar[1] = sb1;
         h->xbar_part = xbar_part;
-        h->staging = staging; h->aid = aid; h->mat = mat; h->bcount = bcount; h->ccount = ccount; h->ccursor = ccursor; h->scan_part = scan_part; h->keys = keys;
+        h->staging = staging; h->aid = aid; h->mat = mat; h->bcount = bcount; h->cursor = cursor; h->scan_part = scan_part; h->keys = keys;
         h->ubar = ubar; h->part = part; h->abar_part = abar_part;
         h->obs = obs; h->obs_cnt = obs_cnt; h->obs_part = obs_part; h->obs_inc = obs_inc;
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
@@ -253,6 +254,7 @@ SlotView slot_at(mpm_ctx* h, int t) {
     const size_t EN = (size_t)k.E * k.N;
     SlotView s;
     s.sigma = h->sigma_store + EN * t;
+    s.scell = h->scell_ring[t & 1];
     s.spid = h->spid_ring[t & 1];
     s.blist = h->blist_pool;
     s.bstart = h->bstart_pool;
@@ -325,9 +327,9 @@ void bin_fresh(mpm_ctx* h, const KParams& k, int t) {
     const SlotView sl = slot_at(h, t);
     KScope sc(h, KC_BIN);
     h->launches += 2;
-    launch_bin_keys(k, state_at(h, t).x, h->dd ? h->n0 : k.N * k.E, h->keys, h->bins(), h->flags, h->stream);
-    launch_bin_scan(k, h->bins(), sl, h->scan_part, h->flags, h->stream);
-    launch_bin_scatter(k, h->keys, state_at(h, t).pid, h->bins(), sl, h->stream);
+    launch_bin_keys(k, state_at(h, t).x, h->dd ? h->n0 : k.N * k.E, h->keys, h->bcount, h->flags, h->stream);
+    launch_bin_scan(k, h->bcount, h->cursor, sl, h->scan_part, h->flags, h->stream);
+    launch_bin_scatter(k, h->keys, state_at(h, t).pid, h->cursor, sl, h->stream);
 }
 
 // advance() for step t; write_next: produce S_{t+1}; bin_next: bin it into slot(t+1)
@@ -344,18 +346,18 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
         launch_ctrl_obs_fwd(k, h->theta, t, h->obs_part, h->obs + (size_t)t * k.E * no, h->obs_cnt,
                             const_cast<float*>(alpha_at(h, t)), h->stream);
     }
-    { KScope sc(h, KC_P2G);
-      launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), bin_next ? h->keys : nullptr, h->flags, h->stream); }
+    { KScope sc(h, KC_CANON); launch_canon(k, sl, Sn.pid, bin_next ? h->keys : nullptr, h->flags, h->stream); }
+    { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
     { KScope sc(h, KC_GRID_OP); launch_grid_op(k, sl, h->stream); }
     if (!write_next) return;
     { KScope sc(h, KC_G2P);
-      launch_g2p(k, sl, S, Sn, bin_next ? h->keys : nullptr, h->bins(), h->flags, false, Migr{}, h->stream); }
+      launch_g2p(k, sl, S, Sn, bin_next ? h->keys : nullptr, h->bcount, h->flags, false, Migr{}, h->stream); }
     if (bin_next) {
         const SlotView nx = slot_at(h, t + 1);
         KScope sc(h, KC_BIN);
         h->launches += 1;
-        launch_bin_scan(k, h->bins(), nx, h->scan_part, h->flags, h->stream);
-        launch_bin_scatter(k, h->keys, Sn.pid, h->bins(), nx, h->stream);
+        launch_bin_scan(k, h->bcount, h->cursor, nx, h->scan_part, h->flags, h->stream);
+        launch_bin_scatter(k, h->keys, Sn.pid, h->cursor, nx, h->stream);
     }
 }
 
@@ -363,7 +365,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
 // store, so only g2p runs (plus F_{t+1} = (I + dt C) F and the particle ids)
 void step_reforward(mpm_ctx* h, const KParams& k, int t, cudaStream_t st) {
     KScope sc(h, KC_G2P);
-    launch_g2p(k, slot_at(h, t), state_at(h, t), state_at(h, t + 1), nullptr, h->bins(), h->flags, true, Migr{}, st);
+    launch_g2p(k, slot_at(h, t), state_at(h, t), state_at(h, t + 1), nullptr, h->bcount, h->flags, true, Migr{}, st);
 }
 
 // advance_grad() for step t, using the grid tiles stored for step t
@@ -602,7 +604,6 @@ mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     CU(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
     CU(cudaMemsetAsync(h->scan_part, 0, sizeof(int64_t) * (scan_chunks(kparams(h)) + 2), h->stream));
     CU(cudaMemsetAsync(h->bcount, 0, sizeof(int) * k.TB, h->stream));
-    CU(cudaMemsetAsync(h->ccount, 0, sizeof(int) * (size_t)k.TB * kCellStride, h->stream));
     CU(cudaMemsetAsync(h->theta, 0, sizeof(float) * (n_theta_of(h->prm, h->dim) > 0 ? n_theta_of(h->prm, h->dim) : 1), h->stream));
     h->phase = kBound;
     return MPM_OK;

@@ -63,6 +63,7 @@ struct mpm_ctx {
     // grid store (all steps): sorted lists, block maps, and a pool of block lists /
     // cell starts / node tiles addressed by a per-step device-side base
     int* sigma_store = nullptr;    // [T_max][EN]
+    unsigned char* scell_ring[2] = {nullptr, nullptr};  // [EN] (consumed by the next p2g only)
     int* spid_ring[2] = {nullptr, nullptr};
     int* bmap_store = nullptr;     // [T_max][TB]
     int* nactive_arr = nullptr;    // [T_max]
@@ -77,8 +78,7 @@ struct mpm_ctx {
     float* staging = nullptr;
     int32_t* aid = nullptr;        // caller order
     int* bcount = nullptr;         // [TB] block histogram (kept zero between uses)
-    int* ccount = nullptr;         // [TB][kCellStride] (block, cell) histogram (kept zero between uses)
-    int* ccursor = nullptr;        // [TB][kCellStride] per-cell scatter cursors
+    int* cursor = nullptr;         // [TB]
     int* scan_part = nullptr;      // [scan chunks + 2] int64: epoch-tagged chunk totals, epoch, ticket
     int* keys = nullptr;           // [EN]
     float4* ubar = nullptr;        // [max_active][TN]  U_bar partial tiles of the current step
@@ -131,7 +131,6 @@ struct mpm_ctx {
     int* imm_base = nullptr;       // [T_max + 1][2]    first row of S_t's immigrants from each side
     int* nrows_arr = nullptr;      // [T_max + 1]       rows of S_t (sorted of t-1 + immigrants)
     cudaEvent_t dd_ev[4] = {};     // per-phase events of the decomposed step
-    mpm::BinCounts bins() const { return mpm::BinCounts{bcount, ccount, ccursor}; }
 };
 
 namespace eng {

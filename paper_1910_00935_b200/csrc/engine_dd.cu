@@ -198,19 +198,19 @@ mpm_status mpm_dd_forward(mpm_handle* hs, int32_t n, int32_t steps) {
         CU(cudaMemsetAsync(h->out_cnt, 0, sizeof(int) * 2 * ((size_t)steps + 1), h->stream));
         KScope sc(h, KC_BIN);
         h->launches += 2;
-        launch_bin_keys(K[g], state_at(h, 0).x, h->n0, h->keys, h->bins(), h->flags, h->stream);
-        launch_bin_scan(K[g], h->bins(), slot_at(h, 0), h->scan_part, h->flags, h->stream);
-        launch_bin_scatter(K[g], h->keys, state_at(h, 0).pid, h->bins(), slot_at(h, 0), h->stream);
+        launch_bin_keys(K[g], state_at(h, 0).x, h->n0, h->keys, h->bcount, h->flags, h->stream);
+        launch_bin_scan(K[g], h->bcount, h->cursor, slot_at(h, 0), h->scan_part, h->flags, h->stream);
+        launch_bin_scatter(K[g], h->keys, state_at(h, 0).pid, h->cursor, slot_at(h, 0), h->stream);
     }
     for (int t = 0; t < steps; ++t) {
         const bool last = t + 1 == steps;
-        for (int g = 0; g < n; ++g) {  // p2g (local; canonical order of each block's list first)
+        for (int g = 0; g < n; ++g) {  // canon + p2g (local)
             mpm_ctx* h = hs[g];
             DevGuard dg(h);
             const SlotView sl = slot_at(h, t);
             const StateView S = state_at(h, t), Sn = state_at(h, t + 1);
-            { KScope sc(h, KC_P2G);
-              launch_p2g(K[g], sl, S, Sn, nullptr, nullptr, last ? nullptr : h->keys, h->flags, h->stream); }
+            { KScope sc(h, KC_CANON); launch_canon(K[g], sl, Sn.pid, last ? nullptr : h->keys, h->flags, h->stream); }
+            { KScope sc(h, KC_P2G); launch_p2g(K[g], sl, S, Sn, nullptr, nullptr, h->flags, h->stream); }
             CU(cudaEventRecord(h->dd_ev[EV_P2G], h->stream));
         }
         for (int g = 0; g < n; ++g) {  // grid_op over the slab faces
@@ -225,7 +225,7 @@ mpm_status mpm_dd_forward(mpm_handle* hs, int32_t n, int32_t steps) {
             DevGuard dg(h);
             if (!last) CU(cudaMemsetAsync(h->keys, 0xff, sizeof(int) * (size_t)K[g].EN, h->stream));
             { KScope sc(h, KC_G2P);
-              launch_g2p(K[g], slot_at(h, t), state_at(h, t), state_at(h, t + 1), last ? nullptr : h->keys, h->bins(),
+              launch_g2p(K[g], slot_at(h, t), state_at(h, t), state_at(h, t + 1), last ? nullptr : h->keys, h->bcount,
                          h->flags, false, last ? Migr{} : migr_of(h, t), h->stream); }
             CU(cudaEventRecord(h->dd_ev[EV_G2P], h->stream));
         }
@@ -246,11 +246,11 @@ mpm_status mpm_dd_forward(mpm_handle* hs, int32_t n, int32_t steps) {
             KScope sc(h, KC_BIN);
             h->launches += 2;
             launch_immigrate(K[g], state_at(h, t + 1), h->ntot_arr + t, src[0], src[1], h->x_lo, h->x_hi, h->mig_cap,
-                             h->keys, h->bins(), h->imm_base + (size_t)2 * (t + 1), h->nrows_arr + t + 1, h->flags,
+                             h->keys, h->bcount, h->imm_base + (size_t)2 * (t + 1), h->nrows_arr + t + 1, h->flags,
                              h->stream);
             const SlotView nx = slot_at(h, t + 1);
-            launch_bin_scan(K[g], h->bins(), nx, h->scan_part, h->flags, h->stream);
-            launch_bin_scatter(K[g], h->keys, state_at(h, t + 1).pid, h->bins(), nx, h->stream);
+            launch_bin_scan(K[g], h->bcount, h->cursor, nx, h->scan_part, h->flags, h->stream);
+            launch_bin_scatter(K[g], h->keys, state_at(h, t + 1).pid, h->cursor, nx, h->stream);
         }
     }
     for (int g = 0; g < n; ++g) {

@@ -71,6 +71,7 @@ struct Migr {
 // each step take space.  bmap holds pool (global) tile indices.
 struct SlotView {
     int* sigma;              // [EN]   sorted order -> index into that step's state array
+    unsigned char* scell;    // [EN]   cell (0..63, 64 = junk) of the sorted entry (set by bin_scatter)
     int* spid;               // [EN]   particle id of the sorted entry (set by bin_scatter)
     int* blist;              // pool [P]          active block ids of a step (block-id order)
     int* bstart;             // pool [P + T + 1]  segment starts; step t uses [base + t, base + t + n]
@@ -88,35 +89,27 @@ struct SlotView {
 
 cudaError_t tile_init();
 
-// binning histograms: bcount[TB] per block, ccount[TB][kCellStride] per (block, cell) (kept zero
-// between uses; the scan clears what it consumed) and the per-cell scatter cursors
-struct BinCounts {
-    int* bcount;
-    int* ccount;
-    int* ccursor;
-};
-
 // ---- binning (bin_keys only for a fresh sort; g2p emits keys for the next step)
 // rows >= n_live get key -1 (not binned); n_live = N * E in a single-domain run
-void launch_bin_keys(const KParams& p, const float* x, int64_t n_live, int* keys, const BinCounts& bc, int* flags,
+void launch_bin_keys(const KParams& p, const float* x, int64_t n_live, int* keys, int* bcount, int* flags,
                      cudaStream_t s);
 int scan_chunks(const KParams& p);  // entries of `part` (int2) the scan needs
-// block scan -> active list, block starts, block map; per active block the cell starts (cstart)
-// and the per-cell cursors
-void launch_bin_scan(const KParams& p, const BinCounts& bc, const SlotView& sl, int* part, int* flags,
+void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
                      cudaStream_t s);
-// keys[j] = block * 128 + cell of entry j; pid[j] its particle id -> sigma / spid in cell buckets
-// (arbitrary order inside a cell: p2g ranks each cell by particle id)
-void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, const BinCounts& bc, const SlotView& sl,
+// keys[j] = block * 128 + cell of entry j; pid[j] its particle id
+void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
                         cudaStream_t s);
 
+// canonical (cell, particle id) order of every active block's list; cell starts; the
+// particle ids of S_{t+1} (pid_next, nullable) in that order.  Runs before each p2g.  A block
+// with more than MAXP particles is dropped (FLAG_BLOCK_OVERFLOW) and its rows' next bin keys
+// (keys_next, nullable) are set to -1.
+void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* keys_next, int* flags, cudaStream_t s);
+
 // ---- one forward step (advance())
-// p2g first puts each block's list in canonical (cell, particle id) order (sigma rewritten in
-// place; the particle ids of S_{t+1} -> Sn.pid, nullable), then writes F_{t+1} (Sn.f, nullable).
-// A block with more than MAXP particles is dropped (FLAG_BLOCK_OVERFLOW) and its rows' next bin
-// keys (keys_next, nullable) are set to -1.
+// p2g writes F_{t+1} and particle ids of S_{t+1} when Sn.rec / Sn.pid are non-null
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
-                const int32_t* aid, const float* alpha_t, int* keys_next, int* flags, cudaStream_t s);
+                const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s);
 // grid_op: sum of the covering partial tiles -> resolved tile of every active block
 void launch_grid_op(const KParams& p, const SlotView& sl, cudaStream_t s);
 // g2p writes x, v, C of S_{t+1}; keys != null -> next bin keys;
@@ -124,7 +117,7 @@ void launch_grid_op(const KParams& p, const SlotView& sl, cudaStream_t s);
 // mg.cnt != null (f3): particles whose next block leaves [mg.x_lo, mg.x_hi) get key -1 and are listed
 // in the outbox mg.rows by direction
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
-                const BinCounts& bc, int* flags, bool refwd, const Migr& mg, cudaStream_t s);
+                int* bcount, int* flags, bool refwd, const Migr& mg, cudaStream_t s);
 
 // ---- f3 migration (engine_dd.cu)
 // append the neighbours' emigrants of step t to S_{t+1} (rows nsorted_t + ...), bin keys + histogram;
@@ -135,8 +128,8 @@ struct MigSrc {
     const int* rows;
 };
 void launch_immigrate(const KParams& p, const StateView& S, const int* nsorted, MigSrc left, MigSrc right,
-                      int x_lo, int x_hi, int cap, int* keys, const BinCounts& bc, int* imm_base, int* nrows,
-                      int* flags, cudaStream_t s);
+                      int x_lo, int x_hi, int cap, int* keys, int* bcount, int* imm_base, int* nrows, int* flags,
+                      cudaStream_t s);
 // backward: S_bar_{t+1} rows of this subdomain's emigrants of step t <- the neighbour's immigrant rows
 void launch_adj_pull(const KParams& p, const AdjView& Sb, const int* cnt, const int* rows, int cap,
                      const AdjView& nb_left, const int* nb_left_base, const AdjView& nb_right,

@@ -79,6 +79,55 @@ template <int D> __device__ __forceinline__ int cell_of(const int lb[3]) {
     return D == 2 ? lb[0] * G::B + lb[1] : (lb[0] * G::B + lb[1]) * G::B + lb[2];
 }
 
+// Sum of the <= 2^d block tiles that cover global node g (episode e): every
+// block whose cells [c0, c0 + B) satisfy c0 <= g < c0 + B + 2 holds a partial
+// of that node.  Fixed enumeration order -> deterministic.
+// f3: a covering block outside this subdomain's slab [x_lo, x_hi) belongs to a neighbour, whose
+// block map and (pool-indexed) tiles nt[0] (left) / nt[1] (right) are read instead -- the same
+// blocks in the same order as a single-domain run.
+// HALO = false (a single domain, no neighbours) compiles the neighbour branch out.
+template <int D, bool HALO>
+__device__ __forceinline__ float4 covered_sum(const KParams& p, int e, const int g[3],
+                                              const int* __restrict__ bmap,
+                                              const float4* __restrict__ tiles, const Halo& hl,
+                                              const float4* nt0, const float4* nt1) {
+    using G = Geo<D>;
+    // per axis: option 0 = the block holding g (local l0), option 1 = the previous
+    // block (local l0 + B), valid when l0 < 2.  All 2^d combinations unrolled.
+    int b0[3], l0[3];
+    bool ok1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        b0[k] = k < D ? g[k] >> G::LOGB : 0;
+        l0[k] = k < D ? g[k] & (G::B - 1) : 0;
+        ok1[k] = k < D && l0[k] < 2 && b0[k] >= 1;
+    }
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < (D == 3 ? 2 : 1); ++c) {
+                if ((a && !ok1[0]) || (b && !ok1[1]) || (c && !ok1[2])) continue;
+                const int bb[3] = {b0[0] - a, b0[1] - b, b0[2] - c};
+                if (bb[0] >= p.nb || bb[1] >= p.nb || (D == 3 && bb[2] >= p.nb)) continue;
+                const int* bm = bmap;
+                const float4* tl = tiles;
+                if (HALO) {
+                    if (bb[0] < hl.x_lo) { bm = hl.bmap[0]; tl = nt0; }
+                    else if (bb[0] >= hl.x_hi) { bm = hl.bmap[1]; tl = nt1; }
+                    if (bm == nullptr) continue;
+                }
+                const int ti = __ldg(bm + block_lin<D>(p, e, bb));
+                if (ti < 0) continue;
+                const int lq = tile_lin<D>(l0[0] + a * G::B, l0[1] + b * G::B, l0[2] + c * G::B);
+                const float4 v = __ldg(tl + (int64_t)ti * G::TN + lq);
+                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+    return acc;
+}
+
 // neighbour tiles indexed by the neighbour's pool (tile) indices of this step (f3)
 template <int D> __device__ __forceinline__ const float4* halo_tiles(const Halo& hl, int s) {
     return hl.tiles[s] ? hl.tiles[s] - (int64_t)(*hl.base[s]) * Geo<D>::TN : nullptr;
@@ -170,12 +219,6 @@ __device__ __forceinline__ void count_key(bool valid, int key, int* bcount) {
     const int leader = __ffs(peers) - 1;
     if (valid && (int)(threadIdx.x & 31) == leader) atomicAdd(&bcount[key], __popc(peers));
 }
-// block and (block, cell) histograms of a binned entry: bcount[block], ccount[block][cell]
-// (cell 64 = the junk bucket of an out-of-domain particle)
-__device__ __forceinline__ void count_bin(bool valid, int block, int cell, int* bcount, int* ccount) {
-    count_key(valid, block, bcount);
-    count_key(valid, block * kCellStride + cell, ccount);
-}
 
 // weights and base of a particle relative to the block origin
 template <int D>
@@ -197,12 +240,12 @@ __device__ __forceinline__ void particle_weights(const KParams& p, const float* 
 template <int D>
 __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restrict__ X, int64_t n_live,
                                                  int* __restrict__ keys, int* __restrict__ bcount,
-                                                 int* __restrict__ ccount, int* flags) {
+                                                 int* flags) {
     pdl_begin();
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n_live && i < p.N * p.E) keys[i] = -1;  // rows beyond the live ones (f3 capacity)
     const bool in = i < n_live;
-    int key = 0, cell = 0;
+    int key = 0;
     if (in) {
         float x[3];
 #pragma unroll
@@ -213,7 +256,7 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
         int bb[3] = {b[0] >> Geo<D>::LOGB, b[1] >> Geo<D>::LOGB, b[2] >> Geo<D>::LOGB};
         int lb[3] = {b[0] & (Geo<D>::B - 1), b[1] & (Geo<D>::B - 1), b[2] & (Geo<D>::B - 1)};
         key = block_lin<D>(p, e, bb);
-        cell = cell_of<D>(lb);
+        int cell = cell_of<D>(lb);
         if (!ok) { atomicOr(flags, FLAG_OUT_OF_DOMAIN); key = e * p.nbe; cell = Geo<D>::CELLS; }
         if (ok && (bb[0] < p.x_lo || bb[0] >= p.x_hi)) {  // f3: a particle outside the subdomain's slab
             atomicOr(flags, FLAG_MIGRATION);
@@ -221,10 +264,7 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
         }
         keys[i] = key < 0 ? -1 : key * 128 + cell;
     }
-#ifdef MPM_DEBUG_CST
-    if (i < 6) printf("bin_keys i %d key %d cell %d ccount %p bcount %p\n", (int)i, key, cell, ccount, bcount);
-#endif
-    count_bin(in && key >= 0, key, cell, bcount, ccount);
+    count_key(in && key >= 0, key, bcount);
 }
 
 // Exclusive scan of the dense block histogram -> active block list (block-id order),
@@ -237,41 +277,12 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
 // (MPS, concurrent kernels).  The last CTA to finish (second ticket) resets the chunk ticket
 // and advances the epoch for the next launch.
 #ifndef MPM_SCAN_PER
-#define MPM_SCAN_PER 1  // blocks per thread: each thread scans the cells of at most this many blocks
+#define MPM_SCAN_PER 4
 #endif
 constexpr int kScanPer = MPM_SCAN_PER;
 constexpr int kScanChunk = kT * kScanPer;
-// Also, per active block, the exclusive scan of its 65 cell counts (cells 0..63, junk): the cell
-// starts within the block segment (sl.cstart) and the per-cell scatter cursors; clears the counts.
-// cst == null: a block past the active-list capacity (its cell starts are not kept)
-__device__ __forceinline__ void cell_scan(int* __restrict__ cc, int* __restrict__ ccursor, int pos,
-                                          unsigned short* __restrict__ cst) {
-    constexpr int NQ = kCellStride / 4;
-    int4 v[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) v[q] = reinterpret_cast<const int4*>(cc)[q];
-    int run = 0;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int c[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-        int o[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            o[u] = run;
-            if (cst && 4 * q + u <= Geo<3>::CELLS) cst[4 * q + u] = (unsigned short)run;
-            run += c[u];
-        }
-        reinterpret_cast<int4*>(ccursor)[q] = make_int4(pos + o[0], pos + o[1], pos + o[2], pos + o[3]);
-        reinterpret_cast<int4*>(cc)[q] = make_int4(0, 0, 0, 0);
-    }
-#ifdef MPM_DEBUG_CST
-    printf("cell_scan cc %p cst %p run %d v6 %d %d v8 %d %d cst64 %d\n", cc, cst, run, v[6].x, v[6].y, v[8].x, v[8].y, (int)cst[64]);
-#endif
-}
-
-__global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bcount, int* __restrict__ ccount,
-                                                int* __restrict__ ccursor, SlotView sl, int2* __restrict__ part,
-                                                int* flags) {
+__global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bcount, int* __restrict__ cursor,
+                                                SlotView sl, int2* __restrict__ part, int* flags) {
     pdl_begin();
     __shared__ int s_wt[kW], s_wa[kW];
     __shared__ int s_base[2];
@@ -289,7 +300,7 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
     const int chunk = s_chunk;
     const int i0 = chunk * kScanChunk + tid * kScanPer;
     int c[kScanPer];
-    if (kScanPer % 4 == 0 && i0 + kScanPer <= TB) {
+    if (i0 + kScanPer <= TB) {
 #pragma unroll
         for (int q = 0; q < kScanPer / 4; ++q) {
             const int4 v = *reinterpret_cast<const int4*>(bcount + i0 + 4 * q);
@@ -357,13 +368,7 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
                 sl.bmap[b] = -1;
                 atomicOr(flags, FLAG_ACTIVE_OVERFLOW);
             }
-#ifdef MPM_DEBUG_CST
-            if (b < 4) printf("scan step %d b %d c %d li %d cap %d pos %d b0 %d ccount %p cc %d %d %d %d .. %d\n", sl.step, b, c[q], li, cap, pos, b0,
-                              ccount, ccount[b * kCellStride], ccount[b * kCellStride + 1], ccount[b * kCellStride + 8],
-                              ccount[b * kCellStride + 9], ccount[b * kCellStride + 64]);
-#endif
-            cell_scan(ccount + (int64_t)b * kCellStride, ccursor + (int64_t)b * kCellStride, pos,
-                      li < cap ? sl.cstart + (int64_t)(b0 + li) * (Geo<3>::CELLS + 1) : nullptr);
+            cursor[b] = pos;
             pos += c[q];
             ++li;
             bcount[b] = 0;
@@ -391,12 +396,12 @@ __global__ void __launch_bounds__(kT) k_bin_scan(KParams p, int* __restrict__ bc
     }
 }
 
-// scatter of particle indices into the cell buckets of their block (kernels.h: the order inside
-// a cell is arbitrary; p2g ranks each cell by particle id).  kScatterPer particles per thread, all
-// loads and cursor atomics issued before any result is used (memory-level parallelism).
+// stable-free scatter of particle indices by block key (position inside a block is
+// arbitrary; p2g canonicalises).  kScatterPer particles per thread, all loads and
+// cursor atomics issued before any result is used (memory-level parallelism).
 constexpr int kScatterPer = 4;
 __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __restrict__ keys,
-                                                    const int* __restrict__ pid, int* __restrict__ ccursor,
+                                                    const int* __restrict__ pid, int* __restrict__ cursor,
                                                     SlotView sl) {
     pdl_begin();
     const int64_t n = p.N * p.E;
@@ -413,11 +418,11 @@ __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __rest
     }
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) {
-        const int slot = kc[u] >= 0 ? (kc[u] >> 7) * kCellStride + (kc[u] & 127) : -1;
-        peers[u] = __match_any_sync(0xffffffffu, slot);
+        const int key = kc[u] >= 0 ? kc[u] >> 7 : -1;
+        peers[u] = __match_any_sync(0xffffffffu, key);
         const int leader = __ffs(peers[u]) - 1;
         base[u] = 0;
-        if (kc[u] >= 0 && lane == leader) base[u] = atomicAdd(&ccursor[slot], __popc(peers[u]));
+        if (kc[u] >= 0 && lane == leader) base[u] = atomicAdd(&cursor[key], __popc(peers[u]));
     }
 #pragma unroll
     for (int u = 0; u < kScatterPer; ++u) {
@@ -425,6 +430,7 @@ __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __rest
         if (kc[u] >= 0) {
             const int pos = b + __popc(peers[u] & ((1u << lane) - 1u));
             sl.sigma[pos] = (int)j[u];
+            sl.scell[pos] = (unsigned char)(kc[u] & 127);
             sl.spid[pos] = pj[u];
         }
     }
@@ -483,22 +489,11 @@ constexpr int kTQ = MPM_SCATTER_THREADS;  // p2g / g2p_grad CTA (>= kACC; the ex
 static_assert(kTQ >= kACC, "scatter CTA smaller than the accumulation phase");
 constexpr int kCH = MPM_P2G_CHUNK;  // rows per chunk: most blocks fit one chunk -> all 64 cells busy in phase 2
 
-// particle row in shared memory (floats).  Row r starts at r * STRIDE + 4 (r / 8): the stride
-// keeps 8 consecutive rows (one quarter-warp's STS.128 in phase 1) on distinct bank groups, and
-// the one-float4 skew every 8 rows does the same for the phase-2 readers, whose quarter-warps read
-// the rows of ~3 consecutive cells -- 8 particles per cell in the 3D workloads (2 per axis), so
-// rows exactly 8 apart, which a plain stride maps to the same banks (ncu: 30% / 52% of p2g's /
-// the U_bar scatter's shared wavefronts were conflicts).
-template <int D> struct RowL {
+template <int D> struct RowL {  // particle row in shared memory (floats); stride avoids STS.128 conflicts
     static constexpr int STRIDE = D == 3 ? 28 : 12;
-#ifndef MPM_ROW_SKEW
-#define MPM_ROW_SKEW 1
-#endif
-    static __device__ __forceinline__ int off(int r) { return r * STRIDE + (MPM_ROW_SKEW ? 4 * (r >> 3) : 0); }
-    static constexpr int bytes(int rows) { return (rows * STRIDE + (MPM_ROW_SKEW ? 4 * (rows / 8 + 1) : 0)) * 4; }
 };
 template <int D> constexpr int p2g_union_bytes() {
-    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = RowL<D>::bytes(kCH);
+    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 template <int D> constexpr int p2g_smem_bytes() {
@@ -611,6 +606,110 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
     return ok;
 }
 
+// ------------------------------------------------------------ canonical order
+// Per active block: put the scattered list in canonical (cell, particle id) order, so every
+// sum downstream has a fixed order (bitwise reproducible, independent of the scatter's
+// atomics).  Bucket by cell (warp-aggregated smem counters), then rank by particle id
+// inside the cell.  Writes sigma (canonical), the cell starts and -- when the step writes
+// S_{t+1} -- the particle ids of S_{t+1} (p2g's output order).  Its own high-occupancy
+// pass (256 threads, 26 KB smem) ahead of p2g.
+constexpr int canon_smem_bytes() { return 1728 * 15 + 2 * 66 * 4; }
+__global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __restrict__ pid_next,
+                                              int* __restrict__ keys_next, int* flags) {
+    pdl_begin();
+    constexpr int MAXP = 1728, CELLS = 64;
+    using G = Geo<3>;  // CELLS = 64 in 2D and 3D
+    extern __shared__ __align__(16) unsigned char smem[];
+    int* s_idx = reinterpret_cast<int*>(smem);
+    int* s_pid = s_idx + MAXP;
+    int* s_bpid = s_pid + MAXP;
+    int* s_cnt = s_bpid + MAXP;
+    int* s_cst = s_cnt + CELLS + 2;
+    short* s_tmp = reinterpret_cast<short*>(s_cst + CELLS + 2);
+    unsigned char* s_cell = reinterpret_cast<unsigned char*>(s_tmp + MAXP);
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int nact = *sl.nactive;
+    const int b0 = *sl.base;
+    const int* bstart = sl.bstart + b0 + sl.step;
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (CELLS + 1);
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
+        const int start = bstart[bi], n = bstart[bi + 1] - start;
+        if (n > MAXP) {  // reported; the block is dropped (no valid entries downstream)
+            if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
+            for (int c = tid; c <= CELLS; c += kT) cstart[(int64_t)bi * (CELLS + 1) + c] = 0;
+            // g2p writes no bin key for the dropped rows of S_{t+1}: mark them so the next
+            // binning skips them instead of scattering stale keys
+            if (keys_next)
+                for (int q = tid; q < n; q += kT) keys_next[start + q] = -1;
+            continue;
+        }
+        // ---- phase 0: canonical (cell, particle id) order of the block's list.  The
+        // scatter wrote each entry's cell and particle id next to it: coalesced loads only.
+        for (int q = tid; q < G::CELLS + 2; q += kT) s_cnt[q] = 0;
+#pragma unroll 4
+        for (int q = tid; q < n; q += kT) {
+            s_idx[q] = sl.sigma[start + q];
+            s_pid[q] = sl.spid[start + q];
+            s_cell[q] = sl.scell[start + q];
+        }
+        __syncthreads();
+        for (int q0 = 0; q0 < n; q0 += kT) {
+            const int q = q0 + tid;
+            const bool in = q < n;
+            const int cell = in ? (int)s_cell[q] : -1;
+            const unsigned peers = __match_any_sync(0xffffffffu, cell);
+            if (in && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[cell], __popc(peers));
+        }
+        __syncthreads();
+        if (tid < 32) {  // exclusive scan of the 65 bucket counts (one warp)
+            int carry = 0;
+            for (int c = lane; c - lane <= G::CELLS; c += 32) {
+                const int v = c <= G::CELLS ? s_cnt[c] : 0;
+                int inc = v;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int t = __shfl_up_sync(0xffffffffu, inc, off);
+                    if (lane >= off) inc += t;
+                }
+                if (c <= G::CELLS) { s_cst[c] = carry + inc - v; s_cnt[c] = carry + inc - v; }
+                carry += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            if (lane == 0) s_cst[G::CELLS + 1] = carry;
+        }
+        __syncthreads();
+        for (int q0 = 0; q0 < n; q0 += kT) {  // bucket by cell (order inside a cell arbitrary)
+            const int q = q0 + tid;
+            const bool in = q < n;
+            const int cell = in ? (int)s_cell[q] : -1;
+            const unsigned peers = __match_any_sync(0xffffffffu, cell);
+            const int leader = __ffs(peers) - 1;
+            int base = 0;
+            if (in && lane == leader) base = atomicAdd(&s_cnt[cell], __popc(peers));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (in) {
+                const int pos = base + __popc(peers & ((1u << lane) - 1u));
+                s_tmp[pos] = (short)q;
+                s_bpid[pos] = s_pid[q];
+            }
+        }
+        __syncthreads();
+        for (int r = tid; r < n; r += kT) {  // rank by particle id inside the cell
+            const int q = s_tmp[r];
+            const int cell = s_cell[q], pq = s_bpid[r];
+            int rank = 0;
+            const int m1 = s_cst[cell + 1];
+            for (int m = s_cst[cell]; m < m1; ++m) rank += s_bpid[m] < pq;
+            const int fl = s_cst[cell] + rank;
+            sl.sigma[start + fl] = s_idx[q];
+            if (pid_next) pid_next[start + fl] = pq;
+        }
+        for (int c = tid; c <= G::CELLS; c += kT) cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
+        if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
+        __syncthreads();
+    }
+    (void)p;
+}
+
 // ---------------------------------------------------------------- P2G
 // p2g: canonicalise the block list, then per particle
 // Ft = (I + dt C) F; tau = tau(Ft) [+ actuation]; A = -dt V 4/dx^2 tau + m C;
@@ -619,11 +718,11 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
 template <int D>
 __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
                                                const int32_t* __restrict__ aid,
-                                               const float* __restrict__ alpha, int* __restrict__ keys_next,
-                                               int* flags) {
+                                               const float* __restrict__ alpha, int* flags) {
     pdl_begin();
     using G = Geo<D>;
     using L = Lay<D>;
+    constexpr int RS = RowL<D>::STRIDE;
     extern __shared__ __align__(16) unsigned char smem[];
     float* s_row = reinterpret_cast<float*>(smem);                   // phase 1/2 rows ...
     float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... node partials
@@ -642,52 +741,14 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         const int start = bstart[bi], n = bstart[bi + 1] - start;
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        if (n > G::MAXP) {  // reported; the block is dropped (no valid entries downstream)
+        if (n > G::MAXP) {
             if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
-            for (int c = tid; c <= G::CELLS; c += kTQ) cstart[(int64_t)bi * (G::CELLS + 1) + c] = 0;
-            // g2p writes no bin key for the dropped rows of S_{t+1}: mark them so the next
-            // binning skips them instead of scattering stale keys
-            if (keys_next)
-                for (int q = tid; q < n; q += kTQ) keys_next[start + q] = -1;
             continue;
         }
-        // ---- canonical (cell, particle id) order of the block's list: the scatter left each
-        // cell's entries in arbitrary order; rank them by particle id inside the cell (fixed
-        // order of every sum below -> bitwise reproducible).  Scratch in the row region.
-        {
-            int* s_raw = reinterpret_cast<int*>(smem);   // [n] state index (scatter order)
-            int* s_rpid = s_raw + G::MAXP;                // [n] particle id
-            unsigned char* s_rcell = reinterpret_cast<unsigned char*>(s_rpid + G::MAXP);  // [n] cell of entry
-            for (int q = tid; q < n; q += kTQ) {
-                s_raw[q] = sl.sigma[start + q];
-                s_rpid[q] = sl.spid[start + q];
-            }
-            for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
-            __syncthreads();
-            for (int c = tid; c <= G::CELLS; c += kTQ) {
-                const int hi = c < G::CELLS ? s_cst[c + 1] : n;
-                for (int r = s_cst[c]; r < hi; ++r) s_rcell[r] = (unsigned char)c;
-            }
-            __syncthreads();
-            for (int r = tid; r < n; r += kTQ) {
-                const int c = s_rcell[r];
-                const int lo = s_cst[c], hi = c < G::CELLS ? s_cst[c + 1] : n;
-                const int pr = s_rpid[r];
-                int rank = 0;
-                for (int q = lo; q < hi; ++q) rank += s_rpid[q] < pr;
-                const int rr = lo + rank;
-                s_ci[rr] = s_raw[r];
-                sl.sigma[start + rr] = s_raw[r];
-                if (Sn.pid) Sn.pid[start + rr] = pr;
-            }
-            if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
-#ifdef MPM_DEBUG_CST
-            if (tid == 0 && s_cst[G::CELLS] != n)
-                printf("p2g step %d bi %d bid %d b0 %d start %d n %d cst0 %d cst1 %d cst63 %d cst64 %d cstart %p\n", sl.step, bi, bid, b0,
-                       start, n, s_cst[0], s_cst[1], s_cst[63], s_cst[64], cstart);
-#endif
-            __syncthreads();
-        }
+        // ---- the block's list in canonical (cell, particle id) order (k_canon)
+        for (int q = tid; q < n; q += kTQ) s_ci[q] = sl.sigma[start + q];
+        for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
+        __syncthreads();
         const int nvalid = s_cst[G::CELLS];
         // ---- phases 1 + 2 over chunks of kTQ particles in canonical order; the particle
         // loads of chunk k+1 are issued before the accumulation of chunk k (same registers)
@@ -716,7 +777,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
                 const float act = (aid && a_id >= 0 && a_id < p.n_act) ? alpha[e * p.a_estride + a_id] : 0.0f;
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
                 if (!p2g_particle<D>(p, x, vc, F, act, fluid, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
-                write_row<D>(s_row + RowL<D>::off(r - ch), w, c, Adx);
+                write_row<D>(s_row + (r - ch) * RS, w, c, Adx);
                 if (Sn.f) {
                     if (fluid) fluid_reset<D>(Ft, Ft);  // R23 (Ft is dead after the row)
 #pragma unroll
@@ -727,7 +788,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
             __syncthreads();
             if (tid < kACC) {
                 const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], cend);
-                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + RowL<D>::off(rr - ch), my_ox);
+                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
             }
             __syncthreads();
         }
@@ -746,169 +807,72 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
 }
 
 // ------------------------------------------------------------- grid_op
-// The covering tiles of a COLUMN of tile nodes (fixed local (n1, n2), n0 = 0..TE-1) of block
-// (e, c0): along x the blocks bx-1, bx, bx+1 (x option xo = 0, 1, 2), along y / z the node's
-// block and the previous one.  The pool tile indices are looked up once per column (12 in 3D,
-// instead of up to 8 per node); a block outside this subdomain's slab is looked up in the
-// neighbour (f3).  col_sum adds them per node in the fixed (a, b, c) order: every node is the
-// sum of the <= 2^d partial tiles whose block's cells [c0, c0 + B) satisfy c0 <= g < c0 + B + 2.
-template <int D> struct ColCover {
-    int ti[3][2][2];       // pool tile index per (x option, y option, z option), -1 = none
-    const float4* tl[3];   // pool-indexed tiles per x option (own or a neighbour's)
-    int l1, l2;            // local offsets of the column's y / z node inside their block
-    bool ok1y, ok1z;       // the previous block along y / z covers it too
-};
-
-template <int D>
-__device__ __forceinline__ void col_cover(const KParams& p, int e, const int c0[3], int g1, int g2,
-                                          const int* __restrict__ bmap, const float4* tiles, const Halo& hl,
-                                          const float4* nt0, const float4* nt1, ColCover<D>& cc) {
-    using G = Geo<D>;
-    const int bx = c0[0] >> G::LOGB;
-    const int by = g1 >> G::LOGB, bz = D == 3 ? g2 >> G::LOGB : 0;
-    cc.l1 = g1 & (G::B - 1);
-    cc.l2 = D == 3 ? g2 & (G::B - 1) : 0;
-    cc.ok1y = cc.l1 < 2 && by >= 1;
-    cc.ok1z = D == 3 && cc.l2 < 2 && bz >= 1;
-#pragma unroll
-    for (int xo = 0; xo < 3; ++xo) {
-        const int xb = bx - 1 + xo;
-        const int* bm = bmap;
-        const float4* tl = tiles;
-        if (xb < hl.x_lo) { bm = hl.bmap[0]; tl = nt0; }
-        else if (xb >= hl.x_hi) { bm = hl.bmap[1]; tl = nt1; }
-        cc.tl[xo] = tl;
-        const bool xok = bm != nullptr && xb >= 0 && xb < p.nb;
-#pragma unroll
-        for (int b = 0; b < 2; ++b)
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int bb[3] = {xb, by - b, bz - c};
-                const bool ok = xok && (b == 0 || cc.ok1y) && (c == 0 || cc.ok1z) && (D == 3 || c == 0) &&
-                                bb[1] < p.nb && (D == 2 || bb[2] < p.nb);
-                cc.ti[xo][b][c] = ok ? __ldg(bm + block_lin<D>(p, e, bb)) : -1;
-            }
-    }
-}
-
-// node n0 of the column (n0 a compile-time constant after unrolling: static register indexing)
-template <int D>
-__device__ __forceinline__ float4 col_sum(const ColCover<D>& cc, int n0, bool bx_ge1) {
-    using G = Geo<D>;
-    const int l0 = n0 < G::B ? n0 : n0 - G::B;               // local x inside the node's block
-    const bool ok1x = n0 < G::B ? (n0 < 2 && bx_ge1) : true;  // previous x block covers it too
-    const int xo0 = n0 < G::B ? 1 : 2;                         // x option of the node's own block
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-        if (a && !ok1x) continue;
-        const int xo = xo0 - a;
-#pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            if (b && !cc.ok1y) continue;
-#pragma unroll
-            for (int c = 0; c < (D == 3 ? 2 : 1); ++c) {
-                if (c && !cc.ok1z) continue;
-                const int ti = cc.ti[xo][b][c];
-                if (ti < 0) continue;
-                const int lq = tile_lin<D>(l0 + a * G::B, cc.l1 + b * G::B, cc.l2 + c * G::B);
-                const float4 v = __ldg(cc.tl[xo] + (int64_t)ti * G::TN + lq);
-                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-            }
-        }
-    }
-    return acc;
-}
-
-template <int D> constexpr int tile_cols() { return D == 3 ? Geo<D>::TE * Geo<D>::TE : Geo<D>::TE; }
-
-// P:579 (R5-R7): thread per node column of every active block's (B+2)^d tile:
+// P:579 (R5-R7): thread per node of every active block's (B+2)^d tile:
 // (P, M) = sum of the covering partial tiles; u1 = P/(M + eps) - dt g e_y; sticky walls.
 // Resolved tile entry: (u1, M), or (0, 0, 0, -M) where the wall zeroed the velocity
-// (sign bit set, also for M = 0: -0.0f; nodes outside the grid: (0, 0, 0, -0)).  Stored per
-// step: g2p / g2p_grad / grid_op_grad read it.
-template <int D>
+// (sign bit set, also for M = 0: -0.0f; nodes outside the grid: (0, 0, 0, -0)).  Stored per step: g2p / g2p_grad / grid_op_grad read it.
+template <int D, bool HALO>
 __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
     pdl_begin();
     using G = Geo<D>;
-    constexpr int NC = tile_cols<D>();
     const int nact = *sl.nactive;
     const int b0 = *sl.base;
     const int* blist = sl.blist + b0;
     const float4* part_g = sl.part - (int64_t)b0 * G::TN;  // bmap holds pool indices
     float4* rt = sl.tiles + (int64_t)b0 * G::TN;
-    const int64_t total = (int64_t)nact * NC;
+    const int64_t total = (int64_t)nact * G::TN;
     const float4* nt0 = halo_tiles<D>(sl.halo, 0);
     const float4* nt1 = halo_tiles<D>(sl.halo, 1);
     for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
-        const int bi = (int)(idx / NC), col = (int)(idx - (int64_t)bi * NC);
-        const int n1 = D == 3 ? col / G::TE : col, n2 = D == 3 ? col % G::TE : 0;
-        int e, c0[3];
+        const int bi = (int)(idx / G::TN), q = (int)(idx - (int64_t)bi * G::TN);
+        int e, c0[3], n[3];
         block_origin<D>(p, __ldg(blist + bi), e, c0);
-        const int g1 = c0[1] + n1, g2 = D == 3 ? c0[2] + n2 : 0;
-        ColCover<D> cc;
-        col_cover<D>(p, e, c0, g1, g2, sl.bmap, part_g, sl.halo, nt0, nt1, cc);
-        const bool in12 = g1 < p.n_grid && (D == 2 || g2 < p.n_grid);
-        const bool bx_ge1 = (c0[0] >> G::LOGB) >= 1;
-        float4* out_t = rt + (int64_t)bi * G::TN;
-#pragma unroll
-        for (int n0 = 0; n0 < G::TE; ++n0) {
-            const int g[3] = {c0[0] + n0, g1, g2};
-            float4 out = make_float4(0.f, 0.f, 0.f, -0.0f);
-            if (in12 && g[0] < p.n_grid) {
-                const float4 pm = col_sum<D>(cc, n0, bx_ge1);
-                float u0[3], u1[3];
-                out = grid_velocity<D>(p, g, pm, u0, u1) ? make_float4(0.f, 0.f, 0.f, -pm.w)
-                                                          : make_float4(u1[0], u1[1], u1[2], pm.w);
-            }
-            out_t[tile_lin<D>(n0, n1, n2)] = out;
+        local_node<D>(q, n);
+        const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
+        const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
+        float4 out = make_float4(0.f, 0.f, 0.f, -0.0f);
+        if (inside) {
+            const float4 pm = covered_sum<D, HALO>(p, e, g, sl.bmap, part_g, sl.halo, nt0, nt1);
+            float u0[3], u1[3];
+            out = grid_velocity<D>(p, g, pm, u0, u1) ? make_float4(0.f, 0.f, 0.f, -pm.w)
+                                                      : make_float4(u1[0], u1[1], u1[2], pm.w);
         }
+        rt[idx] = out;
     }
 }
 
 // --------------------------------------------------------- grid_op_grad
 // P:589 (select rule): per node, ub = sum of the covering U_bar partial tiles;
 // sticky (sign bit of w): Pb = Mb = 0; else u0 = u1 + dt g e_y, Pb = ub/(M + eps),
-// Mb = -(ub . u0)/(M + eps).  Output tile (Pb, Mb) -> sl.part (local block index).  Thread per
-// node column as grid_op.
-template <int D>
+// Mb = -(ub . u0)/(M + eps).  Output tile (Pb, Mb) -> sl.part (local block index).
+template <int D, bool HALO>
 __global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, const float4* __restrict__ ubar) {
     pdl_begin();
     using G = Geo<D>;
-    constexpr int NC = tile_cols<D>();
     const int nact = *sl.nactive;
     const int b0 = *sl.base;
     const int* blist = sl.blist + b0;
     const float4* ub_g = ubar - (int64_t)b0 * G::TN;
     const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
-    const int64_t total = (int64_t)nact * NC;
+    const int64_t total = (int64_t)nact * G::TN;
     const float4* nt0 = halo_tiles<D>(sl.halo, 0);
     const float4* nt1 = halo_tiles<D>(sl.halo, 1);
     for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
-        const int bi = (int)(idx / NC), col = (int)(idx - (int64_t)bi * NC);
-        const int n1 = D == 3 ? col / G::TE : col, n2 = D == 3 ? col % G::TE : 0;
-        int e, c0[3];
-        block_origin<D>(p, __ldg(blist + bi), e, c0);
-        const int g1 = c0[1] + n1, g2 = D == 3 ? c0[2] + n2 : 0;
-        ColCover<D> cc;
-        col_cover<D>(p, e, c0, g1, g2, sl.bmap, ub_g, sl.halo, nt0, nt1, cc);
-        const bool bx_ge1 = (c0[0] >> G::LOGB) >= 1;
-        const float4* r_t = rt + (int64_t)bi * G::TN;
-        float4* out_t = sl.part + (int64_t)bi * G::TN;
-#pragma unroll
-        for (int n0 = 0; n0 < G::TE; ++n0) {
-            const int q = tile_lin<D>(n0, n1, n2);
-            const float4 r = __ldg(r_t + q);
-            float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (!signbit(r.w)) {  // outside the grid: -0 sign bit set
-                const float4 ub = col_sum<D>(cc, n0, bx_ge1);
-                const float u0[3] = {r.x, r.y + p.dt * p.gravity, r.z};
-                const float denom = r.w + p.eps_mass;
-                const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
-                out = make_float4(ub.x / denom, ub.y / denom, D == 3 ? ub.z / denom : 0.0f, -dot / denom);
-            }
-            out_t[q] = out;
+        const float4 r = __ldg(rt + idx);
+        float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (!signbit(r.w)) {
+            const int bi = (int)(idx / G::TN), q = (int)(idx - (int64_t)bi * G::TN);
+            int e, c0[3], n[3];
+            block_origin<D>(p, __ldg(blist + bi), e, c0);
+            local_node<D>(q, n);
+            const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
+            const float4 ub = covered_sum<D, HALO>(p, e, g, sl.bmap, ub_g, sl.halo, nt0, nt1);
+            const float u0[3] = {r.x, r.y + p.dt * p.gravity, r.z};
+            const float denom = r.w + p.eps_mass;
+            const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
+            out = make_float4(ub.x / denom, ub.y / denom, D == 3 ? ub.z / denom : 0.0f, -dot / denom);
         }
+        sl.part[idx] = out;
     }
 }
 
@@ -1025,7 +989,6 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
             key = bid;  // p2g of the next step drops it into the junk bucket
         }
         keys[j] = key * 128 + cell;
-        return key * 128 + cell;
     }
     return key;
 }
@@ -1036,8 +999,8 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
 // from the forward's (checkpoint invariance is tested bitwise).
 template <int D>
 __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
-                                            int* __restrict__ keys, int* __restrict__ bcount,
-                                            int* __restrict__ ccount, int* flags, bool refwd, Migr mg) {
+                                            int* __restrict__ keys, int* __restrict__ bcount, int* flags,
+                                            bool refwd, Migr mg) {
     pdl_begin();
     using G = Geo<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
@@ -1078,10 +1041,10 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
         const float4* sU = pipe.wait(it);
         int key = -1;
         if (va) key = g2p_particle<D>(p, sU, xa, c0, start + tid, e, bid, Sn, keys, flags, refwd, S, ia, mg);
-        if (keys) count_bin(va && key >= 0, key >> 7, key & 127, bcount, ccount);
+        if (keys) count_key(va && key >= 0, key, bcount);
         key = -1;
         if (vb) key = g2p_particle<D>(p, sU, xb, c0, start + tid + kTG, e, bid, Sn, keys, flags, refwd, S, ib, mg);
-        if (keys) count_bin(vb && key >= 0, key >> 7, key & 127, bcount, ccount);
+        if (keys) count_key(vb && key >= 0, key, bcount);
         for (int r0 = 2 * kTG; r0 < nvalid; r0 += kTG) {
             const int r = r0 + tid;
             const bool in = r < nvalid;
@@ -1093,7 +1056,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
                 for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i));
                 key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags, refwd, S, i, mg);
             }
-            if (keys) count_bin(in && key >= 0, key >> 7, key & 127, bcount, ccount);
+            if (keys) count_key(in && key >= 0, key, bcount);
         }
         __syncthreads();
     }
@@ -1106,7 +1069,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
 // CTA = 192 threads: phase 1 thread per particle (rows in smem), phase 2 thread per
 // (cell, o_x) accumulating U_bar like p2g's momentum.
 template <int D> constexpr int g2pg_union_bytes() {
-    constexpr int a = Geo<D>::CELLS * Geo<D>::NST * 16, c = RowL<D>::bytes(kCH);
+    constexpr int a = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
     return a > c ? a : c;
 }
 template <int D> constexpr int g2pg_smem_bytes() { return g2pg_union_bytes<D>() + (Geo<D>::CELLS + 2) * 4; }
@@ -1206,6 +1169,7 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
                                                             float4* __restrict__ ubar) {
     pdl_begin();
     using G = Geo<D>;
+    constexpr int RS = RowL<D>::STRIDE;
     extern __shared__ __align__(16) unsigned char smem[];
     float* s_row = reinterpret_cast<float*>(smem);   // rows, then ...
     float4* s_cb = reinterpret_cast<float4*>(smem);  // ... node partials
@@ -1243,13 +1207,13 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
                 float w[3][3], cp[3], B[D * D];
                 g2pg_row<D>(p, x, xb, vbn, Cbn, c0, w, cp, B);
-                write_row<D>(s_row + RowL<D>::off(r - ch), w, cp, B);
+                write_row<D>(s_row + (r - ch) * RS, w, cp, B);
                 if (r + kTQ < nvalid) MPM_G2PG_LOAD(r + kTQ);  // this thread's next particle
             }
             __syncthreads();
             if (tid < kACC) {
                 const int lo = max(s_cst[my_cell], ch), hi = min(s_cst[my_cell + 1], cend);
-                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + RowL<D>::off(rr - ch), my_ox);
+                for (int rr = lo; rr < hi; ++rr) acc.row(s_row + (rr - ch) * RS, my_ox);
             }
             __syncthreads();
         }
@@ -1650,8 +1614,7 @@ template <int D>
 __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const int* __restrict__ nsorted,
                                                   MigSrc left, MigSrc right, int x_lo, int x_hi, int cap,
                                                   int* __restrict__ keys, int* __restrict__ bcount,
-                                                  int* __restrict__ ccount, int* __restrict__ imm_base,
-                                                  int* __restrict__ nrows, int* flags) {
+                                                  int* __restrict__ imm_base, int* __restrict__ nrows, int* flags) {
     pdl_begin();
     using L = Lay<D>;
     const int side = blockIdx.y;
@@ -1666,7 +1629,7 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
     const int n = side == 0 ? n_left : n_right;
     const int m = blockIdx.x * kT + threadIdx.x;
     const bool in = m < n;
-    int key = -1, cell = 0;
+    int key = -1;
     if (in) {
         const int j = src.rows[(side == 0 ? 1 : 0) * cap + m];  // the neighbour's outbox toward us
         const int64_t dst = (int64_t)base + m;
@@ -1690,8 +1653,7 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
                 const int lc[3] = {b[0] & (Geo<D>::B - 1), b[1] & (Geo<D>::B - 1), b[2] & (Geo<D>::B - 1)};
                 if (bb[0] >= x_lo && bb[0] < x_hi) {
                     key = block_lin<D>(p, 0, bb);
-                    cell = cell_of<D>(lc);
-                    keys[dst] = key * 128 + cell;
+                    keys[dst] = key * 128 + cell_of<D>(lc);
                 } else {
                     atomicOr(flags, FLAG_MIGRATION);  // moved past this slab in one step
                     keys[dst] = -1;
@@ -1702,7 +1664,7 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
             }
         }
     }
-    count_bin(in && key >= 0, key, cell, bcount, ccount);
+    count_key(in && key >= 0, key, bcount);
 }
 
 // backward of the migration: the adjoint of an emigrant's S_{t+1} row was computed by the
@@ -1766,6 +1728,7 @@ inline unsigned nblk(int64_t n) { return (unsigned)((n + kT - 1) / kT); }
 struct DevTab {
     int grid[5][2];  // persistent grid size per kernel kind and dimension
     int sms = 148;
+    int canon_grid = 148 * 8;
 };
 constexpr int kMaxDev = 64;
 DevTab g_tab[kMaxDev];
@@ -1823,6 +1786,9 @@ cudaError_t tile_init() {
     if ((done_mask >> dev) & 1ull) return cudaSuccess;
     DevTab& T = g_tab[dev];
     cudaDeviceGetAttribute(&T.sms, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaFuncSetAttribute(k_canon, cudaFuncAttributeMaxDynamicSharedMemorySize, canon_smem_bytes());
+    if (e) return e;
+    T.canon_grid = occupancy_grid((const void*)k_canon, canon_smem_bytes(), kT);
 #define MPM_INIT_DIM(DI)                                                                                          \
     do {                                                                                                          \
         constexpr int DIM = (DI) == 2 ? 2 : 3;                                                                    \
@@ -1863,42 +1829,46 @@ static unsigned pgrid(const KParams& p, int kind) {
     return (unsigned)(p.step_blocks < g ? p.step_blocks : g);
 }
 
-void launch_bin_keys(const KParams& p, const float* x, int64_t n_live, int* keys, const BinCounts& bc, int* flags,
+void launch_bin_keys(const KParams& p, const float* x, int64_t n_live, int* keys, int* bcount, int* flags,
                      cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_bin_keys<DIM>, nblk(p.N * p.E), kT, 0, s, p, x, n_live, keys, bc.bcount, bc.ccount,
-                             flags));
+    DISPATCH(p.dim, launch_k(k_bin_keys<DIM>, nblk(p.N * p.E), kT, 0, s, p, x, n_live, keys, bcount, flags));
 }
 int scan_chunks(const KParams& p) { return (p.TB + kScanChunk - 1) / kScanChunk; }
-void launch_bin_scan(const KParams& p, const BinCounts& bc, const SlotView& sl, int* part, int* flags,
+void launch_bin_scan(const KParams& p, int* bcount, int* cursor, const SlotView& sl, int* part, int* flags,
                      cudaStream_t s) {
     const int nc = scan_chunks(p);
-    launch_k(k_bin_scan, nc, kT, 0, s, p, bc.bcount, bc.ccount, bc.ccursor, sl, (int2*)part, flags);
+    launch_k(k_bin_scan, nc, kT, 0, s, p, bcount, cursor, sl, (int2*)part, flags);
 }
-void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, const BinCounts& bc, const SlotView& sl,
+void launch_bin_scatter(const KParams& p, const int* keys, const int* pid, int* cursor, const SlotView& sl,
                         cudaStream_t s) {
-    launch_k(k_bin_scatter, (unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s, p, keys,
-             pid, bc.ccursor, sl);
+    launch_k(k_bin_scatter, (unsigned)((p.N * p.E + kT * kScatterPer - 1) / (kT * kScatterPer)), kT, 0, s, p, keys, pid, cursor, sl);
+}
+void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* keys_next, int* flags, cudaStream_t s) {
+    const int cg = tab().canon_grid;
+    launch_k(k_canon, cg < p.step_blocks ? cg : (p.step_blocks > 0 ? p.step_blocks : 1), kT, canon_smem_bytes(), s, p, sl,
+             pid_next, keys_next, flags);
 }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
-                const int32_t* aid, const float* alpha_t, int* keys_next, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t,
-                             keys_next, flags));
+                const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
+    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t, flags));
 }
-static unsigned node_grid(const KParams& p) {  // thread per tile node column
-    const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? tile_cols<3>() : tile_cols<2>()) + kT - 1) / kT;
+static unsigned node_grid(const KParams& p) {
+    const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? Geo<3>::TN : Geo<2>::TN) + kT - 1) / kT;
     const int64_t cap = (int64_t)tab().sms * 8;
     return (unsigned)(need < cap ? (need > 0 ? need : 1) : cap);
 }
+static bool has_halo(const SlotView& sl) { return sl.halo.tiles[0] != nullptr || sl.halo.tiles[1] != nullptr; }
 void launch_grid_op(const KParams& p, const SlotView& sl, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_grid_op<DIM>, node_grid(p), kT, 0, s, p, sl));
+    if (has_halo(sl)) DISPATCH(p.dim, launch_k(k_grid_op<DIM, true>, node_grid(p), kT, 0, s, p, sl));
+    else DISPATCH(p.dim, launch_k(k_grid_op<DIM, false>, node_grid(p), kT, 0, s, p, sl));
 }
 void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* ubar, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM>, node_grid(p), kT, 0, s, p, sl, ubar));
+    if (has_halo(sl)) DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM, true>, node_grid(p), kT, 0, s, p, sl, ubar));
+    else DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM, false>, node_grid(p), kT, 0, s, p, sl, ubar));
 }
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
-                const BinCounts& bc, int* flags, bool refwd, const Migr& mg, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_g2p<DIM>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bc.bcount, bc.ccount, flags, refwd,
-                             mg));
+                int* bcount, int* flags, bool refwd, const Migr& mg, cudaStream_t s) {
+    DISPATCH(p.dim, launch_k(k_g2p<DIM>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bcount, flags, refwd, mg));
 }
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, cudaStream_t s) {
@@ -1927,11 +1897,11 @@ void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_
 
 namespace mpm {
 void launch_immigrate(const KParams& p, const StateView& S, const int* nsorted, MigSrc left, MigSrc right,
-                      int x_lo, int x_hi, int cap, int* keys, const BinCounts& bc, int* imm_base, int* nrows,
-                      int* flags, cudaStream_t s) {
+                      int x_lo, int x_hi, int cap, int* keys, int* bcount, int* imm_base, int* nrows, int* flags,
+                      cudaStream_t s) {
     const dim3 grid((unsigned)((cap + kT - 1) / kT), 2);
     DISPATCH(p.dim, launch_k(k_immigrate<DIM>, grid, kT, 0, s, p, S, nsorted, left, right, x_lo, x_hi, cap, keys,
-                             bc.bcount, bc.ccount, imm_base, nrows, flags));
+                             bcount, imm_base, nrows, flags));
 }
 void launch_adj_pull(const KParams& p, const AdjView& Sb, const int* cnt, const int* rows, int cap,
                      const AdjView& nb_left, const int* nb_left_base, const AdjView& nb_right,

@@ -49,9 +49,6 @@ template <int D> struct Geo {
     static constexpr int NST = D == 3 ? 27 : 9;      // stencil offsets
     static constexpr int MAXP = 1728;                // particles per block (27 per cell)
 };
-// per-block stride of the (block, cell) histogram and cursors: 64 cells + the junk bucket, padded
-// to whole int4
-constexpr int kCellStride = 68;
 
 // State layout: three component-major (SoA) arrays per
 // state -- component k of particle i at ptr[k * EN + i] -- so a warp's access to one
