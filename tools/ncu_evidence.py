@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 COLS = [("DRAM MB", ["dram__bytes_read.sum", "dram__bytes_write.sum"], "MB"),
-        ("DRAM % peak", ["FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed"], None),
+        ("DRAM % peak", ["dram__throughput.avg.pct_of_peak_sustained_elapsed"], None),
         ("L2 red+atom sectors", ["lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum"], None),
         ("smem bank conflicts", ["l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"], None),
         ("smem wavefronts", ["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"], None),
@@ -18,7 +18,10 @@ COLS = [("DRAM MB", ["dram__bytes_read.sum", "dram__bytes_write.sum"], "MB"),
 
 def val(row, col, units, name):
     if name not in col:
-        return None
+        alt = [c for c in col if c.endswith("." + name)]  # section-prefixed copies
+        if not alt:
+            return None
+        name = alt[0]
     try:
         v = float(row[col[name]])
     except ValueError:
