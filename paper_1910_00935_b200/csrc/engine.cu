@@ -101,7 +101,6 @@ KParams kparams(const mpm_ctx* h) {
     k.n_body = h->dd ? h->n_body : h->N;
     k.x_lo = h->dd ? h->x_lo : 0;
     k.x_hi = h->dd ? h->x_hi : k.nb;
-    k.sched = h->sched;
     return k;
 }
 
@@ -215,7 +214,6 @@ size_t carve(mpm_ctx* h, char* base) {
     float* loss = (float*)take(sizeof(float) * E);
     float* com_part = (float*)take(sizeof(float) * E * (lblk + 2) * 3);
     int64_t* counter = (int64_t*)take(sizeof(int64_t) * 2);
-    int* sched = (int*)take(sizeof(int) * 16);  // block-scheduler counters (kernels_tile.cu BlockSched)
     int* flags = (int*)take(sizeof(int) * 4);
     if (base) {
         h->max_active = max_active;
@@ -238,7 +236,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
         h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
         h->flags = flags;
-        h->ntot_arr = ntot_arr; h->blk_part = blk_part; h->sched = sched;
+        h->ntot_arr = ntot_arr; h->blk_part = blk_part;
         h->out_cnt = out_cnt; h->out_rows = out_rows; h->imm_base = imm_base; h->nrows_arr = nrows_arr;
     }
     return off;
@@ -604,7 +602,6 @@ mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     carve(h, h->ws);
     const KParams k = kparams(h);
     CU(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
-    CU(cudaMemsetAsync(h->sched, 0, sizeof(int) * 16, h->stream));
     CU(cudaMemsetAsync(h->scan_part, 0, sizeof(int64_t) * (scan_chunks(kparams(h)) + 2), h->stream));
     CU(cudaMemsetAsync(h->bcount, 0, sizeof(int) * k.TB, h->stream));
     CU(cudaMemsetAsync(h->theta, 0, sizeof(float) * (n_theta_of(h->prm, h->dim) > 0 ? n_theta_of(h->prm, h->dim) : 1), h->stream));

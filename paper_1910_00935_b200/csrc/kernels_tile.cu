@@ -213,49 +213,6 @@ template <int D> struct TilePipe {
     }
 };
 
-// Block scheduling of the persistent kernels.  Static (ctr == null): CTA c takes blocks c,
-// c + grid, ...  Dynamic: the first block of a CTA is blockIdx.x and every further one is the next
-// ticket of an atomic counter (greedy list scheduling, so the CTAs finish within about one block
-// of each other; with the static stride the busiest CTA has ~18% more particles than the mean at
-// C5).  The results do not change: every output of a block depends only on that block.  The
-// ticket after the next one is fetched at the top of each iteration, so the next block is known
-// an iteration ahead (the TMA tile pipelines prefetch its tile).  The last CTA to finish resets
-// the counter pair for the next launch.
-#ifndef MPM_DYN_SCHED
-#define MPM_DYN_SCHED 1
-#endif
-struct BlockSched {
-    int* ctr;   // [2] tickets handed out, CTAs finished (workspace, zero between launches); null = static
-    int* s_tk;  // shared [2]
-    int bi, nxt;
-    __device__ __forceinline__ void begin() {
-        bi = blockIdx.x;
-        nxt = bi + gridDim.x;
-        if (MPM_DYN_SCHED && ctr) {
-            if (threadIdx.x == 0) s_tk[0] = gridDim.x + atomicAdd(ctr, 1);
-            __syncthreads();
-            nxt = s_tk[0];
-        }
-    }
-    __device__ __forceinline__ void fetch(int it) {
-        if (MPM_DYN_SCHED && ctr && threadIdx.x == 0) s_tk[(it + 1) & 1] = gridDim.x + atomicAdd(ctr, 1);
-    }
-    // after the iteration's closing __syncthreads
-    __device__ __forceinline__ void advance(int it) {
-        bi = nxt;
-        nxt = (MPM_DYN_SCHED && ctr) ? s_tk[(it + 1) & 1] : nxt + gridDim.x;
-    }
-    __device__ __forceinline__ void end() {
-        if (MPM_DYN_SCHED && ctr && threadIdx.x == 0) {
-            __threadfence();
-            if (atomicAdd(ctr + 1, 1) == (int)gridDim.x - 1) {
-                ctr[0] = 0;
-                ctr[1] = 0;
-            }
-        }
-    }
-};
-
 // warp-aggregated histogram increment (keys in a warp are mostly equal)
 __device__ __forceinline__ void count_key(bool valid, int key, int* bcount) {
     const unsigned peers = __match_any_sync(0xffffffffu, valid ? key : -1);
@@ -761,7 +718,7 @@ __global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __res
 template <int D>
 __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
                                                const int32_t* __restrict__ aid,
-                                               const float* __restrict__ alpha, int* flags, int* sched) {
+                                               const float* __restrict__ alpha, int* flags) {
     pdl_begin();
     using G = Geo<D>;
     using L = Lay<D>;
@@ -779,20 +736,13 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
     const int* bstart = sl.bstart + b0 + sl.step;
     unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
     float4* tiles_l = sl.part;  // partial tiles of this step (local block index)
-    __shared__ int s_tk[2];
-    BlockSched sch{sched, s_tk};
-    sch.begin();
-    for (int it = 0; sch.bi < nact; ++it) {
-        const int bi = sch.bi;
-        sch.fetch(it);
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         const int bid = blist[bi];
         const int start = bstart[bi], n = bstart[bi + 1] - start;
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         if (n > G::MAXP) {
             if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
-            __syncthreads();
-            sch.advance(it);
             continue;
         }
         // ---- the block's list in canonical (cell, particle id) order (k_canon)
@@ -853,9 +803,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
             tile[q] = s4;
         }
         __syncthreads();
-        sch.advance(it);
     }
-    sch.end();
 }
 
 // ------------------------------------------------------------- grid_op
@@ -1533,14 +1481,13 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
                                                  const int32_t* __restrict__ aid,
                                                  const float* __restrict__ alpha, AdjView Sbn,
                                                  const float* __restrict__ xbp, AdjView Sb,
-                                                 float* __restrict__ abar_part, int* flags, int* sched) {
+                                                 float* __restrict__ abar_part, int* flags) {
     pdl_begin();
     using G = Geo<D>;
     using L = Lay<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ float s_ab[kTP / 32][32];
-    __shared__ int s_tk[2];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nact = *sl.nactive;
     const int b0 = *sl.base;  // this step's offset in the grid-store pool
@@ -1550,14 +1497,11 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
     const float4* gt = sl.part;  // (Pb, Mb) tiles from grid_op_grad (local block index)
     TilePipe<D> pipe{s_buf, s_bar};
     pipe.init();
-    BlockSched sch{sched, s_tk};
-    sch.begin();
     __syncthreads();
-    pipe.start(gt, sch.bi, nact);
-    for (int it = 0; sch.bi < nact; ++it) {
-        const int bi = sch.bi;
-        sch.fetch(it);
-        pipe.next(gt, sch.nxt, nact, it);
+    pipe.start(gt, blockIdx.x, nact);
+    int it = 0;
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
+        pipe.next(gt, bi + gridDim.x, nact, it);
         const int bid = blist[bi];
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
@@ -1621,9 +1565,7 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
             abar_part[(int64_t)bi * p.n_act + tid] = s;
         }
         __syncthreads();
-        sch.advance(it);
     }
-    sch.end();
 }
 
 // alpha_bar_t[a] = sum over active blocks (list order) of abar_part[b][a]
@@ -1906,11 +1848,9 @@ void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* keys
     launch_k(k_canon, cg < p.step_blocks ? cg : (p.step_blocks > 0 ? p.step_blocks : 1), kT, canon_smem_bytes(), s, p, sl,
              pid_next, keys_next, flags);
 }
-static int* sched_ctr(const KParams& p, int kind) { return MPM_DYN_SCHED && p.sched ? p.sched + 2 * kind : nullptr; }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t, flags,
-                             sched_ctr(p, 0)));
+    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t, flags));
 }
 static unsigned node_grid(const KParams& p) {
     const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? Geo<3>::TN : Geo<2>::TN) + kT - 1) / kT;
@@ -1941,8 +1881,7 @@ void launch_g2p_grad_gather(const KParams& p, const SlotView& sl, const StateVie
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
                      const float* alpha_t, const AdjView& Sbn, const float* xbp,
                      const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_p2g_grad<DIM>, pgrid(p, 3), kTP, 0, s, p, sl, S, aid, alpha_t, Sbn, xbp, Sb, abar_part, flags,
-                             sched_ctr(p, 3)));
+    DISPATCH(p.dim, launch_k(k_p2g_grad<DIM>, pgrid(p, 3), kTP, 0, s, p, sl, S, aid, alpha_t, Sbn, xbp, Sb, abar_part, flags));
 }
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s) {
     cudaMemsetAsync(count, 0, sizeof(int64_t), s);

@@ -31,7 +31,6 @@ struct KParams {
     int64_t n_body;      // particles of one whole body (episode): N, or the total over the
                          // subdomains of a decomposed body (f3; N is then a subdomain's capacity)
     int32_t x_lo, x_hi;  // owned block x-index range (f3 subdomain); single domain: [0, nb)
-    int* sched;          // [8][2] block-scheduler counters of the persistent kernels (zero between launches)
 };
 
 enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8,
