@@ -289,3 +289,41 @@ def test_c5_full_size_64_steps_through_landing():
     rows, ref = compare_episode("c5@64", p, inp, got, steps=64, grads=("dx0", "dv0"))
     check(rows, "c5@64")
     assert ref["x"][:, 1].min() < 3.5 / 128  # it did reach the floor
+
+
+def test_dense_2d_block_multi_chunk():
+    """2D blocks holding more than one shared-memory chunk of particle rows (> 576 particles in an
+    8^2-cell block: ~12 particles per cell at h = dx / 3.5), so p2g's and the U_bar scatter's
+    chunk loops run more than once: states and gradients vs the oracle, and checkpoint invariance."""
+    p = W.config("c1a", steps=32, counts=(56, 56), h=1.0 / 224)
+    inp = W.make_inputs(p)
+    x = inp["x"].astype(np.float32)
+    b = np.floor(x * np.float32(64) - np.float32(0.5)).astype(np.int64) // 8
+    _, per_block = np.unique(b[:, 0] * 8 + b[:, 1], return_counts=True)
+    assert per_block.max() > 576 and per_block.max() <= 1728, per_block.max()
+    got = gpu_run(p, inp)
+    rows, _ = compare_episode("c1a_dense2d@32", p, inp, got, grads=("dx0", "dv0", "dC0", "dF0"))
+    check(rows, "dense2d")
+    got4 = gpu_run(p, inp, k_ckpt=4)
+    for key in ("x", "v", "C", "F", "dx0", "dv0", "dC0", "dF0", "loss"):
+        assert np.array_equal(got[key], got4[key]), key
+
+
+def test_binning_scan_beside_a_concurrent_kernel():
+    """The one-launch binning scan looks back only over chunks whose CTAs started earlier (atomic
+    chunk tickets), so it makes progress whatever else occupies the SMs: a C4 batch (16 episodes,
+    65,536 grid blocks -> 64 scan chunks per step) runs while another stream keeps the GPU busy
+    with large matmuls, finishes, and gives the same bytes as a solo run."""
+    import torch
+    p = W.config("c4", steps=24)
+    inps = [W.make_inputs(p, episode=e) for e in range(16)]
+    solo = gpu_run(p, inps, k_ckpt=8)
+    other = torch.cuda.Stream()
+    a = torch.randn(8192, 8192, device="cuda")
+    with torch.cuda.stream(other):
+        for _ in range(40):
+            a = torch.tanh(a @ a * 1e-4)
+    busy = gpu_run(p, inps, k_ckpt=8)
+    torch.cuda.synchronize()
+    for key in ("x", "v", "C", "F", "dx0", "dv0", "dtheta", "loss"):
+        assert np.array_equal(solo[key], busy[key]), key
