@@ -1562,25 +1562,56 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
         if (p.n_act > 0 && tid < p.n_act) {
             float s = 0.0f;
             for (int wv = 0; wv < kTP / 32; ++wv) s += s_ab[wv][tid];
-            abar_part[(int64_t)bi * p.n_act + tid] = s;
+            abar_part[(int64_t)tid * p.step_blocks + bi] = s;  // [n_act][step_blocks]: the reduction reads rows
         }
         __syncthreads();
     }
 }
 
-// alpha_bar_t[a] = sum over active blocks (list order) of abar_part[b][a]
-// (closed loop: per episode e = blockIdx.y, over the blocks of that episode)
-__global__ void k_reduce_abar(KParams p, SlotView sl, const float* __restrict__ part, float* __restrict__ out) {
+// alpha_bar_t[a] = fixed-order sum over the step's active blocks of abar_part[a][b]: thread i sums
+// blocks i, i + 256, ... in order (four interleaved accumulators, combined in order), then the
+// warps' butterflies and the 8 warp sums in warp order.
+// Closed loop: per episode e = blockIdx.y over that episode's blocks (a contiguous range of the
+// block-id-ordered list, found by binary search).  256 threads per actuator: with 64 robot
+// episodes a step has ~6,400 blocks, which one warp per actuator summed in ~20 us.
+constexpr int kRA = 256;
+__global__ void __launch_bounds__(kRA) k_reduce_abar(KParams p, SlotView sl, const float* __restrict__ part,
+                                                     float* __restrict__ out) {
     pdl_begin();
+    __shared__ float s_w[kRA / 32];
     const int a = blockIdx.x, e = blockIdx.y, n_act = p.n_act;
     const int n = *sl.nactive;
     const int* blist = sl.blist + *sl.base;
-    float s = 0.0f;
-    for (int b = threadIdx.x; b < n; b += 32)
-        if (!p.closed_loop || blist[b] / p.nbe == e) s += part[(int64_t)b * n_act + a];
+    int lo = 0, hi = n;
+    if (p.closed_loop) {  // first entries of episode e and e + 1 (block ids are episode-major)
+        int l = 0, h = n;
+        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe < e) l = m + 1; else h = m; }
+        lo = l;
+        h = n;
+        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe <= e) l = m + 1; else h = m; }
+        hi = l;
+    }
+    const float* row = part + (int64_t)a * p.step_blocks;
+    float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    int b = lo + (int)threadIdx.x;
+    for (; b + 3 * kRA < hi; b += 4 * kRA) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s4[u] += row[b + u * kRA];
+    }
+    if (b < hi) s4[0] += row[b];  // at most three left
+    if (b + kRA < hi) s4[1] += row[b + kRA];
+    if (b + 2 * kRA < hi) s4[2] += row[b + 2 * kRA];
+    float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if (threadIdx.x == 0) out[e * n_act + a] = s;
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kRA / 32; ++w) t += s_w[w];
+        out[e * n_act + a] = t;
+    }
 }
 
 // measurement: number of distinct grid nodes with M > 0 in a step's resolved tiles.
@@ -1890,7 +1921,7 @@ void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, c
 void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s) {
     if (p.n_act > 0)
-        launch_k(k_reduce_abar, dim3(p.n_act, p.closed_loop ? p.E : 1), 32, 0, s, p, sl, abar_part, alpha_bar_t);
+        launch_k(k_reduce_abar, dim3(p.n_act, p.closed_loop ? p.E : 1), kRA, 0, s, p, sl, abar_part, alpha_bar_t);
 }
 
 }  // namespace mpm
