@@ -190,7 +190,7 @@ size_t carve(mpm_ctx* h, char* base) {
     int* keys = (int*)take(sizeof(int) * EN);
     float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
     float4* part = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
-    float* abar_part = (float*)take(sizeof(float) * (size_t)max_active * A);  // per-step buffers
+    float* abar_part = (float*)take(sizeof(float) * (size_t)max_active * kMaxSplit * A);  // per work item
     float* alpha = (float*)take(sizeof(float) * (size_t)p.max_steps * AE);
     float* alpha_bar = (float*)take(sizeof(float) * (size_t)p.max_steps * AE);
     // closed loop (R22): observations of every step, group sizes, reduction partials, and the

@@ -213,6 +213,24 @@ template <int D> struct TilePipe {
     }
 };
 
+// Sub-block work split of the thread-per-particle kernels (g2p, g2p_grad's gather part, p2g_grad):
+// when a step has fewer active blocks than the persistent grid has CTAs (the small configurations:
+// C2 ~40 blocks, C3 ~120, on 400-600 CTAs) each block's particles are split into `split` (<= 4)
+// pass-aligned ranges taken by different CTAs, so more SMs work on the step.  split depends only
+// on the step's block count and the grid size, so the work decomposition -- and every result --
+// is deterministic.  Work item w = (block w / split, part w % split).
+__device__ __forceinline__ int item_split(int nact, int grid) {
+    return nact > 0 ? max(1, min(kMaxSplit, grid / nact)) : 1;
+}
+// particle range [rb, re) of part `part` of a block with n particles, in whole passes of NT
+template <int NT>
+__device__ __forceinline__ void item_range(int n, int part, int split, int& rb, int& re) {
+    const int passes = (n + NT - 1) / NT;
+    const int per = (passes + split - 1) / split;
+    rb = min(n, part * per * NT);
+    re = min(n, (part + 1) * per * NT);
+}
+
 // warp-aggregated histogram increment (keys in a warp are mostly equal)
 __device__ __forceinline__ void count_key(bool valid, int key, int* bcount) {
     const unsigned peers = __match_any_sync(0xffffffffu, valid ? key : -1);
@@ -1015,39 +1033,43 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
     TilePipe<D> pipe{s_buf, s_bar};
     pipe.init();
     __syncthreads();
-    pipe.start(rt, blockIdx.x, nact);
+    const int split = item_split(nact, gridDim.x), nitems = nact * split;
+    pipe.start(rt, blockIdx.x / split, nact);
     int it = 0;
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
-        pipe.next(rt, bi + gridDim.x, nact, it);
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+        const int bi = w / split;
+        pipe.next(rt, (w + gridDim.x) / split, nact, it);
         const int bid = blist[bi];
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
+        int rb, re;
+        item_range<kTG>(nvalid, w - bi * split, split, rb, re);
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         // particle loads of the first two passes go out before waiting for the tile
         float xa[3], xb[3];
-        const bool va = tid < nvalid, vb = tid + kTG < nvalid;
+        const bool va = rb + tid < re, vb = rb + tid + kTG < re;
         int ia = 0, ib = 0;
         if (va) {
-            ia = sl.sigma[start + tid];
+            ia = sl.sigma[start + rb + tid];
 #pragma unroll
             for (int k = 0; k < D; ++k) xa[k] = __ldg(S.x + soa(p.EN, k, ia));
         }
         if (vb) {
-            ib = sl.sigma[start + tid + kTG];
+            ib = sl.sigma[start + rb + tid + kTG];
 #pragma unroll
             for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + soa(p.EN, k, ib));
         }
         const float4* sU = pipe.wait(it);
         int key = -1;
-        if (va) key = g2p_particle<D>(p, sU, xa, c0, start + tid, e, bid, Sn, keys, flags, refwd, S, ia, mg);
+        if (va) key = g2p_particle<D>(p, sU, xa, c0, start + rb + tid, e, bid, Sn, keys, flags, refwd, S, ia, mg);
         if (keys) count_key(va && key >= 0, key, bcount);
         key = -1;
-        if (vb) key = g2p_particle<D>(p, sU, xb, c0, start + tid + kTG, e, bid, Sn, keys, flags, refwd, S, ib, mg);
+        if (vb) key = g2p_particle<D>(p, sU, xb, c0, start + rb + tid + kTG, e, bid, Sn, keys, flags, refwd, S, ib, mg);
         if (keys) count_key(vb && key >= 0, key, bcount);
-        for (int r0 = 2 * kTG; r0 < nvalid; r0 += kTG) {
+        for (int r0 = rb + 2 * kTG; r0 < re; r0 += kTG) {
             const int r = r0 + tid;
-            const bool in = r < nvalid;
+            const bool in = r < re;
             key = -1;
             if (in) {
                 const int i = sl.sigma[start + r];
@@ -1246,19 +1268,23 @@ __global__ void __launch_bounds__(kTG) k_g2p_grad_gather(KParams p, SlotView sl,
     TilePipe<D> pipe{s_buf, s_bar};
     pipe.init();
     __syncthreads();
-    pipe.start(rt, blockIdx.x, nact);
+    const int split = item_split(nact, gridDim.x), nitems = nact * split;
+    pipe.start(rt, blockIdx.x / split, nact);
     int it = 0;
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
-        pipe.next(rt, bi + gridDim.x, nact, it);
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+        const int bi = w / split;
+        pipe.next(rt, (w + gridDim.x) / split, nact, it);
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
+        int rb, re;
+        item_range<kTG>(nvalid, w - bi * split, split, rb, re);
         int e, c0[3];
         block_origin<D>(p, blist[bi], e, c0);
         const float4* sU = nullptr;
-        if (nvalid == 0) pipe.wait(it);
-        for (int r0 = 0; r0 < nvalid; r0 += kTG) {
+        if (rb >= re) pipe.wait(it);
+        for (int r0 = rb; r0 < re; r0 += kTG) {
             const int r = r0 + tid;
-            const bool in = r < nvalid;
+            const bool in = r < re;
             float x[3], xb[3], vbn[3], Cbn[D * D];
             const int j = start + r;
             if (in) {
@@ -1272,12 +1298,12 @@ __global__ void __launch_bounds__(kTG) k_g2p_grad_gather(KParams p, SlotView sl,
 #pragma unroll
                 for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + soa(p.EN, D + q, j));
             }
-            if (r0 == 0) sU = pipe.wait(it);
+            if (r0 == rb) sU = pipe.wait(it);
             if (in) {
                 int lb[3];
-                float fx[3], w[3][3], dw[3][3], xo[3];
-                particle_weights<D>(p, x, c0, lb, fx, w, dw);
-                g2pg_gather<D>(p, sU, lb, fx, w, dw, xb, vbn, Cbn, xo);
+                float fx[3], wt[3][3], dw[3][3], xo[3];
+                particle_weights<D>(p, x, c0, lb, fx, wt, dw);
+                g2pg_gather<D>(p, sU, lb, fx, wt, dw, xb, vbn, Cbn, xo);
 #pragma unroll
                 for (int k = 0; k < D; ++k) xbp[soa(p.EN, k, j)] = xo[k];
             }
@@ -1498,22 +1524,26 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
     TilePipe<D> pipe{s_buf, s_bar};
     pipe.init();
     __syncthreads();
-    pipe.start(gt, blockIdx.x, nact);
+    const int split = item_split(nact, gridDim.x), nitems = nact * split;
+    pipe.start(gt, blockIdx.x / split, nact);
     int it = 0;
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
-        pipe.next(gt, bi + gridDim.x, nact, it);
+    for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
+        const int bi = w / split;
+        pipe.next(gt, (w + gridDim.x) / split, nact, it);
         const int bid = blist[bi];
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
+        int rb, re;
+        item_range<kTP>(nvalid, w - bi * split, split, rb, re);
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         s_ab[warp][lane] = 0.0f;  // each warp owns its row
         __syncwarp();
         const float4* sG = nullptr;
-        if (nvalid == 0) pipe.wait(it);
-        for (int r0 = 0; r0 < nvalid; r0 += kTP) {
+        if (rb >= re) pipe.wait(it);
+        for (int r0 = rb; r0 < re; r0 += kTP) {
             const int r = r0 + tid;
-            const bool in = r < nvalid;
+            const bool in = r < re;
             // particle loads go out before the (first pass's) tile staging
             float x[3], vc[L::VC], F[L::FF], Fbn[L::FF], xb[3];
             int64_t i = 0;
@@ -1538,7 +1568,7 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
                     if (p.mat) fluid = __ldg(p.mat + pd) != 0;
                 }
             }
-            if (r0 == 0) sG = pipe.wait(it);
+            if (r0 == rb) sG = pipe.wait(it);
             float abar = 0.0f;
             if (in) {
                 const bool has_act = aid && a_id >= 0 && a_id < p.n_act;
@@ -1562,21 +1592,22 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
         if (p.n_act > 0 && tid < p.n_act) {
             float s = 0.0f;
             for (int wv = 0; wv < kTP / 32; ++wv) s += s_ab[wv][tid];
-            abar_part[(int64_t)tid * p.step_blocks + bi] = s;  // [n_act][step_blocks]: the reduction reads rows
+            // per work item, [n_act][step_blocks * kMaxSplit]: the reduction reads rows
+            abar_part[(int64_t)tid * p.step_blocks * kMaxSplit + w] = s;
         }
         __syncthreads();
     }
 }
 
-// alpha_bar_t[a] = fixed-order sum over the step's active blocks of abar_part[a][b]: thread i sums
-// blocks i, i + 256, ... in order (four interleaved accumulators, combined in order), then the
-// warps' butterflies and the 8 warp sums in warp order.
+// alpha_bar_t[a] = fixed-order sum over p2g_grad's work items of the step (blocks, or parts of
+// blocks) of abar_part[a][w]: thread i sums items i, i + 256, ... in order (four interleaved
+// accumulators, combined in order), then the warps' butterflies and the 8 warp sums in order.
 // Closed loop: per episode e = blockIdx.y over that episode's blocks (a contiguous range of the
 // block-id-ordered list, found by binary search).  256 threads per actuator: with 64 robot
 // episodes a step has ~6,400 blocks, which one warp per actuator summed in ~20 us.
 constexpr int kRA = 256;
 __global__ void __launch_bounds__(kRA) k_reduce_abar(KParams p, SlotView sl, const float* __restrict__ part,
-                                                     float* __restrict__ out) {
+                                                     float* __restrict__ out, int grid_p2gg) {
     pdl_begin();
     __shared__ float s_w[kRA / 32];
     const int a = blockIdx.x, e = blockIdx.y, n_act = p.n_act;
@@ -1591,7 +1622,10 @@ __global__ void __launch_bounds__(kRA) k_reduce_abar(KParams p, SlotView sl, con
         while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe <= e) l = m + 1; else h = m; }
         hi = l;
     }
-    const float* row = part + (int64_t)a * p.step_blocks;
+    const int split = item_split(n, grid_p2gg);  // p2g_grad's work items of this step
+    lo *= split;
+    hi *= split;
+    const float* row = part + (int64_t)a * p.step_blocks * kMaxSplit;
     float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
     int b = lo + (int)threadIdx.x;
     for (; b + 3 * kRA < hi; b += 4 * kRA) {
@@ -1921,7 +1955,8 @@ void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, c
 void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s) {
     if (p.n_act > 0)
-        launch_k(k_reduce_abar, dim3(p.n_act, p.closed_loop ? p.E : 1), kRA, 0, s, p, sl, abar_part, alpha_bar_t);
+        launch_k(k_reduce_abar, dim3(p.n_act, p.closed_loop ? p.E : 1), kRA, 0, s, p, sl, abar_part, alpha_bar_t,
+                 (int)pgrid(p, 3));
 }
 
 }  // namespace mpm

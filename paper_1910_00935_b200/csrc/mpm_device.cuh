@@ -49,6 +49,9 @@ template <int D> struct Geo {
     static constexpr int NST = D == 3 ? 27 : 9;      // stencil offsets
     static constexpr int MAXP = 1728;                // particles per block (27 per cell)
 };
+// at most this many CTAs share one block's particles in the thread-per-particle kernels
+// (kernels_tile.cu item_split); sizes the per-item actuator-gradient partials
+constexpr int kMaxSplit = 4;
 
 // State layout: three component-major (SoA) arrays per
 // state -- component k of particle i at ptr[k * EN + i] -- so a warp's access to one
