@@ -1251,8 +1251,11 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
 // g2p_grad's gather part as its own pass: thread per particle of a block,
 // U tile staged like g2p.  Runs on a second stream, concurrently with the U_bar scatter
 // (k_g2p_grad) and grid_op_grad; writes xb_t (partial) for p2g_grad.
+#ifndef MPM_GATHER_MINB
+#define MPM_GATHER_MINB 5  // 5 CTAs of 128 threads per SM: <= 102 registers
+#endif
 template <int D>
-__global__ void __launch_bounds__(kTG) k_g2p_grad_gather(KParams p, SlotView sl, StateView S, AdjView Sbn,
+__global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParams p, SlotView sl, StateView S, AdjView Sbn,
                                                         float* __restrict__ xbp) {
     pdl_begin();
     using G = Geo<D>;
