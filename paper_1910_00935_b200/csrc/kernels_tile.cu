@@ -218,7 +218,10 @@ template <int D> struct TilePipe {
 // C2 ~40 blocks, C3 ~120, on 400-600 CTAs) each block's particles are split into `split` (<= 4)
 // pass-aligned ranges taken by different CTAs, so more SMs work on the step.  split depends only
 // on the step's block count and the grid size, so the work decomposition -- and every result --
-// is deterministic.  Work item w = (block w / split, part w % split).
+// is deterministic.  Work item w = (block w / split, part w % split).  The kernels are instantiated
+// with and without it (SPLIT): small problems (<= 256K particles per launch) take the split
+// variant; large ones, whose blocks outnumber the CTAs anyway, keep the plain per-block loop
+// (the index math costs g2p ~9% there).
 __device__ __forceinline__ int item_split(int nact, int grid) {
     return nact > 0 ? max(1, min(kMaxSplit, grid / nact)) : 1;
 }
@@ -1015,7 +1018,7 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
 // runtime flag, not a template parameter): two instantiations may contract the FMAs of the
 // shared math differently, and the re-forwarded S_{t+1} would then differ in the last bit
 // from the forward's (checkpoint invariance is tested bitwise).
-template <int D>
+template <int D, bool SPLIT>
 __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
                                             int* __restrict__ keys, int* __restrict__ bcount, int* flags,
                                             bool refwd, Migr mg) {
@@ -1033,7 +1036,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
     TilePipe<D> pipe{s_buf, s_bar};
     pipe.init();
     __syncthreads();
-    const int split = item_split(nact, gridDim.x), nitems = nact * split;
+    const int split = SPLIT ? item_split(nact, gridDim.x) : 1, nitems = nact * split;
     pipe.start(rt, blockIdx.x / split, nact);
     int it = 0;
     for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
@@ -1043,7 +1046,8 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int rb, re;
-        item_range<kTG>(nvalid, w - bi * split, split, rb, re);
+        if (SPLIT) item_range<kTG>(nvalid, w - bi * split, split, rb, re);
+        else { rb = 0; re = nvalid; }
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         // particle loads of the first two passes go out before waiting for the tile
@@ -1254,7 +1258,7 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
 #ifndef MPM_GATHER_MINB
 #define MPM_GATHER_MINB 5  // 5 CTAs of 128 threads per SM: <= 102 registers
 #endif
-template <int D>
+template <int D, bool SPLIT>
 __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParams p, SlotView sl, StateView S, AdjView Sbn,
                                                         float* __restrict__ xbp) {
     pdl_begin();
@@ -1271,7 +1275,7 @@ __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParam
     TilePipe<D> pipe{s_buf, s_bar};
     pipe.init();
     __syncthreads();
-    const int split = item_split(nact, gridDim.x), nitems = nact * split;
+    const int split = SPLIT ? item_split(nact, gridDim.x) : 1, nitems = nact * split;
     pipe.start(rt, blockIdx.x / split, nact);
     int it = 0;
     for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
@@ -1280,7 +1284,8 @@ __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParam
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int rb, re;
-        item_range<kTG>(nvalid, w - bi * split, split, rb, re);
+        if (SPLIT) item_range<kTG>(nvalid, w - bi * split, split, rb, re);
+        else { rb = 0; re = nvalid; }
         int e, c0[3];
         block_origin<D>(p, blist[bi], e, c0);
         const float4* sU = nullptr;
@@ -1505,7 +1510,7 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
 
 constexpr int kTP = 128;  // p2g_grad CTA
 
-template <int D>
+template <int D, bool SPLIT>
 __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, SlotView sl, StateView S,
                                                  const int32_t* __restrict__ aid,
                                                  const float* __restrict__ alpha, AdjView Sbn,
@@ -1527,7 +1532,7 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
     TilePipe<D> pipe{s_buf, s_bar};
     pipe.init();
     __syncthreads();
-    const int split = item_split(nact, gridDim.x), nitems = nact * split;
+    const int split = SPLIT ? item_split(nact, gridDim.x) : 1, nitems = nact * split;
     pipe.start(gt, blockIdx.x / split, nact);
     int it = 0;
     for (int w = blockIdx.x; w < nitems; w += gridDim.x, ++it) {
@@ -1537,7 +1542,8 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
         const int start = bstart[bi];
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int rb, re;
-        item_range<kTP>(nvalid, w - bi * split, split, rb, re);
+        if (SPLIT) item_range<kTP>(nvalid, w - bi * split, split, rb, re);
+        else { rb = 0; re = nvalid; }
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
         s_ab[warp][lane] = 0.0f;  // each warp owns its row
@@ -1871,10 +1877,10 @@ cudaError_t tile_init() {
         if (e) return e;                                                                                          \
         const int di = DIM == 3 ? 1 : 0;                                                                          \
         T.grid[0][di] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);                      \
-        T.grid[1][di] = occupancy_grid((const void*)k_g2p<DIM>, 0, kTG);                                          \
+        T.grid[1][di] = occupancy_grid((const void*)k_g2p<DIM, false>, 0, kTG);                                          \
         T.grid[2][di] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTQ);                \
-        T.grid[3][di] = occupancy_grid((const void*)k_p2g_grad<DIM>, 0, kTP);                                     \
-        T.grid[4][di] = occupancy_grid((const void*)k_g2p_grad_gather<DIM>, 0, kTG);                              \
+        T.grid[3][di] = occupancy_grid((const void*)k_p2g_grad<DIM, false>, 0, kTP);                                     \
+        T.grid[4][di] = occupancy_grid((const void*)k_g2p_grad_gather<DIM, false>, 0, kTG);                              \
     } while (0)
     MPM_INIT_DIM(2);
     MPM_INIT_DIM(3);
@@ -1934,9 +1940,13 @@ void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* uba
     if (has_halo(sl)) DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM, true>, node_grid(p), kT, 0, s, p, sl, ubar));
     else DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM, false>, node_grid(p), kT, 0, s, p, sl, ubar));
 }
+static bool split_blocks(const KParams& p) { return p.N * p.E <= 262144; }  // see item_split
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
                 int* bcount, int* flags, bool refwd, const Migr& mg, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_g2p<DIM>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bcount, flags, refwd, mg));
+    if (split_blocks(p))
+        DISPATCH(p.dim, launch_k(k_g2p<DIM, true>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bcount, flags, refwd, mg));
+    else
+        DISPATCH(p.dim, launch_k(k_g2p<DIM, false>, pgrid(p, 1), kTG, 0, s, p, sl, S, Sn, keys, bcount, flags, refwd, mg));
 }
 void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                      float4* ubar, cudaStream_t s) {
@@ -1944,12 +1954,18 @@ void launch_g2p_grad(const KParams& p, const SlotView& sl, const StateView& S, c
 }
 void launch_g2p_grad_gather(const KParams& p, const SlotView& sl, const StateView& S, const AdjView& Sbn,
                             float* xbp, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_g2p_grad_gather<DIM>, pgrid(p, 4), kTG, 0, s, p, sl, S, Sbn, xbp));
+    if (split_blocks(p)) DISPATCH(p.dim, launch_k(k_g2p_grad_gather<DIM, true>, pgrid(p, 4), kTG, 0, s, p, sl, S, Sbn, xbp));
+    else DISPATCH(p.dim, launch_k(k_g2p_grad_gather<DIM, false>, pgrid(p, 4), kTG, 0, s, p, sl, S, Sbn, xbp));
 }
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
                      const float* alpha_t, const AdjView& Sbn, const float* xbp,
                      const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_p2g_grad<DIM>, pgrid(p, 3), kTP, 0, s, p, sl, S, aid, alpha_t, Sbn, xbp, Sb, abar_part, flags));
+    if (split_blocks(p))
+        DISPATCH(p.dim, launch_k(k_p2g_grad<DIM, true>, pgrid(p, 3), kTP, 0, s, p, sl, S, aid, alpha_t, Sbn, xbp, Sb,
+                                 abar_part, flags));
+    else
+        DISPATCH(p.dim, launch_k(k_p2g_grad<DIM, false>, pgrid(p, 3), kTP, 0, s, p, sl, S, aid, alpha_t, Sbn, xbp, Sb,
+                                 abar_part, flags));
 }
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s) {
     cudaMemsetAsync(count, 0, sizeof(int64_t), s);
@@ -1959,7 +1975,7 @@ void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_
                         cudaStream_t s) {
     if (p.n_act > 0)
         launch_k(k_reduce_abar, dim3(p.n_act, p.closed_loop ? p.E : 1), kRA, 0, s, p, sl, abar_part, alpha_bar_t,
-                 (int)pgrid(p, 3));
+                 split_blocks(p) ? (int)pgrid(p, 3) : 0);  // 0: p2g_grad ran one item per block
 }
 
 }  // namespace mpm
