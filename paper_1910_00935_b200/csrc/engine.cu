@@ -214,7 +214,6 @@ size_t carve(mpm_ctx* h, char* base) {
     float* loss = (float*)take(sizeof(float) * E);
     float* com_part = (float*)take(sizeof(float) * E * (lblk + 2) * 3);
     int64_t* counter = (int64_t*)take(sizeof(int64_t) * 2);
-    int* tick = (int*)take(sizeof(int) * 4);  // last-CTA ticket of p2g_grad's fused reduction
     int* flags = (int*)take(sizeof(int) * 4);
     if (base) {
         h->max_active = max_active;
@@ -237,7 +236,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
         h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
         h->flags = flags;
-        h->ntot_arr = ntot_arr; h->blk_part = blk_part; h->tick = tick;
+        h->ntot_arr = ntot_arr; h->blk_part = blk_part;
         h->out_cnt = out_cnt; h->out_rows = out_rows; h->imm_base = imm_base; h->nrows_arr = nrows_arr;
     }
     return off;
@@ -392,13 +391,13 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
     { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, sl, S, Sbn, h->ubar, h->stream); }
     { KScope sc(h, KC_GRID_OP_GRAD); launch_grid_op_grad(k, sl, h->ubar, h->stream); }
     if (fork) cudaStreamWaitEvent(h->stream, h->ev_join, 0);
-    float* abar_t = h->alpha_bar + (size_t)t * A * (k.closed_loop ? k.E : 1);
     { KScope sc(h, KC_P2G_GRAD);
       launch_p2g_grad(k, sl, S, h->has_aid ? h->aid : nullptr, alpha_at(h, t), Sbn, h->xbar_part,
-                      Sb, h->abar_part, h->flags, abar_t, h->tick, h->stream); }
-    if (k.n_act > 0 && !p2g_grad_reduces_abar(k)) {
+                      Sb, h->abar_part, h->flags, h->stream); }
+    if (k.n_act > 0) {
         KScope sc(h, KC_REDUCE_ABAR);
-        launch_reduce_abar(k, sl, h->abar_part, abar_t, h->stream);
+        launch_reduce_abar(k, sl, h->abar_part, h->alpha_bar + (size_t)t * A * (k.closed_loop ? k.E : 1),
+                           h->stream);
     }
     if (k.closed_loop) {  // controller adjoint of step t; observation adjoint into S_bar_t
         KScope sc(h, KC_CTRL);
@@ -603,7 +602,6 @@ mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     carve(h, h->ws);
     const KParams k = kparams(h);
     CU(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
-    CU(cudaMemsetAsync(h->tick, 0, sizeof(int) * 4, h->stream));
     CU(cudaMemsetAsync(h->scan_part, 0, sizeof(int64_t) * (scan_chunks(kparams(h)) + 2), h->stream));
     CU(cudaMemsetAsync(h->bcount, 0, sizeof(int) * k.TB, h->stream));
     CU(cudaMemsetAsync(h->theta, 0, sizeof(float) * (n_theta_of(h->prm, h->dim) > 0 ? n_theta_of(h->prm, h->dim) : 1), h->stream));

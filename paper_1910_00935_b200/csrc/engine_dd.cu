@@ -356,7 +356,7 @@ mpm_status mpm_dd_backward(mpm_handle* hs, int32_t n, int32_t steps) {
             const int cur = h->sbar_cur;
             { KScope sc(h, KC_P2G_GRAD);
               launch_p2g_grad(K[g], slot_at(h, t), state_at(h, t), nullptr, nullptr, h->sbar[cur], h->xbar_part,
-                              h->sbar[cur ^ 1], h->abar_part, h->flags, nullptr, nullptr, h->stream); }
+                              h->sbar[cur ^ 1], h->abar_part, h->flags, h->stream); }
         }
         for (int g = 0; g < n; ++g) {
             mpm_ctx* h = hs[g];

@@ -157,13 +157,9 @@ void launch_g2p_grad_gather(const KParams& p, const SlotView& sl, const StateVie
                             float* xbar_part, cudaStream_t s);
 // grid_op_grad: covering sums of the U_bar partial tiles -> (P_bar, M_bar) tiles in sl.part
 void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* ubar, cudaStream_t s);
-// alpha_bar_t / tick (a zero device counter): when p2g_grad_reduces_abar(p) (small problems) the
-// last CTA also writes alpha_bar_t and launch_reduce_abar is not needed; else ignored (nullable)
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
                      const float* alpha_t, const AdjView& Sbn, const float* xbar_part,
-                     const AdjView& Sb, float* abar_part, int* flags, float* alpha_bar_t, int* tick,
-                     cudaStream_t s);
-bool p2g_grad_reduces_abar(const KParams& p);
+                     const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s);
 // alpha_bar_t[a] (open loop) or alpha_bar_t[e][a] (closed loop) = fixed-order sum of the
 // per-block partials of the step
 void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,

@@ -1320,63 +1320,6 @@ __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParam
     }
 }
 
-// alpha_bar_t[a] = fixed-order sum over p2g_grad's work items of the step (blocks, or parts of
-// blocks) of abar_part[a][w]: thread i sums items i, i + 256, ... in order (four interleaved
-// accumulators, combined in order), then the warps' butterflies and the 8 warp sums in order.
-// Closed loop: per episode e = blockIdx.y over that episode's blocks (a contiguous range of the
-// block-id-ordered list, found by binary search).  256 threads per actuator: with 64 robot
-// episodes a step has ~6,400 blocks, which one warp per actuator summed in ~20 us.
-// alpha_bar_t[e][a] of one (actuator a, episode e) with NT threads (s_w: NT / 32 floats)
-template <int NT>
-__device__ __forceinline__ void reduce_abar_one(const KParams& p, const SlotView& sl, const float* __restrict__ part,
-                                                float* __restrict__ out, int grid_p2gg, int a, int e, float* s_w) {
-    const int n_act = p.n_act;
-    const int n = *sl.nactive;
-    const int* blist = sl.blist + *sl.base;
-    int lo = 0, hi = n;
-    if (p.closed_loop) {  // first entries of episode e and e + 1 (block ids are episode-major)
-        int l = 0, h = n;
-        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe < e) l = m + 1; else h = m; }
-        lo = l;
-        h = n;
-        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe <= e) l = m + 1; else h = m; }
-        hi = l;
-    }
-    const int split = item_split(n, grid_p2gg);  // p2g_grad's work items of this step
-    lo *= split;
-    hi *= split;
-    const float* row = part + (int64_t)a * p.step_blocks * kMaxSplit;
-    float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    int b = lo + (int)threadIdx.x;
-    for (; b + 3 * NT < hi; b += 4 * NT) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s4[u] += row[b + u * NT];
-    }
-    if (b < hi) s4[0] += row[b];  // at most three left
-    if (b + NT < hi) s4[1] += row[b + NT];
-    if (b + 2 * NT < hi) s4[2] += row[b + 2 * NT];
-    float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float t = 0.0f;
-#pragma unroll
-        for (int w = 0; w < NT / 32; ++w) t += s_w[w];
-        out[e * n_act + a] = t;
-    }
-    __syncthreads();
-}
-
-constexpr int kRA = 256;
-__global__ void __launch_bounds__(kRA) k_reduce_abar(KParams p, SlotView sl, const float* __restrict__ part,
-                                                     float* __restrict__ out, int grid_p2gg) {
-    pdl_begin();
-    __shared__ float s_w[kRA / 32];
-    reduce_abar_one<kRA>(p, sl, part, out, grid_p2gg, blockIdx.x, blockIdx.y, s_w);
-}
-
 // ------------------------------------------------------------ p2g_grad
 // staging fuses grid_op_grad (select rule): ub = z ? 0 : Ub;
 // Pb = ub/(M + eps); Mb = -(ub . u0)/(M + eps).  Then per particle:
@@ -1572,15 +1515,13 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
                                                  const int32_t* __restrict__ aid,
                                                  const float* __restrict__ alpha, AdjView Sbn,
                                                  const float* __restrict__ xbp, AdjView Sb,
-                                                 float* __restrict__ abar_part, int* flags,
-                                                 float* __restrict__ alpha_bar_t, int* __restrict__ tick) {
+                                                 float* __restrict__ abar_part, int* flags) {
     pdl_begin();
     using G = Geo<D>;
     using L = Lay<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
     __shared__ __align__(8) uint64_t s_bar[2];
     __shared__ float s_ab[kTP / 32][32];
-    __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nact = *sl.nactive;
     const int b0 = *sl.base;  // this step's offset in the grid-store pool
@@ -1665,22 +1606,54 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
         }
         __syncthreads();
     }
-    // small problems (the split variant): the last CTA to finish also reduces the step's actuator
-    // gradients (one launch fewer per step; the same fixed order as k_reduce_abar)
-    if (SPLIT && alpha_bar_t && p.n_act > 0) {
-        if (tid == 0) {
-            __threadfence();
-            s_last = atomicAdd(tick, 1) == (int)gridDim.x - 1;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            float* s_w = &s_ab[0][0];
-            const int ne = p.closed_loop ? p.E : 1;
-            for (int e = 0; e < ne; ++e)
-                for (int a = 0; a < p.n_act; ++a) reduce_abar_one<kTP>(p, sl, abar_part, alpha_bar_t, gridDim.x, a, e, s_w);
-            if (tid == 0) *tick = 0;
-        }
+}
+
+// alpha_bar_t[a] = fixed-order sum over p2g_grad's work items of the step (blocks, or parts of
+// blocks) of abar_part[a][w]: thread i sums items i, i + 256, ... in order (four interleaved
+// accumulators, combined in order), then the warps' butterflies and the 8 warp sums in order.
+// Closed loop: per episode e = blockIdx.y over that episode's blocks (a contiguous range of the
+// block-id-ordered list, found by binary search).  256 threads per actuator: with 64 robot
+// episodes a step has ~6,400 blocks, which one warp per actuator summed in ~20 us.
+constexpr int kRA = 256;
+__global__ void __launch_bounds__(kRA) k_reduce_abar(KParams p, SlotView sl, const float* __restrict__ part,
+                                                     float* __restrict__ out, int grid_p2gg) {
+    pdl_begin();
+    __shared__ float s_w[kRA / 32];
+    const int a = blockIdx.x, e = blockIdx.y, n_act = p.n_act;
+    const int n = *sl.nactive;
+    const int* blist = sl.blist + *sl.base;
+    int lo = 0, hi = n;
+    if (p.closed_loop) {  // first entries of episode e and e + 1 (block ids are episode-major)
+        int l = 0, h = n;
+        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe < e) l = m + 1; else h = m; }
+        lo = l;
+        h = n;
+        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe <= e) l = m + 1; else h = m; }
+        hi = l;
+    }
+    const int split = item_split(n, grid_p2gg);  // p2g_grad's work items of this step
+    lo *= split;
+    hi *= split;
+    const float* row = part + (int64_t)a * p.step_blocks * kMaxSplit;
+    float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    int b = lo + (int)threadIdx.x;
+    for (; b + 3 * kRA < hi; b += 4 * kRA) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s4[u] += row[b + u * kRA];
+    }
+    if (b < hi) s4[0] += row[b];  // at most three left
+    if (b + kRA < hi) s4[1] += row[b + kRA];
+    if (b + 2 * kRA < hi) s4[2] += row[b + 2 * kRA];
+    float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kRA / 32; ++w) t += s_w[w];
+        out[e * n_act + a] = t;
     }
 }
 
@@ -1986,16 +1959,14 @@ void launch_g2p_grad_gather(const KParams& p, const SlotView& sl, const StateVie
 }
 void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, const int32_t* aid,
                      const float* alpha_t, const AdjView& Sbn, const float* xbp,
-                     const AdjView& Sb, float* abar_part, int* flags, float* alpha_bar_t, int* tick,
-                     cudaStream_t s) {
+                     const AdjView& Sb, float* abar_part, int* flags, cudaStream_t s) {
     if (split_blocks(p))
         DISPATCH(p.dim, launch_k(k_p2g_grad<DIM, true>, pgrid(p, 3), kTP, 0, s, p, sl, S, aid, alpha_t, Sbn, xbp, Sb,
-                                 abar_part, flags, alpha_bar_t, tick));
+                                 abar_part, flags));
     else
         DISPATCH(p.dim, launch_k(k_p2g_grad<DIM, false>, pgrid(p, 3), kTP, 0, s, p, sl, S, aid, alpha_t, Sbn, xbp, Sb,
-                                 abar_part, flags, (float*)nullptr, (int*)nullptr));
+                                 abar_part, flags));
 }
-bool p2g_grad_reduces_abar(const KParams& p) { return split_blocks(p) && p.n_act > 0; }
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s) {
     cudaMemsetAsync(count, 0, sizeof(int64_t), s);
     DISPATCH(p.dim, launch_k(k_count_active<DIM>, node_grid(p), kT, 0, s, p, sl, (unsigned long long*)count));
