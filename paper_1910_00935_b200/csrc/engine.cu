@@ -214,7 +214,6 @@ size_t carve(mpm_ctx* h, char* base) {
     float* loss = (float*)take(sizeof(float) * E);
     float* com_part = (float*)take(sizeof(float) * E * (lblk + 2) * 3);
     int64_t* counter = (int64_t*)take(sizeof(int64_t) * 2);
-    int* cl_tick = (int*)take(sizeof(int) * (E + 1));  // closed loop: last-CTA tickets (observe per episode, reduce)
     int* flags = (int*)take(sizeof(int) * 4);
     if (base) {
         h->max_active = max_active;
@@ -237,7 +236,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
         h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
         h->flags = flags;
-        h->ntot_arr = ntot_arr; h->blk_part = blk_part; h->cl_tick = cl_tick;
+        h->ntot_arr = ntot_arr; h->blk_part = blk_part;
         h->out_cnt = out_cnt; h->out_rows = out_rows; h->imm_base = imm_base; h->nrows_arr = nrows_arr;
     }
     return off;
@@ -339,11 +338,13 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     const StateView S = state_at(h, t);
     const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr, nullptr, nullptr};
     const int32_t* aid = h->has_aid ? h->aid : nullptr;
-    if (k.closed_loop) {  // R22: alpha_t from the observation of S_t (one launch: sums + controller)
+    if (k.closed_loop) {  // R22: alpha_t from the observation of S_t
         KScope sc(h, KC_CTRL);
+        h->launches += 1;
+        launch_observe(k, S.x, S.vc, S.pid, aid, h->obs_part, h->stream);
         const size_t no = (size_t)2 * k.dim * k.n_act;
-        launch_observe_ctrl(k, S.x, S.vc, S.pid, aid, h->obs_part, h->theta, t, h->obs + (size_t)t * k.E * no,
-                            h->obs_cnt, const_cast<float*>(alpha_at(h, t)), h->cl_tick, h->stream);
+        launch_ctrl_obs_fwd(k, h->theta, t, h->obs_part, h->obs + (size_t)t * k.E * no, h->obs_cnt,
+                            const_cast<float*>(alpha_at(h, t)), h->stream);
     }
     { KScope sc(h, KC_CANON); launch_canon(k, sl, Sn.pid, bin_next ? h->keys : nullptr, h->flags, h->stream); }
     { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
@@ -393,17 +394,18 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
     { KScope sc(h, KC_P2G_GRAD);
       launch_p2g_grad(k, sl, S, h->has_aid ? h->aid : nullptr, alpha_at(h, t), Sbn, h->xbar_part,
                       Sb, h->abar_part, h->flags, h->stream); }
-    float* abar_t = h->alpha_bar + (size_t)t * A * (k.closed_loop ? k.E : 1);
-    if (k.n_act > 0 && !k.closed_loop) {
+    if (k.n_act > 0) {
         KScope sc(h, KC_REDUCE_ABAR);
-        launch_reduce_abar(k, sl, h->abar_part, abar_t, h->stream);
+        launch_reduce_abar(k, sl, h->abar_part, h->alpha_bar + (size_t)t * A * (k.closed_loop ? k.E : 1),
+                           h->stream);
     }
-    if (k.closed_loop) {  // alpha_bar_t + controller adjoint of step t (one launch); observation adjoint into S_bar_t
+    if (k.closed_loop) {  // controller adjoint of step t; observation adjoint into S_bar_t
         KScope sc(h, KC_CTRL);
         h->launches += 1;
         const size_t no = (size_t)2 * k.dim * k.n_act;
-        launch_reduce_abar_obs(k, sl, h->abar_part, abar_t, h->theta, t, h->obs + (size_t)t * k.E * no,
-                               alpha_at(h, t), h->obs_cnt, h->theta_bar, h->obs_inc, h->cl_tick + k.E, h->stream);
+        launch_ctrl_obs_bwd(k, h->theta, t, h->obs + (size_t)t * k.E * no, alpha_at(h, t),
+                            h->alpha_bar + (size_t)t * A * k.E, h->obs_cnt, h->theta_bar, h->obs_inc,
+                            h->stream);
         launch_observe_adj(k, Sb, S.pid, h->has_aid ? h->aid : nullptr, h->obs_inc, h->stream);
     }
 }
@@ -600,7 +602,6 @@ mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     carve(h, h->ws);
     const KParams k = kparams(h);
     CU(cudaMemsetAsync(h->flags, 0, sizeof(int) * 4, h->stream));
-    CU(cudaMemsetAsync(h->cl_tick, 0, sizeof(int) * (h->prm.n_episodes + 1), h->stream));
     CU(cudaMemsetAsync(h->scan_part, 0, sizeof(int64_t) * (scan_chunks(kparams(h)) + 2), h->stream));
     CU(cudaMemsetAsync(h->bcount, 0, sizeof(int) * k.TB, h->stream));
     CU(cudaMemsetAsync(h->theta, 0, sizeof(float) * (n_theta_of(h->prm, h->dim) > 0 ? n_theta_of(h->prm, h->dim) : 1), h->stream));

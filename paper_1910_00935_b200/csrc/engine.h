@@ -119,7 +119,6 @@ struct mpm_ctx {
     bool use_graphs = true;
     int* ntot_arr = nullptr;       // [T_max + 1] sorted particles per step (set by the scan)
     float* blk_part = nullptr;     // [max_active][d] per-block COM partials of the loss
-    int* cl_tick = nullptr;        // closed loop: [E + 1] last-CTA tickets (observe per episode, reduce)
     // ---- slab subdomain of a decomposed body (engine_dd.cu)
     bool dd = false;               // set by mpm_set_subdomain
     int x_lo = 0, x_hi = 0;        // owned block x-index range

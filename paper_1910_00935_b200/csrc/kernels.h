@@ -87,58 +87,6 @@ struct SlotView {
     Halo halo;               // f3 neighbours (covered sums of grid_op / grid_op_grad)
 };
 
-// number of parts a block's particles are split into by the thread-per-particle kernels of a step
-// with nact active blocks on `grid` CTAs (kernels_tile.cu, "Sub-block work split"); grid 0 = 1
-__device__ __forceinline__ int item_split(int nact, int grid) {
-    return nact > 0 ? max(1, min(kMaxSplit, grid / nact)) : 1;
-}
-
-// alpha_bar_t[e][a] = fixed-order sum over p2g_grad's work items of the step (blocks, or parts of
-// blocks; [n_act][step_blocks * kMaxSplit] partials): thread i sums items i, i + NT, ... in order
-// (four interleaved accumulators, combined in order), then the warps' butterflies and the warp
-// sums in warp order.  Closed loop: over episode e's items (its blocks are a contiguous range of
-// the block-id-ordered list, found by binary search).  s_w: NT / 32 shared floats.
-template <int NT>
-__device__ __forceinline__ void reduce_abar_one(const KParams& p, const SlotView& sl, const float* __restrict__ part,
-                                                float* __restrict__ out, int grid_p2gg, int a, int e, float* s_w) {
-    const int n = *sl.nactive;
-    const int* blist = sl.blist + *sl.base;
-    int lo = 0, hi = n;
-    if (p.closed_loop) {
-        int l = 0, h = n;
-        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe < e) l = m + 1; else h = m; }
-        lo = l;
-        h = n;
-        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe <= e) l = m + 1; else h = m; }
-        hi = l;
-    }
-    const int split = item_split(n, grid_p2gg);
-    lo *= split;
-    hi *= split;
-    const float* row = part + (int64_t)a * p.step_blocks * kMaxSplit;
-    float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-    int b = lo + (int)threadIdx.x;
-    for (; b + 3 * NT < hi; b += 4 * NT) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s4[u] += row[b + u * NT];
-    }
-    if (b < hi) s4[0] += row[b];  // at most three left
-    if (b + NT < hi) s4[1] += row[b + NT];
-    if (b + 2 * NT < hi) s4[2] += row[b + 2 * NT];
-    float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float t = 0.0f;
-#pragma unroll
-        for (int w = 0; w < NT / 32; ++w) t += s_w[w];
-        out[e * p.n_act + a] = t;
-    }
-    __syncthreads();
-}
-
 cudaError_t tile_init();
 
 // ---- binning (bin_keys only for a fresh sort; g2p emits keys for the next step)
@@ -216,8 +164,6 @@ void launch_p2g_grad(const KParams& p, const SlotView& sl, const StateView& S, c
 // per-block partials of the step
 void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s);
-// p2g_grad's grid when it splits blocks into work items (small problems), else 0
-int p2g_grad_item_grid(const KParams& p);
 
 // ---- measurement: distinct grid nodes with M > 0 in a slot's tiles -> *count (device)
 void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, cudaStream_t s);
@@ -228,19 +174,18 @@ void launch_check_aid(const KParams& p, const int32_t* aid, int* flags, cudaStre
 // ---- closed-loop controller (R22)
 int obs_parts(const KParams& p);   // per-CTA partials of one observation: [E][chunks]
 int obs_values(const KParams& p);  // values per partial: n_act (2d + 1) + d
-// per-CTA sums over S_t (x, v in its split arrays; particle id -> actuator id) -> part; the last
-// CTA of each episode then forms o_t, stores it and the group sizes, and runs the MLP -> alpha_t
-// (tick: [E] zero device counters)
-void launch_observe_ctrl(const KParams& p, const float* x, const float* vc, const int* pid, const int32_t* aid,
-                         float* part, const float* theta, int32_t t, float* obs_t, float* counts, float* alpha_t,
-                         int* tick, cudaStream_t s);
-// closed loop: alpha_bar_t (as launch_reduce_abar), then in the same launch (last CTA) the
-// controller adjoint, episodes in order (fixed accumulation order of theta_bar, no atomics):
-// theta_bar += sum_e (d alpha_t[e]/d theta)^T alpha_bar_t[e]; inc[e] = per-group adjoint increments
-// of x_bar / v_bar from (d alpha_t/d o_t)^T alpha_bar_t (tick: one zero device counter)
-void launch_reduce_abar_obs(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,
-                            const float* theta, int32_t t, const float* obs_t, const float* alpha_t,
-                            const float* counts, float* theta_bar, float* inc, int* tick, cudaStream_t s);
+// per-CTA sums over S_t (x, v in its split arrays; particle id -> actuator id) -> part
+void launch_observe(const KParams& p, const float* x, const float* vc, const int* pid, const int32_t* aid,
+                    float* part, cudaStream_t s);
+// o_t per episode from the partials (fixed order), alpha_t[e] = MLP([phi(t), o_t[e]]);
+// stores o_t [E][2 d n_act] and the group sizes [E][n_act]
+void launch_ctrl_obs_fwd(const KParams& p, const float* theta, int32_t t, const float* part, float* obs_t,
+                         float* counts, float* alpha_t, cudaStream_t s);
+// theta_bar += sum_e (d alpha_t[e]/d theta)^T alpha_bar_t[e] (episodes in order, one CTA);
+// inc[e] = per-group adjoint increments of x_bar / v_bar from (d alpha_t/d o_t)^T alpha_bar_t
+void launch_ctrl_obs_bwd(const KParams& p, const float* theta, int32_t t, const float* obs_t,
+                         const float* alpha_t, const float* alpha_bar_t, const float* counts,
+                         float* theta_bar, float* inc, cudaStream_t s);
 // S_bar_t.x, .v += the observation adjoint (particle i of episode i / N, group aid[pid[i]])
 void launch_observe_adj(const KParams& p, const AdjView& Sb, const int* pid, const int32_t* aid,
                         const float* inc, cudaStream_t s);

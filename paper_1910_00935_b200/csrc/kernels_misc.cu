@@ -105,71 +105,15 @@ constexpr int kMaxIn = 1024;
 
 __host__ __device__ inline int obs_nvals(int n_act, int dim) { return n_act * (2 * dim + 1) + dim; }
 
-// episode e: reduce the partials (chunk order), form o_t[e], run the MLP (one CTA)
-template <int D>
-__device__ __forceinline__ void ctrl_obs_fwd_episode(const KParams& p, const float* __restrict__ th, int t,
-                                                     const float* __restrict__ part, int nch,
-                                                     float* __restrict__ obs_t, float* __restrict__ counts,
-                                                     float* __restrict__ alpha_t, int e) {
-    __shared__ float tot[kMaxIn], u[kMaxIn], h[kMaxHidden];
-    const int A = p.n_act, NV = obs_nvals(A, D), S = p.n_in, ns = p.n_sin, H = p.hidden;
-    const int no = 2 * D * A;
-    for (int q = threadIdx.x; q < NV; q += blockDim.x) {
-        float s = 0.0f;
-        for (int c = 0; c < nch; ++c) s += part[((int64_t)e * nch + c) * NV + q];
-        tot[q] = s;
-    }
-    for (int j = threadIdx.x; j < ns; j += blockDim.x) u[j] = feature(p, t, j);
-    __syncthreads();
-    for (int q = threadIdx.x; q < no; q += blockDim.x) {
-        const int a = q / (2 * D), k = q % (2 * D);
-        const float n = tot[a * (2 * D + 1) + 2 * D];
-        float o = 0.0f;
-        if (n > 0.0f) {
-            if (k < D) o = p.obs_sx * (tot[a * (2 * D + 1) + k] / n - tot[A * (2 * D + 1) + k] / (float)p.N);
-            else o = p.obs_sv * (tot[a * (2 * D + 1) + k] / n);
-        }
-        u[ns + q] = o;
-        obs_t[(int64_t)e * no + q] = o;
-    }
-    for (int a = threadIdx.x; a < A; a += blockDim.x) counts[e * A + a] = tot[a * (2 * D + 1) + 2 * D];
-    __syncthreads();
-    if (H > 0) {
-        const float *W1 = th, *b1 = W1 + H * S, *W2 = b1 + H, *b2 = W2 + A * H;
-        for (int i = threadIdx.x; i < H; i += blockDim.x) {
-            float z = b1[i];
-            for (int j = 0; j < S; ++j) z = fmaf(W1[i * S + j], u[j], z);
-            h[i] = tanhf(z);
-        }
-        __syncthreads();
-        for (int a = threadIdx.x; a < A; a += blockDim.x) {
-            float z = b2[a];
-            for (int i = 0; i < H; ++i) z = fmaf(W2[a * H + i], h[i], z);
-            alpha_t[e * A + a] = tanhf(z);
-        }
-    } else {
-        const float *Wm = th, *b = Wm + A * S;
-        for (int a = threadIdx.x; a < A; a += blockDim.x) {
-            float z = b[a];
-            for (int j = 0; j < S; ++j) z = fmaf(Wm[a * S + j], u[j], z);
-            alpha_t[e * A + a] = tanhf(z);
-        }
-    }
-}
-
 // CTA (c, e): particles [c * 256, (c + 1) * 256) of episode e (S_t keeps each episode's
 // particles in one contiguous index range).  Per group a: sums of x, v and the count; plus
 // the sum of x over all particles.  Masked warp butterflies + warp order: fixed summation order.
-// tick != null: also the controller (see the end)
 template <int D>
 __global__ void __launch_bounds__(kObsThreads) k_observe(KParams p, const float* __restrict__ X,
                                                          const float* __restrict__ VC,
                                                          const int* __restrict__ pid,
                                                          const int32_t* __restrict__ aid,
-                                                         float* __restrict__ part, const float* __restrict__ th,
-                                                         int t, float* __restrict__ obs_t,
-                                                         float* __restrict__ counts, float* __restrict__ alpha_t,
-                                                         int* __restrict__ tick) {
+                                                         float* __restrict__ part) {
     pdl_begin();
     constexpr int W = kObsThreads / 32;
     extern __shared__ float s_w[];  // [W][NV]
@@ -221,32 +165,70 @@ __global__ void __launch_bounds__(kObsThreads) k_observe(KParams p, const float*
         for (int ww = 0; ww < W; ++ww) t += s_w[ww * NV + q];
         part[((int64_t)e * gridDim.x + c) * NV + q] = t;
     }
-    if (!tick) return;
-    // the last CTA of episode e reduces the partials and runs the controller (ctrl_obs_fwd's work
-    // in the same launch: one kernel boundary fewer per closed-loop step)
-    __shared__ int s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(tick + e, 1) == (int)gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    ctrl_obs_fwd_episode<D>(p, th, t, part, gridDim.x, obs_t, counts, alpha_t, e);
-    if (threadIdx.x == 0) tick[e] = 0;
 }
 
+// one CTA per episode: reduce the partials (chunk order), form o_t[e], run the MLP
+template <int D>
+__global__ void k_ctrl_obs_fwd(KParams p, const float* __restrict__ th, int t, const float* __restrict__ part,
+                               int nch, float* __restrict__ obs_t, float* __restrict__ counts,
+                               float* __restrict__ alpha_t) {
+    pdl_begin();
+    __shared__ float tot[kMaxIn], u[kMaxIn], h[kMaxHidden];
+    const int e = blockIdx.x, A = p.n_act, NV = obs_nvals(A, D), S = p.n_in, ns = p.n_sin, H = p.hidden;
+    const int no = 2 * D * A;
+    for (int q = threadIdx.x; q < NV; q += blockDim.x) {
+        float s = 0.0f;
+        for (int c = 0; c < nch; ++c) s += part[((int64_t)e * nch + c) * NV + q];
+        tot[q] = s;
+    }
+    for (int j = threadIdx.x; j < ns; j += blockDim.x) u[j] = feature(p, t, j);
+    __syncthreads();
+    for (int q = threadIdx.x; q < no; q += blockDim.x) {
+        const int a = q / (2 * D), k = q % (2 * D);
+        const float n = tot[a * (2 * D + 1) + 2 * D];
+        float o = 0.0f;
+        if (n > 0.0f) {
+            if (k < D) o = p.obs_sx * (tot[a * (2 * D + 1) + k] / n - tot[A * (2 * D + 1) + k] / (float)p.N);
+            else o = p.obs_sv * (tot[a * (2 * D + 1) + k] / n);
+        }
+        u[ns + q] = o;
+        obs_t[(int64_t)e * no + q] = o;
+    }
+    for (int a = threadIdx.x; a < A; a += blockDim.x) counts[e * A + a] = tot[a * (2 * D + 1) + 2 * D];
+    __syncthreads();
+    if (H > 0) {
+        const float *W1 = th, *b1 = W1 + H * S, *W2 = b1 + H, *b2 = W2 + A * H;
+        for (int i = threadIdx.x; i < H; i += blockDim.x) {
+            float z = b1[i];
+            for (int j = 0; j < S; ++j) z = fmaf(W1[i * S + j], u[j], z);
+            h[i] = tanhf(z);
+        }
+        __syncthreads();
+        for (int a = threadIdx.x; a < A; a += blockDim.x) {
+            float z = b2[a];
+            for (int i = 0; i < H; ++i) z = fmaf(W2[a * H + i], h[i], z);
+            alpha_t[e * A + a] = tanhf(z);
+        }
+    } else {
+        const float *Wm = th, *b = Wm + A * S;
+        for (int a = threadIdx.x; a < A; a += blockDim.x) {
+            float z = b[a];
+            for (int j = 0; j < S; ++j) z = fmaf(Wm[a * S + j], u[j], z);
+            alpha_t[e * A + a] = tanhf(z);
+        }
+    }
+}
 
 // one CTA, episodes in order (fixed accumulation order of theta_bar, no atomics):
 // z2b = ab (1 - alpha^2); theta_bar += outer products; u_bar = W^T (.); the observation part
 // of u_bar -> per-group increments inc[e] = [s_x ob_x[a] / n_a, s_v ob_v[a] / n_a]_a,
 // [-s_x sum_a ob_x[a] / N]  (groups with n_a = 0 observe 0 and get no gradient)
 template <int D>
-__device__ __forceinline__ void ctrl_obs_bwd_body(const KParams& p, const float* __restrict__ th, int t,
-                                                  const float* __restrict__ obs_t, const float* __restrict__ alpha_t,
-                                                  const float* __restrict__ abar_t, const float* __restrict__ counts,
-                                                  float* __restrict__ thb, float* __restrict__ inc) {
+__global__ void k_ctrl_obs_bwd(KParams p, const float* __restrict__ th, int t, const float* __restrict__ obs_t,
+                               const float* __restrict__ alpha_t, const float* __restrict__ abar_t,
+                               const float* __restrict__ counts, float* __restrict__ thb,
+                               float* __restrict__ inc) {
+    pdl_begin();
     __shared__ float u[kMaxIn], h[kMaxHidden], z2b[kMaxAct], hb[kMaxHidden], ub[kMaxIn];
     const int A = p.n_act, S = p.n_in, ns = p.n_sin, H = p.hidden, no = 2 * D * A;
     for (int e = 0; e < p.E; ++e) {
@@ -307,33 +289,6 @@ __device__ __forceinline__ void ctrl_obs_bwd_body(const KParams& p, const float*
         }
         __syncthreads();
     }
-}
-
-
-// closed loop, one launch: the step's actuator gradients alpha_bar_t[e][a] (one CTA per (a, e),
-// kernels.h reduce_abar_one), then the last CTA runs the controller adjoint (ctrl_obs_bwd's work)
-constexpr int kRAO = 256;
-template <int D>
-__global__ void __launch_bounds__(kRAO) k_reduce_abar_obs(KParams p, SlotView sl, const float* __restrict__ abar_part,
-                                                          float* __restrict__ abar_t, int grid_p2gg,
-                                                          const float* __restrict__ th, int t,
-                                                          const float* __restrict__ obs_t,
-                                                          const float* __restrict__ alpha_t,
-                                                          const float* __restrict__ counts, float* __restrict__ thb,
-                                                          float* __restrict__ inc, int* __restrict__ tick) {
-    pdl_begin();
-    __shared__ float s_w[kRAO / 32];
-    __shared__ int s_last;
-    reduce_abar_one<kRAO>(p, sl, abar_part, abar_t, grid_p2gg, blockIdx.x, blockIdx.y, s_w);
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(tick, 1) == (int)(gridDim.x * gridDim.y) - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    ctrl_obs_bwd_body<D>(p, th, t, obs_t, alpha_t, abar_t, counts, thb, inc);
-    if (threadIdx.x == 0) *tick = 0;
 }
 
 // x_bar_i += inc_x[a(i)] + inc_all, v_bar_i += inc_v[a(i)]  (particle i of episode i / N)
@@ -593,19 +548,22 @@ void launch_check_aid(const KParams& p, const int32_t* aid, int* flags, cudaStre
 int obs_parts(const KParams& p) { return p.E * (int)((p.N + kObsThreads - 1) / kObsThreads); }
 int obs_values(const KParams& p) { return obs_nvals(p.n_act, p.dim); }
 
-void launch_observe_ctrl(const KParams& p, const float* x, const float* vc, const int* pid, const int32_t* aid,
-                         float* part, const float* theta, int32_t t, float* obs_t, float* counts, float* alpha_t,
-                         int* tick, cudaStream_t s) {
+void launch_observe(const KParams& p, const float* x, const float* vc, const int* pid, const int32_t* aid,
+                    float* part, cudaStream_t s) {
     const int nch = (int)((p.N + kObsThreads - 1) / kObsThreads);
     const size_t smem = sizeof(float) * (kObsThreads / 32) * obs_nvals(p.n_act, p.dim);
-    DISPATCH(p.dim, launch_k(k_observe<DIM>, dim3(nch, p.E), kObsThreads, smem, s, p, x, vc, pid, aid, part, theta, t,
-                             obs_t, counts, alpha_t, tick));
+    DISPATCH(p.dim, launch_k(k_observe<DIM>, dim3(nch, p.E), kObsThreads, smem, s, p, x, vc, pid, aid, part));
 }
-void launch_reduce_abar_obs(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,
-                            const float* theta, int32_t t, const float* obs_t, const float* alpha_t,
-                            const float* counts, float* theta_bar, float* inc, int* tick, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_reduce_abar_obs<DIM>, dim3(p.n_act, p.E), kRAO, 0, s, p, sl, abar_part, alpha_bar_t,
-                             p2g_grad_item_grid(p), theta, t, obs_t, alpha_t, counts, theta_bar, inc, tick));
+void launch_ctrl_obs_fwd(const KParams& p, const float* theta, int32_t t, const float* part, float* obs_t,
+                         float* counts, float* alpha_t, cudaStream_t s) {
+    const int nch = (int)((p.N + kObsThreads - 1) / kObsThreads);
+    DISPATCH(p.dim, launch_k(k_ctrl_obs_fwd<DIM>, p.E, 128, 0, s, p, theta, t, part, nch, obs_t, counts, alpha_t));
+}
+void launch_ctrl_obs_bwd(const KParams& p, const float* theta, int32_t t, const float* obs_t,
+                         const float* alpha_t, const float* alpha_bar_t, const float* counts,
+                         float* theta_bar, float* inc, cudaStream_t s) {
+    DISPATCH(p.dim, launch_k(k_ctrl_obs_bwd<DIM>, 1, 256, 0, s, p, theta, t, obs_t, alpha_t, alpha_bar_t, counts,
+                                                         theta_bar, inc));
 }
 void launch_observe_adj(const KParams& p, const AdjView& Sb, const int* pid, const int32_t* aid,
                         const float* inc, cudaStream_t s) {

@@ -222,6 +222,9 @@ template <int D> struct TilePipe {
 // with and without it (SPLIT): small problems (<= 256K particles per launch) take the split
 // variant; large ones, whose blocks outnumber the CTAs anyway, keep the plain per-block loop
 // (the index math costs g2p ~9% there).
+__device__ __forceinline__ int item_split(int nact, int grid) {
+    return nact > 0 ? max(1, min(kMaxSplit, grid / nact)) : 1;
+}
 // particle range [rb, re) of part `part` of a block with n particles, in whole passes of NT
 template <int NT>
 __device__ __forceinline__ void item_range(int n, int part, int split, int& rb, int& re) {
@@ -1605,13 +1608,53 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
     }
 }
 
-// the step's actuator gradients (kernels.h reduce_abar_one), one CTA per (actuator, episode)
+// alpha_bar_t[a] = fixed-order sum over p2g_grad's work items of the step (blocks, or parts of
+// blocks) of abar_part[a][w]: thread i sums items i, i + 256, ... in order (four interleaved
+// accumulators, combined in order), then the warps' butterflies and the 8 warp sums in order.
+// Closed loop: per episode e = blockIdx.y over that episode's blocks (a contiguous range of the
+// block-id-ordered list, found by binary search).  256 threads per actuator: with 64 robot
+// episodes a step has ~6,400 blocks, which one warp per actuator summed in ~20 us.
 constexpr int kRA = 256;
 __global__ void __launch_bounds__(kRA) k_reduce_abar(KParams p, SlotView sl, const float* __restrict__ part,
                                                      float* __restrict__ out, int grid_p2gg) {
     pdl_begin();
     __shared__ float s_w[kRA / 32];
-    reduce_abar_one<kRA>(p, sl, part, out, grid_p2gg, blockIdx.x, blockIdx.y, s_w);
+    const int a = blockIdx.x, e = blockIdx.y, n_act = p.n_act;
+    const int n = *sl.nactive;
+    const int* blist = sl.blist + *sl.base;
+    int lo = 0, hi = n;
+    if (p.closed_loop) {  // first entries of episode e and e + 1 (block ids are episode-major)
+        int l = 0, h = n;
+        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe < e) l = m + 1; else h = m; }
+        lo = l;
+        h = n;
+        while (l < h) { const int m = (l + h) >> 1; if (blist[m] / p.nbe <= e) l = m + 1; else h = m; }
+        hi = l;
+    }
+    const int split = item_split(n, grid_p2gg);  // p2g_grad's work items of this step
+    lo *= split;
+    hi *= split;
+    const float* row = part + (int64_t)a * p.step_blocks * kMaxSplit;
+    float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    int b = lo + (int)threadIdx.x;
+    for (; b + 3 * kRA < hi; b += 4 * kRA) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s4[u] += row[b + u * kRA];
+    }
+    if (b < hi) s4[0] += row[b];  // at most three left
+    if (b + kRA < hi) s4[1] += row[b + kRA];
+    if (b + 2 * kRA < hi) s4[2] += row[b + 2 * kRA];
+    float s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.0f;
+#pragma unroll
+        for (int w = 0; w < kRA / 32; ++w) t += s_w[w];
+        out[e * n_act + a] = t;
+    }
 }
 
 // measurement: number of distinct grid nodes with M > 0 in a step's resolved tiles.
@@ -1928,12 +1971,11 @@ void launch_count_active(const KParams& p, const SlotView& sl, int64_t* count, c
     cudaMemsetAsync(count, 0, sizeof(int64_t), s);
     DISPATCH(p.dim, launch_k(k_count_active<DIM>, node_grid(p), kT, 0, s, p, sl, (unsigned long long*)count));
 }
-int p2g_grad_item_grid(const KParams& p) { return split_blocks(p) ? (int)pgrid(p, 3) : 0; }
 void launch_reduce_abar(const KParams& p, const SlotView& sl, const float* abar_part, float* alpha_bar_t,
                         cudaStream_t s) {
     if (p.n_act > 0)
         launch_k(k_reduce_abar, dim3(p.n_act, p.closed_loop ? p.E : 1), kRA, 0, s, p, sl, abar_part, alpha_bar_t,
-                 p2g_grad_item_grid(p));  // 0: p2g_grad ran one item per block
+                 split_blocks(p) ? (int)pgrid(p, 3) : 0);  // 0: p2g_grad ran one item per block
 }
 
 }  // namespace mpm
