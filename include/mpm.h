@@ -124,6 +124,9 @@ mpm_status mpm_set_stream(mpm_handle h, void* cuda_stream);
 /* Bytes of device workspace needed for the current params (max_steps, k_ckpt,
  * n_episodes).  Bind a device allocation of at least that size (256-B aligned). */
 mpm_status mpm_workspace_bytes(mpm_handle h, size_t* bytes);
+/* The same for a tape of `steps` steps (SURVEY 8(b) form), without changing the handle's
+ * max_steps; steps >= 1. */
+mpm_status mpm_workspace_bytes_for(mpm_handle h, int32_t steps, size_t* bytes);
 mpm_status mpm_bind_workspace(mpm_handle h, void* device_ptr, size_t bytes);
 
 /* Copy in the initial state S_0 (host or device pointers, layouts above).

@@ -590,6 +590,15 @@ mpm_status mpm_workspace_bytes(mpm_handle h, size_t* bytes) {
     return MPM_OK;
 }
 
+mpm_status mpm_workspace_bytes_for(mpm_handle h, int32_t steps, size_t* bytes) {
+    if (!h || !bytes || steps < 1) return MPM_ERR_INVALID_ARG;
+    const int32_t keep = h->prm.max_steps;
+    h->prm.max_steps = steps;  // size only; the handle's parameters are unchanged on return
+    *bytes = carve(h, nullptr);
+    h->prm.max_steps = keep;
+    return MPM_OK;
+}
+
 mpm_status mpm_bind_workspace(mpm_handle h, void* dptr, size_t bytes) {
     if (!h || !dptr) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
@@ -613,6 +622,7 @@ mpm_status mpm_set_state(mpm_handle h, const float* x, const float* v, const flo
                          const float* F, const int32_t* actuator_id) {
     if (!h) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
+    NvtxRange nv("mpm_set_state");
     if (h->dd) return fail(h, MPM_ERR_BAD_SEQUENCE, "a subdomain handle takes mpm_set_state_ids");
     if (h->phase < kBound) return fail(h, MPM_ERR_BAD_SEQUENCE, "set_state before bind_workspace");
     if (!x) return fail(h, MPM_ERR_INVALID_ARG, "x is required");
@@ -680,6 +690,7 @@ mpm_status mpm_set_controller(mpm_handle h, const float* theta, int64_t n) {
 mpm_status mpm_forward(mpm_handle h, int32_t steps) {
     if (!h) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
+    NvtxRange nv("mpm_forward");
     if (h->dd) return fail(h, MPM_ERR_BAD_SEQUENCE, "a subdomain handle runs through mpm_dd_forward");
     if (h->phase < kHasState) return fail(h, MPM_ERR_BAD_SEQUENCE, "forward before set_state");
     if (steps < 1 || steps > h->prm.max_steps)
@@ -708,6 +719,7 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
 mpm_status mpm_loss(mpm_handle h, float* loss_out) {
     if (!h) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
+    NvtxRange nv("mpm_loss");
     if (h->dd) return fail(h, MPM_ERR_BAD_SEQUENCE, "a subdomain handle runs through mpm_dd_loss");
     if (h->phase < kForward) return fail(h, MPM_ERR_BAD_SEQUENCE, "loss before forward");
     const KParams k = kparams(h);
@@ -752,6 +764,7 @@ mpm_status mpm_seed_adjoint(mpm_handle h, const float* dx, const float* dv, cons
 mpm_status mpm_backward(mpm_handle h, int32_t steps) {
     if (!h) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
+    NvtxRange nv("mpm_backward");
     if (h->dd) return fail(h, MPM_ERR_BAD_SEQUENCE, "a subdomain handle runs through mpm_dd_backward");
     if (h->phase != kSeeded) return fail(h, MPM_ERR_BAD_SEQUENCE, "backward needs forward + loss/seed_adjoint");
     if (steps != h->recorded)
@@ -814,6 +827,7 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
 mpm_status mpm_grads(mpm_handle h, float* dx0, float* dv0, float* dC0, float* dF0, float* dtheta) {
     if (!h) return MPM_ERR_INVALID_ARG;
     DevGuard dg(h);
+    NvtxRange nv("mpm_grads");
     if (h->phase != kBackward) return fail(h, MPM_ERR_BAD_SEQUENCE, "grads before backward");
     const KParams k = kparams(h);
     const size_t EN = (size_t)k.E * k.N, d = (size_t)h->dim;

@@ -10,6 +10,8 @@
 #include <utility>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/mpm.h"
 #include "kernels.h"
 
@@ -149,6 +151,13 @@ struct DevGuard {
 };
 
 mpm_status fail(mpm_handle h, mpm_status st, const std::string& msg);
+
+// NVTX range around a C-ABI call (visible in Nsight Systems / ncu --nvtx; graph replays of the
+// steps are device-side and show as the enclosing call's range)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 #define CU(call)                                                                           \
     do {                                                                                   \

@@ -181,6 +181,7 @@ mpm_status mpm_set_state_ids(mpm_handle h, int64_t n, const float* x, const floa
 }
 
 mpm_status mpm_dd_forward(mpm_handle* hs, int32_t n, int32_t steps) {
+    NvtxRange nv("mpm_dd_forward");
     mpm_status st = check_set(hs, n);
     if (st) return st;
     for (int g = 0; g < n; ++g) {
@@ -268,6 +269,7 @@ mpm_status mpm_dd_forward(mpm_handle* hs, int32_t n, int32_t steps) {
 }
 
 mpm_status mpm_dd_loss(mpm_handle* hs, int32_t n, float* loss_out) {
+    NvtxRange nv("mpm_dd_loss");
     mpm_status st = check_set(hs, n);
     if (st) return st;
     for (int g = 0; g < n; ++g)
@@ -310,6 +312,7 @@ mpm_status mpm_dd_loss(mpm_handle* hs, int32_t n, float* loss_out) {
 }
 
 mpm_status mpm_dd_backward(mpm_handle* hs, int32_t n, int32_t steps) {
+    NvtxRange nv("mpm_dd_backward");
     mpm_status st = check_set(hs, n);
     if (st) return st;
     for (int g = 0; g < n; ++g) {

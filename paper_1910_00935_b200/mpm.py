@@ -23,7 +23,7 @@ MODEL_NEOHOOKEAN, MODEL_FIXED_COROTATED = 0, 1
 LOSS_COM_TARGET, LOSS_MOVE_FORWARD = 0, 1
 
 EXPORTS = ["mpm_create", "mpm_destroy", "mpm_last_error", "mpm_default_params", "mpm_get_params",
-           "mpm_set_params", "mpm_set_stream", "mpm_workspace_bytes", "mpm_bind_workspace",
+           "mpm_set_params", "mpm_set_stream", "mpm_workspace_bytes", "mpm_workspace_bytes_for", "mpm_bind_workspace",
            "mpm_set_state", "mpm_n_theta", "mpm_set_controller", "mpm_forward", "mpm_loss",
            "mpm_seed_adjoint", "mpm_backward", "mpm_grads", "mpm_get_state", "mpm_launch_count",
            "mpm_grad_v0_sum", "mpm_set_profiling", "mpm_reset_kernel_stats", "mpm_kernel_stats", "mpm_active_nodes",
@@ -69,6 +69,7 @@ def load() -> ct.CDLL:
             "mpm_get_params": [H, ct.POINTER(mpm_params)],
             "mpm_set_params": [H, ct.POINTER(mpm_params)], "mpm_set_stream": [H, P],
             "mpm_workspace_bytes": [H, ct.POINTER(ct.c_size_t)],
+            "mpm_workspace_bytes_for": [H, ct.c_int32, ct.POINTER(ct.c_size_t)],
             "mpm_bind_workspace": [H, P, ct.c_size_t], "mpm_set_state": [H, P, P, P, P, P],
             "mpm_n_theta": [H, ct.POINTER(ct.c_int64)], "mpm_set_controller": [H, P, ct.c_int64],
             "mpm_forward": [H, ct.c_int32], "mpm_loss": [H, P], "mpm_seed_adjoint": [H, P, P, P, P],

@@ -327,3 +327,22 @@ def test_binning_scan_beside_a_concurrent_kernel():
     torch.cuda.synchronize()
     for key in ("x", "v", "C", "F", "dx0", "dv0", "dtheta", "loss"):
         assert np.array_equal(solo[key], busy[key]), key
+
+
+def test_workspace_bytes_for_steps():
+    """mpm_workspace_bytes_for(steps) (SURVEY 8(b)'s form) sizes a tape of `steps` without changing
+    the handle: equal to mpm_workspace_bytes at max_steps, growing with steps."""
+    import ctypes as ct
+    from paper_1910_00935_b200 import mpm
+    p = W.config("c3", steps=64)
+    sim = mpm.sim_from_config(p, 29952, max_steps=64, k_ckpt=1, probe_only=True)
+    L = mpm.load()
+    b64, b128, b1 = ct.c_size_t(), ct.c_size_t(), ct.c_size_t()
+    assert L.mpm_workspace_bytes_for(sim.h, 64, ct.byref(b64)) == 0
+    assert L.mpm_workspace_bytes_for(sim.h, 128, ct.byref(b128)) == 0
+    assert L.mpm_workspace_bytes_for(sim.h, 1, ct.byref(b1)) == 0
+    assert b64.value == sim.workspace_bytes and b1.value < b64.value < b128.value
+    assert L.mpm_workspace_bytes_for(sim.h, 0, ct.byref(b1)) == 1
+    now = ct.c_size_t()
+    assert L.mpm_workspace_bytes(sim.h, ct.byref(now)) == 0 and now.value == sim.workspace_bytes
+    sim.close()
