@@ -3,13 +3,14 @@
 # the bench's k and k = 32, every config), ncu launch list + --set full captures of the step
 # kernels, compute-sanitizer logs.  Everything lands in gpurun_out/r2/.
 cd "$(dirname "$0")/.."
-O=gpurun_out/r2; mkdir -p $O/configs
+O=gpurun_out/${EVID:-r2}; mkdir -p $O/configs
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total,driver_version --format=csv > $O/smi.txt
 lscpu | grep -E "Model name|^CPU\(s\)" > $O/host.txt
 python -m paper_1910_00935_b200.build > /dev/null
 export MPM_PARITY_RECORD=$O/parity_record.jsonl; rm -f $MPM_PARITY_RECORD
 timeout 1500 python -m pytest tests -m gpu -q -s --durations=30 > $O/pytest_gpu.txt 2>&1; echo "pytest exit $?" >> $O/pytest_gpu.txt
 tail -3 $O/pytest_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; tail -1 $O/smoke.txt
 timeout 900 python bench.py > $O/bench_c5.json 2> $O/bench_c5.err; tail -c 300 $O/bench_c5.json
 timeout 900 python bench.py --k-ckpt 32 --no-cpu-baseline > $O/bench_c5_k32.json 2> $O/bench_c5_k32.err; tail -c 200 $O/bench_c5_k32.json
 for c in c1a c1b c2 c2cl c3 c3cl c3liquid c4; do
