@@ -22,7 +22,6 @@
 #include "kernels.h"
 
 #include <algorithm>
-#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
