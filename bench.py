@@ -431,6 +431,82 @@ def run_ours(args):
     return 0
 
 
+def run_dd(args):
+    """ONE body decomposed into `--dd` slab subdomains (include/mpm.h mpm_dd_*), one
+    process driving one handle per slab -- on as many GPUs as are visible (round robin), else all on
+    cuda:0.  Same metric (fwd+bwd particle-steps/s of the whole body); k = 1 (the decomposed
+    tape keeps every state), so the horizon is capped by memory: BENCH_HORIZON (default 256)."""
+    import torch
+    from paper_1910_00935_b200 import mpm, workloads as W
+    p = W.config(args.config, steps=int(os.environ.get("BENCH_HORIZON", 256)))
+    if int(p.get("n_act", 0)) != 0:
+        raise SystemExit("--dd needs a passive body (c1a, c1b, c5)")
+    T, G = int(p["steps"]), int(args.dd)
+    inp = W.make_inputs(p)
+    N = len(inp["x"])
+    B = 4 if p["dim"] == 3 else 8
+    nb = -(-p["n_grid"] // B)
+    xs = inp["x"][:, 0].astype(np.float32)
+    bx = np.floor(xs * np.float32(p["n_grid"]) - np.float32(0.5)).astype(np.int64) // B
+    # slabs with about equal particle counts (block-column boundaries)
+    cuts = sorted({min(nb - 1, max(1, int(np.quantile(bx, g / G)))) for g in range(1, G)})
+    bounds = [0] + cuts + [nb]
+    ndev = max(1, torch.cuda.device_count())
+    sims, sel, streams = [], [], []
+    for g, (lo, hi) in enumerate(zip(bounds[:-1], bounds[1:])):
+        ids = np.nonzero((bx >= lo) & (bx < hi))[0].astype(np.int32)
+        dev = g % ndev
+        torch.cuda.set_device(dev)
+        st = torch.cuda.Stream(device=dev)
+        with torch.cuda.stream(st):
+            sims.append(mpm.sim_from_config(p, int(len(ids) * 1.25) + 8192, max_steps=T, k_ckpt=1,
+                                            subdomain=(lo, hi, N)))
+        sel.append(ids)
+        streams.append(st)
+    mpm.dd_link(sims)
+    dev_in = []
+    for sim, ids, g in zip(sims, sel, range(len(sims))):
+        d = g % ndev
+        dev_in.append({k: torch.from_numpy(np.ascontiguousarray(inp[k][ids])).to(f"cuda:{d}") for k in "xvCF"} |
+                      {"ids": torch.from_numpy(ids).to(f"cuda:{d}")})
+
+    def step():
+        for sim, di in zip(sims, dev_in):
+            sim.set_state_ids(di["x"], di["v"], di["C"], di["F"], di["ids"])
+        mpm.dd_forward(sims, T)
+        mpm.dd_loss(sims)
+        mpm.dd_backward(sims, T)
+
+    for _ in range(args.warmup):
+        step()
+    for d in range(ndev):
+        torch.cuda.synchronize(d)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ndev)]
+    for d in range(ndev):
+        with torch.cuda.device(d):
+            ev[d][0].record(streams[d])
+    for _ in range(args.steps):
+        step()
+    for d in range(ndev):
+        with torch.cuda.device(d):
+            ev[d][1].record(streams[d])
+    for d in range(ndev):
+        torch.cuda.synchronize(d)
+    ms = max(ev[d][0].elapsed_time(ev[d][1]) for d in range(min(ndev, len(sims))))
+    value = float(N) * T * args.steps / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": min(ndev, G), "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{p['name']}: one body of {N:,} particles over {G} slab subdomains (f3) on "
+                                   f"{min(ndev, G)} GPU(s), {p['n_grid']}^{p['dim']} grid, {T} steps, k = 1",
+                       "slabs_block_x": bounds, "particles_per_slab": [int(len(s)) for s in sel]},
+            "gpu_launches": int(sum(s.launch_count() for s in sims))}
+    print(json.dumps(line), flush=True)
+    for s in sims:
+        s.close()
+    return 0
+
+
 def run_ours_on_stream(args):
     """the library captures its forward/backward tapes as CUDA graphs, which needs a
     non-default stream: run the whole arm on a dedicated torch stream."""
@@ -450,9 +526,12 @@ def main():
     ap.add_argument("--config", default="c5", choices=["c1a", "c1b", "c2", "c2cl", "c3", "c3cl", "c3liquid", "c4", "c5"])
     ap.add_argument("--k-ckpt", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dd", type=int, default=0, help="f3: one body over this many slab subdomains (one process)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.dd:
+        return run_dd(args)
     return run_ours_on_stream(args)
 
 
