@@ -469,6 +469,8 @@ def run_dd(args):
         d = g % ndev
         dev_in.append({k: torch.from_numpy(np.ascontiguousarray(inp[k][ids])).to(f"cuda:{d}") for k in "xvCF"} |
                       {"ids": torch.from_numpy(ids).to(f"cuda:{d}")})
+    for d in range(ndev):  # the inputs were copied on torch's current stream, the handles use their own
+        torch.cuda.synchronize(d)
 
     def step():
         for sim, di in zip(sims, dev_in):
