@@ -459,8 +459,9 @@ def run_dd(args):
         torch.cuda.set_device(dev)
         st = torch.cuda.Stream(device=dev)
         with torch.cuda.stream(st):
-            sims.append(mpm.sim_from_config(p, int(len(ids) * 1.25) + 8192, max_steps=T, k_ckpt=1,
-                                            subdomain=(lo, hi, N)))
+            # capacity: the slab's particles plus room for the body drifting across slabs
+            cap = min(N, int(len(ids) + max(0.5 * len(ids), N / G))) + 8192
+            sims.append(mpm.sim_from_config(p, cap, max_steps=T, k_ckpt=1, subdomain=(lo, hi, N)))
         sel.append(ids)
         streams.append(st)
     mpm.dd_link(sims)

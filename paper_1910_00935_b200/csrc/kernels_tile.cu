@@ -1692,8 +1692,8 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
     using L = Lay<D>;
     const int side = blockIdx.y;
     const MigSrc& src = side == 0 ? left : right;
-    const int n_left = left.cnt ? min(*left.cnt, cap) : 0;
-    const int n_right = right.cnt ? min(*right.cnt, cap) : 0;
+    const int n_left = left.cnt ? min(*left.cnt, left.cap) : 0;
+    const int n_right = right.cnt ? min(*right.cnt, right.cap) : 0;
     const int base = *nsorted + (side == 0 ? 0 : n_left);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         imm_base[side] = base;
@@ -1704,7 +1704,7 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
     const bool in = m < n;
     int key = -1;
     if (in) {
-        const int j = src.rows[(side == 0 ? 1 : 0) * cap + m];  // the neighbour's outbox toward us
+        const int j = src.rows[(side == 0 ? 1 : 0) * src.cap + m];  // the neighbour's outbox toward us
         const int64_t dst = (int64_t)base + m;
         if (dst >= p.N) {
             atomicOr(flags, FLAG_MIGRATION);  // capacity of this subdomain exceeded
@@ -1712,13 +1712,13 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
             float x[3];
 #pragma unroll
             for (int k = 0; k < D; ++k) {
-                x[k] = src.S.x[soa(p.EN, k, j)];
+                x[k] = src.S.x[soa(src.en, k, j)];
                 S.x[soa(p.EN, k, dst)] = x[k];
             }
 #pragma unroll
-            for (int q = 0; q < L::VC; ++q) S.vc[soa(p.EN, q, dst)] = src.S.vc[soa(p.EN, q, j)];
+            for (int q = 0; q < L::VC; ++q) S.vc[soa(p.EN, q, dst)] = src.S.vc[soa(src.en, q, j)];
 #pragma unroll
-            for (int q = 0; q < L::FF; ++q) S.f[soa(p.EN, q, dst)] = src.S.f[soa(p.EN, q, j)];
+            for (int q = 0; q < L::FF; ++q) S.f[soa(p.EN, q, dst)] = src.S.f[soa(src.en, q, j)];
             S.pid[dst] = src.S.pid[j];
             int b[3];
             if (base_cell<D>(p, x, b)) {
@@ -1745,13 +1745,14 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
 template <int D>
 __global__ void __launch_bounds__(kT) k_adj_pull(KParams p, AdjView Sb, const int* __restrict__ cnt,
                                                  const int* __restrict__ rows, int cap, AdjView nbl,
-                                                 const int* __restrict__ nbl_base, AdjView nbr,
-                                                 const int* __restrict__ nbr_base) {
+                                                 const int* __restrict__ nbl_base, int64_t nbl_en, AdjView nbr,
+                                                 const int* __restrict__ nbr_base, int64_t nbr_en) {
     pdl_begin();
     using L = Lay<D>;
     const int dir = blockIdx.y;  // 0: emigrants to the left neighbour, 1: to the right
     const AdjView& nb = dir == 0 ? nbl : nbr;
     const int* nbase = dir == 0 ? nbl_base : nbr_base;
+    const int64_t en = dir == 0 ? nbl_en : nbr_en;
     if (!nbase) return;
     const int n = min(cnt[dir], cap);
     const int m = blockIdx.x * kT + threadIdx.x;
@@ -1759,11 +1760,11 @@ __global__ void __launch_bounds__(kT) k_adj_pull(KParams p, AdjView Sb, const in
     const int j = rows[dir * cap + m];
     const int64_t src = (int64_t)nbase[dir == 0 ? 1 : 0] + m;  // we are the neighbour's right / left side
 #pragma unroll
-    for (int k = 0; k < D; ++k) Sb.x[soa(p.EN, k, j)] = nb.x[soa(p.EN, k, src)];
+    for (int k = 0; k < D; ++k) Sb.x[soa(p.EN, k, j)] = nb.x[soa(en, k, src)];
 #pragma unroll
-    for (int q = 0; q < L::VC; ++q) Sb.vc[soa(p.EN, q, j)] = nb.vc[soa(p.EN, q, src)];
+    for (int q = 0; q < L::VC; ++q) Sb.vc[soa(p.EN, q, j)] = nb.vc[soa(en, q, src)];
 #pragma unroll
-    for (int q = 0; q < L::FF; ++q) Sb.f[soa(p.EN, q, j)] = nb.f[soa(p.EN, q, src)];
+    for (int q = 0; q < L::FF; ++q) Sb.f[soa(p.EN, q, j)] = nb.f[soa(en, q, src)];
 }
 
 // per-block sums of x over the rows S_T holds for the blocks of step T-1 (sorted order, fixed
@@ -1983,16 +1984,17 @@ namespace mpm {
 void launch_immigrate(const KParams& p, const StateView& S, const int* nsorted, MigSrc left, MigSrc right,
                       int x_lo, int x_hi, int cap, int* keys, int* bcount, int* imm_base, int* nrows, int* flags,
                       cudaStream_t s) {
-    const dim3 grid((unsigned)((cap + kT - 1) / kT), 2);
+    const int most = std::max(left.cnt ? left.cap : 0, right.cnt ? right.cap : 0);  // the neighbours' outboxes
+    const dim3 grid((unsigned)std::max(1, (most + kT - 1) / kT), 2);
     DISPATCH(p.dim, launch_k(k_immigrate<DIM>, grid, kT, 0, s, p, S, nsorted, left, right, x_lo, x_hi, cap, keys,
                              bcount, imm_base, nrows, flags));
 }
 void launch_adj_pull(const KParams& p, const AdjView& Sb, const int* cnt, const int* rows, int cap,
-                     const AdjView& nb_left, const int* nb_left_base, const AdjView& nb_right,
-                     const int* nb_right_base, cudaStream_t s) {
+                     const AdjView& nb_left, const int* nb_left_base, int64_t nb_left_en, const AdjView& nb_right,
+                     const int* nb_right_base, int64_t nb_right_en, cudaStream_t s) {
     const dim3 grid((unsigned)((cap + kT - 1) / kT), 2);
     DISPATCH(p.dim, launch_k(k_adj_pull<DIM>, grid, kT, 0, s, p, Sb, cnt, rows, cap, nb_left, nb_left_base,
-                             nb_right, nb_right_base));
+                             nb_left_en, nb_right, nb_right_base, nb_right_en));
 }
 void launch_block_com(const KParams& p, const SlotView& sl_last, const float* x, float* part, cudaStream_t s) {
     const int grid = (int)std::min<int64_t>(((int64_t)p.step_blocks + kW - 1) / kW, (int64_t)tab().sms * 8);

@@ -36,17 +36,19 @@ def _single(p, inp, T, mat=None):
     return out
 
 
-def _split(p, inp, T, cuts, cap_frac=0.75, mat=None):
+def _split(p, inp, T, cuts, cap_frac=0.75, mat=None, cap_per_slab=False):
+    """cap_per_slab: each subdomain's capacity from its own particle count (unequal capacities, so
+    unequal component strides of the neighbours' state arrays); else cap_frac * N for all."""
     N = len(inp["x"])
     B = 4 if p["dim"] == 3 else 8
     nb = -(-p["n_grid"] // B)
     bounds = [0] + list(cuts) + [nb]
     bx = _block_x(p, inp["x"])
-    cap = int(cap_frac * N) + 4096
     sims, sel = [], []
     for lo, hi in zip(bounds[:-1], bounds[1:]):
         ids = np.nonzero((bx >= lo) & (bx < hi))[0].astype(np.int32)
         sel.append(ids)
+        cap = int(1.25 * len(ids)) + 8192 if cap_per_slab else int(cap_frac * N) + 4096
         sims.append(mpm.sim_from_config(p, cap, max_steps=T, k_ckpt=1, subdomain=(lo, hi, N)))
     assert sum(len(s) for s in sel) == N and all(len(s) > 0 for s in sel)
     mpm.dd_link(sims)
@@ -100,6 +102,20 @@ def test_c5_two_slabs_bitwise_64_steps():
     print(f"[f3] c5 2 slabs: {got['migrated']} particles changed slab, loss {got['loss']:.9g}")
     assert got["migrated"] > 0
     _assert_bitwise(got, ref, "c5/2")
+
+
+def test_c5_four_unequal_slabs_bitwise_32_steps():
+    """C5 at full size in 4 slabs of unequal width and capacity (each subdomain sized from its own
+    particle count, so the neighbours' state arrays have different component strides), 32 steps:
+    bitwise equal to one domain."""
+    T = 32
+    p = W.config("c5", steps=T)
+    inp = W.make_inputs(p)
+    ref = _single(p, inp, T)
+    got = _split(p, inp, T, cuts=[12, 15, 19], cap_per_slab=True)
+    print(f"[f3] c5 4 unequal slabs: {got['migrated']} particles changed slab")
+    assert got["migrated"] > 0
+    _assert_bitwise(got, ref, "c5/4")
 
 
 def test_block2d_three_slabs_with_fluid_bitwise():
