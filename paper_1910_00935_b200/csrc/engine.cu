@@ -146,19 +146,21 @@ size_t carve(mpm_ctx* h, char* base) {
         off += align_up(bytes);
         return ptr;
     };
+    // AoSoA state arrays (mpm_device.cuh soa<NC>): whole 32-particle tiles
+    const size_t ENT = (EN + kTile - 1) / kTile * kTile;
     auto state = [&]() {
         StateView s;
-        s.x = (float*)take(sizeof(float) * EN * d);
-        s.vc = (float*)take(sizeof(float) * EN * (d + d * d));
-        s.f = (float*)take(sizeof(float) * EN * d * d);
+        s.x = (float*)take(sizeof(float) * ENT * d);
+        s.vc = (float*)take(sizeof(float) * ENT * (d + d * d));
+        s.f = (float*)take(sizeof(float) * ENT * d * d);
         s.pid = (int*)take(sizeof(int) * EN);
         return s;
     };
     auto adj = [&]() {
         AdjView s;
-        s.x = (float*)take(sizeof(float) * EN * d);
-        s.vc = (float*)take(sizeof(float) * EN * (d + d * d));
-        s.f = (float*)take(sizeof(float) * EN * d * d);
+        s.x = (float*)take(sizeof(float) * ENT * d);
+        s.vc = (float*)take(sizeof(float) * ENT * (d + d * d));
+        s.f = (float*)take(sizeof(float) * ENT * d * d);
         return s;
     };
     std::vector<StateView> ckpt, window;
@@ -183,7 +185,7 @@ size_t carve(mpm_ctx* h, char* base) {
     float* staging = (float*)take(sizeof(float) * sf);
     int32_t* aid = (int32_t*)take(sizeof(int32_t) * EN);
     int32_t* mat = (int32_t*)take(sizeof(int32_t) * std::max<size_t>(EN, (size_t)h->n_body));  // by particle id
-    float* xbar_part = (float*)take(sizeof(float) * EN * h->dim);
+    float* xbar_part = (float*)take(sizeof(float) * ENT * h->dim);
     int* bcount = (int*)take(sizeof(int) * k.TB);
     int* cursor = (int*)take(sizeof(int) * k.TB);
     int* scan_part = (int*)take(sizeof(int64_t) * (scan_chunks(k) + 2));  // chunk totals, epoch, ticket

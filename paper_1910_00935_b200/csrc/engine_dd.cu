@@ -238,10 +238,9 @@ mpm_status mpm_dd_forward(mpm_handle* hs, int32_t n, int32_t steps) {
             MigSrc src[2];
             for (int s = 0; s < 2; ++s) {
                 mpm_ctx* nb = h->nbr[s];
-                src[s] = MigSrc{StateView{nullptr, nullptr, nullptr, nullptr}, nullptr, nullptr, 0, 0};
+                src[s] = MigSrc{StateView{nullptr, nullptr, nullptr, nullptr}, nullptr, nullptr, 0};
                 if (!nb) continue;
                 src[s].S = state_at(nb, t + 1);
-                src[s].en = kparams(nb).EN;  // the neighbour's capacities may differ from ours
                 src[s].cap = nb->mig_cap;
                 src[s].cnt = nb->out_cnt + (size_t)2 * t + (s == 0 ? 1 : 0);  // toward us
                 src[s].rows = nb->out_rows + (size_t)2 * nb->mig_cap * t;
@@ -342,9 +341,9 @@ mpm_status mpm_dd_backward(mpm_handle* hs, int32_t n, int32_t steps) {
                 KScope sc(h, KC_LAYOUT);
                 launch_adj_pull(K[g], Sbn, h->out_cnt + (size_t)2 * t, h->out_rows + (size_t)2 * h->mig_cap * t,
                                 h->mig_cap, L ? L->sbar[cur] : AdjView{nullptr, nullptr, nullptr},
-                                L ? L->imm_base + (size_t)2 * (t + 1) : nullptr, L ? kparams(L).EN : 0,
+                                L ? L->imm_base + (size_t)2 * (t + 1) : nullptr,
                                 R ? R->sbar[cur] : AdjView{nullptr, nullptr, nullptr},
-                                R ? R->imm_base + (size_t)2 * (t + 1) : nullptr, R ? kparams(R).EN : 0, h->stream);
+                                R ? R->imm_base + (size_t)2 * (t + 1) : nullptr, h->stream);
             }
             const SlotView sl = slot_at(h, t);
             const StateView S = state_at(h, t);

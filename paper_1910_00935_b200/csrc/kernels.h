@@ -126,17 +126,16 @@ struct MigSrc {
     StateView S;     // the neighbour's S_{t+1} (peer pointers)
     const int* cnt;  // the neighbour's outbox count toward this subdomain (null: no neighbour)
     const int* rows;
-    int64_t en;      // component stride of the neighbour's state arrays (its particle capacity)
     int cap;         // the neighbour's outbox capacity per direction (rows is [2][cap])
 };
 void launch_immigrate(const KParams& p, const StateView& S, const int* nsorted, MigSrc left, MigSrc right,
                       int x_lo, int x_hi, int cap, int* keys, int* bcount, int* imm_base, int* nrows, int* flags,
                       cudaStream_t s);
 // backward: S_bar_{t+1} rows of this subdomain's emigrants of step t <- the neighbour's immigrant rows
-// (nb_*_en: component stride of that neighbour's arrays, its particle capacity)
+// (the AoSoA state layout has no capacity-dependent stride, so neighbours of any capacity read alike)
 void launch_adj_pull(const KParams& p, const AdjView& Sb, const int* cnt, const int* rows, int cap,
-                     const AdjView& nb_left, const int* nb_left_base, int64_t nb_left_en, const AdjView& nb_right,
-                     const int* nb_right_base, int64_t nb_right_en, cudaStream_t s);
+                     const AdjView& nb_left, const int* nb_left_base, const AdjView& nb_right,
+                     const int* nb_right_base, cudaStream_t s);
 
 // ---- COM loss in fixed block order (partition independent, f3): per-block sums of x over the
 // rows S_T holds in step T-1's sorted order, then per episode a fixed-order sum over the

@@ -126,8 +126,8 @@ __global__ void __launch_bounds__(kObsThreads) k_observe(KParams p, const float*
     int a_id = -1;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        x[k] = in ? X[soa(p.EN, k, i)] : 0.0f;
-        v[k] = in ? VC[soa(p.EN, k, i)] : 0.0f;
+        x[k] = in ? X[soa<Lay<D>::X>(k, i)] : 0.0f;
+        v[k] = in ? VC[soa<Lay<D>::VC>(k, i)] : 0.0f;
     }
     if (in && aid) a_id = aid[pid[i]];
     float* w = s_w + warp * NV;
@@ -305,8 +305,8 @@ __global__ void k_observe_adj(KParams p, AdjView Sb, const int* __restrict__ pid
 #pragma unroll
     for (int k = 0; k < D; ++k) {
         const float gx = ie[no + k] + (a >= 0 ? ie[a * 2 * D + k] : 0.0f);
-        Sb.x[soa(p.EN, k, i)] += gx;
-        if (a >= 0) Sb.vc[soa(p.EN, k, i)] += ie[a * 2 * D + D + k];
+        Sb.x[soa<Lay<D>::X>(k, i)] += gx;
+        if (a >= 0) Sb.vc[soa<Lay<D>::VC>(k, i)] += ie[a * 2 * D + D + k];
     }
 }
 
@@ -314,8 +314,8 @@ __global__ void k_observe_adj(KParams p, AdjView Sb, const int* __restrict__ pid
 constexpr int kLossThreads = 256;
 
 // partial sums of a d-vector field over a contiguous particle chunk (fixed tree order);
-// component k of particle i = base[k * EN + i] (the first d components of a state array)
-template <int D>
+// component k of particle i = the first d components of an AoSoA state array of NC components
+template <int D, int NC>
 __global__ void k_sum_partial(KParams p, const float* __restrict__ base, float* __restrict__ part) {
     pdl_begin();
     __shared__ float red[D][kLossThreads];
@@ -327,7 +327,7 @@ __global__ void k_sum_partial(KParams p, const float* __restrict__ base, float* 
     for (int k = 0; k < D; ++k) acc[k] = 0.0f;
     for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
 #pragma unroll
-        for (int k = 0; k < D; ++k) acc[k] += base[soa(p.EN, k, (int64_t)e * p.N + i)];
+        for (int k = 0; k < D; ++k) acc[k] += base[soa<NC>(k, (int64_t)e * p.N + i)];
     }
 #pragma unroll
     for (int k = 0; k < D; ++k) red[k][threadIdx.x] = acc[k];
@@ -399,11 +399,11 @@ __global__ void k_seed(KParams p, const float* __restrict__ seed, AdjView Sb) {
     if (i >= p.N * p.E) return;
     const int64_t e = i / p.N;
 #pragma unroll
-    for (int k = 0; k < D; ++k) Sb.x[soa(p.EN, k, i)] = seed[e * D + k];
+    for (int k = 0; k < D; ++k) Sb.x[soa<Lay<D>::X>(k, i)] = seed[e * D + k];
 #pragma unroll
-    for (int q = 0; q < Lay<D>::VC; ++q) Sb.vc[soa(p.EN, q, i)] = 0.0f;
+    for (int q = 0; q < Lay<D>::VC; ++q) Sb.vc[soa<Lay<D>::VC>(q, i)] = 0.0f;
 #pragma unroll
-    for (int q = 0; q < Lay<D>::FF; ++q) Sb.f[soa(p.EN, q, i)] = 0.0f;
+    for (int q = 0; q < Lay<D>::FF; ++q) Sb.f[soa<Lay<D>::FF>(q, i)] = 0.0f;
 }
 
 // ------------------------------------------------------------- layout
@@ -419,13 +419,13 @@ __global__ void k_pack(KParams p, const float* __restrict__ x, const float* __re
     const int64_t s = src ? (int64_t)src[i] : i;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        dx[soa(p.EN, k, i)] = x ? x[s * D + k] : 0.0f;
-        dvc[soa(p.EN, k, i)] = v ? v[s * D + k] : 0.0f;
+        dx[soa<Lay<D>::X>(k, i)] = x ? x[s * D + k] : 0.0f;
+        dvc[soa<Lay<D>::VC>(k, i)] = v ? v[s * D + k] : 0.0f;
     }
 #pragma unroll
     for (int q = 0; q < D * D; ++q) {
-        dvc[soa(p.EN, D + q, i)] = C ? C[s * D * D + q] : 0.0f;
-        df[soa(p.EN, q, i)] = F ? F[s * D * D + q] : ((!zero_f && (q % (D + 1)) == 0) ? 1.0f : 0.0f);
+        dvc[soa<Lay<D>::VC>(D + q, i)] = C ? C[s * D * D + q] : 0.0f;
+        df[soa<Lay<D>::FF>(q, i)] = F ? F[s * D * D + q] : ((!zero_f && (q % (D + 1)) == 0) ? 1.0f : 0.0f);
     }
 }
 
@@ -440,13 +440,13 @@ __global__ void k_unpack(KParams p, const float* __restrict__ sx, const float* _
     const int64_t o = dst ? (int64_t)dst[i] : i;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        if (x) x[o * D + k] = sx[soa(p.EN, k, i)];
-        if (v) v[o * D + k] = svc[soa(p.EN, k, i)];
+        if (x) x[o * D + k] = sx[soa<Lay<D>::X>(k, i)];
+        if (v) v[o * D + k] = svc[soa<Lay<D>::VC>(k, i)];
     }
 #pragma unroll
     for (int q = 0; q < D * D; ++q) {
-        if (C) C[o * D * D + q] = svc[soa(p.EN, D + q, i)];
-        if (F) F[o * D * D + q] = sf[soa(p.EN, q, i)];
+        if (C) C[o * D * D + q] = svc[soa<Lay<D>::VC>(D + q, i)];
+        if (F) F[o * D * D + q] = sf[soa<Lay<D>::FF>(q, i)];
     }
 }
 
@@ -580,7 +580,7 @@ void launch_loss(const KParams& p, const float* x, int loss_kind, float3 target,
     const int nb = loss_blocks_per_episode(p);
     float* seed = com_part + (int64_t)p.E * nb * p.dim;
     DISPATCH(p.dim, {
-        launch_k(k_sum_partial<DIM>, dim3(nb, p.E), kLossThreads, 0, s, p, x, com_part);
+        launch_k(k_sum_partial<DIM, DIM>, dim3(nb, p.E), kLossThreads, 0, s, p, x, com_part);
         launch_k(k_loss_final<DIM>, p.E, 32, 0, s, p, com_part, nb, loss_kind, target, loss, seed, flags);
         launch_k(k_seed<DIM>, nblk(p.N * p.E, 256), 256, 0, s, p, seed, Sb);
     });
@@ -600,7 +600,7 @@ void launch_loss_blocks(const KParams& p, const ListSrc* src, int nsrc, int loss
 void launch_v_sum(const KParams& p, const float* vc_bar, float* part, float* out, cudaStream_t s) {
     const int nb = loss_blocks_per_episode(p);
     DISPATCH(p.dim, {
-        launch_k(k_sum_partial<DIM>, dim3(nb, p.E), kLossThreads, 0, s, p, vc_bar, part);
+        launch_k(k_sum_partial<DIM, DIM + DIM * DIM>, dim3(nb, p.E), kLossThreads, 0, s, p, vc_bar, part);
         launch_k(k_sum_parts<DIM>, p.E, 32, 0, s, part, nb, out);
     });
 }

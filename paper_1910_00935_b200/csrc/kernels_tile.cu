@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kT) k_bin_keys(KParams p, const float* __restr
     if (in) {
         float x[3];
 #pragma unroll
-        for (int k = 0; k < D; ++k) x[k] = X[soa(p.EN, k, i)];
+        for (int k = 0; k < D; ++k) x[k] = X[soa<Lay<D>::X>(k, i)];
         int b[3];
         const bool ok = base_cell<D>(p, x, b);
         const int e = (int)(i / p.N);
@@ -780,9 +780,9 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
 #define MPM_P2G_LOAD(R)                                                                          \
     do {                                                                                         \
         const int i_ = s_ci[(R)];                                                                 \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i_));      \
-        _Pragma("unroll") for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + soa(p.EN, q, i_)); \
-        _Pragma("unroll") for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + soa(p.EN, q, i_));  \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i_));      \
+        _Pragma("unroll") for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + soa<Lay<D>::VC>(q, i_)); \
+        _Pragma("unroll") for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + soa<Lay<D>::FF>(q, i_));  \
         if (aid || p.mat) {                                                                       \
             const int pd_ = __ldg(S.pid + i_);                                                    \
             if (aid) a_id = __ldg(aid + pd_);                                                     \
@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
                 if (Sn.f) {
                     if (fluid) fluid_reset<D>(Ft, Ft);  // R23 (Ft is dead after the row)
 #pragma unroll
-                    for (int q = 0; q < D * D; ++q) Sn.f[soa(p.EN, q, start + r)] = Ft[q];
+                    for (int q = 0; q < D * D; ++q) Sn.f[soa<Lay<D>::FF>(q, start + r)] = Ft[q];
                 }
                 if (r + kTQ < nvalid) MPM_P2G_LOAD(r + kTQ);  // this thread's next particle
             }
@@ -966,25 +966,25 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         xn[a] = fmaf(p.dt, S0[a], x[a]);
-        Sn.x[soa(p.EN, a, j)] = xn[a];
-        Sn.vc[soa(p.EN, a, j)] = S0[a];
+        Sn.x[soa<Lay<D>::X>(a, j)] = xn[a];
+        Sn.vc[soa<Lay<D>::VC>(a, j)] = S0[a];
         fin = fin && isfinite(S0[a]);
 #pragma unroll
-        for (int b = 0; b < D; ++b) Sn.vc[soa(p.EN, D + a * D + b, j)] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
+        for (int b = 0; b < D; ++b) Sn.vc[soa<Lay<D>::VC>(D + a * D + b, j)] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
     }
     if (!fin) atomicOr(flags, FLAG_NONFINITE);
     if (refwd) {  // re-forward from stored tiles: F_{t+1} and the particle id too
         float C[D * D], F[D * D], Ft[D * D];
 #pragma unroll
         for (int q = 0; q < D * D; ++q) {
-            C[q] = __ldg(S.vc + soa(p.EN, D + q, i));
-            F[q] = __ldg(S.f + soa(p.EN, q, i));
+            C[q] = __ldg(S.vc + soa<Lay<D>::VC>(D + q, i));
+            F[q] = __ldg(S.f + soa<Lay<D>::FF>(q, i));
         }
         deform_update<D>(p.dt, C, F, Ft);
         const int pd = __ldg(S.pid + i);
         if (p.mat && __ldg(p.mat + pd) != 0) fluid_reset<D>(Ft, Ft);  // R23
 #pragma unroll
-        for (int q = 0; q < D * D; ++q) Sn.f[soa(p.EN, q, j)] = Ft[q];
+        for (int q = 0; q < D * D; ++q) Sn.f[soa<Lay<D>::FF>(q, j)] = Ft[q];
         Sn.pid[j] = pd;
     }
     int key = -1;
@@ -1056,12 +1056,12 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
         if (va) {
             ia = sl.sigma[start + rb + tid];
 #pragma unroll
-            for (int k = 0; k < D; ++k) xa[k] = __ldg(S.x + soa(p.EN, k, ia));
+            for (int k = 0; k < D; ++k) xa[k] = __ldg(S.x + soa<Lay<D>::X>(k, ia));
         }
         if (vb) {
             ib = sl.sigma[start + rb + tid + kTG];
 #pragma unroll
-            for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + soa(p.EN, k, ib));
+            for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + soa<Lay<D>::X>(k, ib));
         }
         const float4* sU = pipe.wait(it);
         int key = -1;
@@ -1078,7 +1078,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
                 const int i = sl.sigma[start + r];
                 float x[3];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i));
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i));
                 key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags, refwd, S, i, mg);
             }
             if (keys) count_key(in && key >= 0, key, bcount);
@@ -1217,10 +1217,10 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
     do {                                                                                      \
         const int j_ = start + (R);                                                           \
         const int i_ = sl.sigma[j_];                                                          \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i_));   \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) xb[k] = __ldg(Sbn.x + soa(p.EN, k, j_)); \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) vbn[k] = __ldg(Sbn.vc + soa(p.EN, k, j_)); \
-        _Pragma("unroll") for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + soa(p.EN, D + q, j_)); \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i_));   \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) xb[k] = __ldg(Sbn.x + soa<Lay<D>::X>(k, j_)); \
+        _Pragma("unroll") for (int k = 0; k < D; ++k) vbn[k] = __ldg(Sbn.vc + soa<Lay<D>::VC>(k, j_)); \
+        _Pragma("unroll") for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + soa<Lay<D>::VC>(D + q, j_)); \
     } while (0)
         if (tid < nvalid) MPM_G2PG_LOAD(tid);
         for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
@@ -1298,12 +1298,12 @@ __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParam
                 const int i = sl.sigma[j];
 #pragma unroll
                 for (int k = 0; k < D; ++k) {
-                    x[k] = __ldg(S.x + soa(p.EN, k, i));
-                    xb[k] = __ldg(Sbn.x + soa(p.EN, k, j));
-                    vbn[k] = __ldg(Sbn.vc + soa(p.EN, k, j));
+                    x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i));
+                    xb[k] = __ldg(Sbn.x + soa<Lay<D>::X>(k, j));
+                    vbn[k] = __ldg(Sbn.vc + soa<Lay<D>::VC>(k, j));
                 }
 #pragma unroll
-                for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + soa(p.EN, D + q, j));
+                for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + soa<Lay<D>::VC>(D + q, j));
             }
             if (r0 == rb) sU = pipe.wait(it);
             if (in) {
@@ -1312,7 +1312,7 @@ __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParam
                 particle_weights<D>(p, x, c0, lb, fx, wt, dw);
                 g2pg_gather<D>(p, sU, lb, fx, wt, dw, xb, vbn, Cbn, xo);
 #pragma unroll
-                for (int k = 0; k < D; ++k) xbp[soa(p.EN, k, j)] = xo[k];
+                for (int k = 0; k < D; ++k) xbp[soa<Lay<D>::X>(k, j)] = xo[k];
             }
         }
         __syncthreads();
@@ -1494,14 +1494,14 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
                 sF = fmaf(p.dt * C[k * D + a], Ftb[k * D + b], sF);
                 sC = fmaf(Ftb[a * D + k], F[b * D + k], sC);
             }
-            Sb.f[soa(p.EN, a * D + b, i)] = sF;
-            Sb.vc[soa(p.EN, D + a * D + b, i)] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
+            Sb.f[soa<Lay<D>::FF>(a * D + b, i)] = sF;
+            Sb.vc[soa<Lay<D>::VC>(D + a * D + b, i)] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
             fin = fin && isfinite(sF);
         }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        Sb.x[soa(p.EN, a, i)] = fmaf(p.inv_dx, fb[a], xbp[a]);
-        Sb.vc[soa(p.EN, a, i)] = p.p_mass * S0[a];
+        Sb.x[soa<Lay<D>::X>(a, i)] = fmaf(p.inv_dx, fb[a], xbp[a]);
+        Sb.vc[soa<Lay<D>::VC>(a, i)] = p.p_mass * S0[a];
     }
     if (!fin) atomicOr(flags, FLAG_NONFINITE);
     return abar;
@@ -1561,15 +1561,15 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
                 const int j = start + r;
                 i = sl.sigma[j];
 #pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa(p.EN, k, i));
+                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i));
 #pragma unroll
-                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + soa(p.EN, q, i));
+                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + soa<Lay<D>::VC>(q, i));
 #pragma unroll
-                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + soa(p.EN, q, i));
+                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + soa<Lay<D>::FF>(q, i));
 #pragma unroll
-                for (int q = 0; q < L::FF; ++q) Fbn[q] = __ldg(Sbn.f + soa(p.EN, q, j));
+                for (int q = 0; q < L::FF; ++q) Fbn[q] = __ldg(Sbn.f + soa<Lay<D>::FF>(q, j));
 #pragma unroll
-                for (int k = 0; k < D; ++k) xb[k] = __ldg(xbp + soa(p.EN, k, j));
+                for (int k = 0; k < D; ++k) xb[k] = __ldg(xbp + soa<Lay<D>::X>(k, j));
                 if (aid || p.mat) {
                     const int pd = __ldg(S.pid + i);
                     if (aid) a_id = __ldg(aid + pd);
@@ -1712,13 +1712,13 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
             float x[3];
 #pragma unroll
             for (int k = 0; k < D; ++k) {
-                x[k] = src.S.x[soa(src.en, k, j)];
-                S.x[soa(p.EN, k, dst)] = x[k];
+                x[k] = src.S.x[soa<Lay<D>::X>(k, j)];
+                S.x[soa<Lay<D>::X>(k, dst)] = x[k];
             }
 #pragma unroll
-            for (int q = 0; q < L::VC; ++q) S.vc[soa(p.EN, q, dst)] = src.S.vc[soa(src.en, q, j)];
+            for (int q = 0; q < L::VC; ++q) S.vc[soa<Lay<D>::VC>(q, dst)] = src.S.vc[soa<Lay<D>::VC>(q, j)];
 #pragma unroll
-            for (int q = 0; q < L::FF; ++q) S.f[soa(p.EN, q, dst)] = src.S.f[soa(src.en, q, j)];
+            for (int q = 0; q < L::FF; ++q) S.f[soa<Lay<D>::FF>(q, dst)] = src.S.f[soa<Lay<D>::FF>(q, j)];
             S.pid[dst] = src.S.pid[j];
             int b[3];
             if (base_cell<D>(p, x, b)) {
@@ -1745,14 +1745,13 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
 template <int D>
 __global__ void __launch_bounds__(kT) k_adj_pull(KParams p, AdjView Sb, const int* __restrict__ cnt,
                                                  const int* __restrict__ rows, int cap, AdjView nbl,
-                                                 const int* __restrict__ nbl_base, int64_t nbl_en, AdjView nbr,
-                                                 const int* __restrict__ nbr_base, int64_t nbr_en) {
+                                                 const int* __restrict__ nbl_base, AdjView nbr,
+                                                 const int* __restrict__ nbr_base) {
     pdl_begin();
     using L = Lay<D>;
     const int dir = blockIdx.y;  // 0: emigrants to the left neighbour, 1: to the right
     const AdjView& nb = dir == 0 ? nbl : nbr;
     const int* nbase = dir == 0 ? nbl_base : nbr_base;
-    const int64_t en = dir == 0 ? nbl_en : nbr_en;
     if (!nbase) return;
     const int n = min(cnt[dir], cap);
     const int m = blockIdx.x * kT + threadIdx.x;
@@ -1760,11 +1759,11 @@ __global__ void __launch_bounds__(kT) k_adj_pull(KParams p, AdjView Sb, const in
     const int j = rows[dir * cap + m];
     const int64_t src = (int64_t)nbase[dir == 0 ? 1 : 0] + m;  // we are the neighbour's right / left side
 #pragma unroll
-    for (int k = 0; k < D; ++k) Sb.x[soa(p.EN, k, j)] = nb.x[soa(en, k, src)];
+    for (int k = 0; k < D; ++k) Sb.x[soa<Lay<D>::X>(k, j)] = nb.x[soa<Lay<D>::X>(k, src)];
 #pragma unroll
-    for (int q = 0; q < L::VC; ++q) Sb.vc[soa(p.EN, q, j)] = nb.vc[soa(en, q, src)];
+    for (int q = 0; q < L::VC; ++q) Sb.vc[soa<Lay<D>::VC>(q, j)] = nb.vc[soa<Lay<D>::VC>(q, src)];
 #pragma unroll
-    for (int q = 0; q < L::FF; ++q) Sb.f[soa(p.EN, q, j)] = nb.f[soa(en, q, src)];
+    for (int q = 0; q < L::FF; ++q) Sb.f[soa<Lay<D>::FF>(q, j)] = nb.f[soa<Lay<D>::FF>(q, src)];
 }
 
 // per-block sums of x over the rows S_T holds for the blocks of step T-1 (sorted order, fixed
@@ -1784,7 +1783,7 @@ __global__ void __launch_bounds__(kT) k_block_com(KParams p, SlotView sl, const 
         float acc[3] = {0.f, 0.f, 0.f};
         for (int r = lane; r < nvalid; r += 32)
 #pragma unroll
-            for (int k = 0; k < D; ++k) acc[k] += X[soa(p.EN, k, start + r)];
+            for (int k = 0; k < D; ++k) acc[k] += X[soa<Lay<D>::X>(k, start + r)];
 #pragma unroll
         for (int k = 0; k < D; ++k) {
 #pragma unroll
@@ -1990,11 +1989,11 @@ void launch_immigrate(const KParams& p, const StateView& S, const int* nsorted, 
                              bcount, imm_base, nrows, flags));
 }
 void launch_adj_pull(const KParams& p, const AdjView& Sb, const int* cnt, const int* rows, int cap,
-                     const AdjView& nb_left, const int* nb_left_base, int64_t nb_left_en, const AdjView& nb_right,
-                     const int* nb_right_base, int64_t nb_right_en, cudaStream_t s) {
+                     const AdjView& nb_left, const int* nb_left_base, const AdjView& nb_right,
+                     const int* nb_right_base, cudaStream_t s) {
     const dim3 grid((unsigned)((cap + kT - 1) / kT), 2);
     DISPATCH(p.dim, launch_k(k_adj_pull<DIM>, grid, kT, 0, s, p, Sb, cnt, rows, cap, nb_left, nb_left_base,
-                             nb_left_en, nb_right, nb_right_base, nb_right_en));
+                             nb_right, nb_right_base));
 }
 void launch_block_com(const KParams& p, const SlotView& sl_last, const float* x, float* part, cudaStream_t s) {
     const int grid = (int)std::min<int64_t>(((int64_t)p.step_blocks + kW - 1) / kW, (int64_t)tab().sms * 8);

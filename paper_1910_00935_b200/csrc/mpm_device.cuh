@@ -53,17 +53,24 @@ template <int D> struct Geo {
 // (kernels_tile.cu item_split); sizes the per-item actuator-gradient partials
 constexpr int kMaxSplit = 4;
 
-// State layout: three component-major (SoA) arrays per
-// state -- component k of particle i at ptr[k * EN + i] -- so a warp's access to one
-// component of consecutive particles is one contiguous segment, and a kernel that
-// needs only x (g2p, g2p_grad, binning, loss) reads 4d bytes per particle.
+// State layout: three arrays per state (x; v and C; F), each
+// AoSoA with 32-particle tiles -- component k of particle i at
+// ptr[((i / 32) * NC + k) * 32 + i % 32] for an array of NC components -- so a warp's access
+// to one component of 32 consecutive particles is one contiguous 128-B segment (as
+// component-major SoA), a kernel that needs only x reads 4d bytes per particle, and all
+// components of a particle sit at compile-time offsets (k * 128 B) from one address: one
+// address computation per particle and array instead of one 64-bit add per component.
+// Capacities are rounded up to whole tiles (kTile particles).
+constexpr int kTile = 32;
 template <int D> struct Lay {
-    static constexpr int X = D;           // x        [d][n]
-    static constexpr int VC = D + D * D;  // (v, C)   [d + d^2][n]   (v first, C row-major)
-    static constexpr int FF = D * D;      // F        [d^2][n]       row-major
+    static constexpr int X = D;           // x        d components
+    static constexpr int VC = D + D * D;  // (v, C)   d + d^2 (v first, C row-major)
+    static constexpr int FF = D * D;      // F        d^2, row-major
 };
-// element (component k, particle i) of a component-major array with n particles
-__device__ __forceinline__ int64_t soa(int64_t n, int k, int64_t i) { return (int64_t)k * n + i; }
+// element (component k, particle i) of an AoSoA-32 array with NC components
+template <int NC> __device__ __forceinline__ int64_t soa(int k, int64_t i) {
+    return (int64_t)(uint32_t)(i >> 5) * (NC * kTile) + k * kTile + (int)(i & (kTile - 1));
+}
 
 // Programmatic dependent launch (sm_90+): every kernel is launched with programmatic stream
 // serialization allowed (launch_k in kernels.h), waits for its predecessor grid's results as
