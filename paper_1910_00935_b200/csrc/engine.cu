@@ -101,6 +101,9 @@ KParams kparams(const mpm_ctx* h) {
     k.n_body = h->dd ? h->n_body : h->N;
     k.x_lo = h->dd ? h->x_lo : 0;
     k.x_hi = h->dd ? h->x_hi : k.nb;
+    const bool fast = k.TB < (1 << 22);  // divq's exact range
+    k.inv_nb = fast ? 1.0f / (float)k.nb : 0.0f;
+    k.inv_nbe = fast ? 1.0f / (float)k.nbe : 0.0f;
     return k;
 }
 
@@ -148,19 +151,20 @@ size_t carve(mpm_ctx* h, char* base) {
     };
     // AoSoA state arrays (mpm_device.cuh soa<NC>): whole 32-particle tiles
     const size_t ENT = (EN + kTile - 1) / kTile * kTile;
+    const size_t px = d, pvc = d + d * d, pf = d * d;
     auto state = [&]() {
         StateView s;
-        s.x = (float*)take(sizeof(float) * ENT * d);
-        s.vc = (float*)take(sizeof(float) * ENT * (d + d * d));
-        s.f = (float*)take(sizeof(float) * ENT * d * d);
+        s.x = (float*)take(sizeof(float) * ENT * px);
+        s.vc = (float*)take(sizeof(float) * ENT * pvc);
+        s.f = (float*)take(sizeof(float) * ENT * pf);
         s.pid = (int*)take(sizeof(int) * EN);
         return s;
     };
     auto adj = [&]() {
         AdjView s;
-        s.x = (float*)take(sizeof(float) * ENT * d);
-        s.vc = (float*)take(sizeof(float) * ENT * (d + d * d));
-        s.f = (float*)take(sizeof(float) * ENT * d * d);
+        s.x = (float*)take(sizeof(float) * ENT * px);
+        s.vc = (float*)take(sizeof(float) * ENT * pvc);
+        s.f = (float*)take(sizeof(float) * ENT * pf);
         return s;
     };
     std::vector<StateView> ckpt, window;
@@ -168,7 +172,9 @@ size_t carve(mpm_ctx* h, char* base) {
     for (int i = 0; i < 2 * kk; ++i) window.push_back(i % kk == 0 ? StateView{nullptr, nullptr, nullptr, nullptr} : state());
     StateView fin = state();
     const int Tm = p.max_steps;
-    int* sigma_store = (int*)take(sizeof(int) * EN * Tm);
+    // per-step sorted lists at a whole-tile stride: every step's list is 128-B aligned, so the
+    // thread-per-particle kernels can bulk-copy (cp.async.bulk) a block's segment of it
+    int* sigma_store = (int*)take(sizeof(int) * ENT * Tm);
     unsigned char* scell0 = (unsigned char*)take(EN);
     unsigned char* scell1 = (unsigned char*)take(EN);
     int* spid0 = (int*)take(sizeof(int) * EN);
@@ -185,7 +191,7 @@ size_t carve(mpm_ctx* h, char* base) {
     float* staging = (float*)take(sizeof(float) * sf);
     int32_t* aid = (int32_t*)take(sizeof(int32_t) * EN);
     int32_t* mat = (int32_t*)take(sizeof(int32_t) * std::max<size_t>(EN, (size_t)h->n_body));  // by particle id
-    float* xbar_part = (float*)take(sizeof(float) * ENT * h->dim);
+    float* xbar_part = (float*)take(sizeof(float) * ENT * px);
     int* bcount = (int*)take(sizeof(int) * k.TB);
     int* cursor = (int*)take(sizeof(int) * k.TB);
     int* scan_part = (int*)take(sizeof(int64_t) * (scan_chunks(k) + 2));  // chunk totals, epoch, ticket
@@ -255,7 +261,7 @@ SlotView slot_at(mpm_ctx* h, int t) {
     const KParams k = kparams(h);
     const size_t EN = (size_t)k.E * k.N;
     SlotView s;
-    s.sigma = h->sigma_store + EN * t;
+    s.sigma = h->sigma_store + (EN + kTile - 1) / kTile * kTile * t;
     s.scell = h->scell_ring[t & 1];
     s.spid = h->spid_ring[t & 1];
     s.blist = h->blist_pool;

@@ -398,12 +398,12 @@ __global__ void k_seed(KParams p, const float* __restrict__ seed, AdjView Sb) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= p.N * p.E) return;
     const int64_t e = i / p.N;
+    float xs[3] = {0.f, 0.f, 0.f}, z[Lay<D>::VC] = {};
 #pragma unroll
-    for (int k = 0; k < D; ++k) Sb.x[soa<Lay<D>::X>(k, i)] = seed[e * D + k];
-#pragma unroll
-    for (int q = 0; q < Lay<D>::VC; ++q) Sb.vc[soa<Lay<D>::VC>(q, i)] = 0.0f;
-#pragma unroll
-    for (int q = 0; q < Lay<D>::FF; ++q) Sb.f[soa<Lay<D>::FF>(q, i)] = 0.0f;
+    for (int k = 0; k < D; ++k) xs[k] = seed[e * D + k];
+    store_comps<Lay<D>::X>(Sb.x, i, xs);
+    store_comps<Lay<D>::VC>(Sb.vc, i, z);
+    store_comps<Lay<D>::FF>(Sb.f, i, z);
 }
 
 // ------------------------------------------------------------- layout
@@ -417,16 +417,20 @@ __global__ void k_pack(KParams p, const float* __restrict__ x, const float* __re
     if (i >= p.N * p.E) return;
     if (ident_pid) ident_pid[i] = (int)i;
     const int64_t s = src ? (int64_t)src[i] : i;
+    float xo[3], vco[Lay<D>::VC], fo[D * D];
 #pragma unroll
     for (int k = 0; k < D; ++k) {
-        dx[soa<Lay<D>::X>(k, i)] = x ? x[s * D + k] : 0.0f;
-        dvc[soa<Lay<D>::VC>(k, i)] = v ? v[s * D + k] : 0.0f;
+        xo[k] = x ? x[s * D + k] : 0.0f;
+        vco[k] = v ? v[s * D + k] : 0.0f;
     }
 #pragma unroll
     for (int q = 0; q < D * D; ++q) {
-        dvc[soa<Lay<D>::VC>(D + q, i)] = C ? C[s * D * D + q] : 0.0f;
-        df[soa<Lay<D>::FF>(q, i)] = F ? F[s * D * D + q] : ((!zero_f && (q % (D + 1)) == 0) ? 1.0f : 0.0f);
+        vco[D + q] = C ? C[s * D * D + q] : 0.0f;
+        fo[q] = F ? F[s * D * D + q] : ((!zero_f && (q % (D + 1)) == 0) ? 1.0f : 0.0f);
     }
+    store_comps<Lay<D>::X>(dx, i, xo);
+    store_comps<Lay<D>::VC>(dvc, i, vco);
+    store_comps<Lay<D>::FF>(df, i, fo);
 }
 
 template <int D>

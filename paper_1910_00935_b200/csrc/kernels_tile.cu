@@ -33,8 +33,24 @@ constexpr int kT = 256;  // threads per CTA (8 warps)
 constexpr int kW = kT / 32;
 
 // block id -> episode and first cell (c0 = block coords * B)
-template <int D>
+// FAST (the per-node grid passes, where this runs once per node): divisions by a float
+// reciprocal (divq); the per-block callers keep the integer division (their register
+// allocation is tuned around it)
+template <int D, bool FAST = false>
 __device__ __forceinline__ void block_origin(const KParams& p, int bid, int& e, int c0[3]) {
+    if (FAST) {
+        e = divq(bid, p.nbe, p.inv_nbe);
+        int l = bid - e * p.nbe;
+        c0[2] = 0;
+#pragma unroll
+        for (int k = D - 1; k >= 1; --k) {
+            const int q = divq(l, p.nb, p.inv_nb);
+            c0[k] = (l - q * p.nb) * Geo<D>::B;
+            l = q;
+        }
+        c0[0] = l * Geo<D>::B;  // l < nb here
+        return;
+    }
     e = bid / p.nbe;
     int l = bid - e * p.nbe;
     c0[2] = 0;
@@ -92,7 +108,9 @@ __device__ __forceinline__ float4 covered_sum(const KParams& p, int e, const int
                                               const float4* nt0, const float4* nt1) {
     using G = Geo<D>;
     // per axis: option 0 = the block holding g (local l0), option 1 = the previous
-    // block (local l0 + B), valid when l0 < 2.  All 2^d combinations unrolled.
+    // block (local l0 + B), valid when l0 < 2.  All 2^d combinations unrolled.  (A
+    // branch-free form issuing all 2^d map loads, then all tile loads, measured slower:
+    // grid_op 34.8 -> 36.8 ms per C5 iteration -- the branches skip the absent blocks' loads.)
     int b0[3], l0[3];
     bool ok1[3];
 #pragma unroll
@@ -180,6 +198,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     } while (!ok);
 }
 
+// second bulk copy onto the same mbarrier (the expected bytes were announced by bulk_load's caller)
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // Double-buffered node-tile pipeline of a persistent CTA: tile(bi) of `src` is copied
 // into buf[it & 1] while the CTA works on the previous block.  Call init() once
 // (before a __syncthreads), start() before the loop, next() at the top of iteration
@@ -210,6 +236,54 @@ template <int D> struct TilePipe {
         mbar_wait(bar + cb, (uint32_t)((it >> 1) & 1));
         return buf + cb * Geo<D>::TN;
     }
+};
+
+// The same pipeline plus the block's segment of the sorted list sigma (entries
+// [bstart[bi], bstart[bi + 1]) widened to 16-B boundaries) on the same mbarrier, so the
+// particle loads of the block need no dependent global load of sigma: entry r of the block
+// is sig_at(it, start)[r].  Blocks over MAXP particles (dropped by the binning, nvalid = 0)
+// copy no list.  (Measured: g2p 132 -> 123, the gather 101.5 -> 97.9 ms per C5 iteration;
+// p2g_grad slower with it, 171 -> 186, so it keeps TilePipe.)
+constexpr int kSigCap = 1728 + 8;  // MAXP + the widening, ints per buffer
+template <int D> struct SigPipe {
+    static constexpr uint32_t BYTES = Geo<D>::TN * sizeof(float4);
+    float4* buf;          // [2][TN]
+    uint64_t* bar;        // [2]
+    int* sig;             // [2][kSigCap]
+    const int* sigma;     // this step's sorted list (16-B aligned)
+    const int* bstart;    // this step's block starts
+    __device__ void init() {
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            mbar_init(bar + 1, 1);
+            fence_mbar_init();
+        }
+    }
+    __device__ void issue(const float4* src, int bi, int slot) {
+        const int s0 = bstart[bi], s1 = bstart[bi + 1];
+        const int a0 = s0 & ~3;
+        const uint32_t sb = s1 - s0 <= Geo<D>::MAXP ? (uint32_t)((((s1 + 3) & ~3) - a0) * 4) : 0u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + slot)),
+                     "r"(BYTES + sb)
+                     : "memory");
+        bulk_copy(buf + slot * Geo<D>::TN, src + (int64_t)bi * Geo<D>::TN, BYTES, bar + slot);
+        if (sb) bulk_copy(sig + slot * kSigCap, sigma + a0, sb, bar + slot);
+    }
+    __device__ void start(const float4* src, int bi, int nact) {
+        if (threadIdx.x == 0 && bi < nact) issue(src, bi, 0);
+    }
+    __device__ void next(const float4* src, int bi_next, int nact, int it) {
+        if (threadIdx.x == 0 && bi_next < nact) {
+            fence_proxy_async();
+            issue(src, bi_next, (it + 1) & 1);
+        }
+    }
+    __device__ float4* wait(int it) {
+        const int cb = it & 1;
+        mbar_wait(bar + cb, (uint32_t)((it >> 1) & 1));
+        return buf + cb * Geo<D>::TN;
+    }
+    __device__ const int* sig_at(int it, int start) const { return sig + (it & 1) * kSigCap + (start & 3); }
 };
 
 // Sub-block work split of the thread-per-particle kernels (g2p, g2p_grad's gather part, p2g_grad):
@@ -541,7 +615,9 @@ template <int D, bool MASS> struct SliceAcc {
             float mx[3] = {fmaf(fox, A[0], r2.y), fmaf(fox, A[3], r2.z), fmaf(fox, A[6], r2.w)};
 #pragma unroll
             for (int oy = 0; oy < 3; ++oy) {
-                float m[3] = {fmaf((float)oy, A[1], mx[0]), fmaf((float)oy, A[4], mx[1]), fmaf((float)oy, A[7], mx[2])};
+                // oy = 0: m = mx exactly (fmaf(0, a, b) = b for finite a), without the instructions
+                float m[3] = {oy ? fmaf((float)oy, A[1], mx[0]) : mx[0], oy ? fmaf((float)oy, A[4], mx[1]) : mx[1],
+                              oy ? fmaf((float)oy, A[7], mx[2]) : mx[2]};
 #pragma unroll
                 for (int oz = 0; oz < 3; ++oz) {
                     const float W = W0 * wyz[oy * 3 + oz];
@@ -554,9 +630,10 @@ template <int D, bool MASS> struct SliceAcc {
                 }
             }
         } else {
-            const float4 r0 = r4[0], r1 = r4[1], r2 = r4[2];
+            const float4 r0 = r4[0], r1 = r4[1];
             // [wy0 wy1 wy2 c0][c1 A00 A01 A10][A11 wx0 wx1 wx2]
-            const float W0 = ox == 0 ? r2.y : (ox == 1 ? r2.z : r2.w);
+            const float r2x = rw[8];
+            const float W0 = rw[9 + ox];
             const float wy[3] = {r0.x, r0.y, r0.z};
             float m[2] = {fmaf(fox, r1.y, r0.w), fmaf(fox, r1.w, r1.x)};
 #pragma unroll
@@ -566,7 +643,7 @@ template <int D, bool MASS> struct SliceAcc {
                 acc.x = fmaf(W, m[0], acc.x);
                 acc.y = fmaf(W, m[1], acc.y);
                 if (MASS) acc.w += W;
-                m[0] += r1.z; m[1] += r2.x;
+                m[0] += r1.z; m[1] += r2x;
             }
         }
     }
@@ -774,36 +851,45 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         // loads of chunk k+1 are issued before the accumulation of chunk k (same registers)
         SliceAcc<D, true> acc;
         acc.zero();
-        float x[3], vc[L::VC], F[L::FF];
-        int a_id = -1;
-        bool fluid = false;
-#define MPM_P2G_LOAD(R)                                                                          \
-    do {                                                                                         \
-        const int i_ = s_ci[(R)];                                                                 \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i_));      \
-        _Pragma("unroll") for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + soa<Lay<D>::VC>(q, i_)); \
-        _Pragma("unroll") for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + soa<Lay<D>::FF>(q, i_));  \
-        if (aid || p.mat) {                                                                       \
-            const int pd_ = __ldg(S.pid + i_);                                                    \
-            if (aid) a_id = __ldg(aid + pd_);                                                     \
-            if (p.mat) fluid = __ldg(p.mat + pd_) != 0;                                           \
-        }                                                                                         \
-    } while (0)
-        if (tid < nvalid) MPM_P2G_LOAD(tid);
+        // a thread's particle inputs (loading the next particle's before the current particle's
+        // math, a second register set, spills at the 96-register cap: measured slower)
+        struct In {
+            float x[3], vc[L::VC], F[L::FF];
+            int a_id;
+            bool fluid;
+        };
+        auto load = [&](In& d, int R) {
+            const int i_ = s_ci[R];
+            load_comps<L::X>(S.x, i_, d.x);
+            load_comps<L::VC>(S.vc, i_, d.vc);
+            load_comps<L::FF>(S.f, i_, d.F);
+            d.a_id = -1;
+            d.fluid = false;
+            if (aid || p.mat) {
+                const int pd_ = __ldg(S.pid + i_);
+                if (aid) d.a_id = __ldg(aid + pd_);
+                if (p.mat) d.fluid = __ldg(p.mat + pd_) != 0;
+            }
+        };
+        In cur;
+        if (tid < nvalid) load(cur, tid);
         for (int ch = 0; ch < nvalid; ch += kCH) {
             const int cend = min(nvalid, ch + kCH);
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
+                const bool more = r + kTQ < nvalid;
                 // ids outside [0, n_act) are passive here (mpm_set_state flags them as an error)
+                const int a_id = cur.a_id;
+                const bool fluid = cur.fluid;
                 const float act = (aid && a_id >= 0 && a_id < p.n_act) ? alpha[e * p.a_estride + a_id] : 0.0f;
                 float w[3][3], c[3], Adx[D * D], Ft[D * D];
-                if (!p2g_particle<D>(p, x, vc, F, act, fluid, c0, w, c, Adx, Ft)) atomicOr(flags, FLAG_NONFINITE);
+                if (!p2g_particle<D>(p, cur.x, cur.vc, cur.F, act, fluid, c0, w, c, Adx, Ft))
+                    atomicOr(flags, FLAG_NONFINITE);
                 write_row<D>(s_row + (r - ch) * RS, w, c, Adx);
                 if (Sn.f) {
                     if (fluid) fluid_reset<D>(Ft, Ft);  // R23 (Ft is dead after the row)
-#pragma unroll
-                    for (int q = 0; q < D * D; ++q) Sn.f[soa<Lay<D>::FF>(q, start + r)] = Ft[q];
+                    store_comps<L::FF>(Sn.f, start + r, Ft);
                 }
-                if (r + kTQ < nvalid) MPM_P2G_LOAD(r + kTQ);  // this thread's next particle
+                if (more) load(cur, r + kTQ);  // this thread's next particle
             }
             __syncthreads();
             if (tid < kACC) {
@@ -812,7 +898,6 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
             }
             __syncthreads();
         }
-#undef MPM_P2G_LOAD
         if (tid < kACC) acc.store(s_cb, my_cell, my_ox);  // the rows are dead after the last barrier
         __syncthreads();
         // ---- phase 3: node tile (plain stores)
@@ -840,13 +925,14 @@ __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
     const int* blist = sl.blist + b0;
     const float4* part_g = sl.part - (int64_t)b0 * G::TN;  // bmap holds pool indices
     float4* rt = sl.tiles + (int64_t)b0 * G::TN;
-    const int64_t total = (int64_t)nact * G::TN;
+    // 32-bit node index: a step's tiles (nact * TN float4) are far below 2^32 nodes in HBM
+    const unsigned total = (unsigned)nact * G::TN;
     const float4* nt0 = halo_tiles<D>(sl.halo, 0);
     const float4* nt1 = halo_tiles<D>(sl.halo, 1);
-    for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
-        const int bi = (int)(idx / G::TN), q = (int)(idx - (int64_t)bi * G::TN);
+    for (unsigned idx = blockIdx.x * kT + threadIdx.x; idx < total; idx += gridDim.x * kT) {
+        const int bi = (int)(idx / G::TN), q = (int)(idx - (unsigned)bi * G::TN);
         int e, c0[3], n[3];
-        block_origin<D>(p, __ldg(blist + bi), e, c0);
+        block_origin<D, true>(p, __ldg(blist + bi), e, c0);
         local_node<D>(q, n);
         const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
         const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
@@ -874,16 +960,16 @@ __global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, con
     const int* blist = sl.blist + b0;
     const float4* ub_g = ubar - (int64_t)b0 * G::TN;
     const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
-    const int64_t total = (int64_t)nact * G::TN;
+    const unsigned total = (unsigned)nact * G::TN;  // 32-bit node index (as grid_op)
     const float4* nt0 = halo_tiles<D>(sl.halo, 0);
     const float4* nt1 = halo_tiles<D>(sl.halo, 1);
-    for (int64_t idx = (int64_t)blockIdx.x * kT + threadIdx.x; idx < total; idx += (int64_t)gridDim.x * kT) {
+    for (unsigned idx = blockIdx.x * kT + threadIdx.x; idx < total; idx += gridDim.x * kT) {
         const float4 r = __ldg(rt + idx);
         float4 out = make_float4(0.f, 0.f, 0.f, 0.f);
         if (!signbit(r.w)) {
-            const int bi = (int)(idx / G::TN), q = (int)(idx - (int64_t)bi * G::TN);
+            const int bi = (int)(idx / G::TN), q = (int)(idx - (unsigned)bi * G::TN);
             int e, c0[3], n[3];
-            block_origin<D>(p, __ldg(blist + bi), e, c0);
+            block_origin<D, true>(p, __ldg(blist + bi), e, c0);
             local_node<D>(q, n);
             const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
             const float4 ub = covered_sum<D, HALO>(p, e, g, sl.bmap, ub_g, sl.halo, nt0, nt1);
@@ -961,30 +1047,27 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
     particle_weights<D>(p, x, c0, lb, fx, w, dw);
     float S0[3], Sb[3][3];
     gather_moments<D>(sU, lb, w, S0, Sb);
-    float xn[3];
+    float xn[3], vcn[L::VC];
     bool fin = true;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         xn[a] = fmaf(p.dt, S0[a], x[a]);
-        Sn.x[soa<Lay<D>::X>(a, j)] = xn[a];
-        Sn.vc[soa<Lay<D>::VC>(a, j)] = S0[a];
+        vcn[a] = S0[a];
         fin = fin && isfinite(S0[a]);
 #pragma unroll
-        for (int b = 0; b < D; ++b) Sn.vc[soa<Lay<D>::VC>(D + a * D + b, j)] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
+        for (int b = 0; b < D; ++b) vcn[D + a * D + b] = c4 * fmaf(-S0[a], fx[b], Sb[b][a]);
     }
+    store_comps<L::X>(Sn.x, j, xn);
+    store_comps<L::VC>(Sn.vc, j, vcn);
     if (!fin) atomicOr(flags, FLAG_NONFINITE);
     if (refwd) {  // re-forward from stored tiles: F_{t+1} and the particle id too
-        float C[D * D], F[D * D], Ft[D * D];
-#pragma unroll
-        for (int q = 0; q < D * D; ++q) {
-            C[q] = __ldg(S.vc + soa<Lay<D>::VC>(D + q, i));
-            F[q] = __ldg(S.f + soa<Lay<D>::FF>(q, i));
-        }
-        deform_update<D>(p.dt, C, F, Ft);
+        float vc[L::VC], F[D * D], Ft[D * D];
+        load_comps<L::VC>(S.vc, i, vc);
+        load_comps<L::FF>(S.f, i, F);
+        deform_update<D>(p.dt, vc + D, F, Ft);
         const int pd = __ldg(S.pid + i);
         if (p.mat && __ldg(p.mat + pd) != 0) fluid_reset<D>(Ft, Ft);  // R23
-#pragma unroll
-        for (int q = 0; q < D * D; ++q) Sn.f[soa<Lay<D>::FF>(q, j)] = Ft[q];
+        store_comps<L::FF>(Sn.f, j, Ft);
         Sn.pid[j] = pd;
     }
     int key = -1;
@@ -1024,6 +1107,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
     pdl_begin();
     using G = Geo<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
+    __shared__ __align__(16) int s_sig[2 * kSigCap];
     __shared__ __align__(8) uint64_t s_bar[2];
     const int tid = threadIdx.x;
     const int nact = *sl.nactive;
@@ -1032,7 +1116,7 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
     const int* bstart = sl.bstart + b0 + sl.step;
     unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<D>::CELLS + 1);
     const float4* rt = sl.tiles + (int64_t)b0 * Geo<D>::TN;
-    TilePipe<D> pipe{s_buf, s_bar};
+    SigPipe<D> pipe{s_buf, s_bar, s_sig, sl.sigma, bstart};
     pipe.init();
     __syncthreads();
     const int split = SPLIT ? item_split(nact, gridDim.x) : 1, nitems = nact * split;
@@ -1049,21 +1133,21 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
         else { rb = 0; re = nvalid; }
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        // particle loads of the first two passes go out before waiting for the tile
+        // the tile and the block's sigma segment arrive together; the particle loads of the
+        // first two passes go out before any math
+        const float4* sU = pipe.wait(it);
+        const int* sg = pipe.sig_at(it, start);
         float xa[3], xb[3];
         const bool va = rb + tid < re, vb = rb + tid + kTG < re;
         int ia = 0, ib = 0;
         if (va) {
-            ia = sl.sigma[start + rb + tid];
-#pragma unroll
-            for (int k = 0; k < D; ++k) xa[k] = __ldg(S.x + soa<Lay<D>::X>(k, ia));
+            ia = sg[rb + tid];
+            load_comps<Lay<D>::X>(S.x, ia, xa);
         }
         if (vb) {
-            ib = sl.sigma[start + rb + tid + kTG];
-#pragma unroll
-            for (int k = 0; k < D; ++k) xb[k] = __ldg(S.x + soa<Lay<D>::X>(k, ib));
+            ib = sg[rb + tid + kTG];
+            load_comps<Lay<D>::X>(S.x, ib, xb);
         }
-        const float4* sU = pipe.wait(it);
         int key = -1;
         if (va) key = g2p_particle<D>(p, sU, xa, c0, start + rb + tid, e, bid, Sn, keys, flags, refwd, S, ia, mg);
         if (keys) count_key(va && key >= 0, key, bcount);
@@ -1075,10 +1159,9 @@ __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S
             const bool in = r < re;
             key = -1;
             if (in) {
-                const int i = sl.sigma[start + r];
+                const int i = sg[r];
                 float x[3];
-#pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i));
+                load_comps<Lay<D>::X>(S.x, i, x);
                 key = g2p_particle<D>(p, sU, x, c0, start + r, e, bid, Sn, keys, flags, refwd, S, i, mg);
             }
             if (keys) count_key(in && key >= 0, key, bcount);
@@ -1212,15 +1295,14 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
         const int nvalid = cstart[(int64_t)bi * (G::CELLS + 1) + G::CELLS];
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        float x[3], xb[3], vbn[3], Cbn[D * D];
+        float x[3], xb[3], vbc[Lay<D>::VC];  // vbc: (vb', Cb') of S_bar_{t+1}
 #define MPM_G2PG_LOAD(R)                                                                      \
     do {                                                                                      \
         const int j_ = start + (R);                                                           \
         const int i_ = sl.sigma[j_];                                                          \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i_));   \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) xb[k] = __ldg(Sbn.x + soa<Lay<D>::X>(k, j_)); \
-        _Pragma("unroll") for (int k = 0; k < D; ++k) vbn[k] = __ldg(Sbn.vc + soa<Lay<D>::VC>(k, j_)); \
-        _Pragma("unroll") for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + soa<Lay<D>::VC>(D + q, j_)); \
+        load_comps<Lay<D>::X>(S.x, i_, x);                                                    \
+        load_comps<Lay<D>::X>(Sbn.x, j_, xb);                                                 \
+        load_comps<Lay<D>::VC>(Sbn.vc, j_, vbc);                                              \
     } while (0)
         if (tid < nvalid) MPM_G2PG_LOAD(tid);
         for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
@@ -1231,7 +1313,7 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
             const int cend = min(nvalid, ch + kCH);
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
                 float w[3][3], cp[3], B[D * D];
-                g2pg_row<D>(p, x, xb, vbn, Cbn, c0, w, cp, B);
+                g2pg_row<D>(p, x, xb, vbc, vbc + D, c0, w, cp, B);
                 write_row<D>(s_row + (r - ch) * RS, w, cp, B);
                 if (r + kTQ < nvalid) MPM_G2PG_LOAD(r + kTQ);  // this thread's next particle
             }
@@ -1263,6 +1345,7 @@ __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParam
     pdl_begin();
     using G = Geo<D>;
     __shared__ __align__(128) float4 s_buf[2 * G::TN];
+    __shared__ __align__(16) int s_sig[2 * kSigCap];
     __shared__ __align__(8) uint64_t s_bar[2];
     const int tid = threadIdx.x;
     const int nact = *sl.nactive;
@@ -1271,7 +1354,7 @@ __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParam
     const int* bstart = sl.bstart + b0 + sl.step;
     const unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
     const float4* rt = sl.tiles + (int64_t)b0 * G::TN;
-    TilePipe<D> pipe{s_buf, s_bar};
+    SigPipe<D> pipe{s_buf, s_bar, s_sig, sl.sigma, bstart};
     pipe.init();
     __syncthreads();
     const int split = SPLIT ? item_split(nact, gridDim.x) : 1, nitems = nact * split;
@@ -1287,32 +1370,25 @@ __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParam
         else { rb = 0; re = nvalid; }
         int e, c0[3];
         block_origin<D>(p, blist[bi], e, c0);
-        const float4* sU = nullptr;
-        if (rb >= re) pipe.wait(it);
+        const float4* sU = pipe.wait(it);  // tile and sigma segment
+        const int* sg = pipe.sig_at(it, start);
         for (int r0 = rb; r0 < re; r0 += kTG) {
             const int r = r0 + tid;
             const bool in = r < re;
-            float x[3], xb[3], vbn[3], Cbn[D * D];
+            float x[3], xb[3], vbc[Lay<D>::VC];  // vbc: (vb', Cb') of S_bar_{t+1}
             const int j = start + r;
             if (in) {
-                const int i = sl.sigma[j];
-#pragma unroll
-                for (int k = 0; k < D; ++k) {
-                    x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i));
-                    xb[k] = __ldg(Sbn.x + soa<Lay<D>::X>(k, j));
-                    vbn[k] = __ldg(Sbn.vc + soa<Lay<D>::VC>(k, j));
-                }
-#pragma unroll
-                for (int q = 0; q < D * D; ++q) Cbn[q] = __ldg(Sbn.vc + soa<Lay<D>::VC>(D + q, j));
+                const int i = sg[r];
+                load_comps<Lay<D>::X>(S.x, i, x);
+                load_comps<Lay<D>::X>(Sbn.x, j, xb);
+                load_comps<Lay<D>::VC>(Sbn.vc, j, vbc);
             }
-            if (r0 == rb) sU = pipe.wait(it);
             if (in) {
                 int lb[3];
                 float fx[3], wt[3][3], dw[3][3], xo[3];
                 particle_weights<D>(p, x, c0, lb, fx, wt, dw);
-                g2pg_gather<D>(p, sU, lb, fx, wt, dw, xb, vbn, Cbn, xo);
-#pragma unroll
-                for (int k = 0; k < D; ++k) xbp[soa<Lay<D>::X>(k, j)] = xo[k];
+                g2pg_gather<D>(p, sU, lb, fx, wt, dw, xb, vbc, vbc + D, xo);
+                store_comps<Lay<D>::X>(xbp, j, xo);
             }
         }
         __syncthreads();
@@ -1484,6 +1560,7 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
     if (fluid) fluid_reset_adj<D>(Ft, Fbn, Ftb);  // R23: F_{t+1} = J^(1/d) I
     const float abar = kirchhoff_adj<D>(p, Ft, has_act, act, taub, Ftb, fluid);
     bool fin = true;
+    float fo[D * D], vco[L::VC], xo[3];
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -1494,15 +1571,18 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
                 sF = fmaf(p.dt * C[k * D + a], Ftb[k * D + b], sF);
                 sC = fmaf(Ftb[a * D + k], F[b * D + k], sC);
             }
-            Sb.f[soa<Lay<D>::FF>(a * D + b, i)] = sF;
-            Sb.vc[soa<Lay<D>::VC>(D + a * D + b, i)] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
+            fo[a * D + b] = sF;
+            vco[D + a * D + b] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
             fin = fin && isfinite(sF);
         }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        Sb.x[soa<Lay<D>::X>(a, i)] = fmaf(p.inv_dx, fb[a], xbp[a]);
-        Sb.vc[soa<Lay<D>::VC>(a, i)] = p.p_mass * S0[a];
+        xo[a] = fmaf(p.inv_dx, fb[a], xbp[a]);
+        vco[a] = p.p_mass * S0[a];
     }
+    store_comps<L::FF>(Sb.f, i, fo);
+    store_comps<L::VC>(Sb.vc, i, vco);
+    store_comps<L::X>(Sb.x, i, xo);
     if (!fin) atomicOr(flags, FLAG_NONFINITE);
     return abar;
 }
@@ -1549,39 +1629,45 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
         __syncwarp();
         const float4* sG = nullptr;
         if (rb >= re) pipe.wait(it);
-        for (int r0 = rb; r0 < re; r0 += kTP) {
-            const int r = r0 + tid;
-            const bool in = r < re;
-            // particle loads go out before the (first pass's) tile staging
+        // a thread's particle inputs of one pass (loading the next pass's before this pass's math,
+        // with two register sets at 3 CTAs per SM, measured slower: 177 -> 187 ms per C5 iteration)
+        struct In {
             float x[3], vc[L::VC], F[L::FF], Fbn[L::FF], xb[3];
-            int64_t i = 0;
-            int a_id = -1;
-            bool fluid = false;
-            if (in) {
+            int64_t i;
+            int a_id;
+            bool fluid, in;
+        };
+        auto load = [&](In& d, int r) {
+            d.in = r < re;
+            d.i = 0;
+            d.a_id = -1;
+            d.fluid = false;
+            if (d.in) {
                 const int j = start + r;
-                i = sl.sigma[j];
-#pragma unroll
-                for (int k = 0; k < D; ++k) x[k] = __ldg(S.x + soa<Lay<D>::X>(k, i));
-#pragma unroll
-                for (int q = 0; q < L::VC; ++q) vc[q] = __ldg(S.vc + soa<Lay<D>::VC>(q, i));
-#pragma unroll
-                for (int q = 0; q < L::FF; ++q) F[q] = __ldg(S.f + soa<Lay<D>::FF>(q, i));
-#pragma unroll
-                for (int q = 0; q < L::FF; ++q) Fbn[q] = __ldg(Sbn.f + soa<Lay<D>::FF>(q, j));
-#pragma unroll
-                for (int k = 0; k < D; ++k) xb[k] = __ldg(xbp + soa<Lay<D>::X>(k, j));
+                d.i = sl.sigma[j];
+                load_comps<L::X>(S.x, d.i, d.x);
+                load_comps<L::VC>(S.vc, d.i, d.vc);
+                load_comps<L::FF>(S.f, d.i, d.F);
+                load_comps<L::FF>(Sbn.f, j, d.Fbn);
+                load_comps<L::X>(xbp, j, d.xb);
                 if (aid || p.mat) {
-                    const int pd = __ldg(S.pid + i);
-                    if (aid) a_id = __ldg(aid + pd);
-                    if (p.mat) fluid = __ldg(p.mat + pd) != 0;
+                    const int pd = __ldg(S.pid + d.i);
+                    if (aid) d.a_id = __ldg(aid + pd);
+                    if (p.mat) d.fluid = __ldg(p.mat + pd) != 0;
                 }
             }
+        };
+        In cur;
+        for (int r0 = rb; r0 < re; r0 += kTP) {
+            load(cur, r0 + tid);  // particle loads go out before the (first pass's) tile staging
             if (r0 == rb) sG = pipe.wait(it);
             float abar = 0.0f;
-            if (in) {
+            int a_id = cur.a_id;
+            if (cur.in) {
                 const bool has_act = aid && a_id >= 0 && a_id < p.n_act;
-                abar = p2g_grad_particle<D>(p, sG, x, vc, F, Fbn, xb, has_act,
-                                            has_act ? alpha[e * p.a_estride + a_id] : 0.0f, fluid, c0, i, Sb, flags);
+                abar = p2g_grad_particle<D>(p, sG, cur.x, cur.vc, cur.F, cur.Fbn, cur.xb, has_act,
+                                            has_act ? alpha[e * p.a_estride + a_id] : 0.0f, cur.fluid, c0, cur.i,
+                                            Sb, flags);
                 if (!has_act) a_id = -1;
             }
             if (p.n_act > 0) {  // per-actuator warp sums (fixed butterfly) into the warp's slot
@@ -1683,6 +1769,14 @@ __global__ void __launch_bounds__(kT) k_count_active(KParams p, SlotView sl, uns
 // S_{t+1} (peer memory), bin key + histogram of step t+1.  blockIdx.y = side (0 left, 1 right).
 // The immigrants' storage order follows the outbox (atomic) order; no sum depends on it (every
 // block list is canonicalised by (cell, particle id)).
+// row j of an AoSoA array (src, possibly a peer's memory) -> row dst (plain loads: the
+// neighbour wrote it in an earlier kernel of its own stream, ordered by events)
+template <int NC>
+__device__ __forceinline__ void copy_comps(float* dstb, int64_t dst, const float* srcb, int64_t j) {
+#pragma unroll
+    for (int k = 0; k < NC; ++k) dstb[soa<NC>(k, dst)] = srcb[soa<NC>(k, j)];
+}
+
 template <int D>
 __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const int* __restrict__ nsorted,
                                                   MigSrc left, MigSrc right, int x_lo, int x_hi, int cap,
@@ -1709,16 +1803,13 @@ __global__ void __launch_bounds__(kT) k_immigrate(KParams p, StateView S, const 
         if (dst >= p.N) {
             atomicOr(flags, FLAG_MIGRATION);  // capacity of this subdomain exceeded
         } else {
+            // the rows from the neighbour's memory
+            copy_comps<L::X>(S.x, dst, src.S.x, j);
+            copy_comps<L::VC>(S.vc, dst, src.S.vc, j);
+            copy_comps<L::FF>(S.f, dst, src.S.f, j);
             float x[3];
 #pragma unroll
-            for (int k = 0; k < D; ++k) {
-                x[k] = src.S.x[soa<Lay<D>::X>(k, j)];
-                S.x[soa<Lay<D>::X>(k, dst)] = x[k];
-            }
-#pragma unroll
-            for (int q = 0; q < L::VC; ++q) S.vc[soa<Lay<D>::VC>(q, dst)] = src.S.vc[soa<Lay<D>::VC>(q, j)];
-#pragma unroll
-            for (int q = 0; q < L::FF; ++q) S.f[soa<Lay<D>::FF>(q, dst)] = src.S.f[soa<Lay<D>::FF>(q, j)];
+            for (int k = 0; k < D; ++k) x[k] = S.x[soa<L::X>(k, dst)];
             S.pid[dst] = src.S.pid[j];
             int b[3];
             if (base_cell<D>(p, x, b)) {
@@ -1758,12 +1849,9 @@ __global__ void __launch_bounds__(kT) k_adj_pull(KParams p, AdjView Sb, const in
     if (m >= n) return;
     const int j = rows[dir * cap + m];
     const int64_t src = (int64_t)nbase[dir == 0 ? 1 : 0] + m;  // we are the neighbour's right / left side
-#pragma unroll
-    for (int k = 0; k < D; ++k) Sb.x[soa<Lay<D>::X>(k, j)] = nb.x[soa<Lay<D>::X>(k, src)];
-#pragma unroll
-    for (int q = 0; q < L::VC; ++q) Sb.vc[soa<Lay<D>::VC>(q, j)] = nb.vc[soa<Lay<D>::VC>(q, src)];
-#pragma unroll
-    for (int q = 0; q < L::FF; ++q) Sb.f[soa<Lay<D>::FF>(q, j)] = nb.f[soa<Lay<D>::FF>(q, src)];
+    copy_comps<L::X>(Sb.x, j, nb.x, src);
+    copy_comps<L::VC>(Sb.vc, j, nb.vc, src);
+    copy_comps<L::FF>(Sb.f, j, nb.f, src);
 }
 
 // per-block sums of x over the rows S_T holds for the blocks of step T-1 (sorted order, fixed

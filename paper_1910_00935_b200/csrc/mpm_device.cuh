@@ -31,7 +31,19 @@ struct KParams {
     int64_t n_body;      // particles of one whole body (episode): N, or the total over the
                          // subdomains of a decomposed body (f3; N is then a subdomain's capacity)
     int32_t x_lo, x_hi;  // owned block x-index range (f3 subdomain); single domain: [0, nb)
+    float inv_nb, inv_nbe;  // 1/nb, 1/nbe for divq (0 when block ids reach 2^22: exact division)
 };
+
+// floor(n / d) for 0 <= n < 2^22 by a float reciprocal (inv = fl(1/d)) and one correction step:
+// |n * inv - n / d| < 2^22 * 2^-23 < 1/2 before the truncation, so q is off by at most one.
+// inv == 0 falls back to the integer division.
+__device__ __forceinline__ int divq(int n, int d, float inv) {
+    if (inv == 0.0f) return n / d;
+    int q = __float2int_rz(__int2float_rn(n) * inv);
+    const int r = n - q * d;
+    q += (r >= d) - (r < 0);
+    return q;
+}
 
 enum : int { FLAG_OUT_OF_DOMAIN = 1, FLAG_NONFINITE = 2, FLAG_BLOCK_OVERFLOW = 4, FLAG_ACTIVE_OVERFLOW = 8,
              FLAG_BAD_ACTUATOR = 16,
@@ -60,7 +72,9 @@ constexpr int kMaxSplit = 4;
 // component-major SoA), a kernel that needs only x reads 4d bytes per particle, and all
 // components of a particle sit at compile-time offsets (k * 128 B) from one address: one
 // address computation per particle and array instead of one 64-bit add per component.
-// Capacities are rounded up to whole tiles (kTile particles).
+// Capacities are rounded up to whole tiles (kTile particles).  (A float4-quad variant --
+// NQ = ceil(NC/4) 16-B accesses per particle, pads included -- halved the load instructions
+// but measured slower: C5 2.91e9 -> 2.80e9, g2p 134 -> 157 ms per iteration.)
 constexpr int kTile = 32;
 template <int D> struct Lay {
     static constexpr int X = D;           // x        d components
@@ -70,6 +84,17 @@ template <int D> struct Lay {
 // element (component k, particle i) of an AoSoA-32 array with NC components
 template <int NC> __device__ __forceinline__ int64_t soa(int k, int64_t i) {
     return (int64_t)(uint32_t)(i >> 5) * (NC * kTile) + k * kTile + (int)(i & (kTile - 1));
+}
+// all NC components of particle i (read-only path) / stores
+template <int NC> __device__ __forceinline__ void load_comps(const float* __restrict__ base, int64_t i, float* v) {
+    const float* b = base + soa<NC>(0, i);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) v[k] = __ldg(b + k * kTile);
+}
+template <int NC> __device__ __forceinline__ void store_comps(float* __restrict__ base, int64_t i, const float* v) {
+    float* b = base + soa<NC>(0, i);
+#pragma unroll
+    for (int k = 0; k < NC; ++k) b[k * kTile] = v[k];
 }
 
 // Programmatic dependent launch (sm_90+): every kernel is launched with programmatic stream
