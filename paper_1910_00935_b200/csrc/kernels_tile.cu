@@ -1406,7 +1406,7 @@ template <int D>
 __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float4* __restrict__ sG,
                                                    const float* x, const float* vc, const float* F,
                                                    const float* Fbn, const float* xbp, bool has_act,
-                                                   float act, bool fluid, const int c0[3], int64_t i,
+                                                   float act, bool fluid, const int c0[3], int i,
                                                    const AdjView& Sb, int* flags) {
     using L = Lay<D>;
     const float* v = vc;
@@ -1560,7 +1560,8 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
     if (fluid) fluid_reset_adj<D>(Ft, Fbn, Ftb);  // R23: F_{t+1} = J^(1/d) I
     const float abar = kirchhoff_adj<D>(p, Ft, has_act, act, taub, Ftb, fluid);
     bool fin = true;
-    float fo[D * D], vco[L::VC], xo[3];
+    // stores interleaved with the arithmetic (whole-row stores at the end keep 24 more values
+    // live at the 128-register cap)
 #pragma unroll
     for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -1571,18 +1572,15 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
                 sF = fmaf(p.dt * C[k * D + a], Ftb[k * D + b], sF);
                 sC = fmaf(Ftb[a * D + k], F[b * D + k], sC);
             }
-            fo[a * D + b] = sF;
-            vco[D + a * D + b] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
+            Sb.f[soa<L::FF>(a * D + b, i)] = sF;
+            Sb.vc[soa<L::VC>(D + a * D + b, i)] = fmaf(p.dt, sC, p.p_mass * Ab[a * D + b]);
             fin = fin && isfinite(sF);
         }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        xo[a] = fmaf(p.inv_dx, fb[a], xbp[a]);
-        vco[a] = p.p_mass * S0[a];
+        Sb.x[soa<L::X>(a, i)] = fmaf(p.inv_dx, fb[a], xbp[a]);
+        Sb.vc[soa<L::VC>(a, i)] = p.p_mass * S0[a];
     }
-    store_comps<L::FF>(Sb.f, i, fo);
-    store_comps<L::VC>(Sb.vc, i, vco);
-    store_comps<L::X>(Sb.x, i, xo);
     if (!fin) atomicOr(flags, FLAG_NONFINITE);
     return abar;
 }
@@ -1633,7 +1631,7 @@ __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, Slot
         // with two register sets at 3 CTAs per SM, measured slower: 177 -> 187 ms per C5 iteration)
         struct In {
             float x[3], vc[L::VC], F[L::FF], Fbn[L::FF], xb[3];
-            int64_t i;
+            int i;  // row of S_t (state rows are < 2^31)
             int a_id;
             bool fluid, in;
         };
