@@ -354,8 +354,11 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
         launch_ctrl_obs_fwd(k, h->theta, t, h->obs_part, h->obs + (size_t)t * k.E * no, h->obs_cnt,
                             const_cast<float*>(alpha_at(h, t)), h->stream);
     }
-    { KScope sc(h, KC_CANON); launch_canon(k, sl, Sn.pid, bin_next ? h->keys : nullptr, h->flags, h->stream); }
-    { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), h->flags, h->stream); }
+    if (!canon_fused()) {
+        KScope sc(h, KC_CANON);
+        launch_canon(k, sl, Sn.pid, bin_next ? h->keys : nullptr, h->flags, h->stream);
+    }
+    { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), bin_next ? h->keys : nullptr, h->flags, h->stream); }
     { KScope sc(h, KC_GRID_OP); launch_grid_op(k, sl, h->stream); }
     if (!write_next) return;
     { KScope sc(h, KC_G2P);

@@ -210,8 +210,11 @@ mpm_status mpm_dd_forward(mpm_handle* hs, int32_t n, int32_t steps) {
             DevGuard dg(h);
             const SlotView sl = slot_at(h, t);
             const StateView S = state_at(h, t), Sn = state_at(h, t + 1);
-            { KScope sc(h, KC_CANON); launch_canon(K[g], sl, Sn.pid, last ? nullptr : h->keys, h->flags, h->stream); }
-            { KScope sc(h, KC_P2G); launch_p2g(K[g], sl, S, Sn, nullptr, nullptr, h->flags, h->stream); }
+            if (!canon_fused()) {
+                KScope sc(h, KC_CANON);
+                launch_canon(K[g], sl, Sn.pid, last ? nullptr : h->keys, h->flags, h->stream);
+            }
+            { KScope sc(h, KC_P2G); launch_p2g(K[g], sl, S, Sn, nullptr, nullptr, last ? nullptr : h->keys, h->flags, h->stream); }
             CU(cudaEventRecord(h->dd_ev[EV_P2G], h->stream));
         }
         for (int g = 0; g < n; ++g) {  // grid_op over the slab faces

@@ -530,6 +530,9 @@ __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __rest
     }
 }
 
+#ifndef MPM_NODE_FADD2
+#define MPM_NODE_FADD2 0
+#endif
 // ----------------------------------------------------- cell accumulation
 // thread per tile node: sum the (cell, o) partials with cell + o = node (fixed order)
 template <int D>
@@ -551,17 +554,41 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
                 const int cl = D == 2 ? c[0] * G::B + c[1] : (c[0] * G::B + c[1]) * G::B + c[2];
                 const int ol = D == 2 ? o0 * 3 + o1 : (o0 * 3 + o1) * 3 + o2;
                 const float4 v = s_cb[cl * G::NST + ol];
-                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+                if (MPM_NODE_FADD2) {  // packed f32x2 adds (per lane the same IEEE add)
+                    const float2 xy = __fadd2_rn(make_float2(s.x, s.y), make_float2(v.x, v.y));
+                    const float2 zw = __fadd2_rn(make_float2(s.z, s.w), make_float2(v.z, v.w));
+                    s = make_float4(xy.x, xy.y, zw.x, zw.y);
+                } else {
+                    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+                }
             }
     return s;
 }
 
 // Tuning knobs (overridable with -D for A/B builds, tools/build_variant.py)
+#ifndef MPM_P2GG_FFMA2
+#define MPM_P2GG_FFMA2 0
+#endif
 #ifndef MPM_P2GG_NESTED
 #define MPM_P2GG_NESTED 1
 #endif
 #ifndef MPM_P2G_CHUNK
 #define MPM_P2G_CHUNK 576
+#endif
+#ifndef MPM_CANON_IN_P2G
+#define MPM_CANON_IN_P2G 0  // p2g puts its block's list in canonical order itself (no k_canon pass)
+#endif
+#ifndef MPM_ROW_FFMA2
+#define MPM_ROW_FFMA2 1  // U_bar scatter 112.2 -> 109.6 ms per C5 iteration (p2g unchanged)
+#endif
+#ifndef MPM_GATHER_FFMA2
+#define MPM_GATHER_FFMA2 1  // g2p 123.2 -> 121.7 ms per C5 iteration
+#endif
+#ifndef MPM_G2PG_FFMA2
+#define MPM_G2PG_FFMA2 1  // g2p_grad gather 97.8 -> 90.6 ms per C5 iteration
+#endif
+#ifndef MPM_ROW_ELIDE
+#define MPM_ROW_ELIDE 1
 #endif
 #ifndef MPM_P2G_MINB
 #define MPM_P2G_MINB 3
@@ -597,6 +624,13 @@ template <int D> constexpr int p2g_smem_bytes() {
 // Thread (cell, o_x): sums over the cell's rows W_o (c + A o) (and W_o) for the
 // 3^(d-1) nodes o = (o_x, .) in registers.  Row: [wy*wz (9) | c (3) | A dx (9) | wx (3)] (3D),
 // [wy (3) | c (2) | A dx (4) | wx (3)] (2D).
+// (ax, ay) += w (x, y) as one packed f32x2 FMA (per lane an IEEE fma: bitwise the scalar pair)
+__device__ __forceinline__ void fma2(float& ax, float& ay, float w, float x, float y) {
+    const float2 r = __ffma2_rn(make_float2(w, w), make_float2(x, y), make_float2(ax, ay));
+    ax = r.x;
+    ay = r.y;
+}
+
 template <int D, bool MASS> struct SliceAcc {
     static constexpr int NN = D == 3 ? 9 : 3;
     float4 a[NN];
@@ -607,7 +641,39 @@ template <int D, bool MASS> struct SliceAcc {
     __device__ __forceinline__ void row(const float* __restrict__ rw, int ox) {
         const float4* r4 = reinterpret_cast<const float4*>(rw);
         const float fox = (float)ox;
-        if (D == 3) {
+        if (D == 3 && MPM_ROW_FFMA2) {
+            // the same sums with packed (f32x2) FMAs: (x, y) and (z, mass) per node, each lane an
+            // IEEE fma as in the scalar form (acc.w + W = fma(W, 1, acc.w)): bitwise identical
+            const float4 r0 = r4[0], r1 = r4[1], r2 = r4[2], r3 = r4[3], r4_ = r4[4], r5 = r4[5];
+            const float wyz[9] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x};
+            const float W0 = ox == 0 ? r5.y : (ox == 1 ? r5.z : r5.w);
+            // A dx rows: (A[0] A[1] A[2]) = (r3.x r3.y r3.z), (A[3..5]) = (r3.w r4.x r4.y), (A[6..8]) = (r4.z r4.w r5.x)
+            const float2 Ay = make_float2(r3.y, r4_.x), Az = make_float2(r3.z, r4_.y);
+            const float2 mx = make_float2(fmaf(fox, r3.x, r2.y), fmaf(fox, r3.w, r2.z));
+            const float mxz = fmaf(fox, r4_.z, r2.w);
+#pragma unroll
+            for (int oy = 0; oy < 3; ++oy) {
+                const float foy = (float)oy;
+                float2 mxy = oy ? __ffma2_rn(make_float2(foy, foy), Ay, mx) : mx;
+                float mz = oy ? fmaf(foy, r4_.w, mxz) : mxz;
+#pragma unroll
+                for (int oz = 0; oz < 3; ++oz) {
+                    const float W = W0 * wyz[oy * 3 + oz];
+                    const float2 W2 = make_float2(W, W);
+                    float4& acc = a[oy * 3 + oz];
+                    float2 xy = __ffma2_rn(W2, mxy, make_float2(acc.x, acc.y));
+                    acc.x = xy.x; acc.y = xy.y;
+                    if (MASS) {
+                        float2 zw = __ffma2_rn(W2, make_float2(mz, 1.0f), make_float2(acc.z, acc.w));
+                        acc.z = zw.x; acc.w = zw.y;
+                    } else {
+                        acc.z = fmaf(W, mz, acc.z);
+                    }
+                    mxy = __fadd2_rn(mxy, Az);
+                    mz += r5.x;
+                }
+            }
+        } else if (D == 3) {
             const float4 r0 = r4[0], r1 = r4[1], r2 = r4[2], r3 = r4[3], r4_ = r4[4], r5 = r4[5];
             const float wyz[9] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w, r2.x};
             const float A[9] = {r3.x, r3.y, r3.z, r3.w, r4_.x, r4_.y, r4_.z, r4_.w, r5.x};
@@ -615,9 +681,10 @@ template <int D, bool MASS> struct SliceAcc {
             float mx[3] = {fmaf(fox, A[0], r2.y), fmaf(fox, A[3], r2.z), fmaf(fox, A[6], r2.w)};
 #pragma unroll
             for (int oy = 0; oy < 3; ++oy) {
-                // oy = 0: m = mx exactly (fmaf(0, a, b) = b for finite a), without the instructions
-                float m[3] = {oy ? fmaf((float)oy, A[1], mx[0]) : mx[0], oy ? fmaf((float)oy, A[4], mx[1]) : mx[1],
-                              oy ? fmaf((float)oy, A[7], mx[2]) : mx[2]};
+                // MPM_ROW_ELIDE: oy = 0: m = mx exactly (fmaf(0, a, b) = b for finite a), without the instructions
+                const bool el = MPM_ROW_ELIDE && oy == 0;
+                float m[3] = {el ? mx[0] : fmaf((float)oy, A[1], mx[0]), el ? mx[1] : fmaf((float)oy, A[4], mx[1]),
+                              el ? mx[2] : fmaf((float)oy, A[7], mx[2])};
 #pragma unroll
                 for (int oz = 0; oz < 3; ++oz) {
                     const float W = W0 * wyz[oy * 3 + oz];
@@ -710,99 +777,116 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
 // inside the cell.  Writes sigma (canonical), the cell starts and -- when the step writes
 // S_{t+1} -- the particle ids of S_{t+1} (p2g's output order).  Its own high-occupancy
 // pass (256 threads, 26 KB smem) ahead of p2g.
-constexpr int canon_smem_bytes() { return 1728 * 15 + 2 * 66 * 4; }
-__global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __restrict__ pid_next,
-                                              int* __restrict__ keys_next, int* flags) {
-    pdl_begin();
+// One block's list in canonical order (NT threads, all calling).  scratch: 26,184 B of shared
+// memory (list, particle ids, cells, bucket counters); s_cst [CELLS + 2] receives the cell
+// starts; s_ci (nullable) the canonical list.  Writes sigma (canonical), the cell starts and
+// the particle ids of S_{t+1} (pid_next, nullable).  Returns false for a dropped block (over
+// MAXP particles: reported, its rows' next bin keys marked invalid).  Ends with a barrier.
+constexpr int kCanonScratch = 1728 * 15 + 66 * 4;
+template <int NT>
+__device__ __forceinline__ bool canon_block(const SlotView& sl, int bi, int start, int n, unsigned short* cstart,
+                                            int* __restrict__ pid_next, int* __restrict__ keys_next, int* flags,
+                                            unsigned char* scratch, int* s_cst, int* s_ci) {
     constexpr int MAXP = 1728, CELLS = 64;
-    using G = Geo<3>;  // CELLS = 64 in 2D and 3D
-    extern __shared__ __align__(16) unsigned char smem[];
-    int* s_idx = reinterpret_cast<int*>(smem);
+    int* s_idx = reinterpret_cast<int*>(scratch);
     int* s_pid = s_idx + MAXP;
     int* s_bpid = s_pid + MAXP;
     int* s_cnt = s_bpid + MAXP;
-    int* s_cst = s_cnt + CELLS + 2;
-    short* s_tmp = reinterpret_cast<short*>(s_cst + CELLS + 2);
+    short* s_tmp = reinterpret_cast<short*>(s_cnt + CELLS + 2);
     unsigned char* s_cell = reinterpret_cast<unsigned char*>(s_tmp + MAXP);
     const int tid = threadIdx.x, lane = tid & 31;
+    if (n > MAXP) {  // reported; the block is dropped (no valid entries downstream)
+        if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
+        for (int c = tid; c <= CELLS; c += NT) cstart[(int64_t)bi * (CELLS + 1) + c] = 0;
+        // g2p writes no bin key for the dropped rows of S_{t+1}: mark them so the next
+        // binning skips them instead of scattering stale keys
+        if (keys_next)
+            for (int q = tid; q < n; q += NT) keys_next[start + q] = -1;
+        __syncthreads();
+        return false;
+    }
+    // ---- canonical (cell, particle id) order of the block's list.  The scatter wrote each
+    // entry's cell and particle id next to it: coalesced loads only.
+    for (int q = tid; q < CELLS + 2; q += NT) s_cnt[q] = 0;
+#pragma unroll 4
+    for (int q = tid; q < n; q += NT) {
+        s_idx[q] = sl.sigma[start + q];
+        s_pid[q] = sl.spid[start + q];
+        s_cell[q] = sl.scell[start + q];
+    }
+    __syncthreads();
+    for (int q0 = 0; q0 < n; q0 += NT) {
+        const int q = q0 + tid;
+        const bool in = q < n;
+        const int cell = in ? (int)s_cell[q] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, cell);
+        if (in && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[cell], __popc(peers));
+    }
+    __syncthreads();
+    if (tid < 32) {  // exclusive scan of the 65 bucket counts (one warp)
+        int carry = 0;
+        for (int c = lane; c - lane <= CELLS; c += 32) {
+            const int v = c <= CELLS ? s_cnt[c] : 0;
+            int inc = v;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, inc, off);
+                if (lane >= off) inc += t;
+            }
+            if (c <= CELLS) { s_cst[c] = carry + inc - v; s_cnt[c] = carry + inc - v; }
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) s_cst[CELLS + 1] = carry;
+    }
+    __syncthreads();
+    for (int q0 = 0; q0 < n; q0 += NT) {  // bucket by cell (order inside a cell arbitrary)
+        const int q = q0 + tid;
+        const bool in = q < n;
+        const int cell = in ? (int)s_cell[q] : -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, cell);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (in && lane == leader) base = atomicAdd(&s_cnt[cell], __popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (in) {
+            const int pos = base + __popc(peers & ((1u << lane) - 1u));
+            s_tmp[pos] = (short)q;
+            s_bpid[pos] = s_pid[q];
+        }
+    }
+    __syncthreads();
+    for (int r = tid; r < n; r += NT) {  // rank by particle id inside the cell
+        const int q = s_tmp[r];
+        const int cell = s_cell[q], pq = s_bpid[r];
+        int rank = 0;
+        const int m1 = s_cst[cell + 1];
+        for (int m = s_cst[cell]; m < m1; ++m) rank += s_bpid[m] < pq;
+        const int fl = s_cst[cell] + rank;
+        sl.sigma[start + fl] = s_idx[q];
+        if (s_ci) s_ci[fl] = s_idx[q];
+        if (pid_next) pid_next[start + fl] = pq;
+    }
+    for (int c = tid; c <= CELLS; c += NT) cstart[(int64_t)bi * (CELLS + 1) + c] = (unsigned short)s_cst[c];
+    if (tid == 0 && s_cst[CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
+    __syncthreads();
+    return true;
+}
+
+constexpr int canon_smem_bytes() { return kCanonScratch + 66 * 4; }
+static_assert(p2g_union_bytes<2>() >= kCanonScratch && p2g_union_bytes<3>() >= kCanonScratch,
+              "p2g's row area holds the canonical-order scratch (MPM_CANON_IN_P2G)");
+__global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __restrict__ pid_next,
+                                              int* __restrict__ keys_next, int* flags) {
+    pdl_begin();
+    extern __shared__ __align__(16) unsigned char smem[];
+    int* s_cst = reinterpret_cast<int*>(smem + kCanonScratch);
     const int nact = *sl.nactive;
     const int b0 = *sl.base;
     const int* bstart = sl.bstart + b0 + sl.step;
-    unsigned short* cstart = sl.cstart + (int64_t)b0 * (CELLS + 1);
+    unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<3>::CELLS + 1);
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         const int start = bstart[bi], n = bstart[bi + 1] - start;
-        if (n > MAXP) {  // reported; the block is dropped (no valid entries downstream)
-            if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
-            for (int c = tid; c <= CELLS; c += kT) cstart[(int64_t)bi * (CELLS + 1) + c] = 0;
-            // g2p writes no bin key for the dropped rows of S_{t+1}: mark them so the next
-            // binning skips them instead of scattering stale keys
-            if (keys_next)
-                for (int q = tid; q < n; q += kT) keys_next[start + q] = -1;
-            continue;
-        }
-        // ---- phase 0: canonical (cell, particle id) order of the block's list.  The
-        // scatter wrote each entry's cell and particle id next to it: coalesced loads only.
-        for (int q = tid; q < G::CELLS + 2; q += kT) s_cnt[q] = 0;
-#pragma unroll 4
-        for (int q = tid; q < n; q += kT) {
-            s_idx[q] = sl.sigma[start + q];
-            s_pid[q] = sl.spid[start + q];
-            s_cell[q] = sl.scell[start + q];
-        }
-        __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kT) {
-            const int q = q0 + tid;
-            const bool in = q < n;
-            const int cell = in ? (int)s_cell[q] : -1;
-            const unsigned peers = __match_any_sync(0xffffffffu, cell);
-            if (in && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[cell], __popc(peers));
-        }
-        __syncthreads();
-        if (tid < 32) {  // exclusive scan of the 65 bucket counts (one warp)
-            int carry = 0;
-            for (int c = lane; c - lane <= G::CELLS; c += 32) {
-                const int v = c <= G::CELLS ? s_cnt[c] : 0;
-                int inc = v;
-#pragma unroll
-                for (int off = 1; off < 32; off <<= 1) {
-                    const int t = __shfl_up_sync(0xffffffffu, inc, off);
-                    if (lane >= off) inc += t;
-                }
-                if (c <= G::CELLS) { s_cst[c] = carry + inc - v; s_cnt[c] = carry + inc - v; }
-                carry += __shfl_sync(0xffffffffu, inc, 31);
-            }
-            if (lane == 0) s_cst[G::CELLS + 1] = carry;
-        }
-        __syncthreads();
-        for (int q0 = 0; q0 < n; q0 += kT) {  // bucket by cell (order inside a cell arbitrary)
-            const int q = q0 + tid;
-            const bool in = q < n;
-            const int cell = in ? (int)s_cell[q] : -1;
-            const unsigned peers = __match_any_sync(0xffffffffu, cell);
-            const int leader = __ffs(peers) - 1;
-            int base = 0;
-            if (in && lane == leader) base = atomicAdd(&s_cnt[cell], __popc(peers));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (in) {
-                const int pos = base + __popc(peers & ((1u << lane) - 1u));
-                s_tmp[pos] = (short)q;
-                s_bpid[pos] = s_pid[q];
-            }
-        }
-        __syncthreads();
-        for (int r = tid; r < n; r += kT) {  // rank by particle id inside the cell
-            const int q = s_tmp[r];
-            const int cell = s_cell[q], pq = s_bpid[r];
-            int rank = 0;
-            const int m1 = s_cst[cell + 1];
-            for (int m = s_cst[cell]; m < m1; ++m) rank += s_bpid[m] < pq;
-            const int fl = s_cst[cell] + rank;
-            sl.sigma[start + fl] = s_idx[q];
-            if (pid_next) pid_next[start + fl] = pq;
-        }
-        for (int c = tid; c <= G::CELLS; c += kT) cstart[(int64_t)bi * (G::CELLS + 1) + c] = (unsigned short)s_cst[c];
-        if (tid == 0 && s_cst[G::CELLS] != n) atomicOr(flags, FLAG_OUT_OF_DOMAIN);  // junk entries
-        __syncthreads();
+        canon_block<kT>(sl, bi, start, n, cstart, pid_next, keys_next, flags, smem, s_cst, nullptr);
     }
     (void)p;
 }
@@ -815,7 +899,7 @@ __global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __res
 template <int D>
 __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
                                                const int32_t* __restrict__ aid,
-                                               const float* __restrict__ alpha, int* flags) {
+                                               const float* __restrict__ alpha, int* keys_next, int* flags) {
     pdl_begin();
     using G = Geo<D>;
     using L = Lay<D>;
@@ -838,14 +922,19 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         const int start = bstart[bi], n = bstart[bi + 1] - start;
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        if (n > G::MAXP) {
-            if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
-            continue;
+        if (MPM_CANON_IN_P2G) {
+            // the canonical order of the block's list, in the row area (not live yet)
+            if (!canon_block<kTQ>(sl, bi, start, n, cstart, Sn.pid, keys_next, flags, smem, s_cst, s_ci)) continue;
+        } else {
+            if (n > G::MAXP) {
+                if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
+                continue;
+            }
+            // ---- the block's list in canonical (cell, particle id) order (k_canon)
+            for (int q = tid; q < n; q += kTQ) s_ci[q] = sl.sigma[start + q];
+            for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
+            __syncthreads();
         }
-        // ---- the block's list in canonical (cell, particle id) order (k_canon)
-        for (int q = tid; q < n; q += kTQ) s_ci[q] = sl.sigma[start + q];
-        for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
-        __syncthreads();
         const int nvalid = s_cst[G::CELLS];
         // ---- phases 1 + 2 over chunks of kTQ particles in canonical order; the particle
         // loads of chunk k+1 are issued before the accumulation of chunk k (same registers)
@@ -1002,10 +1091,14 @@ __device__ __forceinline__ void gather_moments(const float4* __restrict__ sU, co
                 for (int oz = 0; oz < 3; ++oz) {
                     const float4 U = sU[tile_lin<D>(lb[0] + ox, lb[1] + oy, lb[2] + oz)];
                     const float wz = w[2][oz];
-                    t0[0] = fmaf(wz, U.x, t0[0]); t0[1] = fmaf(wz, U.y, t0[1]); t0[2] = fmaf(wz, U.z, t0[2]);
+                    if (MPM_GATHER_FFMA2) fma2(t0[0], t0[1], wz, U.x, U.y);
+                    else { t0[0] = fmaf(wz, U.x, t0[0]); t0[1] = fmaf(wz, U.y, t0[1]); }
+                    t0[2] = fmaf(wz, U.z, t0[2]);
                     if (oz) {
                         const float wzo = wz * (float)oz;
-                        tz[0] = fmaf(wzo, U.x, tz[0]); tz[1] = fmaf(wzo, U.y, tz[1]); tz[2] = fmaf(wzo, U.z, tz[2]);
+                        if (MPM_GATHER_FFMA2) fma2(tz[0], tz[1], wzo, U.x, U.y);
+                        else { tz[0] = fmaf(wzo, U.x, tz[0]); tz[1] = fmaf(wzo, U.y, tz[1]); }
+                        tz[2] = fmaf(wzo, U.z, tz[2]);
                     }
                 }
             } else {
@@ -1013,11 +1106,23 @@ __device__ __forceinline__ void gather_moments(const float4* __restrict__ sU, co
                 t0[0] = U.x; t0[1] = U.y;
             }
             const float wy = w[1][oy];
+            if (D == 3 && MPM_GATHER_FFMA2) {
+                const float wyo = wy * (float)oy;
+                fma2(u0[0], u0[1], wy, t0[0], t0[1]);
+                u0[2] = fmaf(wy, t0[2], u0[2]);
+                fma2(uz[0], uz[1], wy, tz[0], tz[1]);
+                uz[2] = fmaf(wy, tz[2], uz[2]);
+                if (oy) {
+                    fma2(uy[0], uy[1], wyo, t0[0], t0[1]);
+                    uy[2] = fmaf(wyo, t0[2], uy[2]);
+                }
+            } else {
 #pragma unroll
-            for (int a = 0; a < D; ++a) {
-                u0[a] = fmaf(wy, t0[a], u0[a]);
-                if (D == 3) uz[a] = fmaf(wy, tz[a], uz[a]);
-                if (oy) uy[a] = fmaf(wy * (float)oy, t0[a], uy[a]);
+                for (int a = 0; a < D; ++a) {
+                    u0[a] = fmaf(wy, t0[a], u0[a]);
+                    if (D == 3) uz[a] = fmaf(wy, tz[a], uz[a]);
+                    if (oy) uy[a] = fmaf(wy * (float)oy, t0[a], uy[a]);
+                }
             }
         }
         const float wx = w[0][ox];
@@ -1100,6 +1205,8 @@ __device__ __forceinline__ int g2p_particle(const KParams& p, const float4* __re
 // runtime flag, not a template parameter): two instantiations may contract the FMAs of the
 // shared math differently, and the re-forwarded S_{t+1} would then differ in the last bit
 // from the forward's (checkpoint invariance is tested bitwise).
+// (no minimum-CTA bound: with __launch_bounds__(kTG, 1) ptxas takes ~125 registers and g2p
+// runs 15% slower; the default heuristic settles at 72-80)
 template <int D, bool SPLIT>
 __global__ void __launch_bounds__(kTG) k_g2p(KParams p, SlotView sl, StateView S, StateView Sn,
                                             int* __restrict__ keys, int* __restrict__ bcount, int* flags,
@@ -1254,12 +1361,18 @@ __device__ __forceinline__ void g2pg_gather(const KParams& p, const float4* __re
                 const float u[3] = {u4.x, u4.y, u4.z};
                 float Wb = 0.0f;
 #pragma unroll
-                for (int a = 0; a < D; ++a) {
-                    Wb = fmaf(u[a], t[a], Wb);
-                    S0[a] = fmaf(W, u[a], S0[a]);
-                }
+                for (int a = 0; a < D; ++a) Wb = fmaf(u[a], t[a], Wb);
+                if (D == 3 && MPM_G2PG_FFMA2) {
+                    fma2(S0[0], S0[1], W, u[0], u[1]);
+                    S0[2] = fmaf(W, u[2], S0[2]);
+                    fma2(fb[0], fb[1], Wb, gW[0], gW[1]);
+                    fb[2] = fmaf(Wb, gW[2], fb[2]);
+                } else {
 #pragma unroll
-                for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
+                    for (int a = 0; a < D; ++a) S0[a] = fmaf(W, u[a], S0[a]);
+#pragma unroll
+                    for (int k = 0; k < D; ++k) fb[k] = fmaf(Wb, gW[k], fb[k]);
+                }
             }
         }
     }
@@ -1438,7 +1551,76 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
     float fb[3] = {0.f, 0.f, 0.f}, S0[3] = {0.f, 0.f, 0.f}, Sm[3][3];
 #pragma unroll
     for (int q = 0; q < 9; ++q) (&Sm[0][0])[q] = 0.f;
-    if (D == 3 && MPM_P2GG_NESTED) {
+    if (D == 3 && MPM_P2GG_FFMA2) {
+        // the nested form below with packed f32x2 FMAs on the (x, y) pairs and on the
+        // (A, B) weight sums; per lane the same IEEE fmas: bitwise identical
+        float fx0 = 0.f, fx1 = 0.f, fx2 = 0.f;
+#pragma unroll
+        for (int o0 = 0; o0 < 3; ++o0) {
+            float Gy[3] = {0.f, 0.f, 0.f}, Hy[3] = {0.f, 0.f, 0.f}, Ky[3] = {0.f, 0.f, 0.f};
+            float Ay = 0.f, By = 0.f, Cy = 0.f;
+            float mx[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) mx[a] = fmaf((float)o0, Adx[a * D], c[a]);
+#pragma unroll
+            for (int o1 = 0; o1 < 3; ++o1) {
+                float Gz[3] = {0.f, 0.f, 0.f}, Hz[3] = {0.f, 0.f, 0.f}, Az = 0.f, Bz = 0.f;
+                float my[3];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) my[a] = fmaf((float)o1, Adx[a * D + 1], mx[a]);
+#pragma unroll
+                for (int o2 = 0; o2 < 3; ++o2) {
+                    const float4 g4 = sG[tile_lin<D>(lb[0] + o0, lb[1] + o1, lb[2] + o2)];
+                    float Wb = g4.w * p.p_mass;
+                    Wb = fmaf(g4.x, fmaf((float)o2, Adx[2], my[0]), Wb);
+                    Wb = fmaf(g4.y, fmaf((float)o2, Adx[5], my[1]), Wb);
+                    Wb = fmaf(g4.z, fmaf((float)o2, Adx[8], my[2]), Wb);
+                    const float w2 = w[2][o2];
+                    fma2(Gz[0], Gz[1], w2, g4.x, g4.y);
+                    Gz[2] = fmaf(w2, g4.z, Gz[2]);
+                    if (o2) {
+                        const float w2o = (float)o2 * w2;
+                        fma2(Hz[0], Hz[1], w2o, g4.x, g4.y);
+                        Hz[2] = fmaf(w2o, g4.z, Hz[2]);
+                    }
+                    const float2 ab = __ffma2_rn(make_float2(w2, dw[2][o2]), make_float2(Wb, Wb), make_float2(Az, Bz));
+                    Az = ab.x;
+                    Bz = ab.y;
+                }
+                const float w1 = w[1][o1];
+                fma2(Gy[0], Gy[1], w1, Gz[0], Gz[1]);
+                Gy[2] = fmaf(w1, Gz[2], Gy[2]);
+                fma2(Hy[0], Hy[1], w1, Hz[0], Hz[1]);
+                Hy[2] = fmaf(w1, Hz[2], Hy[2]);
+                if (o1) {
+                    const float w1o = (float)o1 * w1;
+                    fma2(Ky[0], Ky[1], w1o, Gz[0], Gz[1]);
+                    Ky[2] = fmaf(w1o, Gz[2], Ky[2]);
+                }
+                const float2 ay = __ffma2_rn(make_float2(w1, dw[1][o1]), make_float2(Az, Az), make_float2(Ay, By));
+                Ay = ay.x;
+                By = ay.y;
+                Cy = fmaf(w1, Bz, Cy);
+            }
+            const float w0 = w[0][o0];
+            fma2(S0[0], S0[1], w0, Gy[0], Gy[1]);
+            S0[2] = fmaf(w0, Gy[2], S0[2]);
+            fma2(Sm[2][0], Sm[2][1], w0, Hy[0], Hy[1]);
+            Sm[2][2] = fmaf(w0, Hy[2], Sm[2][2]);
+            fma2(Sm[1][0], Sm[1][1], w0, Ky[0], Ky[1]);
+            Sm[1][2] = fmaf(w0, Ky[2], Sm[1][2]);
+            if (o0) {
+                const float w0o = (float)o0 * w0;
+                fma2(Sm[0][0], Sm[0][1], w0o, Gy[0], Gy[1]);
+                Sm[0][2] = fmaf(w0o, Gy[2], Sm[0][2]);
+            }
+            fx0 = fmaf(dw[0][o0], Ay, fx0);
+            const float2 f12 = __ffma2_rn(make_float2(w0, w0), make_float2(By, Cy), make_float2(fx1, fx2));
+            fx1 = f12.x;
+            fx2 = f12.y;
+        }
+        fb[0] = fx0; fb[1] = fx1; fb[2] = fx2;
+    } else if (D == 3 && MPM_P2GG_NESTED) {
         // Nested separable form of the 27-node gather below (same sums, re-associated): the
         // weights factor per axis, W_o = w0 w1 w2 and dW/df = (dw0 w1 w2, w0 dw1 w2, w0 w1 dw2),
         // so the z sums are formed per (o0, o1), the y sums per o0, then the x sums:
@@ -2007,9 +2189,11 @@ void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* keys
     launch_k(k_canon, cg < p.step_blocks ? cg : (p.step_blocks > 0 ? p.step_blocks : 1), kT, canon_smem_bytes(), s, p, sl,
              pid_next, keys_next, flags);
 }
+bool canon_fused() { return MPM_CANON_IN_P2G != 0; }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
-                const int32_t* aid, const float* alpha_t, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t, flags));
+                const int32_t* aid, const float* alpha_t, int* keys_next, int* flags, cudaStream_t s) {
+    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t,
+                             keys_next, flags));
 }
 static unsigned node_grid(const KParams& p) {
     const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? Geo<3>::TN : Geo<2>::TN) + kT - 1) / kT;

@@ -21,9 +21,10 @@ try:
 except Exception as e:
     print(v, "failed", open(f"gpurun_out/ab_{v}.err").read()[-800:]); raise SystemExit
 r = d["roofline"]; k = r["kernel_ms"]
+g = lambda n: k.get(n, 0.0)  # noqa: E731
 print("%-10s value %.4g ms/it %.1f | p2g %.1f g2p %.1f sc %.1f ga %.1f p2gg %.1f canon %.1f gop %.1f gopg %.1f bin %.1f" % (
-    v, d["value"], d["ms_per_step"], k["p2g"], k["g2p"], k["g2p_grad"], k["g2p_grad_gather"], k["p2g_grad"],
-    k["canon"], k["grid_op"], k["grid_op_grad"], k["bin"]))
+    v, d["value"], d["ms_per_step"], g("p2g"), g("g2p"), g("g2p_grad"), g("g2p_grad_gather"), g("p2g_grad"),
+    g("canon"), g("grid_op"), g("grid_op_grad"), g("bin")))
 PY
 done
 done
