@@ -377,6 +377,8 @@ def run_ours(args):
     # roofline of the dominant kernel (largest share of device time)
     peak, peak_src = _peaks()
     alg = algorithmic_bytes(p["dim"], N * per, A * per)
+    if not stats.get("canon", (0, 0))[1]:  # small problems: p2g orders its blocks itself (no canon pass)
+        alg["p2g"] += alg["canon"]
     kern = {kname: v for kname, v in stats.items() if kname in alg and v[1] > 0}
     dom = max(kern, key=lambda kk: kern[kk][0])
     dom_ms, dom_n = kern[dom]
@@ -388,6 +390,8 @@ def run_ours(args):
                 "share_of_kernel_time": dom_ms / total_ms if total_ms else None,
                 "active_nodes_per_episode": A,
                 "kernel_ms": {kk: round(v[0] / args.steps, 3) for kk, v in stats.items() if v[1]},
+                # every particle / node kernel's algorithmic GB/s over the peak (the dominant one is `frac`)
+                "kernel_frac": {kk: round(alg[kk] / (v[0] / v[1] / 1e3) / 1e9 / peak, 4) for kk, v in kern.items()},
                 "profiled_ms_per_step": ms_prof / args.steps,
                 "kernel_launches_per_step": {kk: v[1] // args.steps for kk, v in stats.items() if v[1]}}
     # whole-step effective bandwidth against the SURVEY 8(d) byte model

@@ -354,7 +354,7 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
         launch_ctrl_obs_fwd(k, h->theta, t, h->obs_part, h->obs + (size_t)t * k.E * no, h->obs_cnt,
                             const_cast<float*>(alpha_at(h, t)), h->stream);
     }
-    if (!canon_fused()) {
+    if (!canon_fused(k)) {
         KScope sc(h, KC_CANON);
         launch_canon(k, sl, Sn.pid, bin_next ? h->keys : nullptr, h->flags, h->stream);
     }

@@ -210,7 +210,7 @@ mpm_status mpm_dd_forward(mpm_handle* hs, int32_t n, int32_t steps) {
             DevGuard dg(h);
             const SlotView sl = slot_at(h, t);
             const StateView S = state_at(h, t), Sn = state_at(h, t + 1);
-            if (!canon_fused()) {
+            if (!canon_fused(K[g])) {
                 KScope sc(h, KC_CANON);
                 launch_canon(K[g], sl, Sn.pid, last ? nullptr : h->keys, h->flags, h->stream);
             }

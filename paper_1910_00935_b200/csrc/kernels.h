@@ -110,7 +110,7 @@ void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* keys
 // p2g writes F_{t+1} and particle ids of S_{t+1} when Sn.rec / Sn.pid are non-null
 // canon_fused(): p2g does the canonical ordering of each block itself (launch_canon is then
 // skipped; p2g takes its pid_next = Sn.pid and keys_next arguments)
-bool canon_fused();
+bool canon_fused(const KParams& p);
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* keys_next, int* flags, cudaStream_t s);
 // grid_op: sum of the covering partial tiles -> resolved tile of every active block

@@ -286,6 +286,44 @@ template <int D> struct SigPipe {
     __device__ const int* sig_at(int it, int start) const { return sig + (it & 1) * kSigCap + (start & 3); }
 };
 
+// The sigma segments alone (p2g: its rows are staged by its own phase 1): the next block's
+// segment is copied while the CTA works on the current one.
+template <int D> struct SigOnlyPipe {
+    uint64_t* bar;        // [2]
+    int* sig;             // [2][kSigCap]
+    const int* sigma;     // this step's sorted list (16-B aligned)
+    const int* bstart;    // this step's block starts
+    __device__ void init() {
+        if (threadIdx.x == 0) {
+            mbar_init(bar, 1);
+            mbar_init(bar + 1, 1);
+            fence_mbar_init();
+        }
+    }
+    __device__ void issue(int bi, int slot) {
+        const int s0 = bstart[bi], s1 = bstart[bi + 1];
+        const int a0 = s0 & ~3;
+        const uint32_t sb = s1 - s0 <= Geo<D>::MAXP ? (uint32_t)((((s1 + 3) & ~3) - a0) * 4) : 0u;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + slot)), "r"(sb)
+                     : "memory");
+        if (sb) bulk_copy(sig + slot * kSigCap, sigma + a0, sb, bar + slot);
+    }
+    __device__ void start(int bi, int nact) {
+        if (threadIdx.x == 0 && bi < nact) issue(bi, 0);
+    }
+    __device__ void next(int bi_next, int nact, int it) {
+        if (threadIdx.x == 0 && bi_next < nact) {
+            fence_proxy_async();
+            issue(bi_next, (it + 1) & 1);
+        }
+    }
+    __device__ const int* wait(int it, int start) {
+        const int cb = it & 1;
+        mbar_wait(bar + cb, (uint32_t)((it >> 1) & 1));
+        return sig + cb * kSigCap + (start & 3);
+    }
+};
+
 // Sub-block work split of the thread-per-particle kernels (g2p, g2p_grad's gather part, p2g_grad):
 // when a step has fewer active blocks than the persistent grid has CTAs (the small configurations:
 // C2 ~40 blocks, C3 ~120, on 400-600 CTAs) each block's particles are split into `split` (<= 4)
@@ -530,9 +568,6 @@ __global__ void __launch_bounds__(kT) k_bin_scatter(KParams p, const int* __rest
     }
 }
 
-#ifndef MPM_NODE_FADD2
-#define MPM_NODE_FADD2 0
-#endif
 // ----------------------------------------------------- cell accumulation
 // thread per tile node: sum the (cell, o) partials with cell + o = node (fixed order)
 template <int D>
@@ -554,13 +589,7 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
                 const int cl = D == 2 ? c[0] * G::B + c[1] : (c[0] * G::B + c[1]) * G::B + c[2];
                 const int ol = D == 2 ? o0 * 3 + o1 : (o0 * 3 + o1) * 3 + o2;
                 const float4 v = s_cb[cl * G::NST + ol];
-                if (MPM_NODE_FADD2) {  // packed f32x2 adds (per lane the same IEEE add)
-                    const float2 xy = __fadd2_rn(make_float2(s.x, s.y), make_float2(v.x, v.y));
-                    const float2 zw = __fadd2_rn(make_float2(s.z, s.w), make_float2(v.z, v.w));
-                    s = make_float4(xy.x, xy.y, zw.x, zw.y);
-                } else {
-                    s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-                }
+                s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
             }
     return s;
 }
@@ -575,8 +604,8 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
 #ifndef MPM_P2G_CHUNK
 #define MPM_P2G_CHUNK 576
 #endif
-#ifndef MPM_CANON_IN_P2G
-#define MPM_CANON_IN_P2G 0  // p2g puts its block's list in canonical order itself (no k_canon pass)
+#ifndef MPM_P2G_SIGPF
+#define MPM_P2G_SIGPF 0  // p2g: the next block's sigma segment by cp.async.bulk during the current block
 #endif
 #ifndef MPM_ROW_FFMA2
 #define MPM_ROW_FFMA2 1  // U_bar scatter 112.2 -> 109.6 ms per C5 iteration (p2g unchanged)
@@ -613,12 +642,15 @@ constexpr int kCH = MPM_P2G_CHUNK;  // rows per chunk: most blocks fit one chunk
 template <int D> struct RowL {  // particle row in shared memory (floats); stride avoids STS.128 conflicts
     static constexpr int STRIDE = D == 3 ? 28 : 12;
 };
+// p2g's rows per chunk: with the sigma prefetch (two list buffers) 544 in 3D, so three CTAs
+// still fit an SM's shared memory
+template <int D> constexpr int p2g_chunk() { return (D == 3 && MPM_P2G_SIGPF) ? 544 : kCH; }
 template <int D> constexpr int p2g_union_bytes() {
-    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
+    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = p2g_chunk<D>() * RowL<D>::STRIDE * 4;
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 template <int D> constexpr int p2g_smem_bytes() {
-    return p2g_union_bytes<D>() + Geo<D>::MAXP * 4 + (Geo<D>::CELLS + 2) * 4;
+    return p2g_union_bytes<D>() + (MPM_P2G_SIGPF ? 2 * kSigCap : Geo<D>::MAXP) * 4 + (Geo<D>::CELLS + 2) * 4;
 }
 
 // Thread (cell, o_x): sums over the cell's rows W_o (c + A o) (and W_o) for the
@@ -896,7 +928,10 @@ __global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __res
 // Ft = (I + dt C) F; tau = tau(Ft) [+ actuation]; A = -dt V 4/dx^2 tau + m C;
 // node b+o receives W_o (m v + A (o - f) dx) and W_o m.  F_{t+1} = Ft.
 // CTA = 192 threads: phase 1 thread per particle (rows in smem), phase 2 thread per (cell, o_x).
-template <int D>
+// CANON: p2g puts each block's list in canonical order itself (no k_canon pass); used for
+// small problems (canon_fused), where one kernel fewer per step pays (C2 +4%), while at C5 the
+// ordering costs more inside p2g (18 warps per SM) than as its own pass (64 warps per SM)
+template <int D, bool CANON>
 __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView sl, StateView S, StateView Sn,
                                                const int32_t* __restrict__ aid,
                                                const float* __restrict__ alpha, int* keys_next, int* flags) {
@@ -907,8 +942,11 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
     extern __shared__ __align__(16) unsigned char smem[];
     float* s_row = reinterpret_cast<float*>(smem);                   // phase 1/2 rows ...
     float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... node partials
+    constexpr int PCH = p2g_chunk<D>();
+    constexpr bool SIGPF = MPM_P2G_SIGPF && !CANON;
     int* s_ci = reinterpret_cast<int*>(smem + p2g_union_bytes<D>());  // canonical state index
-    int* s_cst = s_ci + G::MAXP;  // [CELLS + 1] cell starts
+    int* s_cst = s_ci + (MPM_P2G_SIGPF ? 2 * kSigCap : G::MAXP);  // [CELLS + 1] cell starts
+    __shared__ __align__(8) uint64_t s_bar[2];
     const int tid = threadIdx.x, lane = tid & 31;
     const int my_cell = tid / 3, my_ox = tid - 3 * (tid / 3);
     const int nact = *sl.nactive;
@@ -917,12 +955,30 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
     const int* bstart = sl.bstart + b0 + sl.step;
     unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
     float4* tiles_l = sl.part;  // partial tiles of this step (local block index)
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
+    SigOnlyPipe<D> spipe{s_bar, s_ci, sl.sigma, bstart};
+    if (SIGPF) {
+        spipe.init();
+        __syncthreads();
+        spipe.start(blockIdx.x, nact);
+    }
+    int it = 0;
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
         const int bid = blist[bi];
         const int start = bstart[bi], n = bstart[bi + 1] - start;
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        if (MPM_CANON_IN_P2G) {
+        const int* ci = s_ci;  // the block's canonical list
+        if (SIGPF) {
+            spipe.next(bi + gridDim.x, nact, it);
+            ci = spipe.wait(it, start);
+            if (n > G::MAXP) {
+                if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
+                __syncthreads();  // everyone is past the wait before the buffer is refilled
+                continue;
+            }
+            for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
+            __syncthreads();
+        } else if (CANON) {
             // the canonical order of the block's list, in the row area (not live yet)
             if (!canon_block<kTQ>(sl, bi, start, n, cstart, Sn.pid, keys_next, flags, smem, s_cst, s_ci)) continue;
         } else {
@@ -948,7 +1004,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
             bool fluid;
         };
         auto load = [&](In& d, int R) {
-            const int i_ = s_ci[R];
+            const int i_ = ci[R];
             load_comps<L::X>(S.x, i_, d.x);
             load_comps<L::VC>(S.vc, i_, d.vc);
             load_comps<L::FF>(S.f, i_, d.F);
@@ -962,8 +1018,8 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         };
         In cur;
         if (tid < nvalid) load(cur, tid);
-        for (int ch = 0; ch < nvalid; ch += kCH) {
-            const int cend = min(nvalid, ch + kCH);
+        for (int ch = 0; ch < nvalid; ch += PCH) {
+            const int cend = min(nvalid, ch + PCH);
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
                 const bool more = r + kTQ < nvalid;
                 // ids outside [0, n_act) are passive here (mpm_set_state flags them as an error)
@@ -2111,7 +2167,7 @@ void set_pdl(int64_t particles) {
         const char* v = getenv("MPM_B200_PDL");
         g_pdl_force = v ? (v[0] != '0') : 2;
     }
-    g_pdl = g_pdl_force == 2 ? particles <= 262144 : g_pdl_force == 1;
+    g_pdl = g_pdl_force == 2 ? particles <= kSmallProblem : g_pdl_force == 1;
 }
 
 // Kernel attributes are per device: initialise once for every device a handle is created
@@ -2133,9 +2189,15 @@ cudaError_t tile_init() {
 #define MPM_INIT_DIM(DI)                                                                                          \
     do {                                                                                                          \
         constexpr int DIM = (DI) == 2 ? 2 : 3;                                                                    \
-        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributeMaxDynamicSharedMemorySize, p2g_smem_bytes<DIM>()); \
+        e = cudaFuncSetAttribute(k_p2g<DIM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,                 \
+                                 p2g_smem_bytes<DIM>());                                                          \
         if (e) return e;                                                                                          \
-        e = cudaFuncSetAttribute(k_p2g<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);                \
+        e = cudaFuncSetAttribute(k_p2g<DIM, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);         \
+        if (e) return e;                                                                                          \
+        e = cudaFuncSetAttribute(k_p2g<DIM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,                  \
+                                 p2g_smem_bytes<DIM>());                                                          \
+        if (e) return e;                                                                                          \
+        e = cudaFuncSetAttribute(k_p2g<DIM, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);          \
         if (e) return e;                                                                                          \
         e = cudaFuncSetAttribute(k_g2p_grad<DIM>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);           \
         if (e) return e;                                                                                          \
@@ -2143,7 +2205,7 @@ cudaError_t tile_init() {
                                  g2pg_smem_bytes<DIM>());                                                         \
         if (e) return e;                                                                                          \
         const int di = DIM == 3 ? 1 : 0;                                                                          \
-        T.grid[0][di] = occupancy_grid((const void*)k_p2g<DIM>, p2g_smem_bytes<DIM>(), kTQ);                      \
+        T.grid[0][di] = occupancy_grid((const void*)k_p2g<DIM, false>, p2g_smem_bytes<DIM>(), kTQ);               \
         T.grid[1][di] = occupancy_grid((const void*)k_g2p<DIM, false>, 0, kTG);                                          \
         T.grid[2][di] = occupancy_grid((const void*)k_g2p_grad<DIM>, g2pg_smem_bytes<DIM>(), kTQ);                \
         T.grid[3][di] = occupancy_grid((const void*)k_p2g_grad<DIM, false>, 0, kTP);                                     \
@@ -2189,11 +2251,15 @@ void launch_canon(const KParams& p, const SlotView& sl, int* pid_next, int* keys
     launch_k(k_canon, cg < p.step_blocks ? cg : (p.step_blocks > 0 ? p.step_blocks : 1), kT, canon_smem_bytes(), s, p, sl,
              pid_next, keys_next, flags);
 }
-bool canon_fused() { return MPM_CANON_IN_P2G != 0; }
+bool canon_fused(const KParams& p) { return p.EN <= kSmallProblem; }
 void launch_p2g(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn,
                 const int32_t* aid, const float* alpha_t, int* keys_next, int* flags, cudaStream_t s) {
-    DISPATCH(p.dim, launch_k(k_p2g<DIM>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid, alpha_t,
-                             keys_next, flags));
+    if (canon_fused(p))
+        DISPATCH(p.dim, launch_k(k_p2g<DIM, true>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid,
+                                 alpha_t, keys_next, flags));
+    else
+        DISPATCH(p.dim, launch_k(k_p2g<DIM, false>, pgrid(p, 0), kTQ, p2g_smem_bytes<DIM>(), s, p, sl, S, Sn, aid,
+                                 alpha_t, keys_next, flags));
 }
 static unsigned node_grid(const KParams& p) {
     const int64_t need = ((int64_t)p.step_blocks * (p.dim == 3 ? Geo<3>::TN : Geo<2>::TN) + kT - 1) / kT;
@@ -2209,7 +2275,7 @@ void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* uba
     if (has_halo(sl)) DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM, true>, node_grid(p), kT, 0, s, p, sl, ubar));
     else DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM, false>, node_grid(p), kT, 0, s, p, sl, ubar));
 }
-static bool split_blocks(const KParams& p) { return p.N * p.E <= 262144; }  // see item_split
+static bool split_blocks(const KParams& p) { return p.N * p.E <= kSmallProblem; }  // see item_split
 void launch_g2p(const KParams& p, const SlotView& sl, const StateView& S, const StateView& Sn, int* keys,
                 int* bcount, int* flags, bool refwd, const Migr& mg, cudaStream_t s) {
     if (split_blocks(p))

@@ -61,6 +61,10 @@ template <int D> struct Geo {
     static constexpr int NST = D == 3 ? 27 : 9;      // stencil offsets
     static constexpr int MAXP = 1728;                // particles per block (27 per cell)
 };
+// particles per launch up to which a step is latency bound rather than throughput bound (C1-C4
+// episodes): such launches use programmatic dependent launch, the sub-block work split and the
+// canonical ordering inside p2g (kernels_tile.cu)
+constexpr int64_t kSmallProblem = 262144;
 // at most this many CTAs share one block's particles in the thread-per-particle kernels
 // (kernels_tile.cu item_split); sizes the per-item actuator-gradient partials
 constexpr int kMaxSplit = 4;
