@@ -286,44 +286,6 @@ template <int D> struct SigPipe {
     __device__ const int* sig_at(int it, int start) const { return sig + (it & 1) * kSigCap + (start & 3); }
 };
 
-// The sigma segments alone (p2g: its rows are staged by its own phase 1): the next block's
-// segment is copied while the CTA works on the current one.
-template <int D> struct SigOnlyPipe {
-    uint64_t* bar;        // [2]
-    int* sig;             // [2][kSigCap]
-    const int* sigma;     // this step's sorted list (16-B aligned)
-    const int* bstart;    // this step's block starts
-    __device__ void init() {
-        if (threadIdx.x == 0) {
-            mbar_init(bar, 1);
-            mbar_init(bar + 1, 1);
-            fence_mbar_init();
-        }
-    }
-    __device__ void issue(int bi, int slot) {
-        const int s0 = bstart[bi], s1 = bstart[bi + 1];
-        const int a0 = s0 & ~3;
-        const uint32_t sb = s1 - s0 <= Geo<D>::MAXP ? (uint32_t)((((s1 + 3) & ~3) - a0) * 4) : 0u;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar + slot)), "r"(sb)
-                     : "memory");
-        if (sb) bulk_copy(sig + slot * kSigCap, sigma + a0, sb, bar + slot);
-    }
-    __device__ void start(int bi, int nact) {
-        if (threadIdx.x == 0 && bi < nact) issue(bi, 0);
-    }
-    __device__ void next(int bi_next, int nact, int it) {
-        if (threadIdx.x == 0 && bi_next < nact) {
-            fence_proxy_async();
-            issue(bi_next, (it + 1) & 1);
-        }
-    }
-    __device__ const int* wait(int it, int start) {
-        const int cb = it & 1;
-        mbar_wait(bar + cb, (uint32_t)((it >> 1) & 1));
-        return sig + cb * kSigCap + (start & 3);
-    }
-};
-
 // Sub-block work split of the thread-per-particle kernels (g2p, g2p_grad's gather part, p2g_grad):
 // when a step has fewer active blocks than the persistent grid has CTAs (the small configurations:
 // C2 ~40 blocks, C3 ~120, on 400-600 CTAs) each block's particles are split into `split` (<= 4)
@@ -604,9 +566,6 @@ __device__ __forceinline__ float4 node_gather(const float4* __restrict__ s_cb, i
 #ifndef MPM_P2G_CHUNK
 #define MPM_P2G_CHUNK 576
 #endif
-#ifndef MPM_P2G_SIGPF
-#define MPM_P2G_SIGPF 0  // p2g: the next block's sigma segment by cp.async.bulk during the current block
-#endif
 #ifndef MPM_ROW_FFMA2
 #define MPM_ROW_FFMA2 1  // U_bar scatter 112.2 -> 109.6 ms per C5 iteration (p2g unchanged)
 #endif
@@ -642,15 +601,12 @@ constexpr int kCH = MPM_P2G_CHUNK;  // rows per chunk: most blocks fit one chunk
 template <int D> struct RowL {  // particle row in shared memory (floats); stride avoids STS.128 conflicts
     static constexpr int STRIDE = D == 3 ? 28 : 12;
 };
-// p2g's rows per chunk: with the sigma prefetch (two list buffers) 544 in 3D, so three CTAs
-// still fit an SM's shared memory
-template <int D> constexpr int p2g_chunk() { return (D == 3 && MPM_P2G_SIGPF) ? 544 : kCH; }
 template <int D> constexpr int p2g_union_bytes() {
-    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = p2g_chunk<D>() * RowL<D>::STRIDE * 4;
+    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 template <int D> constexpr int p2g_smem_bytes() {
-    return p2g_union_bytes<D>() + (MPM_P2G_SIGPF ? 2 * kSigCap : Geo<D>::MAXP) * 4 + (Geo<D>::CELLS + 2) * 4;
+    return p2g_union_bytes<D>() + Geo<D>::MAXP * 4 + (Geo<D>::CELLS + 2) * 4;
 }
 
 // Thread (cell, o_x): sums over the cell's rows W_o (c + A o) (and W_o) for the
@@ -942,11 +898,8 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
     extern __shared__ __align__(16) unsigned char smem[];
     float* s_row = reinterpret_cast<float*>(smem);                   // phase 1/2 rows ...
     float4* s_cb = reinterpret_cast<float4*>(smem);                  // ... node partials
-    constexpr int PCH = p2g_chunk<D>();
-    constexpr bool SIGPF = MPM_P2G_SIGPF && !CANON;
     int* s_ci = reinterpret_cast<int*>(smem + p2g_union_bytes<D>());  // canonical state index
-    int* s_cst = s_ci + (MPM_P2G_SIGPF ? 2 * kSigCap : G::MAXP);  // [CELLS + 1] cell starts
-    __shared__ __align__(8) uint64_t s_bar[2];
+    int* s_cst = s_ci + G::MAXP;  // [CELLS + 1] cell starts
     const int tid = threadIdx.x, lane = tid & 31;
     const int my_cell = tid / 3, my_ox = tid - 3 * (tid / 3);
     const int nact = *sl.nactive;
@@ -955,30 +908,14 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
     const int* bstart = sl.bstart + b0 + sl.step;
     unsigned short* cstart = sl.cstart + (int64_t)b0 * (G::CELLS + 1);
     float4* tiles_l = sl.part;  // partial tiles of this step (local block index)
-    SigOnlyPipe<D> spipe{s_bar, s_ci, sl.sigma, bstart};
-    if (SIGPF) {
-        spipe.init();
-        __syncthreads();
-        spipe.start(blockIdx.x, nact);
-    }
-    int it = 0;
-    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x, ++it) {
+    for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
         const int bid = blist[bi];
         const int start = bstart[bi], n = bstart[bi + 1] - start;
         int e, c0[3];
         block_origin<D>(p, bid, e, c0);
-        const int* ci = s_ci;  // the block's canonical list
-        if (SIGPF) {
-            spipe.next(bi + gridDim.x, nact, it);
-            ci = spipe.wait(it, start);
-            if (n > G::MAXP) {
-                if (tid == 0) atomicOr(flags, FLAG_BLOCK_OVERFLOW);
-                __syncthreads();  // everyone is past the wait before the buffer is refilled
-                continue;
-            }
-            for (int c = tid; c <= G::CELLS; c += kTQ) s_cst[c] = cstart[(int64_t)bi * (G::CELLS + 1) + c];
-            __syncthreads();
-        } else if (CANON) {
+        // (the next block's list by cp.async.bulk during this block -- two list buffers, 544-row
+        // chunks to keep three CTAs per SM -- measured slower: 182.7 -> 191.6 ms per C5 iteration)
+        if (CANON) {
             // the canonical order of the block's list, in the row area (not live yet)
             if (!canon_block<kTQ>(sl, bi, start, n, cstart, Sn.pid, keys_next, flags, smem, s_cst, s_ci)) continue;
         } else {
@@ -1004,7 +941,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
             bool fluid;
         };
         auto load = [&](In& d, int R) {
-            const int i_ = ci[R];
+            const int i_ = s_ci[R];
             load_comps<L::X>(S.x, i_, d.x);
             load_comps<L::VC>(S.vc, i_, d.vc);
             load_comps<L::FF>(S.f, i_, d.F);
@@ -1018,8 +955,8 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         };
         In cur;
         if (tid < nvalid) load(cur, tid);
-        for (int ch = 0; ch < nvalid; ch += PCH) {
-            const int cend = min(nvalid, ch + PCH);
+        for (int ch = 0; ch < nvalid; ch += kCH) {
+            const int cend = min(nvalid, ch + kCH);
             for (int r = ch + tid; r < cend; r += kTQ) {  // data of r is in registers
                 const bool more = r + kTQ < nvalid;
                 // ids outside [0, n_act) are passive here (mpm_set_state flags them as an error)
