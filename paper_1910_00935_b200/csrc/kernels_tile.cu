@@ -1760,7 +1760,10 @@ __device__ __forceinline__ float p2g_grad_particle(const KParams& p, const float
     return abar;
 }
 
-constexpr int kTP = 128;  // p2g_grad CTA
+#ifndef MPM_P2GG_THREADS
+#define MPM_P2GG_THREADS 128
+#endif
+constexpr int kTP = MPM_P2GG_THREADS;  // p2g_grad CTA
 
 template <int D, bool SPLIT>
 __global__ void __launch_bounds__(kTP, MPM_P2GG_MINB) k_p2g_grad(KParams p, SlotView sl, StateView S,
