@@ -226,7 +226,7 @@ def run_reference(args):
     return 0
 
 
-def _pick_k(p, N, per, T, dev, world=1):
+def _pick_k(p, N, per, T, dev, use_dist=False):
     """Smallest checkpoint interval whose tape fits in 90% of free HBM (Appendix D.2:
     k trades re-forward work for memory; on a 180 GB B200 the 1M-particle cube fits k = 2).
     Under torchrun every rank must run the same k (the same re-forward work): the ranks agree
@@ -234,7 +234,7 @@ def _pick_k(p, N, per, T, dev, world=1):
     import torch
     from paper_1910_00935_b200 import mpm
     free, _ = torch.cuda.mem_get_info(dev)
-    if world > 1:
+    if use_dist:
         import torch.distributed as dist
         t = torch.tensor([float(free), -float(per)], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
@@ -261,7 +261,10 @@ def run_ours(args):
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    # under torchrun the process group is set up even at world size 1 (the NCCL path runs as
+    # it would on N GPUs: init, the agreed k, the gradient all-reduce, max-over-ranks timing)
+    use_dist = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ
+    if use_dist:
         # NCCL over NVLink/NVSwitch; BENCH_DIST_BACKEND=gloo only for exercising the
         # multi-rank code path with several ranks on one GPU (NCCL rejects that)
         backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
@@ -283,7 +286,7 @@ def run_ours(args):
     host["theta"] = torch.from_numpy(inps[0]["theta"]).pin_memory()
     devin = {key: t.to(dev) for key, t in host.items()}
 
-    k = int(args.k_ckpt) if args.k_ckpt else _pick_k(p, N, per, T, dev, world)
+    k = int(args.k_ckpt) if args.k_ckpt else _pick_k(p, N, per, T, dev, use_dist)
     sim = mpm.sim_from_config(p, N, episodes=per, max_steps=T, k_ckpt=k)
     if any(np.any(i["mat"]) for i in inps):  # fluid particles (R23): a property of the workload
         sim.set_materials(cat("mat"))
@@ -311,7 +314,7 @@ def run_ours(args):
             if grads_out:
                 sim.grads(grads_out)
             sim.grad_v0_sum(shared_buf)
-        if world > 1:
+        if use_dist:
             # the one exchange of the path: sum of the shared-parameter gradient over ranks
             if shared_buf.is_cuda:
                 allreduce_shared_grad(shared_buf)
@@ -322,7 +325,7 @@ def run_ours(args):
 
     def timed(K, fn):
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dist:
             dist.barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
@@ -330,7 +333,7 @@ def run_ours(args):
             fn()
         e.record()
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dist:
             dist.barrier()
         return max_over_ranks(s.elapsed_time(e), dev)
 
@@ -363,7 +366,7 @@ def run_ours(args):
     ms_e2e = timed(args.steps, host_step)
 
     # units of all ranks (C4 shards may differ by one episode: count them exactly)
-    if world > 1:
+    if use_dist:
         tot = torch.tensor([float(N) * per * T * args.steps], dtype=torch.float64, device=dev)
         dist.all_reduce(tot)
         particle_steps = float(tot.item())
@@ -430,7 +433,7 @@ def run_ours(args):
                 "loss": [float(x) for x in loss_d.cpu()]}
         print(json.dumps(line), flush=True)
     sim.close()
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
     return 0
 

@@ -24,14 +24,14 @@ def episode_shard(total: int, rank: int, world: int) -> range:
 
 def allreduce_shared_grad(grad: torch.Tensor) -> torch.Tensor:
     """Sum the shared-parameter gradient over ranks, in place (no-op without a group)."""
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(grad, op=dist.ReduceOp.SUM)
     return grad
 
 
 def max_over_ranks(value: float, device: torch.device | str = "cpu") -> float:
     """Max of a per-rank scalar (e.g. elapsed device ms) over all ranks."""
-    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1):
+    if not (dist.is_available() and dist.is_initialized()):
         return float(value)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)

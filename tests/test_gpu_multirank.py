@@ -41,6 +41,26 @@ def test_two_ranks_on_one_gpu(config, scaling, episodes_total):
     assert d["value"] > 0 and d["e2e"]["value"] > 0
 
 
+def test_nccl_backend_single_rank():
+    """The bench under torchrun with the NCCL backend (its default) on the one GPU this pool
+    gives: process-group init with device_id, the all-reduce of the shared-parameter gradient,
+    the agreed checkpoint interval (all-reduce MIN) and the max-over-ranks timing all go through
+    NCCL.  NCCL_DEBUG=INFO must show the communicator came up (nranks 1)."""
+    env = dict(os.environ, NCCL_DEBUG="INFO", BENCH_HORIZON="64")
+    env.pop("BENCH_DIST_BACKEND", None)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), "bench.py", "--gpus", "1",
+           "--config", "c4", "--steps", "2", "--warmup", "3", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["value"] > 0 and d["e2e"]["value"] > 0
+    log = out.stdout + out.stderr
+    assert "NCCL INFO" in log and "nranks 1" in log, log[-3000:]
+
+
 def _t6_worker(rank, world, port, T, out):
     """one C4 episode per rank on the same GPU, theta_bar all-reduced over gloo"""
     import torch
