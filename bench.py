@@ -273,7 +273,9 @@ def run_ours(args):
         else:
             dist.init_process_group(backend)
     from paper_1910_00935_b200.dist import allreduce_shared_grad, max_over_ranks
-    p, shard, scaling = _workload(args.config, world, rank)
+    if args.shard_of and world > 1:
+        raise SystemExit("--shard-of is a one-process projection; run it without torchrun")
+    p, shard, scaling = _workload(args.config, args.shard_of or world, rank)
     per = len(shard)
     T = int(p["steps"])
     if args.config == "c4":
@@ -431,6 +433,10 @@ def run_ours(args):
                                    "into device buffers"},
                 "gpu_launches": int(launches), "clocks": clocks.summary(),
                 "loss": [float(x) for x in loss_d.cpu()]}
+        if args.shard_of:
+            line["shard_of"] = {"n_gpus": args.shard_of, "rank": 0, "episodes": per,
+                                "note": "one GPU running rank 0's share of an N-GPU job (no all-reduce): "
+                                        "`value` is this GPU's own rate, not a whole-job number"}
         print(json.dumps(line), flush=True)
     sim.close()
     if use_dist:
@@ -537,6 +543,9 @@ def main():
     ap.add_argument("--k-ckpt", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--dd", type=int, default=0, help="f3: one body over this many slab subdomains (one process)")
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="one GPU runs rank 0's share of an N-GPU job (C4: 64/N episodes): the per-rank "
+                         "compute of the N-GPU run without its all-reduce, a strong-scaling projection")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

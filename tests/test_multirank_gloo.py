@@ -90,3 +90,20 @@ def test_weak_scaling_value():
     # 2 ranks x 1,061,208 particles x 2,048 steps in 1.5 s (max over ranks)
     v = weak_scaling_value(1061208 * 2048, 2, 1500.0)
     assert v == pytest.approx(1061208 * 2048 * 2 / 1.5)
+
+
+def test_bench_workload_shards():
+    """bench.py's work split: C4's 64 episodes over N ranks (strong; --shard-of N sizes rank 0's
+    share on one GPU), one episode per rank otherwise (weak)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "bench_mod", os.path.join(os.path.dirname(os.path.dirname(__file__)), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for n in (1, 2, 4, 8):
+        parts = [list(bench._workload("c4", n, r)[1]) for r in range(n)]
+        assert sum(parts, []) == list(range(64)) and all(len(q) == 64 // n for q in parts)
+        assert bench._workload("c4", n, 0)[2] == "strong"
+        p, shard, kind = bench._workload("c5", n, n - 1)
+        assert list(shard) == [n - 1] and kind == "weak"
