@@ -601,8 +601,12 @@ constexpr int kCH = MPM_P2G_CHUNK;  // rows per chunk: most blocks fit one chunk
 template <int D> struct RowL {  // particle row in shared memory (floats); stride avoids STS.128 conflicts
     static constexpr int STRIDE = D == 3 ? 28 : 12;
 };
+// canonical-order scratch (canon_block): the list, particle ids, cells and bucket counters
+constexpr int kCanonScratch = 1728 * 15 + 66 * 4;
+// p2g / U_bar scatter shared area: the phase-1/2 rows, the node partials, or (p2g for small
+// problems) the canonical-order scratch -- whichever is largest
 template <int D> constexpr int p2g_union_bytes() {
-    constexpr int a = 0, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
+    constexpr int a = kCanonScratch, b = Geo<D>::CELLS * Geo<D>::NST * 16, c = kCH * RowL<D>::STRIDE * 4;
     return a > b ? (a > c ? a : c) : (b > c ? b : c);
 }
 template <int D> constexpr int p2g_smem_bytes() {
@@ -770,7 +774,6 @@ __device__ __forceinline__ bool p2g_particle(const KParams& p, const float* x, c
 // starts; s_ci (nullable) the canonical list.  Writes sigma (canonical), the cell starts and
 // the particle ids of S_{t+1} (pid_next, nullable).  Returns false for a dropped block (over
 // MAXP particles: reported, its rows' next bin keys marked invalid).  Ends with a barrier.
-constexpr int kCanonScratch = 1728 * 15 + 66 * 4;
 template <int NT>
 __device__ __forceinline__ bool canon_block(const SlotView& sl, int bi, int start, int n, unsigned short* cstart,
                                             int* __restrict__ pid_next, int* __restrict__ keys_next, int* flags,

@@ -64,7 +64,10 @@ template <int D> struct Geo {
 // particles per launch up to which a step is latency bound rather than throughput bound (C1-C4
 // episodes): such launches use programmatic dependent launch, the sub-block work split and the
 // canonical ordering inside p2g (kernels_tile.cu)
-constexpr int64_t kSmallProblem = 262144;
+#ifndef MPM_SMALL_PROBLEM
+#define MPM_SMALL_PROBLEM 262144
+#endif
+constexpr int64_t kSmallProblem = MPM_SMALL_PROBLEM;
 // at most this many CTAs share one block's particles in the thread-per-particle kernels
 // (kernels_tile.cu item_split); sizes the per-item actuator-gradient partials
 constexpr int kMaxSplit = 4;
