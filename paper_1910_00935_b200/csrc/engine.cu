@@ -405,7 +405,17 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
     { KScope sc(h, KC_P2G_GRAD);
       launch_p2g_grad(k, sl, S, h->has_aid ? h->aid : nullptr, alpha_at(h, t), Sbn, h->xbar_part,
                       Sb, h->abar_part, h->flags, h->stream); }
-    if (k.n_act > 0) {
+    if (k.n_act > 0 && fork && !k.closed_loop && MPM_ABAR_SIDE) {
+        // open loop: alpha_bar_t is read only by the controller adjoint after the whole reverse,
+        // so its reduction leaves the critical path.  The side stream is in order: the next
+        // step's gather follows it there, and main joins that gather before p2g_grad(t - 1)
+        // rewrites abar_part; mpm_backward joins the side stream before the controller adjoint.
+        cudaEventRecord(h->ev_fork, h->stream);
+        cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+        launch_reduce_abar(k, sl, h->abar_part, h->alpha_bar + (size_t)t * A, h->side);
+        h->launches += 1;
+        h->side_pending = true;
+    } else if (k.n_act > 0) {
         KScope sc(h, KC_REDUCE_ABAR);
         launch_reduce_abar(k, sl, h->abar_part, h->alpha_bar + (size_t)t * A * (k.closed_loop ? k.E : 1),
                            h->stream);
@@ -819,6 +829,11 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
                 step_backward(h, k, t, h->sbar[h->sbar_cur], h->sbar[h->sbar_cur ^ 1]);
                 h->sbar_cur ^= 1;
             }
+        }
+        if (h->side_pending) {  // the last actuator-gradient reduction ran on the side stream
+            cudaEventRecord(h->ev_join, h->side);
+            cudaStreamWaitEvent(h->stream, h->ev_join, 0);
+            h->side_pending = false;
         }
         const int64_t nth = n_theta_of(h->prm, h->dim);
         if (nth > 0 && !k.closed_loop) {

@@ -2,6 +2,9 @@
 // engine.cu (single-domain C-ABI) and engine_dd.cu (one body over several slab
 // subdomains).
 #pragma once
+#ifndef MPM_ABAR_SIDE
+#define MPM_ABAR_SIDE 1  // open-loop actuator-gradient reduction on the side stream (step_backward)
+#endif
 #include <cstdint>
 #include <functional>
 #include <map>
@@ -46,6 +49,7 @@ struct mpm_ctx {
     cudaStream_t stream = 0;
     cudaStream_t side = nullptr;             // second stream (g2p_grad gather || U_bar scatter)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool side_pending = false;     // work enqueued on `side` that main has not joined yet (step_backward)
     cudaStream_t side2 = nullptr;            // third stream: segment re-forward ahead of the reverse
     cudaEvent_t ev_seg = nullptr, ev_refwd = nullptr;
     float* xbar_part = nullptr;    // [d][EN] xb_t partial from g2p_grad's gather part
