@@ -7,7 +7,8 @@
 // k-slot window (half (t / k) & 1); the binning and the resolved node tiles of every
 // step live in the grid store, so the reverse never re-runs p2g and a segment's
 // re-forward is g2p only.  Adjoint states are indexed like the state they belong to.
-// Streams: main; side (g2p_grad's gather part); side2 (segment re-forward), all
+// Streams: main; side (g2p_grad's gather part); side2 (segment re-forward); side3 (the
+// open-loop actuator-gradient reduction of each reverse step), all
 // captured into the forward / backward CUDA graphs.
 #include <algorithm>
 #include <cstdlib>
@@ -198,7 +199,8 @@ size_t carve(mpm_ctx* h, char* base) {
     int* keys = (int*)take(sizeof(int) * EN);
     float4* ubar = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
     float4* part = (float4*)take(sizeof(float4) * (size_t)max_active * TN);
-    float* abar_part = (float*)take(sizeof(float) * (size_t)max_active * kMaxSplit * A);  // per work item
+    // per work item; two buffers (step parity) so the open-loop reduction can trail p2g_grad
+    float* abar_part = (float*)take(sizeof(float) * 2 * (size_t)max_active * kMaxSplit * A);
     float* alpha = (float*)take(sizeof(float) * (size_t)p.max_steps * AE);
     float* alpha_bar = (float*)take(sizeof(float) * (size_t)p.max_steps * AE);
     // closed loop (R22): observations of every step, group sizes, reduction partials, and the
@@ -240,6 +242,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->xbar_part = xbar_part;
         h->staging = staging; h->aid = aid; h->mat = mat; h->bcount = bcount; h->cursor = cursor; h->scan_part = scan_part; h->keys = keys;
         h->ubar = ubar; h->part = part; h->abar_part = abar_part;
+        h->abar_stride = (size_t)max_active * kMaxSplit * A;
         h->obs = obs; h->obs_cnt = obs_cnt; h->obs_part = obs_part; h->obs_inc = obs_inc;
         h->alpha = alpha; h->alpha_bar = alpha_bar; h->theta = theta; h->theta_bar = theta_bar;
         h->theta_part = theta_part; h->loss = loss; h->com_part = com_part; h->counter = counter;
@@ -402,22 +405,32 @@ void step_backward(mpm_ctx* h, const KParams& k, int t, const AdjView& Sbn, cons
     { KScope sc(h, KC_G2P_GRAD); launch_g2p_grad(k, sl, S, Sbn, h->ubar, h->stream); }
     { KScope sc(h, KC_GRID_OP_GRAD); launch_grid_op_grad(k, sl, h->ubar, h->stream); }
     if (fork) cudaStreamWaitEvent(h->stream, h->ev_join, 0);
+    const bool abar_side = k.n_act > 0 && fork && !k.closed_loop && MPM_ABAR_SIDE && h->side3 != nullptr;
+    float* abar_part = h->abar_part + (size_t)(t & 1) * h->abar_stride;  // double buffered by step parity
+    if (h->abar_pending[t & 1]) {  // the reduction of step t + 2 still reads this buffer
+        cudaStreamWaitEvent(h->stream, h->ev_abar[t & 1], 0);
+        h->abar_pending[t & 1] = false;
+    }
     { KScope sc(h, KC_P2G_GRAD);
       launch_p2g_grad(k, sl, S, h->has_aid ? h->aid : nullptr, alpha_at(h, t), Sbn, h->xbar_part,
-                      Sb, h->abar_part, h->flags, h->stream); }
-    if (k.n_act > 0 && fork && !k.closed_loop && MPM_ABAR_SIDE) {
+                      Sb, abar_part, h->flags, h->stream); }
+    if (abar_side) {
         // open loop: alpha_bar_t is read only by the controller adjoint after the whole reverse,
-        // so its reduction leaves the critical path.  The side stream is in order: the next
-        // step's gather follows it there, and main joins that gather before p2g_grad(t - 1)
-        // rewrites abar_part; mpm_backward joins the side stream before the controller adjoint.
-        cudaEventRecord(h->ev_fork, h->stream);
-        cudaStreamWaitEvent(h->side, h->ev_fork, 0);
-        launch_reduce_abar(k, sl, h->abar_part, h->alpha_bar + (size_t)t * A, h->side);
+        // so its reduction leaves the critical path (its partials are double buffered by step
+        // parity; mpm_backward joins before the controller adjoint).  Small problems run it on
+        // its own stream beside the next reverse step (their next gather is on the critical
+        // path); large ones ahead of the next gather on the side stream, which measured faster
+        // there (C4: +2.4% vs +0.3%; C3: -3.5% vs -0.3%; C2: +2.5% vs +2.8%)
+        cudaStream_t rs = canon_fused(k) ? h->side3 : h->side;
+        cudaEventRecord(h->ev_p2gg, h->stream);
+        cudaStreamWaitEvent(rs, h->ev_p2gg, 0);
+        launch_reduce_abar(k, sl, abar_part, h->alpha_bar + (size_t)t * A, rs);
+        cudaEventRecord(h->ev_abar[t & 1], rs);
+        h->abar_pending[t & 1] = true;
         h->launches += 1;
-        h->side_pending = true;
     } else if (k.n_act > 0) {
         KScope sc(h, KC_REDUCE_ABAR);
-        launch_reduce_abar(k, sl, h->abar_part, h->alpha_bar + (size_t)t * A * (k.closed_loop ? k.E : 1),
+        launch_reduce_abar(k, sl, abar_part, h->alpha_bar + (size_t)t * A * (k.closed_loop ? k.E : 1),
                            h->stream);
     }
     if (k.closed_loop) {  // controller adjoint of step t; observation adjoint into S_bar_t
@@ -553,6 +566,10 @@ mpm_status mpm_destroy(mpm_handle h) {
     if (h->side2) cudaStreamDestroy(h->side2);
     if (h->ev_seg) cudaEventDestroy(h->ev_seg);
     if (h->ev_refwd) cudaEventDestroy(h->ev_refwd);
+    if (h->side3) cudaStreamDestroy(h->side3);
+    if (h->ev_p2gg) cudaEventDestroy(h->ev_p2gg);
+    for (auto ev : h->ev_abar)
+        if (ev) cudaEventDestroy(ev);
     delete h;
     return MPM_OK;
 }
@@ -600,6 +617,9 @@ mpm_status mpm_set_stream(mpm_handle h, void* s) {
         CU(cudaStreamCreateWithFlags(&h->side2, cudaStreamNonBlocking));
         CU(cudaEventCreateWithFlags(&h->ev_seg, cudaEventDisableTiming));
         CU(cudaEventCreateWithFlags(&h->ev_refwd, cudaEventDisableTiming));
+        CU(cudaStreamCreateWithFlags(&h->side3, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&h->ev_p2gg, cudaEventDisableTiming));
+        for (auto& ev : h->ev_abar) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     }
     return MPM_OK;
 }
@@ -830,11 +850,11 @@ mpm_status mpm_backward(mpm_handle h, int32_t steps) {
                 h->sbar_cur ^= 1;
             }
         }
-        if (h->side_pending) {  // the last actuator-gradient reduction ran on the side stream
-            cudaEventRecord(h->ev_join, h->side);
-            cudaStreamWaitEvent(h->stream, h->ev_join, 0);
-            h->side_pending = false;
-        }
+        for (int b = 0; b < 2; ++b)  // actuator-gradient reductions still running on side3
+            if (h->abar_pending[b]) {
+                cudaStreamWaitEvent(h->stream, h->ev_abar[b], 0);
+                h->abar_pending[b] = false;
+            }
         const int64_t nth = n_theta_of(h->prm, h->dim);
         if (nth > 0 && !k.closed_loop) {
             KScope sc(h, KC_CTRL);

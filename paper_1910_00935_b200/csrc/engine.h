@@ -3,7 +3,7 @@
 // subdomains).
 #pragma once
 #ifndef MPM_ABAR_SIDE
-#define MPM_ABAR_SIDE 1  // open-loop actuator-gradient reduction on the side stream (step_backward)
+#define MPM_ABAR_SIDE 1  // open-loop actuator-gradient reduction on its own stream (step_backward)
 #endif
 #include <cstdint>
 #include <functional>
@@ -49,9 +49,12 @@ struct mpm_ctx {
     cudaStream_t stream = 0;
     cudaStream_t side = nullptr;             // second stream (g2p_grad gather || U_bar scatter)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    bool side_pending = false;     // work enqueued on `side` that main has not joined yet (step_backward)
     cudaStream_t side2 = nullptr;            // third stream: segment re-forward ahead of the reverse
     cudaEvent_t ev_seg = nullptr, ev_refwd = nullptr;
+    cudaStream_t side3 = nullptr;            // open-loop actuator-gradient reduction (step_backward)
+    cudaEvent_t ev_p2gg = nullptr, ev_abar[2] = {nullptr, nullptr};
+    bool abar_pending[2] = {false, false};   // a reduction on side3 still reads abar_part buffer b
+    size_t abar_stride = 0;                  // floats per abar_part buffer
     float* xbar_part = nullptr;    // [d][EN] xb_t partial from g2p_grad's gather part
     int device = 0;
     std::string err;
