@@ -349,7 +349,9 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
     const StateView S = state_at(h, t);
     const StateView Sn = write_next ? state_at(h, t + 1) : StateView{nullptr, nullptr, nullptr, nullptr};
     const int32_t* aid = h->has_aid ? h->aid : nullptr;
-    if (k.closed_loop) {  // R22: alpha_t from the observation of S_t
+    const bool obs_join = k.closed_loop && h->obs_ahead == t;  // enqueued on `side` by step t - 1
+    if (obs_join) h->obs_ahead = -1;
+    if (k.closed_loop && !obs_join) {  // R22: alpha_t from the observation of S_t
         KScope sc(h, KC_CTRL);
         h->launches += 1;
         launch_observe(k, S.x, S.vc, S.pid, aid, h->obs_part, h->stream);
@@ -361,11 +363,25 @@ void step_forward(mpm_ctx* h, const KParams& k, int t, bool write_next, bool bin
         KScope sc(h, KC_CANON);
         launch_canon(k, sl, Sn.pid, bin_next ? h->keys : nullptr, h->flags, h->stream);
     }
+    if (obs_join) cudaStreamWaitEvent(h->stream, h->ev_join, 0);  // alpha_t is ready
     { KScope sc(h, KC_P2G); launch_p2g(k, sl, S, Sn, aid, alpha_at(h, t), bin_next ? h->keys : nullptr, h->flags, h->stream); }
     { KScope sc(h, KC_GRID_OP); launch_grid_op(k, sl, h->stream); }
     if (!write_next) return;
     { KScope sc(h, KC_G2P);
       launch_g2p(k, sl, S, Sn, bin_next ? h->keys : nullptr, h->bcount, h->flags, false, Migr{}, h->stream); }
+    if (bin_next && k.closed_loop && MPM_OBS_AHEAD && !h->prof.on && h->side != nullptr) {
+        // the observation of S_{t+1} and the controller of step t + 1 need only S_{t+1}: they run
+        // on the side stream beside the binning of S_{t+1} (and k_canon), joined before p2g(t + 1)
+        cudaEventRecord(h->ev_fork, h->stream);
+        cudaStreamWaitEvent(h->side, h->ev_fork, 0);
+        const size_t no = (size_t)2 * k.dim * k.n_act;
+        launch_observe(k, Sn.x, Sn.vc, Sn.pid, aid, h->obs_part, h->side);
+        launch_ctrl_obs_fwd(k, h->theta, t + 1, h->obs_part, h->obs + (size_t)(t + 1) * k.E * no, h->obs_cnt,
+                            const_cast<float*>(alpha_at(h, t + 1)), h->side);
+        cudaEventRecord(h->ev_join, h->side);
+        h->obs_ahead = t + 1;
+        h->launches += 2;
+    }
     if (bin_next) {
         const SlotView nx = slot_at(h, t + 1);
         KScope sc(h, KC_BIN);
@@ -745,6 +761,7 @@ mpm_status mpm_forward(mpm_handle h, int32_t steps) {
             launch_ctrl_fwd(k, h->theta, steps, h->alpha, h->stream);
         }
         bin_fresh(h, k, 0);
+        h->obs_ahead = -1;
         for (int t = 0; t < steps; ++t) step_forward(h, k, t, true, t + 1 < steps);
     });
     if (gs) return gs;

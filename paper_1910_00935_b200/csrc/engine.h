@@ -2,6 +2,9 @@
 // engine.cu (single-domain C-ABI) and engine_dd.cu (one body over several slab
 // subdomains).
 #pragma once
+#ifndef MPM_OBS_AHEAD
+#define MPM_OBS_AHEAD 1  // closed loop: observation + controller of step t+1 beside its binning (step_forward)
+#endif
 #ifndef MPM_ABAR_SIDE
 #define MPM_ABAR_SIDE 1  // open-loop actuator-gradient reduction on its own stream (step_backward)
 #endif
@@ -53,6 +56,7 @@ struct mpm_ctx {
     cudaEvent_t ev_seg = nullptr, ev_refwd = nullptr;
     cudaStream_t side3 = nullptr;            // open-loop actuator-gradient reduction (step_backward)
     cudaEvent_t ev_p2gg = nullptr, ev_abar[2] = {nullptr, nullptr};
+    int obs_ahead = -1;                      // closed loop: step whose observation + controller run on `side`
     bool abar_pending[2] = {false, false};   // a reduction on side3 still reads abar_part buffer b
     size_t abar_stride = 0;                  // floats per abar_part buffer
     float* xbar_part = nullptr;    // [d][EN] xb_t partial from g2p_grad's gather part
