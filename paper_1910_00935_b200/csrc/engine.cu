@@ -184,6 +184,7 @@ size_t carve(mpm_ctx* h, char* base) {
     int* nactive_arr = (int*)take(sizeof(int) * Tm);
     int* base_arr = (int*)take(sizeof(int) * Tm);
     int* blist_pool = (int*)take(sizeof(int) * (size_t)pool);
+    int* nbr_pool = (int*)take(sizeof(int) * (size_t)pool * (d == 3 ? 27 : 9));
     int* bstart_pool = (int*)take(sizeof(int) * ((size_t)pool + Tm + 1));
     unsigned short* cstart_pool = (unsigned short*)take(sizeof(unsigned short) * (size_t)pool * (kCells + 1));
     float4* tiles_pool = (float4*)take(sizeof(float4) * (size_t)pool * TN);
@@ -231,7 +232,7 @@ size_t carve(mpm_ctx* h, char* base) {
         h->pool_blocks = pool;
         h->sigma_store = sigma_store; h->scell_ring[0] = scell0; h->scell_ring[1] = scell1;
         h->spid_ring[0] = spid0; h->spid_ring[1] = spid1; h->bmap_store = bmap_store;
-        h->nactive_arr = nactive_arr; h->base_arr = base_arr; h->blist_pool = blist_pool;
+        h->nactive_arr = nactive_arr; h->base_arr = base_arr; h->blist_pool = blist_pool; h->nbr_pool = nbr_pool;
         h->bstart_pool = bstart_pool; h->cstart_pool = cstart_pool; h->tiles_pool = tiles_pool;
         h->state_floats = sf;
         h->n_ckpt = n_ckpt;
@@ -276,6 +277,7 @@ SlotView slot_at(mpm_ctx* h, int t) {
     s.tiles = h->tiles_pool;
     s.part = h->part;
     s.ntot = h->ntot_arr + t;
+    s.nbr = h->nbr_pool;
     s.step = t;
     s.halo = Halo{0, k.nb, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
     if (h->dd) {

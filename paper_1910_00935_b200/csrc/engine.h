@@ -82,6 +82,7 @@ struct mpm_ctx {
     int* nactive_arr = nullptr;    // [T_max]
     int* base_arr = nullptr;       // [T_max]
     int* blist_pool = nullptr;     // [P]
+    int* nbr_pool = nullptr;       // [P][3^d] neighbour-block pool indices (SlotView::nbr)
     int* bstart_pool = nullptr;    // [P + T_max + 1]
     unsigned short* cstart_pool = nullptr;  // [P][65]
     float4* tiles_pool = nullptr;  // [P][TN]

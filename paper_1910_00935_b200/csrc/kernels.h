@@ -83,6 +83,8 @@ struct SlotView {
     float4* part;            // [max_active][TN]  per-step scratch: p2g partial (P, M) tiles,
                              //                   backward: grid_op_grad output (Pb, Mb)
     int* ntot;               // [1]    sorted particles of this step (set by the scan)
+    int* nbr;                // pool [P][3^d] pool tile index of each neighbour block (offsets -1..1 per
+                             //        axis), or -1; set by k_canon / p2g, read by the grid passes
     int step;                // t
     Halo halo;               // f3 neighbours (covered sums of grid_op / grid_op_grad)
 };

@@ -145,6 +145,73 @@ __device__ __forceinline__ float4 covered_sum(const KParams& p, int e, const int
     return acc;
 }
 
+// Neighbour table (single domain): row bi of step t holds, for each block offset o in {-1, 0, 1}^d
+// (o_0 slowest), the pool tile index of block (block of bi) + o, or -1 -- the block-map lookups
+// of covered_sum done once per block (by k_canon, or p2g for small problems) instead of once per
+// tile node, so a grid pass's tile loads no longer wait on a block-map load.
+#ifndef MPM_NBR_TABLE
+#define MPM_NBR_TABLE 1
+#endif
+template <int D> constexpr int kNbr = D == 3 ? 27 : 9;
+template <int D>
+__device__ __forceinline__ void fill_nbr(const KParams& p, const SlotView& sl, int b0, int bi, int tid) {
+    if (!MPM_NBR_TABLE || tid >= kNbr<D>) return;
+    int e, c0[3];
+    block_origin<D>(p, sl.blist[b0 + bi], e, c0);
+    const int o[3] = {tid / (D == 3 ? 9 : 3) - 1, (D == 3 ? (tid / 3) % 3 : tid % 3) - 1, D == 3 ? tid % 3 - 1 : 0};
+    int bb[3] = {0, 0, 0};
+    bool in = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+        bb[k] = c0[k] / Geo<D>::B + o[k];
+        in = in && bb[k] >= 0 && bb[k] < p.nb;
+    }
+    sl.nbr[(int64_t)(b0 + bi) * kNbr<D> + tid] = in ? sl.bmap[block_lin<D>(p, e, bb)] : -1;
+}
+// covered_sum from the neighbour table row `nb` of the node's block; n = the node's local
+// coordinates in the (B+2)^d tile.  Same covering tiles in the same order as covered_sum.
+template <int D>
+__device__ __forceinline__ float4 covered_sum_nbr(const int* __restrict__ nb, const int n[3],
+                                                  const float4* __restrict__ tiles) {
+    using G = Geo<D>;
+    int h[3], l0[3];  // block offset of the node's own block (0 or 1), local coordinate in it
+    bool ok1[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        h[k] = k < D ? n[k] >> G::LOGB : 0;
+        l0[k] = k < D ? n[k] & (G::B - 1) : 0;
+        ok1[k] = k < D && l0[k] < 2;
+    }
+    // all table entries first (independent loads), then the tiles
+    int ti[8];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < (D == 3 ? 2 : 1); ++c) {
+                const int j = (a * 2 + b) * 2 + c;
+                const bool use = !((a && !ok1[0]) || (b && !ok1[1]) || (c && !ok1[2]));
+                const int o0 = h[0] - a, o1 = h[1] - b, o2 = h[2] - c;  // each in {-1, 0, 1}
+                const int idx = D == 3 ? ((o0 + 1) * 3 + (o1 + 1)) * 3 + (o2 + 1) : (o0 + 1) * 3 + (o1 + 1);
+                ti[j] = use ? __ldg(nb + idx) : -1;
+            }
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int c = 0; c < (D == 3 ? 2 : 1); ++c) {
+                const int j = (a * 2 + b) * 2 + c;
+                if (ti[j] < 0) continue;
+                const int lq = tile_lin<D>(l0[0] + a * G::B, l0[1] + b * G::B, l0[2] + c * G::B);
+                const float4 v = __ldg(tiles + (int64_t)ti[j] * G::TN + lq);
+                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+    return acc;
+}
+
 // neighbour tiles indexed by the neighbour's pool (tile) indices of this step (f3)
 template <int D> __device__ __forceinline__ const float4* halo_tiles(const Halo& hl, int s) {
     return hl.tiles[s] ? hl.tiles[s] - (int64_t)(*hl.base[s]) * Geo<D>::TN : nullptr;
@@ -876,10 +943,11 @@ __global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __res
     const int* bstart = sl.bstart + b0 + sl.step;
     unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<3>::CELLS + 1);
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
+        if (p.dim == 3) fill_nbr<3>(p, sl, b0, bi, threadIdx.x);
+        else fill_nbr<2>(p, sl, b0, bi, threadIdx.x);
         const int start = bstart[bi], n = bstart[bi + 1] - start;
         canon_block<kT>(sl, bi, start, n, cstart, pid_next, keys_next, flags, smem, s_cst, nullptr);
     }
-    (void)p;
 }
 
 // ---------------------------------------------------------------- P2G
@@ -919,6 +987,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
         // (the next block's list by cp.async.bulk during this block -- two list buffers, 544-row
         // chunks to keep three CTAs per SM -- measured slower: 182.7 -> 191.6 ms per C5 iteration)
         if (CANON) {
+            fill_nbr<D>(p, sl, b0, bi, tid);
             // the canonical order of the block's list, in the row area (not live yet)
             if (!canon_block<kTQ>(sl, bi, start, n, cstart, Sn.pid, keys_next, flags, smem, s_cst, s_ci)) continue;
         } else {
@@ -1023,7 +1092,9 @@ __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
         const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
         float4 out = make_float4(0.f, 0.f, 0.f, -0.0f);
         if (inside) {
-            const float4 pm = covered_sum<D, HALO>(p, e, g, sl.bmap, part_g, sl.halo, nt0, nt1);
+            const float4 pm = (!HALO && MPM_NBR_TABLE)
+                                  ? covered_sum_nbr<D>(sl.nbr + (int64_t)(b0 + bi) * kNbr<D>, n, part_g)
+                                  : covered_sum<D, HALO>(p, e, g, sl.bmap, part_g, sl.halo, nt0, nt1);
             float u0[3], u1[3];
             out = grid_velocity<D>(p, g, pm, u0, u1) ? make_float4(0.f, 0.f, 0.f, -pm.w)
                                                       : make_float4(u1[0], u1[1], u1[2], pm.w);
@@ -1057,7 +1128,9 @@ __global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, con
             block_origin<D, true>(p, __ldg(blist + bi), e, c0);
             local_node<D>(q, n);
             const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-            const float4 ub = covered_sum<D, HALO>(p, e, g, sl.bmap, ub_g, sl.halo, nt0, nt1);
+            const float4 ub = (!HALO && MPM_NBR_TABLE)
+                                  ? covered_sum_nbr<D>(sl.nbr + (int64_t)(b0 + bi) * kNbr<D>, n, ub_g)
+                                  : covered_sum<D, HALO>(p, e, g, sl.bmap, ub_g, sl.halo, nt0, nt1);
             const float u0[3] = {r.x, r.y + p.dt * p.gravity, r.z};
             const float denom = r.w + p.eps_mass;
             const float dot = ub.x * u0[0] + ub.y * u0[1] + (D == 3 ? ub.z * u0[2] : 0.0f);
