@@ -277,7 +277,7 @@ SlotView slot_at(mpm_ctx* h, int t) {
     s.tiles = h->tiles_pool;
     s.part = h->part;
     s.ntot = h->ntot_arr + t;
-    s.nbr = h->nbr_pool;
+    s.nbr = canon_fused(k) ? h->nbr_pool : nullptr;  // the neighbour table: small problems (kernels_tile.cu)
     s.step = t;
     s.halo = Halo{0, k.nb, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
     if (h->dd) {

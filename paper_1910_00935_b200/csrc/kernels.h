@@ -84,7 +84,7 @@ struct SlotView {
                              //                   backward: grid_op_grad output (Pb, Mb)
     int* ntot;               // [1]    sorted particles of this step (set by the scan)
     int* nbr;                // pool [P][3^d] pool tile index of each neighbour block (offsets -1..1 per
-                             //        axis), or -1; set by k_canon / p2g, read by the grid passes
+                             //        axis), or -1; set by p2g (small problems; null otherwise), read by the grid passes
     int step;                // t
     Halo halo;               // f3 neighbours (covered sums of grid_op / grid_op_grad)
 };

@@ -147,15 +147,17 @@ __device__ __forceinline__ float4 covered_sum(const KParams& p, int e, const int
 
 // Neighbour table (single domain): row bi of step t holds, for each block offset o in {-1, 0, 1}^d
 // (o_0 slowest), the pool tile index of block (block of bi) + o, or -1 -- the block-map lookups
-// of covered_sum done once per block (by k_canon, or p2g for small problems) instead of once per
-// tile node, so a grid pass's tile loads no longer wait on a block-map load.
+// of covered_sum done once per block (in p2g, with the canonical ordering) instead of once per
+// tile node, so a grid pass's tile loads no longer wait on a block-map load.  Small problems only
+// (SlotView::nbr is null otherwise): C2 +6.5%, but C5 +0.2% at k = 2 and -0.9% at k = 32 (the fill
+// lengthens k_canon by more than the grid passes gain).
 #ifndef MPM_NBR_TABLE
 #define MPM_NBR_TABLE 1
 #endif
 template <int D> constexpr int kNbr = D == 3 ? 27 : 9;
 template <int D>
 __device__ __forceinline__ void fill_nbr(const KParams& p, const SlotView& sl, int b0, int bi, int tid) {
-    if (!MPM_NBR_TABLE || tid >= kNbr<D>) return;
+    if (!MPM_NBR_TABLE || sl.nbr == nullptr || tid >= kNbr<D>) return;
     int e, c0[3];
     block_origin<D>(p, sl.blist[b0 + bi], e, c0);
     const int o[3] = {tid / (D == 3 ? 9 : 3) - 1, (D == 3 ? (tid / 3) % 3 : tid % 3) - 1, D == 3 ? tid % 3 - 1 : 0};
@@ -943,11 +945,10 @@ __global__ void __launch_bounds__(kT) k_canon(KParams p, SlotView sl, int* __res
     const int* bstart = sl.bstart + b0 + sl.step;
     unsigned short* cstart = sl.cstart + (int64_t)b0 * (Geo<3>::CELLS + 1);
     for (int bi = blockIdx.x; bi < nact; bi += gridDim.x) {
-        if (p.dim == 3) fill_nbr<3>(p, sl, b0, bi, threadIdx.x);
-        else fill_nbr<2>(p, sl, b0, bi, threadIdx.x);
         const int start = bstart[bi], n = bstart[bi + 1] - start;
         canon_block<kT>(sl, bi, start, n, cstart, pid_next, keys_next, flags, smem, s_cst, nullptr);
     }
+    (void)p;
 }
 
 // ---------------------------------------------------------------- P2G
@@ -1070,7 +1071,7 @@ __global__ void __launch_bounds__(kTQ, MPM_P2G_MINB) k_p2g(KParams p, SlotView s
 // (P, M) = sum of the covering partial tiles; u1 = P/(M + eps) - dt g e_y; sticky walls.
 // Resolved tile entry: (u1, M), or (0, 0, 0, -M) where the wall zeroed the velocity
 // (sign bit set, also for M = 0: -0.0f; nodes outside the grid: (0, 0, 0, -0)).  Stored per step: g2p / g2p_grad / grid_op_grad read it.
-template <int D, bool HALO>
+template <int D, bool HALO, bool NBR = false>  // NBR: covering tiles from the neighbour table
 __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
     pdl_begin();
     using G = Geo<D>;
@@ -1092,7 +1093,7 @@ __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
         const bool inside = g[0] < p.n_grid && g[1] < p.n_grid && (D == 2 || g[2] < p.n_grid);
         float4 out = make_float4(0.f, 0.f, 0.f, -0.0f);
         if (inside) {
-            const float4 pm = (!HALO && MPM_NBR_TABLE)
+            const float4 pm = (!HALO && NBR)
                                   ? covered_sum_nbr<D>(sl.nbr + (int64_t)(b0 + bi) * kNbr<D>, n, part_g)
                                   : covered_sum<D, HALO>(p, e, g, sl.bmap, part_g, sl.halo, nt0, nt1);
             float u0[3], u1[3];
@@ -1107,7 +1108,7 @@ __global__ void __launch_bounds__(kT) k_grid_op(KParams p, SlotView sl) {
 // P:589 (select rule): per node, ub = sum of the covering U_bar partial tiles;
 // sticky (sign bit of w): Pb = Mb = 0; else u0 = u1 + dt g e_y, Pb = ub/(M + eps),
 // Mb = -(ub . u0)/(M + eps).  Output tile (Pb, Mb) -> sl.part (local block index).
-template <int D, bool HALO>
+template <int D, bool HALO, bool NBR = false>
 __global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, const float4* __restrict__ ubar) {
     pdl_begin();
     using G = Geo<D>;
@@ -1128,7 +1129,7 @@ __global__ void __launch_bounds__(kT) k_grid_op_grad(KParams p, SlotView sl, con
             block_origin<D, true>(p, __ldg(blist + bi), e, c0);
             local_node<D>(q, n);
             const int g[3] = {c0[0] + n[0], c0[1] + n[1], D == 3 ? c0[2] + n[2] : 0};
-            const float4 ub = (!HALO && MPM_NBR_TABLE)
+            const float4 ub = (!HALO && NBR)
                                   ? covered_sum_nbr<D>(sl.nbr + (int64_t)(b0 + bi) * kNbr<D>, n, ub_g)
                                   : covered_sum<D, HALO>(p, e, g, sl.bmap, ub_g, sl.halo, nt0, nt1);
             const float u0[3] = {r.x, r.y + p.dt * p.gravity, r.z};
@@ -2285,10 +2286,13 @@ static unsigned node_grid(const KParams& p) {
 static bool has_halo(const SlotView& sl) { return sl.halo.tiles[0] != nullptr || sl.halo.tiles[1] != nullptr; }
 void launch_grid_op(const KParams& p, const SlotView& sl, cudaStream_t s) {
     if (has_halo(sl)) DISPATCH(p.dim, launch_k(k_grid_op<DIM, true>, node_grid(p), kT, 0, s, p, sl));
+    else if (MPM_NBR_TABLE && sl.nbr) DISPATCH(p.dim, launch_k(k_grid_op<DIM, false, true>, node_grid(p), kT, 0, s, p, sl));
     else DISPATCH(p.dim, launch_k(k_grid_op<DIM, false>, node_grid(p), kT, 0, s, p, sl));
 }
 void launch_grid_op_grad(const KParams& p, const SlotView& sl, const float4* ubar, cudaStream_t s) {
     if (has_halo(sl)) DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM, true>, node_grid(p), kT, 0, s, p, sl, ubar));
+    else if (MPM_NBR_TABLE && sl.nbr)
+        DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM, false, true>, node_grid(p), kT, 0, s, p, sl, ubar));
     else DISPATCH(p.dim, launch_k(k_grid_op_grad<DIM, false>, node_grid(p), kT, 0, s, p, sl, ubar));
 }
 static bool split_blocks(const KParams& p) { return p.N * p.E <= kSmallProblem; }  // see item_split
