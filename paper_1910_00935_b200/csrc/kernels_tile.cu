@@ -1520,7 +1520,7 @@ __global__ void __launch_bounds__(kTQ, MPM_G2PG_MINB) k_g2p_grad(KParams p, Slot
 // U tile staged like g2p.  Runs on a second stream, concurrently with the U_bar scatter
 // (k_g2p_grad) and grid_op_grad; writes xb_t (partial) for p2g_grad.
 #ifndef MPM_GATHER_MINB
-#define MPM_GATHER_MINB 5  // 5 CTAs of 128 threads per SM: <= 102 registers
+#define MPM_GATHER_MINB 6  // 6 CTAs of 128 threads per SM: <= 80 registers (5: C5 -0.3%, C3 -0.5%, C4 -0.4%)
 #endif
 template <int D, bool SPLIT>
 __global__ void __launch_bounds__(kTG, MPM_GATHER_MINB) k_g2p_grad_gather(KParams p, SlotView sl, StateView S, AdjView Sbn,
